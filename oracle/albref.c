@@ -1,0 +1,787 @@
+/*
+ * albref.c -- CPU ORACLE (test infrastructure only; see albref.h).
+ *
+ * Plain scalar C in IEEE double, built with -O2 -ffp-contract=off.  Every
+ * function follows its definition in the order the definition states it; the
+ * citations point at PAPER.md (the method: Table 1 rows at PAPER.md:123-133,
+ * the co-transform text at PAPER.md:74-80, the geometry text at PAPER.md:85-87)
+ * and at SPEC.md for the formula the paper leaves out, with the DESIGN.md
+ * reading (R1..R24, O0..O14) where both are silent.
+ *
+ * Shares no code with the CUDA path (paper_1809_06839_b200/csrc).
+ */
+#include "albref.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ O1 RNG */
+
+/* Philox4x32-10: multipliers 0xD2511F53 / 0xCD9E8D57, Weyl bumps
+ * 0x9E3779B9 / 0xBB67AE85, ten rounds, key bumped before rounds 2..10.
+ * Pinned by the Random123 known-answer vectors (tests/golden/philox_kat.txt). */
+void albref_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* u = ((a >> 5) * 2^26 + (b >> 6)) * 2^-53  (O1). */
+double albref_u53(uint32_t a, uint32_t b) {
+  double hi = (double)(a >> 5);
+  double lo = (double)(b >> 6);
+  return (hi * 67108864.0 + lo) * (1.0 / 9007199254740992.0);
+}
+
+/* draw j of (seed, image, slot): counter (image_lo32, slot, j>>1, TAG_PARAM=0),
+ * key (seed_lo32, seed_hi32); words 2(j&1), 2(j&1)+1 (O1). */
+double albref_draw(uint64_t seed, uint64_t image_index, int32_t slot, int32_t j) {
+  uint32_t ctr[4] = {(uint32_t)image_index, (uint32_t)slot, (uint32_t)(j >> 1), 0u};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t out[4];
+  albref_philox4x32_10(ctr, key, out);
+  int w = 2 * (j & 1);
+  return albref_u53(out[w], out[w + 1]);
+}
+
+/* uniform_int(n) = floor(u * n), clamped to n-1. */
+static int32_t uniform_int(double u, int32_t n) {
+  double f = floor(u * (double)n);
+  int32_t k = (int32_t)f;
+  if (k > n - 1) k = n - 1;
+  return k;
+}
+
+/* U(lo, hi) = lo + (hi - lo) * u  (O1). */
+static double uniform_range(double lo, double hi, double u) {
+  return lo + (hi - lo) * u;
+}
+
+/* --------------------------------------------------------- O0 arithmetic */
+
+/* clip_round(v) = min(255, max(0, floor(v + 0.5)))  (R1). */
+uint8_t albref_clip_round(double v) {
+  double r = floor(v + 0.5);
+  if (r < 0.0) return 0;
+  if (r > 255.0) return 255;
+  return (uint8_t)r;
+}
+
+/* reflect-101: -1 -> 1, n -> n-2; periodic with period 2n-2
+ * beyond one reflection (reading R7). */
+int32_t albref_reflect101(int32_t i, int32_t n) {
+  if (n == 1) return 0;
+  int64_t period = 2 * (int64_t)n - 2;
+  int64_t k = i < 0 ? -(int64_t)i : (int64_t)i;
+  k = k % period;
+  if (k >= n) k = period - k;
+  return (int32_t)k;
+}
+
+/* a mod m into [0, m) */
+static double fmod_pos(double a, double m) {
+  double r = a - m * floor(a / m);
+  if (r >= m) r = 0.0;
+  if (r < 0.0) r = 0.0;
+  return r;
+}
+
+/* ---------------------------------------------------------------- O9 HSV */
+
+/* hexcone RGB -> HSV: v = max/255, s = (max-min)/max,
+ * h from the dominant-channel sector, ties resolved r > g > b. */
+void albref_rgb_to_hsv(double r, double g, double b, double* h, double* s, double* v) {
+  double mx = r, mn = r;
+  if (g > mx) mx = g;
+  if (b > mx) mx = b;
+  if (g < mn) mn = g;
+  if (b < mn) mn = b;
+  double d = mx - mn;
+  *v = mx / 255.0;
+  *s = mx > 0.0 ? d / mx : 0.0;
+  if (d == 0.0) {
+    *h = 0.0;
+  } else if (mx == r) {
+    *h = 60.0 * fmod_pos((g - b) / d, 6.0);
+  } else if (mx == g) {
+    *h = 60.0 * ((b - r) / d + 2.0);
+  } else {
+    *h = 60.0 * ((r - g) / d + 4.0);
+  }
+}
+
+/* hexcone HSV -> RGB (sector decomposition); returns components
+ * scaled to [0,255] before rounding. */
+void albref_hsv_to_rgb(double h, double s, double v, double* r, double* g, double* b) {
+  double C = v * s;
+  double hp = h / 60.0;
+  double X = C * (1.0 - fabs(fmod_pos(hp, 2.0) - 1.0));
+  double m = v - C;
+  int sector = (int)floor(hp);
+  sector = ((sector % 6) + 6) % 6;
+  double r1, g1, b1;
+  switch (sector) {
+    case 0: r1 = C; g1 = X; b1 = 0.0; break;
+    case 1: r1 = X; g1 = C; b1 = 0.0; break;
+    case 2: r1 = 0.0; g1 = C; b1 = X; break;
+    case 3: r1 = 0.0; g1 = X; b1 = C; break;
+    case 4: r1 = X; g1 = 0.0; b1 = C; break;
+    default: r1 = C; g1 = 0.0; b1 = X; break;
+  }
+  *r = 255.0 * (r1 + m);
+  *g = 255.0 * (g1 + m);
+  *b = 255.0 * (b1 + m);
+}
+
+/* ---------------------------------------------------------------- O8 LUT */
+
+static int is_lut_kind(int32_t kind) {
+  return kind == ALBREF_BRIGHTNESS || kind == ALBREF_CONTRAST ||
+         kind == ALBREF_BRIGHTNESS_CONTRAST || kind == ALBREF_GAMMA ||
+         kind == ALBREF_SHIFT_RGB;
+}
+
+/* LUT[c][v] of the LUT-type ops (O8):
+ *   Brightness  clip_round(v*beta)
+ *   Contrast    clip_round(127.5 + (v-127.5)*c)
+ *   BC          Contrast_c(Brightness_beta(v))           reading R12
+ *   Gamma       clip_round(255*(v/255)^g)
+ *   ShiftRGB    clip_round(v + delta_c) */
+int albref_build_lut(int32_t kind, const double* prm, uint8_t* lut) {
+  if (!is_lut_kind(kind)) return ALBREF_E_UNSUPPORTED;
+  for (int c = 0; c < 3; ++c) {
+    for (int v = 0; v < 256; ++v) {
+      double x = (double)v;
+      uint8_t out;
+      switch (kind) {
+        case ALBREF_BRIGHTNESS: out = albref_clip_round(x * prm[0]); break;
+        case ALBREF_CONTRAST: out = albref_clip_round(127.5 + (x - 127.5) * prm[0]); break;
+        case ALBREF_BRIGHTNESS_CONTRAST: {
+          double t = (double)albref_clip_round(x * prm[0]);
+          out = albref_clip_round(127.5 + (t - 127.5) * prm[1]);
+          break;
+        }
+        case ALBREF_GAMMA: out = albref_clip_round(255.0 * pow(x / 255.0, prm[0])); break;
+        default: out = albref_clip_round(x + prm[c]); break; /* SHIFT_RGB */
+      }
+      lut[c * 256 + v] = out;
+    }
+  }
+  return ALBREF_OK;
+}
+
+/* Equalize LUT (reading R15): cdf[v] = sum_{u<=v} hist[u]; c_min = hist of the
+ * first non-empty bin; D = N - c_min; identity when D == 0; otherwise
+ * LUT[v] = floor((2*255*max(cdf[v]-c_min, 0) + D) / (2*D)), i.e. round-half-up
+ * of 255*(cdf[v]-c_min)/D in exact integers. */
+int albref_equalize_lut(const int64_t* hist, uint8_t* lut) {
+  int64_t N = 0;
+  for (int v = 0; v < 256; ++v) N += hist[v];
+  int64_t c_min = 0;
+  for (int v = 0; v < 256; ++v) {
+    if (hist[v] > 0) { c_min = hist[v]; break; }
+  }
+  int64_t D = N - c_min;
+  if (D == 0) {
+    for (int v = 0; v < 256; ++v) lut[v] = (uint8_t)v;
+    return ALBREF_OK;
+  }
+  int64_t cdf = 0;
+  for (int v = 0; v < 256; ++v) {
+    cdf += hist[v];
+    int64_t num = cdf - c_min;
+    if (num < 0) num = 0;
+    int64_t q = (2 * 255 * num + D) / (2 * D);
+    lut[v] = (uint8_t)q;
+  }
+  return ALBREF_OK;
+}
+
+/* ------------------------------------------------------- validation / shape */
+
+static int is_shape_kind(int32_t k) {
+  return k == ALBREF_RANDOM_CROP || k == ALBREF_PAD_TO_SIZE || k == ALBREF_RESIZE ||
+         k == ALBREF_RANDOM_SIZED_CROP || k == ALBREF_CROP;
+}
+
+static int validate_ops(const albref_op* ops, int32_t n_ops) {
+  if (n_ops < 0 || (n_ops > 0 && !ops)) return ALBREF_E_INVALID_ARG;
+  for (int32_t k = 0; k < n_ops; ++k) {
+    const albref_op* o = &ops[k];
+    if (o->kind < 0 || o->kind >= ALBREF_NUM_KINDS) return ALBREF_E_UNKNOWN_OP;
+    if (!(o->p >= 0.0 && o->p <= 1.0)) return ALBREF_E_RANGE;
+    for (int j = 0; j < 4; ++j)
+      if (!(o->lo[j] <= o->hi[j])) return ALBREF_E_RANGE;
+    if (is_shape_kind(o->kind) && o->p != 1.0) return ALBREF_E_RANGE; /* R17 */
+    if (o->interp != ALBREF_INTERP_NEAREST && o->interp != ALBREF_INTERP_BILINEAR)
+      return ALBREF_E_RANGE;
+    if (o->border != ALBREF_BORDER_CONSTANT && o->border != ALBREF_BORDER_REFLECT_101)
+      return ALBREF_E_RANGE;
+    switch (o->kind) {
+      case ALBREF_SHIFT_SCALE_ROTATE: if (!(o->lo[2] > 0.0)) return ALBREF_E_RANGE; break;
+      case ALBREF_BRIGHTNESS: if (!(o->lo[0] >= 0.0)) return ALBREF_E_RANGE; break;
+      case ALBREF_CONTRAST: if (!(o->lo[0] >= 0.0)) return ALBREF_E_RANGE; break;
+      case ALBREF_BRIGHTNESS_CONTRAST:
+        if (!(o->lo[0] >= 0.0) || !(o->lo[1] >= 0.0)) return ALBREF_E_RANGE;
+        break;
+      case ALBREF_GAMMA: if (!(o->lo[0] > 0.0)) return ALBREF_E_RANGE; break;
+      case ALBREF_RANDOM_CROP: case ALBREF_CROP: case ALBREF_PAD_TO_SIZE: case ALBREF_RESIZE:
+        if (o->out_w < 1 || o->out_h < 1) return ALBREF_E_RANGE;
+        break;
+      case ALBREF_RANDOM_SIZED_CROP:
+        if (o->out_w < 1 || o->out_h < 1 || o->min_side < 1 || o->max_side < o->min_side)
+          return ALBREF_E_RANGE;
+        break;
+      case ALBREF_NORMALIZE:
+        if (k != n_ops - 1 || o->p != 1.0) return ALBREF_E_RANGE;
+        for (int c = 0; c < 3; ++c)
+          if (!(o->std[c] != 0.0)) return ALBREF_E_RANGE;
+        break;
+      default: break;
+    }
+  }
+  return ALBREF_OK;
+}
+
+static int step_shape(const albref_op* o, int32_t h, int32_t w, int32_t* oh, int32_t* ow) {
+  switch (o->kind) {
+    case ALBREF_RANDOM_CROP:
+      if (o->out_w > w || o->out_h > h) return ALBREF_E_INVALID_ARG;
+      *oh = o->out_h; *ow = o->out_w; return ALBREF_OK;
+    case ALBREF_CROP:
+      if (o->crop_x < 0 || o->crop_y < 0 || o->crop_x + o->out_w > w || o->crop_y + o->out_h > h)
+        return ALBREF_E_INVALID_ARG;
+      *oh = o->out_h; *ow = o->out_w; return ALBREF_OK;
+    case ALBREF_PAD_TO_SIZE:
+      if (w > o->out_w || h > o->out_h) return ALBREF_E_INVALID_ARG;
+      *oh = o->out_h; *ow = o->out_w; return ALBREF_OK;
+    case ALBREF_RESIZE:
+      *oh = o->out_h; *ow = o->out_w; return ALBREF_OK;
+    case ALBREF_RANDOM_SIZED_CROP: {
+      int32_t mside = h < w ? h : w;
+      if (o->min_side > mside) return ALBREF_E_INVALID_ARG;
+      *oh = o->out_h; *ow = o->out_w; return ALBREF_OK;
+    }
+    default:
+      *oh = h; *ow = w; return ALBREF_OK;
+  }
+}
+
+int albref_output_shape(const albref_op* ops, int32_t n_ops, int32_t in_h, int32_t in_w,
+                        int32_t* out_h, int32_t* out_w) {
+  int rc = validate_ops(ops, n_ops);
+  if (rc) return rc;
+  if (in_h < 1 || in_w < 1) return ALBREF_E_SHAPE;
+  int32_t h = in_h, w = in_w;
+  for (int32_t k = 0; k < n_ops; ++k) {
+    rc = step_shape(&ops[k], h, w, &h, &w);
+    if (rc) return rc;
+  }
+  *out_h = h; *out_w = w;
+  return ALBREF_OK;
+}
+
+/* ---------------------------------------------------------- O1 parameters */
+
+/* Param draws j = 1, 2, ... after the gate (draw 0), in the DESIGN.md O1 table
+ * order; h, w are the dims the slot sees. */
+static void draw_params(const albref_op* o, uint64_t seed, uint64_t idx, int32_t slot,
+                        int32_t h, int32_t w, double* prm) {
+  for (int j = 0; j < ALBREF_MAX_PARAMS; ++j) prm[j] = 0.0;
+  switch (o->kind) {
+    case ALBREF_ROTATE:
+    case ALBREF_BRIGHTNESS:
+    case ALBREF_CONTRAST:
+    case ALBREF_GAMMA:
+      prm[0] = uniform_range(o->lo[0], o->hi[0], albref_draw(seed, idx, slot, 1));
+      break;
+    case ALBREF_BRIGHTNESS_CONTRAST:
+      for (int j = 0; j < 2; ++j)
+        prm[j] = uniform_range(o->lo[j], o->hi[j], albref_draw(seed, idx, slot, 1 + j));
+      break;
+    case ALBREF_SHIFT_RGB:
+    case ALBREF_SHIFT_HSV:
+      for (int j = 0; j < 3; ++j)
+        prm[j] = uniform_range(o->lo[j], o->hi[j], albref_draw(seed, idx, slot, 1 + j));
+      break;
+    case ALBREF_SHIFT_SCALE_ROTATE: /* dx, dy, scale, theta */
+      for (int j = 0; j < 4; ++j)
+        prm[j] = uniform_range(o->lo[j], o->hi[j], albref_draw(seed, idx, slot, 1 + j));
+      break;
+    case ALBREF_RANDOM_CROP: /* x0 then y0 */
+      prm[0] = (double)uniform_int(albref_draw(seed, idx, slot, 1), w - o->out_w + 1);
+      prm[1] = (double)uniform_int(albref_draw(seed, idx, slot, 2), h - o->out_h + 1);
+      break;
+    case ALBREF_CROP:
+      prm[0] = (double)o->crop_x;
+      prm[1] = (double)o->crop_y;
+      break;
+    case ALBREF_RANDOM_SIZED_CROP: { /* side, x0, y0 (R6) */
+      int32_t mside = h < w ? h : w;
+      int32_t hi = o->max_side < mside ? o->max_side : mside;
+      int32_t side = o->min_side + uniform_int(albref_draw(seed, idx, slot, 1), hi - o->min_side + 1);
+      prm[0] = (double)side;
+      prm[1] = (double)uniform_int(albref_draw(seed, idx, slot, 2), w - side + 1);
+      prm[2] = (double)uniform_int(albref_draw(seed, idx, slot, 3), h - side + 1);
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+int albref_sample_params(const albref_op* ops, int32_t n_ops, uint64_t seed,
+                         uint64_t image_index, int32_t in_h, int32_t in_w,
+                         double* params, uint8_t* fired) {
+  int rc = validate_ops(ops, n_ops);
+  if (rc) return rc;
+  if (in_h < 1 || in_w < 1) return ALBREF_E_SHAPE;
+  int32_t h = in_h, w = in_w;
+  for (int32_t k = 0; k < n_ops; ++k) {
+    double gate = albref_draw(seed, image_index, k, 0); /* always drawn */
+    fired[k] = gate < ops[k].p ? 1 : 0;
+    int32_t nh, nw;
+    rc = step_shape(&ops[k], h, w, &nh, &nw);
+    if (rc) return rc;
+    draw_params(&ops[k], seed, image_index, k, h, w, &params[k * ALBREF_MAX_PARAMS]);
+    if (fired[k]) { h = nh; w = nw; }
+  }
+  return ALBREF_OK;
+}
+
+/* ----------------------------------------------------------- image state */
+
+typedef struct {
+  uint8_t* px;      /* [h][w][c] */
+  uint8_t* mask;    /* [h][w] or NULL */
+  int32_t h, w, c;
+  double* box;      /* [n][4] pixel-edge coordinates, unclipped (R18/R19) */
+  int32_t* label;
+  int32_t nbox;
+} state_t;
+
+static uint8_t* xalloc(size_t n) {
+  return (uint8_t*)malloc(n ? n : 1);
+}
+
+/* tap with border policy: reflect-101 remaps, constant substitutes fill
+ * (per tap, reading R7).  Returns 1 and sets *xi,*yi when in range. */
+static int border_index(int32_t border, int32_t x, int32_t y, int32_t w, int32_t h,
+                        int32_t* xi, int32_t* yi) {
+  if (x >= 0 && x < w && y >= 0 && y < h) { *xi = x; *yi = y; return 1; }
+  if (border == ALBREF_BORDER_REFLECT_101) {
+    *xi = albref_reflect101(x, w);
+    *yi = albref_reflect101(y, h);
+    return 1;
+  }
+  return 0;
+}
+
+/* bilinear weights as O5/O7: v = (1-fy)((1-fx)p00 + fx p10) + fy((1-fx)p01 + fx p11) */
+static double bilerp(double p00, double p10, double p01, double p11, double fx, double fy) {
+  return (1.0 - fy) * ((1.0 - fx) * p00 + fx * p10) + fy * ((1.0 - fx) * p01 + fx * p11);
+}
+
+/* Sample image channel values at real source coordinate (xs, ys) with the
+ * affine-op convention (pixel (x,y) at real (x,y)). */
+static void sample_affine(const state_t* s, double xs, double ys, int32_t interp,
+                          int32_t border, const uint8_t* fill, uint8_t* out) {
+  if (interp == ALBREF_INTERP_NEAREST) {
+    int32_t xn = (int32_t)floor(xs + 0.5), yn = (int32_t)floor(ys + 0.5);
+    int32_t xi, yi;
+    for (int c = 0; c < s->c; ++c)
+      out[c] = border_index(border, xn, yn, s->w, s->h, &xi, &yi)
+                   ? s->px[((size_t)yi * s->w + xi) * s->c + c]
+                   : fill[c];
+    return;
+  }
+  double fx0 = floor(xs), fy0 = floor(ys);
+  int32_t x0 = (int32_t)fx0, y0 = (int32_t)fy0;
+  double fx = xs - fx0, fy = ys - fy0;
+  for (int c = 0; c < s->c; ++c) {
+    double p[4];
+    for (int t = 0; t < 4; ++t) {
+      int32_t xi, yi;
+      int32_t tx = x0 + (t & 1), ty = y0 + (t >> 1);
+      p[t] = border_index(border, tx, ty, s->w, s->h, &xi, &yi)
+                 ? (double)s->px[((size_t)yi * s->w + xi) * s->c + c]
+                 : (double)fill[c];
+    }
+    out[c] = albref_clip_round(bilerp(p[0], p[1], p[2], p[3], fx, fy));
+  }
+}
+
+static uint8_t sample_mask_nearest(const state_t* s, double xs, double ys, int32_t border,
+                                   uint8_t mask_fill) {
+  int32_t xn = (int32_t)floor(xs + 0.5), yn = (int32_t)floor(ys + 0.5);
+  int32_t xi, yi;
+  return border_index(border, xn, yn, s->w, s->h, &xi, &yi) ? s->mask[(size_t)yi * s->w + xi]
+                                                            : mask_fill;
+}
+
+static void replace_px(state_t* s, uint8_t* px, uint8_t* mask, int32_t h, int32_t w) {
+  free(s->px);
+  s->px = px;
+  if (s->mask) { free(s->mask); s->mask = mask; }
+  s->h = h; s->w = w;
+}
+
+/* ---------------------------------------------------- O2 flips, O3/O4 window */
+
+/* HFlip: out[y][x] = in[y][W-1-x]; boxes x' = W - x */
+static void op_hflip(state_t* s) {
+  uint8_t* px = xalloc((size_t)s->h * s->w * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)s->h * s->w) : NULL;
+  for (int32_t y = 0; y < s->h; ++y)
+    for (int32_t x = 0; x < s->w; ++x) {
+      for (int c = 0; c < s->c; ++c)
+        px[((size_t)y * s->w + x) * s->c + c] = s->px[((size_t)y * s->w + (s->w - 1 - x)) * s->c + c];
+      if (mk) mk[(size_t)y * s->w + x] = s->mask[(size_t)y * s->w + (s->w - 1 - x)];
+    }
+  for (int32_t b = 0; b < s->nbox; ++b) {
+    double x0 = s->box[4 * b + 0], x1 = s->box[4 * b + 2];
+    s->box[4 * b + 0] = (double)s->w - x1;
+    s->box[4 * b + 2] = (double)s->w - x0;
+  }
+  replace_px(s, px, mk, s->h, s->w);
+}
+
+/* VFlip: out[y] = in[H-1-y]; boxes y' = H - y */
+static void op_vflip(state_t* s) {
+  uint8_t* px = xalloc((size_t)s->h * s->w * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)s->h * s->w) : NULL;
+  for (int32_t y = 0; y < s->h; ++y)
+    for (int32_t x = 0; x < s->w; ++x) {
+      for (int c = 0; c < s->c; ++c)
+        px[((size_t)y * s->w + x) * s->c + c] = s->px[((size_t)(s->h - 1 - y) * s->w + x) * s->c + c];
+      if (mk) mk[(size_t)y * s->w + x] = s->mask[(size_t)(s->h - 1 - y) * s->w + x];
+    }
+  for (int32_t b = 0; b < s->nbox; ++b) {
+    double y0 = s->box[4 * b + 1], y1 = s->box[4 * b + 3];
+    s->box[4 * b + 1] = (double)s->h - y1;
+    s->box[4 * b + 3] = (double)s->h - y0;
+  }
+  replace_px(s, px, mk, s->h, s->w);
+}
+
+/* Crop window (x0, y0, cw, ch): out[y][x] = in[y0+y][x0+x]; boxes translate
+ * (PAPER.md:123); clipping happens at the end (R19). */
+static void op_crop(state_t* s, int32_t x0, int32_t y0, int32_t cw, int32_t ch) {
+  uint8_t* px = xalloc((size_t)ch * cw * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)ch * cw) : NULL;
+  for (int32_t y = 0; y < ch; ++y)
+    for (int32_t x = 0; x < cw; ++x) {
+      for (int c = 0; c < s->c; ++c)
+        px[((size_t)y * cw + x) * s->c + c] = s->px[((size_t)(y0 + y) * s->w + (x0 + x)) * s->c + c];
+      if (mk) mk[(size_t)y * cw + x] = s->mask[(size_t)(y0 + y) * s->w + (x0 + x)];
+    }
+  for (int32_t b = 0; b < s->nbox; ++b) {
+    s->box[4 * b + 0] -= x0; s->box[4 * b + 2] -= x0;
+    s->box[4 * b + 1] -= y0; s->box[4 * b + 3] -= y0;
+  }
+  replace_px(s, px, mk, ch, cw);
+}
+
+/* PadToSize: centred, left = floor((tw-W)/2), top = floor((th-H)/2), constant
+ * fill (R8). */
+static void op_pad(state_t* s, const albref_op* o) {
+  int32_t tw = o->out_w, th = o->out_h;
+  int32_t left = (tw - s->w) / 2, top = (th - s->h) / 2;
+  uint8_t* px = xalloc((size_t)th * tw * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)th * tw) : NULL;
+  for (int32_t y = 0; y < th; ++y)
+    for (int32_t x = 0; x < tw; ++x) {
+      int32_t sx = x - left, sy = y - top;
+      int inside = sx >= 0 && sx < s->w && sy >= 0 && sy < s->h;
+      for (int c = 0; c < s->c; ++c)
+        px[((size_t)y * tw + x) * s->c + c] =
+            inside ? s->px[((size_t)sy * s->w + sx) * s->c + c] : o->fill[c];
+      if (mk) mk[(size_t)y * tw + x] = inside ? s->mask[(size_t)sy * s->w + sx] : o->mask_fill;
+    }
+  for (int32_t b = 0; b < s->nbox; ++b) {
+    s->box[4 * b + 0] += left; s->box[4 * b + 2] += left;
+    s->box[4 * b + 1] += top; s->box[4 * b + 3] += top;
+  }
+  replace_px(s, px, mk, th, tw);
+}
+
+/* ------------------------------------------------------------- O5 resize */
+
+/* Resize of the window [wx0, wx0+ww) x [wy0, wy0+wh) to nw x nh:
+ * x_s = (x_d + 0.5) * W / new_w - 0.5, clamped to the window
+ * (replicate border, R9); bilinear as O5, nearest = round_half_up(x_s)
+ * (SPEC.md:263).  Masks nearest.  Boxes scale (pixel edges). */
+static void op_resize_window(state_t* s, int32_t wx0, int32_t wy0, int32_t ww, int32_t wh,
+                             int32_t nw, int32_t nh, int32_t interp) {
+  uint8_t* px = xalloc((size_t)nh * nw * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)nh * nw) : NULL;
+  for (int32_t y = 0; y < nh; ++y) {
+    double ys = ((double)y + 0.5) * (double)wh / (double)nh - 0.5;
+    if (ys < 0.0) ys = 0.0;
+    if (ys > (double)(wh - 1)) ys = (double)(wh - 1);
+    for (int32_t x = 0; x < nw; ++x) {
+      double xs = ((double)x + 0.5) * (double)ww / (double)nw - 0.5;
+      if (xs < 0.0) xs = 0.0;
+      if (xs > (double)(ww - 1)) xs = (double)(ww - 1);
+      uint8_t* o = &px[((size_t)y * nw + x) * s->c];
+      int32_t xn = (int32_t)floor(xs + 0.5), yn = (int32_t)floor(ys + 0.5);
+      if (interp == ALBREF_INTERP_NEAREST) {
+        for (int c = 0; c < s->c; ++c)
+          o[c] = s->px[((size_t)(wy0 + yn) * s->w + (wx0 + xn)) * s->c + c];
+      } else {
+        double fx0 = floor(xs), fy0 = floor(ys);
+        int32_t x0 = (int32_t)fx0, y0 = (int32_t)fy0;
+        int32_t x1 = x0 + 1 < ww ? x0 + 1 : ww - 1;
+        int32_t y1 = y0 + 1 < wh ? y0 + 1 : wh - 1;
+        double fx = xs - fx0, fy = ys - fy0;
+        for (int c = 0; c < s->c; ++c) {
+          double p00 = s->px[((size_t)(wy0 + y0) * s->w + (wx0 + x0)) * s->c + c];
+          double p10 = s->px[((size_t)(wy0 + y0) * s->w + (wx0 + x1)) * s->c + c];
+          double p01 = s->px[((size_t)(wy0 + y1) * s->w + (wx0 + x0)) * s->c + c];
+          double p11 = s->px[((size_t)(wy0 + y1) * s->w + (wx0 + x1)) * s->c + c];
+          o[c] = albref_clip_round(bilerp(p00, p10, p01, p11, fx, fy));
+        }
+      }
+      if (mk) mk[(size_t)y * nw + x] = s->mask[(size_t)(wy0 + yn) * s->w + (wx0 + xn)];
+    }
+  }
+  for (int32_t b = 0; b < s->nbox; ++b) {
+    s->box[4 * b + 0] = (s->box[4 * b + 0] - wx0) * (double)nw / (double)ww;
+    s->box[4 * b + 2] = (s->box[4 * b + 2] - wx0) * (double)nw / (double)ww;
+    s->box[4 * b + 1] = (s->box[4 * b + 1] - wy0) * (double)nh / (double)wh;
+    s->box[4 * b + 3] = (s->box[4 * b + 3] - wy0) * (double)nh / (double)wh;
+  }
+  replace_px(s, px, mk, nh, nw);
+}
+
+/* ------------------------------------------------------- O7 affine warps */
+
+/* Rotate / ShiftScaleRotate:
+ * centre c = ((W-1)/2, (H-1)/2), t = (dx*W, dy*H), forward p' = c + s R (p-c) + t
+ * with R = [[cos, sin], [-sin, cos]] (CCW as displayed, R2); per output pixel
+ *   x_s = cx + (cos*(x_d-cx-tx) - sin*(y_d-cy-ty)) / s
+ *   y_s = cy + (sin*(x_d-cx-tx) + cos*(y_d-cy-ty)) / s
+ * bilinear/nearest with the op's border, masks nearest.
+ * Boxes: 4 corners in pixel-centre frame through the forward map, envelope
+ * (R18). */
+static void op_affine(state_t* s, const albref_op* o, double dx, double dy, double scale,
+                      double theta_deg) {
+  double th = theta_deg * 3.141592653589793 / 180.0;
+  double cs = cos(th), sn = sin(th);
+  double cx = ((double)s->w - 1.0) / 2.0, cy = ((double)s->h - 1.0) / 2.0;
+  double tx = dx * (double)s->w, ty = dy * (double)s->h;
+  uint8_t* px = xalloc((size_t)s->h * s->w * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)s->h * s->w) : NULL;
+  for (int32_t y = 0; y < s->h; ++y)
+    for (int32_t x = 0; x < s->w; ++x) {
+      double ux = (double)x - cx - tx, uy = (double)y - cy - ty;
+      double xs = cx + (cs * ux - sn * uy) / scale;
+      double ys = cy + (sn * ux + cs * uy) / scale;
+      sample_affine(s, xs, ys, o->interp, o->border, o->fill, &px[((size_t)y * s->w + x) * s->c]);
+      if (mk) mk[(size_t)y * s->w + x] = sample_mask_nearest(s, xs, ys, o->border, o->mask_fill);
+    }
+  for (int32_t b = 0; b < s->nbox; ++b) {
+    double lo_x = 0, lo_y = 0, hi_x = 0, hi_y = 0;
+    for (int k = 0; k < 4; ++k) {
+      double X = s->box[4 * b + ((k & 1) ? 2 : 0)];
+      double Y = s->box[4 * b + ((k & 2) ? 3 : 1)];
+      double xc = X - 0.5, yc = Y - 0.5;
+      double xp = cx + scale * (cs * (xc - cx) + sn * (yc - cy)) + tx;
+      double yp = cy + scale * (-sn * (xc - cx) + cs * (yc - cy)) + ty;
+      double Xp = xp + 0.5, Yp = yp + 0.5;
+      if (k == 0 || Xp < lo_x) lo_x = Xp;
+      if (k == 0 || Xp > hi_x) hi_x = Xp;
+      if (k == 0 || Yp < lo_y) lo_y = Yp;
+      if (k == 0 || Yp > hi_y) hi_y = Yp;
+    }
+    s->box[4 * b + 0] = lo_x; s->box[4 * b + 1] = lo_y;
+    s->box[4 * b + 2] = hi_x; s->box[4 * b + 3] = hi_y;
+  }
+  replace_px(s, px, mk, s->h, s->w);
+}
+
+/* ------------------------------------------------------ O8-O12 colour ops */
+
+static void apply_lut3(state_t* s, const uint8_t* lut) {
+  for (size_t i = 0; i < (size_t)s->h * s->w; ++i)
+    for (int c = 0; c < s->c; ++c) s->px[i * s->c + c] = lut[c * 256 + s->px[i * s->c + c]];
+}
+
+/* ShiftHSV per pixel: to HSV, h = (h+dh) mod 360,
+ * s, v clamped to [0,1], back to RGB with clip_round. */
+static void op_shift_hsv(state_t* s, double dh, double ds, double dv) {
+  for (size_t i = 0; i < (size_t)s->h * s->w; ++i) {
+    uint8_t* p = &s->px[i * 3];
+    double h, sat, val, r, g, b;
+    albref_rgb_to_hsv((double)p[0], (double)p[1], (double)p[2], &h, &sat, &val);
+    h = fmod_pos(h + dh, 360.0);
+    sat = sat + ds; if (sat < 0.0) sat = 0.0; if (sat > 1.0) sat = 1.0;
+    val = val + dv; if (val < 0.0) val = 0.0; if (val > 1.0) val = 1.0;
+    albref_hsv_to_rgb(h, sat, val, &r, &g, &b);
+    p[0] = albref_clip_round(r);
+    p[1] = albref_clip_round(g);
+    p[2] = albref_clip_round(b);
+  }
+}
+
+/* Grayscale: y = round_half_up(0.299R + 0.587G + 0.114B) in exact integers,
+ * floor((299R + 587G + 114B + 500) / 1000), to all 3 channels (
+ * PAPER.md:133; R14). */
+static void op_grayscale(state_t* s) {
+  for (size_t i = 0; i < (size_t)s->h * s->w; ++i) {
+    uint8_t* p = &s->px[i * 3];
+    int32_t y = (299 * (int32_t)p[0] + 587 * (int32_t)p[1] + 114 * (int32_t)p[2] + 500) / 1000;
+    p[0] = p[1] = p[2] = (uint8_t)y;
+  }
+}
+
+/* Equalize per channel (R15). */
+static void op_equalize(state_t* s) {
+  for (int c = 0; c < s->c; ++c) {
+    int64_t hist[256];
+    uint8_t lut[256];
+    memset(hist, 0, sizeof(hist));
+    for (size_t i = 0; i < (size_t)s->h * s->w; ++i) hist[s->px[i * s->c + c]]++;
+    albref_equalize_lut(hist, lut);
+    for (size_t i = 0; i < (size_t)s->h * s->w; ++i) s->px[i * s->c + c] = lut[s->px[i * s->c + c]];
+  }
+}
+
+/* Normalize to fp32 NCHW: (float)((v/255 - mean_c)/std_c) (R16). */
+static void op_normalize(const state_t* s, const albref_op* o, float* out) {
+  for (int c = 0; c < 3; ++c)
+    for (int32_t y = 0; y < s->h; ++y)
+      for (int32_t x = 0; x < s->w; ++x) {
+        double v = (double)s->px[((size_t)y * s->w + x) * 3 + c];
+        out[((size_t)c * s->h + y) * s->w + x] = (float)((v / 255.0 - o->mean[c]) / o->std[c]);
+      }
+}
+
+/* ---------------------------------------------------------- O14 apply */
+
+int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
+                 const uint8_t* img, int32_t h, int32_t w, int32_t channels,
+                 const uint8_t* mask,
+                 const float* boxes, const int32_t* labels, int32_t n_boxes,
+                 float min_visibility,
+                 uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
+                 float* boxes_out, int32_t* labels_out, int32_t* n_boxes_out) {
+  int rc = validate_ops(ops, n_ops);
+  if (rc) return rc;
+  if (h < 1 || w < 1) return ALBREF_E_SHAPE;
+  if (channels != 1 && channels != 3) return ALBREF_E_UNSUPPORTED;
+  if (!img) return ALBREF_E_INVALID_ARG;
+  if (n_boxes < 0 || (n_boxes > 0 && (!boxes || !boxes_out || !n_boxes_out)))
+    return ALBREF_E_INVALID_ARG;
+  for (int32_t k = 0; k < n_ops; ++k) {
+    int32_t kd = ops[k].kind;
+    if (channels != 3 && (kd == ALBREF_SHIFT_RGB || kd == ALBREF_SHIFT_HSV ||
+                          kd == ALBREF_GRAYSCALE || kd == ALBREF_NORMALIZE))
+      return ALBREF_E_UNSUPPORTED;
+  }
+  int ends_norm = n_ops > 0 && ops[n_ops - 1].kind == ALBREF_NORMALIZE;
+  if (ends_norm ? !nchw_out : !img_out) return ALBREF_E_INVALID_ARG;
+
+  /* all params first: validation is atomic */
+  double* prm = (double*)malloc(sizeof(double) * ALBREF_MAX_PARAMS * (n_ops ? n_ops : 1));
+  uint8_t* fired = xalloc((size_t)n_ops);
+  rc = albref_sample_params(ops, n_ops, seed, image_index, h, w, prm, fired);
+  if (rc) { free(prm); free(fired); return rc; }
+
+  state_t s;
+  s.h = h; s.w = w; s.c = channels;
+  s.px = xalloc((size_t)h * w * channels);
+  memcpy(s.px, img, (size_t)h * w * channels);
+  s.mask = NULL;
+  if (mask) { s.mask = xalloc((size_t)h * w); memcpy(s.mask, mask, (size_t)h * w); }
+  s.nbox = n_boxes;
+  s.box = (double*)malloc(sizeof(double) * 4 * (n_boxes ? n_boxes : 1));
+  s.label = (int32_t*)malloc(sizeof(int32_t) * (n_boxes ? n_boxes : 1));
+  for (int32_t b = 0; b < n_boxes; ++b) {
+    s.box[4 * b + 0] = (double)boxes[4 * b + 0] * (double)w;
+    s.box[4 * b + 1] = (double)boxes[4 * b + 1] * (double)h;
+    s.box[4 * b + 2] = (double)boxes[4 * b + 2] * (double)w;
+    s.box[4 * b + 3] = (double)boxes[4 * b + 3] * (double)h;
+    s.label[b] = labels ? labels[b] : 0;
+  }
+
+  for (int32_t k = 0; k < n_ops; ++k) {
+    if (!fired[k]) continue; /* apply iff gate < p */
+    const albref_op* o = &ops[k];
+    const double* q = &prm[k * ALBREF_MAX_PARAMS];
+    uint8_t lut[768];
+    switch (o->kind) {
+      case ALBREF_HFLIP: op_hflip(&s); break;
+      case ALBREF_VFLIP: op_vflip(&s); break;
+      case ALBREF_ROTATE: op_affine(&s, o, 0.0, 0.0, 1.0, q[0]); break;
+      case ALBREF_SHIFT_SCALE_ROTATE: op_affine(&s, o, q[0], q[1], q[2], q[3]); break;
+      case ALBREF_RANDOM_CROP:
+      case ALBREF_CROP:
+        op_crop(&s, (int32_t)q[0], (int32_t)q[1], o->out_w, o->out_h);
+        break;
+      case ALBREF_PAD_TO_SIZE: op_pad(&s, o); break;
+      case ALBREF_RESIZE: op_resize_window(&s, 0, 0, s.w, s.h, o->out_w, o->out_h, o->interp); break;
+      case ALBREF_RANDOM_SIZED_CROP: {
+        int32_t side = (int32_t)q[0];
+        op_resize_window(&s, (int32_t)q[1], (int32_t)q[2], side, side, o->out_w, o->out_h, o->interp);
+        break;
+      }
+      case ALBREF_BRIGHTNESS: case ALBREF_CONTRAST: case ALBREF_BRIGHTNESS_CONTRAST:
+      case ALBREF_GAMMA: case ALBREF_SHIFT_RGB:
+        albref_build_lut(o->kind, q, lut);
+        apply_lut3(&s, lut);
+        break;
+      case ALBREF_SHIFT_HSV: op_shift_hsv(&s, q[0], q[1], q[2]); break;
+      case ALBREF_GRAYSCALE: op_grayscale(&s); break;
+      case ALBREF_EQUALIZE: op_equalize(&s); break;
+      case ALBREF_NORMALIZE: op_normalize(&s, o, nchw_out); break;
+      default: break;
+    }
+  }
+
+  if (!ends_norm) memcpy(img_out, s.px, (size_t)s.h * s.w * s.c);
+  if (mask && mask_out) memcpy(mask_out, s.mask, (size_t)s.h * s.w);
+
+  /* boxes: clip the final unclipped envelope to the image, keep iff non-empty
+   * and clipped area >= min_visibility * unclipped area (R19), stable. */
+  if (n_boxes_out) {
+    int32_t kept = 0;
+    for (int32_t b = 0; b < s.nbox; ++b) {
+      double X0 = s.box[4 * b + 0], Y0 = s.box[4 * b + 1];
+      double X1 = s.box[4 * b + 2], Y1 = s.box[4 * b + 3];
+      double area = (X1 - X0) * (Y1 - Y0);
+      double cx0 = X0 < 0.0 ? 0.0 : X0, cy0 = Y0 < 0.0 ? 0.0 : Y0;
+      double cx1 = X1 > (double)s.w ? (double)s.w : X1;
+      double cy1 = Y1 > (double)s.h ? (double)s.h : Y1;
+      if (!(cx1 > cx0 && cy1 > cy0)) continue;
+      double carea = (cx1 - cx0) * (cy1 - cy0);
+      if (!(carea >= (double)min_visibility * area)) continue;
+      boxes_out[4 * kept + 0] = (float)(cx0 / (double)s.w);
+      boxes_out[4 * kept + 1] = (float)(cy0 / (double)s.h);
+      boxes_out[4 * kept + 2] = (float)(cx1 / (double)s.w);
+      boxes_out[4 * kept + 3] = (float)(cy1 / (double)s.h);
+      if (labels_out) labels_out[kept] = s.label[b];
+      kept++;
+    }
+    *n_boxes_out = kept;
+  }
+
+  free(s.px); free(s.mask); free(s.box); free(s.label); free(prm); free(fired);
+  return ALBREF_OK;
+}

@@ -1,0 +1,117 @@
+/*
+ * albref.h -- CPU ORACLE for the augmentation hot path of arXiv 1809.06839
+ * ("Albumentations: fast and flexible image augmentations").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_1809_06839_b200/, include/alb_b200.h) never links,
+ * imports or calls it, and shares no source with it.
+ *
+ * What it computes: each transform exactly as defined in DESIGN.md "Readings"
+ * (the paper names the transforms -- PAPER.md:123-133, Table 1; PAPER.md:64,
+ * 76, 85-87 -- but gives no formulas; the formulas follow SPEC.md where it has
+ * one and the numbered readings R1..R24 of DESIGN.md otherwise).  Plain scalar
+ * C, IEEE double, compiled with -O2 -ffp-contract=off (no FMA contraction), no
+ * blocking, fusion or reordering.  One image per call.
+ *
+ * Layout: images are packed HWC uint8 (pitch = width*channels), RGB order,
+ * x = column, y = row, origin top-left.  Masks are packed HxW
+ * uint8.  Boxes are normalized xyxy float32 (reading R18).
+ *
+ * Every function returns 0 on success or a negative ALBREF_E_* code.
+ */
+#ifndef ALBREF_H
+#define ALBREF_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* op kinds (the numbering is part of the written contract in DESIGN.md) */
+enum {
+  ALBREF_HFLIP = 0, ALBREF_VFLIP = 1, ALBREF_ROTATE = 2, ALBREF_SHIFT_SCALE_ROTATE = 3,
+  ALBREF_RANDOM_CROP = 4, ALBREF_PAD_TO_SIZE = 5, ALBREF_RESIZE = 6,
+  ALBREF_RANDOM_SIZED_CROP = 7, ALBREF_BRIGHTNESS = 8, ALBREF_CONTRAST = 9,
+  ALBREF_BRIGHTNESS_CONTRAST = 10, ALBREF_GAMMA = 11, ALBREF_SHIFT_RGB = 12,
+  ALBREF_SHIFT_HSV = 13, ALBREF_GRAYSCALE = 14, ALBREF_EQUALIZE = 15,
+  ALBREF_NORMALIZE = 16, ALBREF_CROP = 17,
+  ALBREF_NUM_KINDS = 18
+};
+enum { ALBREF_INTERP_NEAREST = 0, ALBREF_INTERP_BILINEAR = 1 };
+enum { ALBREF_BORDER_CONSTANT = 0, ALBREF_BORDER_REFLECT_101 = 1 };
+enum {
+  ALBREF_OK = 0, ALBREF_E_INVALID_ARG = -1, ALBREF_E_UNKNOWN_OP = -2, ALBREF_E_RANGE = -3,
+  ALBREF_E_SHAPE = -4, ALBREF_E_UNSUPPORTED = -5
+};
+
+/* One transform of a pipeline (SPEC.md:470-474 TransformSpec).  Continuous
+ * parameter j is drawn as lo[j] + (hi[j]-lo[j])*u (O1). */
+typedef struct {
+  int32_t kind;
+  double p;                 /* application probability, [0,1]              */
+  double lo[4], hi[4];      /* per-parameter uniform ranges                 */
+  int32_t out_w, out_h;     /* RandomCrop/Crop/PadToSize/Resize/RSC size    */
+  int32_t min_side, max_side; /* RandomSizedCrop side range (pixels, R6)    */
+  int32_t crop_x, crop_y;   /* Crop window origin                           */
+  int32_t interp, border;   /* ALBREF_INTERP_*, ALBREF_BORDER_*             */
+  uint8_t fill[3], mask_fill;
+  double mean[3], std[3];   /* Normalize                                    */
+} albref_op;
+
+#define ALBREF_MAX_PARAMS 8
+
+/* Philox4x32-10 (Salmon et al., SC'11; O1). */
+void albref_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* u = ((a>>5)*2^26 + (b>>6)) * 2^-53, exact double in [0,1). */
+double albref_u53(uint32_t a, uint32_t b);
+/* draw j of (seed, image_index, slot): DESIGN.md O1 counter layout. */
+double albref_draw(uint64_t seed, uint64_t image_index, int32_t slot, int32_t j);
+
+/* round_half_up + clamp to [0,255]. */
+uint8_t albref_clip_round(double v);
+/* reflect-101 index (periodic extension R7). */
+int32_t albref_reflect101(int32_t i, int32_t n);
+
+/* hexcone colour model, double precision. */
+void albref_rgb_to_hsv(double r, double g, double b, double* h, double* s, double* v);
+void albref_hsv_to_rgb(double h, double s, double v, double* r, double* g, double* b);
+
+/* Per-image LUT of a LUT-type op, params as drawn (O8).  lut is
+ * [3][256] (channel-major).  Returns ALBREF_E_UNSUPPORTED for non-LUT kinds. */
+int albref_build_lut(int32_t kind, const double* params, uint8_t* lut);
+/* Equalize LUT for one channel (reading R15), hist[256] with N = sum. */
+int albref_equalize_lut(const int64_t* hist, uint8_t* lut);
+
+/* Output dims of the pipeline for an h x w input. */
+int albref_output_shape(const albref_op* ops, int32_t n_ops, int32_t in_h, int32_t in_w,
+                        int32_t* out_h, int32_t* out_w);
+
+/* Params of every slot for one image: params[n_ops][8], fired[n_ops].  The
+ * dims each slot sees are tracked through the pipeline (RandomCrop draws
+ * depend on the current image size). */
+int albref_sample_params(const albref_op* ops, int32_t n_ops, uint64_t seed,
+                         uint64_t image_index, int32_t in_h, int32_t in_w,
+                         double* params, uint8_t* fired);
+
+/* Apply the pipeline to one sample (SPEC.md:482-490 with DESIGN.md O14).
+ *   img [h][w][channels]; mask [h][w] or NULL; boxes [n_boxes][4] or NULL.
+ *   Outputs: img_out [oh][ow][channels] (ignored when the pipeline ends in
+ *   Normalize, then nchw_out [3][oh][ow] float32 is written); mask_out [oh][ow];
+ *   boxes_out/labels_out capacity n_boxes, *n_boxes_out = kept count.
+ *   The caller sizes outputs with albref_output_shape. */
+int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
+                 const uint8_t* img, int32_t h, int32_t w, int32_t channels,
+                 const uint8_t* mask,
+                 const float* boxes, const int32_t* labels, int32_t n_boxes,
+                 float min_visibility,
+                 uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
+                 float* boxes_out, int32_t* labels_out, int32_t* n_boxes_out);
+
+/* Synthetic-input generator recipe is NOT here (synth/ owns it). */
+
+#ifdef __cplusplus
+}
+#endif
+#endif
