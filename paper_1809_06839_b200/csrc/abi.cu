@@ -1,0 +1,876 @@
+// abi.cu -- the C ABI (include/alb_b200.h): pipeline validation, batch
+// layouts, the launch planner (fusion into rowgather / resample / affine /
+// pointwise / equalize steps) and the stream-ordered launch sequence.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "stages.cuh"
+
+using namespace alb;
+
+namespace {
+
+thread_local std::string g_err;
+
+alb_status fail(alb_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) return fail(ALB_E_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+bool is_shape_kind(int k) {
+  return k == ALB_RANDOM_CROP || k == ALB_PAD_TO_SIZE || k == ALB_RESIZE ||
+         k == ALB_RANDOM_SIZED_CROP || k == ALB_CROP;
+}
+bool is_exact_kind(int k) {
+  return k == ALB_HFLIP || k == ALB_VFLIP || k == ALB_CROP || k == ALB_RANDOM_CROP ||
+         k == ALB_PAD_TO_SIZE;
+}
+bool is_rgb_only(int k) {
+  return k == ALB_SHIFT_RGB || k == ALB_SHIFT_HSV || k == ALB_GRAYSCALE || k == ALB_NORMALIZE;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct alb_pipeline {
+  std::vector<alb_op> ops;
+};
+
+struct alb_layout {
+  std::vector<alb_image_desc> h;
+  alb_image_desc* d = nullptr;
+  int n = 0, channels = 3;
+  size_t span = 0;  // bytes from offset 0 to the end of the last image
+  ~alb_layout() {
+    if (d) cudaFree(d);
+  }
+};
+
+namespace {
+
+enum StepKind { SK_ROW = 0, SK_POINT = 1, SK_RESAMPLE = 2, SK_AFFINE = 3, SK_EQ = 4 };
+enum BufId { B_IN = 0, B_OUT = 1, B_WS0 = 2, B_WS1 = 3, B_NONE = 4 };
+
+struct PlanStep {
+  StepKind kind;
+  int slot0 = 0, slot1 = 0;
+  std::vector<Stage> stages;
+  bool normalize = false;
+  bool has_image = true;   // ROW step may be mask-only
+  bool has_mask = false;
+  int src = B_IN, dst = B_OUT, msrc = B_NONE, mdst = B_NONE;
+  const alb_layout* src_l = nullptr;
+  const alb_layout* dst_l = nullptr;
+  const alb_layout* msrc_l = nullptr;
+  const alb_layout* mdst_l = nullptr;
+  std::vector<int2> units, munits;
+  size_t units_off = 0, munits_off = 0;  // into the plan's device unit table
+  int unit_size = 0, munit_size = 0;
+  bool flat = false;
+  uint32_t fill = 0, mask_fill = 0;
+  int interp = 1, border = 0;
+  int eq_slot = -1;
+};
+
+constexpr int kChunk = 48 * 512;         // pointwise / histogram bytes per unit
+constexpr int kStageWords = 16 * 1024;   // resample/affine staging capacity (64 KB)
+
+}  // namespace
+
+struct alb_plan {
+  std::vector<alb_op> ops;
+  alb_op* d_ops = nullptr;
+  int n = 0;
+  const alb_layout* in = nullptr;
+  const alb_layout* out = nullptr;
+  const alb_layout* min = nullptr;
+  const alb_layout* mout = nullptr;
+  std::vector<std::unique_ptr<alb_layout>> inter;  // intermediate layouts
+  std::vector<PlanStep> steps;
+  int n_luts = 0;
+  int lut_k0[kMaxStages], lut_k1[kMaxStages];
+  int norm_slot = -1;
+  int out_h = 0, out_w = 0;  // NCHW dims
+  int max_boxes = 0;
+  float min_vis = 0.f;
+  bool has_eq = false;
+  // workspace layout
+  size_t off_params = 0, off_fired = 0, off_dims = 0, off_luts = 0, off_norm = 0,
+         off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, ws_bytes = 0;
+  int2* d_units = nullptr;
+  int n_launches = 0;
+  ~alb_plan() {
+    if (d_ops) cudaFree(d_ops);
+    if (d_units) cudaFree(d_units);
+  }
+};
+
+// ------------------------------------------------------------------ helpers
+
+static alb_status validate_ops(const alb_op* ops, int n_ops) {
+  if (n_ops < 0 || (n_ops > 0 && !ops)) return fail(ALB_E_INVALID_ARG, "null op list");
+  if (n_ops > ALB_MAX_OPS) return fail(ALB_E_UNSUPPORTED, "more than ALB_MAX_OPS ops");
+  for (int k = 0; k < n_ops; ++k) {
+    const alb_op& o = ops[k];
+    const std::string at = "op " + std::to_string(k) + ": ";
+    if (o.kind < 0 || o.kind >= ALB_NUM_KINDS) return fail(ALB_E_UNKNOWN_OP, at + "unknown kind");
+    if (!(o.p >= 0.0 && o.p <= 1.0)) return fail(ALB_E_RANGE, at + "p outside [0,1]");
+    for (int j = 0; j < 4; ++j)
+      if (!(o.lo[j] <= o.hi[j])) return fail(ALB_E_RANGE, at + "lo > hi");
+    if (is_shape_kind(o.kind) && o.p != 1.0)
+      return fail(ALB_E_RANGE, at + "shape-changing ops require p == 1 (R17)");
+    if (o.interp != ALB_INTERP_NEAREST && o.interp != ALB_INTERP_BILINEAR)
+      return fail(ALB_E_RANGE, at + "bad interp");
+    if (o.border != ALB_BORDER_CONSTANT && o.border != ALB_BORDER_REFLECT_101)
+      return fail(ALB_E_RANGE, at + "bad border");
+    switch (o.kind) {
+      case ALB_SHIFT_SCALE_ROTATE:
+        if (!(o.lo[2] > 0.0)) return fail(ALB_E_RANGE, at + "scale <= 0");
+        break;
+      case ALB_BRIGHTNESS: case ALB_CONTRAST:
+        if (!(o.lo[0] >= 0.0)) return fail(ALB_E_RANGE, at + "negative factor");
+        break;
+      case ALB_BRIGHTNESS_CONTRAST:
+        if (!(o.lo[0] >= 0.0) || !(o.lo[1] >= 0.0)) return fail(ALB_E_RANGE, at + "negative factor");
+        break;
+      case ALB_GAMMA:
+        if (!(o.lo[0] > 0.0)) return fail(ALB_E_RANGE, at + "gamma <= 0");
+        break;
+      case ALB_RANDOM_CROP: case ALB_CROP: case ALB_PAD_TO_SIZE: case ALB_RESIZE:
+        if (o.out_w < 1 || o.out_h < 1) return fail(ALB_E_RANGE, at + "output size < 1");
+        break;
+      case ALB_RANDOM_SIZED_CROP:
+        if (o.out_w < 1 || o.out_h < 1 || o.min_side < 1 || o.max_side < o.min_side)
+          return fail(ALB_E_RANGE, at + "bad RandomSizedCrop sides");
+        break;
+      case ALB_NORMALIZE:
+        if (k != n_ops - 1 || o.p != 1.0) return fail(ALB_E_RANGE, at + "Normalize must be last, p = 1");
+        for (int c = 0; c < 3; ++c)
+          if (!(o.std[c] != 0.0)) return fail(ALB_E_RANGE, at + "std == 0");
+        break;
+      default: break;
+    }
+  }
+  return ALB_OK;
+}
+
+// dims each slot sees for an h x w input; error if a window does not fit
+static alb_status track_dims(const std::vector<alb_op>& ops, int h, int w,
+                             std::vector<std::pair<int, int>>& dims) {
+  dims.clear();
+  for (size_t k = 0; k < ops.size(); ++k) {
+    dims.push_back({h, w});
+    const alb_op& o = ops[k];
+    switch (o.kind) {
+      case ALB_RANDOM_CROP:
+        if (o.out_w > w || o.out_h > h) return fail(ALB_E_INVALID_ARG, "RandomCrop larger than image");
+        h = o.out_h; w = o.out_w; break;
+      case ALB_CROP:
+        if (o.crop_x < 0 || o.crop_y < 0 || o.crop_x + o.out_w > w || o.crop_y + o.out_h > h)
+          return fail(ALB_E_INVALID_ARG, "Crop window outside the image");
+        h = o.out_h; w = o.out_w; break;
+      case ALB_PAD_TO_SIZE:
+        if (w > o.out_w || h > o.out_h) return fail(ALB_E_INVALID_ARG, "PadToSize target smaller than image");
+        h = o.out_h; w = o.out_w; break;
+      case ALB_RESIZE:
+        h = o.out_h; w = o.out_w; break;
+      case ALB_RANDOM_SIZED_CROP:
+        if (o.min_side > std::min(h, w)) return fail(ALB_E_INVALID_ARG, "RandomSizedCrop min side > image");
+        h = o.out_h; w = o.out_w; break;
+      default: break;
+    }
+  }
+  dims.push_back({h, w});
+  return ALB_OK;
+}
+
+static alb_status upload_layout(alb_layout* l) {
+  l->span = 0;
+  for (auto& d : l->h) l->span = std::max(l->span, (size_t)(d.offset + (int64_t)d.height * d.pitch));
+  if (l->d) { cudaFree(l->d); l->d = nullptr; }
+  if (l->n > 0) {
+    CUDA_TRY(cudaMalloc(&l->d, sizeof(alb_image_desc) * l->n));
+    CUDA_TRY(cudaMemcpy(l->d, l->h.data(), sizeof(alb_image_desc) * l->n, cudaMemcpyHostToDevice));
+  }
+  return ALB_OK;
+}
+
+// packed 256-aligned layout for intermediate images
+static alb_status make_packed(const std::vector<std::pair<int, int>>& hw, int channels,
+                              std::unique_ptr<alb_layout>& out) {
+  out.reset(new alb_layout);
+  out->n = (int)hw.size();
+  out->channels = channels;
+  int64_t off = 0;
+  for (auto& p : hw) {
+    alb_image_desc d{};
+    d.offset = off;
+    d.height = p.first;
+    d.width = p.second;
+    d.pitch = p.second * channels;
+    out->h.push_back(d);
+    off = (int64_t)align_up((size_t)(off + (int64_t)d.height * d.pitch), 256);
+  }
+  return upload_layout(out.get());
+}
+
+static void row_units(PlanStep& st, const alb_layout* dst, int channels, std::vector<int2>& u,
+                      int& usize) {
+  int wmax = 1;
+  for (auto& d : dst->h) wmax = std::max(wmax, d.width);
+  const int nbmax = 2 + wmax / 16;
+  usize = std::max(1, 1024 / nbmax);
+  (void)channels;
+  (void)st;
+  for (int i = 0; i < dst->n; ++i)
+    for (int y = 0; y < dst->h[i].height; y += usize) u.push_back(make_int2(i, y / usize));
+}
+
+// ----------------------------------------------------------------- the ABI
+
+extern "C" {
+
+const char* alb_last_error(void) { return g_err.c_str(); }
+int32_t alb_version(void) { return 1; }
+
+alb_status alb_pipeline_create(const alb_op* ops, int32_t n_ops, alb_pipeline** out) {
+  if (!out) return fail(ALB_E_INVALID_ARG, "null out");
+  alb_status s = validate_ops(ops, n_ops);
+  if (s) return s;
+  auto* p = new alb_pipeline;
+  p->ops.assign(ops, ops + n_ops);
+  *out = p;
+  return ALB_OK;
+}
+
+void alb_pipeline_destroy(alb_pipeline* p) { delete p; }
+
+alb_status alb_output_shape(const alb_pipeline* p, int32_t in_h, int32_t in_w, int32_t* out_h,
+                            int32_t* out_w) {
+  if (!p || !out_h || !out_w) return fail(ALB_E_INVALID_ARG, "null argument");
+  if (in_h < 1 || in_w < 1) return fail(ALB_E_SHAPE, "image dims < 1");
+  std::vector<std::pair<int, int>> dims;
+  alb_status s = track_dims(p->ops, in_h, in_w, dims);
+  if (s) return s;
+  *out_h = dims.back().first;
+  *out_w = dims.back().second;
+  return ALB_OK;
+}
+
+alb_status alb_layout_create(const alb_image_desc* desc, int32_t n, int32_t channels,
+                             alb_layout** out) {
+  if (!out || n < 0 || (n > 0 && !desc)) return fail(ALB_E_INVALID_ARG, "bad layout arguments");
+  if (channels != 1 && channels != 3) return fail(ALB_E_UNSUPPORTED, "channels must be 1 or 3");
+  for (int i = 0; i < n; ++i) {
+    if (desc[i].height < 1 || desc[i].width < 1) return fail(ALB_E_SHAPE, "image dims < 1");
+    if (desc[i].offset < 0 || desc[i].pitch < desc[i].width * channels)
+      return fail(ALB_E_ALIGN, "negative offset or pitch < width*channels");
+  }
+  std::unique_ptr<alb_layout> l(new alb_layout);
+  l->h.assign(desc, desc + n);
+  l->n = n;
+  l->channels = channels;
+  alb_status s = upload_layout(l.get());
+  if (s) return s;
+  *out = l.release();
+  return ALB_OK;
+}
+
+void alb_layout_destroy(alb_layout* l) { delete l; }
+
+alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const alb_layout* out,
+                           const alb_layout* mask_in, const alb_layout* mask_out,
+                           int32_t max_boxes, float min_visibility, alb_plan** plan_out) {
+  if (!p || !in || !plan_out) return fail(ALB_E_INVALID_ARG, "null argument");
+  if (in->channels != 3) return fail(ALB_E_UNSUPPORTED, "images must have 3 channels");
+  if ((mask_in == nullptr) != (mask_out == nullptr)) return fail(ALB_E_INVALID_ARG, "mask_in/mask_out must both be set");
+  if (max_boxes < 0) return fail(ALB_E_INVALID_ARG, "max_boxes < 0");
+  std::unique_ptr<alb_plan> P(new alb_plan);
+  P->ops = p->ops;
+  P->n = in->n;
+  P->in = in; P->out = out; P->min = mask_in; P->mout = mask_out;
+  P->max_boxes = max_boxes;
+  P->min_vis = min_visibility;
+  const int n_ops = (int)P->ops.size();
+  const bool ends_norm = n_ops > 0 && P->ops.back().kind == ALB_NORMALIZE;
+  if (ends_norm != (out == nullptr)) return fail(ALB_E_INVALID_ARG, "out must be NULL iff the pipeline ends in Normalize");
+  if (out && out->n != in->n) return fail(ALB_E_SHAPE, "in/out batch sizes differ");
+  if (out && out->channels != 3) return fail(ALB_E_SHAPE, "out must have 3 channels");
+  if (mask_in && (mask_in->n != in->n || mask_out->n != in->n || mask_in->channels != 1 || mask_out->channels != 1))
+    return fail(ALB_E_SHAPE, "mask layouts must be 1-channel with the same count");
+
+  // per-image dims through the pipeline
+  std::vector<std::vector<std::pair<int, int>>> dims(P->n);
+  for (int i = 0; i < P->n; ++i) {
+    alb_status s = track_dims(P->ops, in->h[i].height, in->h[i].width, dims[i]);
+    if (s) return s;
+    const auto& f = dims[i].back();
+    if (out && (out->h[i].height != f.first || out->h[i].width != f.second))
+      return fail(ALB_E_SHAPE, "output layout dims differ from the pipeline's output shape (image " + std::to_string(i) + ")");
+    if (ends_norm) {
+      if (i == 0) { P->out_h = f.first; P->out_w = f.second; }
+      else if (P->out_h != f.first || P->out_w != f.second)
+        return fail(ALB_E_SHAPE, "Normalize output needs one output size for the batch");
+    }
+    if (mask_in) {
+      if (mask_in->h[i].height != in->h[i].height || mask_in->h[i].width != in->h[i].width)
+        return fail(ALB_E_SHAPE, "mask dims differ from image dims (SPEC.md:47)");
+      if (mask_out->h[i].height != f.first || mask_out->h[i].width != f.second)
+        return fail(ALB_E_SHAPE, "mask output dims differ from the output shape");
+    }
+  }
+  // identity resizes (input dims == output dims for every image) are no-ops
+  std::vector<bool> ident(n_ops, false);
+  for (int k = 0; k < n_ops; ++k) {
+    if (P->ops[k].kind != ALB_RESIZE) continue;
+    bool all = true;
+    for (int i = 0; i < P->n && all; ++i) all = dims[i][k] == dims[i][k + 1];
+    ident[k] = all;
+  }
+
+  // ---------------------------------------------------------- group ops
+  std::vector<PlanStep>& steps = P->steps;
+  int k = 0;
+  bool geo_open = false;  // last step is resample/affine still accepting post exact ops
+  bool point_open = false;
+  while (k < n_ops) {
+    const alb_op& o = P->ops[k];
+    const int kind = o.kind;
+    if (kind == ALB_NORMALIZE) {
+      if (!steps.empty() && (steps.back().kind == SK_POINT || steps.back().kind == SK_RESAMPLE ||
+                             steps.back().kind == SK_AFFINE) && (point_open || geo_open)) {
+        steps.back().normalize = true;
+      } else {
+        PlanStep st; st.kind = SK_POINT; st.slot0 = k; st.slot1 = k; st.normalize = true;
+        steps.push_back(st);
+      }
+      P->norm_slot = k;
+      ++k;
+      geo_open = point_open = false;
+      continue;
+    }
+    if (is_exact_kind(kind) || (kind == ALB_RESIZE && ident[k])) {
+      if (geo_open && kind != ALB_PAD_TO_SIZE) {  // fuse as a post op (commutes with stages)
+        steps.back().slot1 = k + 1;
+        ++k;
+        continue;
+      }
+      PlanStep st; st.kind = SK_ROW; st.slot0 = k;
+      int pads = 0;
+      int j = k;
+      while (j < n_ops && (is_exact_kind(P->ops[j].kind) || (P->ops[j].kind == ALB_RESIZE && ident[j]))) {
+        if (P->ops[j].kind == ALB_PAD_TO_SIZE) {
+          if (pads == 1) break;
+          ++pads;
+          st.fill = P->ops[j].fill[0] | (P->ops[j].fill[1] << 8) | (P->ops[j].fill[2] << 16);
+          st.mask_fill = P->ops[j].mask_fill;
+        }
+        ++j;
+      }
+      st.slot1 = j;
+      steps.push_back(st);
+      k = j;
+      geo_open = point_open = false;
+      continue;
+    }
+    if (kind == ALB_RESIZE || kind == ALB_RANDOM_SIZED_CROP || kind == ALB_ROTATE ||
+        kind == ALB_SHIFT_SCALE_ROTATE) {
+      PlanStep st;
+      st.kind = (kind == ALB_ROTATE || kind == ALB_SHIFT_SCALE_ROTATE) ? SK_AFFINE : SK_RESAMPLE;
+      st.slot0 = k; st.slot1 = k + 1;
+      st.interp = o.interp; st.border = o.border;
+      st.fill = o.fill[0] | (o.fill[1] << 8) | (o.fill[2] << 16);
+      st.mask_fill = o.mask_fill;
+      steps.push_back(st);
+      ++k;
+      geo_open = true;
+      point_open = false;
+      continue;
+    }
+    if (is_lut_kind(kind) || kind == ALB_SHIFT_HSV || kind == ALB_GRAYSCALE) {
+      if (!(geo_open || point_open)) {
+        PlanStep st; st.kind = SK_POINT; st.slot0 = k; st.slot1 = k;
+        steps.push_back(st);
+        point_open = true;
+      }
+      PlanStep& b = steps.back();
+      if (b.stages.size() >= (size_t)kMaxStages) return fail(ALB_E_UNSUPPORTED, "too many pointwise stages");
+      Stage sg{};
+      sg.slot = k;
+      if (is_lut_kind(kind)) {
+        int j = k;
+        while (j < n_ops && is_lut_kind(P->ops[j].kind)) ++j;
+        if (P->n_luts >= kMaxStages) return fail(ALB_E_UNSUPPORTED, "too many LUT stages");
+        sg.type = ST_LUT;
+        sg.lut = P->n_luts;
+        P->lut_k0[P->n_luts] = k;
+        P->lut_k1[P->n_luts] = j;
+        P->n_luts++;
+        b.stages.push_back(sg);
+        k = j;
+      } else {
+        sg.type = kind == ALB_SHIFT_HSV ? ST_HSV : ST_GRAY;
+        b.stages.push_back(sg);
+        ++k;
+      }
+      continue;
+    }
+    if (kind == ALB_EQUALIZE) {
+      if (P->has_eq) return fail(ALB_E_UNSUPPORTED, "at most one Equalize per pipeline");
+      PlanStep st; st.kind = SK_EQ; st.slot0 = k; st.slot1 = k + 1; st.eq_slot = k;
+      steps.push_back(st);
+      PlanStep ap; ap.kind = SK_POINT; ap.slot0 = k; ap.slot1 = k + 1;
+      Stage sg{}; sg.type = ST_EQ; sg.slot = k;
+      ap.stages.push_back(sg);
+      steps.push_back(ap);
+      P->has_eq = true;
+      point_open = true;
+      geo_open = false;
+      ++k;
+      continue;
+    }
+    return fail(ALB_E_UNKNOWN_OP, "unhandled op kind");
+  }
+  // LUT count per step must fit shared memory (<= 4 stages of 24 KB)
+  for (auto& st : steps) {
+    int nl = 0;
+    for (auto& sg : st.stages) nl += (sg.type == ST_LUT || sg.type == ST_EQ);
+    if (nl > 4) return fail(ALB_E_UNSUPPORTED, "more than 4 LUT stages in one fused step");
+  }
+  // rgb-only ops need 3 channels: images are always 3-channel here.
+  const bool has_geo = std::any_of(steps.begin(), steps.end(), [](const PlanStep& s) {
+    return s.kind == SK_ROW || s.kind == SK_RESAMPLE || s.kind == SK_AFFINE;
+  });
+  // masks ride on geometric steps; without one, an identity mask copy
+  if (mask_in && !has_geo) {
+    PlanStep st; st.kind = SK_ROW; st.slot0 = 0; st.slot1 = 0; st.has_image = false;
+    steps.push_back(st);
+  }
+  if (steps.empty()) {  // empty / all-identity pipeline: copy
+    PlanStep st; st.kind = SK_ROW; st.slot0 = 0; st.slot1 = 0;
+    steps.push_back(st);
+  }
+  // ----------------------------------------------------- buffers + layouts
+  // output dims of each step per image
+  const int ns = (int)steps.size();
+  int last_img = -1, last_mask = -1;
+  for (int s = 0; s < ns; ++s) {
+    if (steps[s].has_image && steps[s].kind != SK_EQ) last_img = s;
+    if (mask_in && steps[s].kind != SK_POINT && steps[s].kind != SK_EQ) last_mask = s;
+  }
+  int cur = B_IN, mcur = mask_in ? B_IN : B_NONE;
+  const alb_layout* cur_l = in;
+  const alb_layout* mcur_l = mask_in;
+  int ping = 0, mping = 0;
+  size_t max_inter = 0, max_minter = 0;
+  for (int s = 0; s < ns; ++s) {
+    PlanStep& st = steps[s];
+    // image
+    if (st.kind == SK_EQ) {
+      st.src = cur; st.src_l = cur_l; st.dst = B_NONE;
+    } else if (st.has_image) {
+      st.src = cur; st.src_l = cur_l;
+      if (s == last_img) {
+        st.dst = ends_norm ? B_NONE : B_OUT;
+        st.dst_l = out;
+      } else {
+        std::vector<std::pair<int, int>> hw(P->n);
+        const int kk = st.kind == SK_POINT ? st.slot0 : st.slot1;
+        for (int i = 0; i < P->n; ++i) hw[i] = st.kind == SK_POINT ? std::make_pair(cur_l->h[i].height, cur_l->h[i].width) : dims[i][kk];
+        std::unique_ptr<alb_layout> L;
+        alb_status e = make_packed(hw, 3, L);
+        if (e) return e;
+        max_inter = std::max(max_inter, L->span);
+        st.dst = B_WS0 + ping; ping ^= 1;
+        st.dst_l = L.get();
+        P->inter.push_back(std::move(L));
+      }
+      cur = st.dst; cur_l = st.dst_l;
+    }
+    // mask
+    if (mask_in && st.kind != SK_POINT && st.kind != SK_EQ) {
+      st.has_mask = true;
+      st.msrc = mcur; st.msrc_l = mcur_l;
+      if (s == last_mask) {
+        st.mdst = B_OUT; st.mdst_l = mask_out;
+      } else {
+        std::vector<std::pair<int, int>> hw(P->n);
+        for (int i = 0; i < P->n; ++i) hw[i] = st.has_image ? dims[i][st.slot1] : dims[i][0];
+        std::unique_ptr<alb_layout> L;
+        alb_status e = make_packed(hw, 1, L);
+        if (e) return e;
+        max_minter = std::max(max_minter, L->span);
+        st.mdst = B_WS0 + mping; mping ^= 1;
+        st.mdst_l = L.get();
+        P->inter.push_back(std::move(L));
+      }
+      mcur = st.mdst; mcur_l = st.mdst_l;
+    }
+  }
+  // ----------------------------------------------------------- work units
+  size_t total_units = 0;
+  for (auto& st : steps) {
+    switch (st.kind) {
+      case SK_ROW:
+        if (st.has_image) row_units(st, st.dst_l, 3, st.units, st.unit_size);
+        if (st.has_mask) row_units(st, st.mdst_l, 1, st.munits, st.munit_size);
+        break;
+      case SK_POINT:
+      case SK_EQ: {
+        const alb_layout* sl = st.src_l;
+        bool flat = true;
+        for (int i = 0; i < P->n; ++i) {
+          flat = flat && sl->h[i].pitch == sl->h[i].width * 3 && sl->h[i].offset % 16 == 0;
+          if (st.kind == SK_POINT && st.dst_l)
+            flat = flat && st.dst_l->h[i].pitch == st.dst_l->h[i].width * 3 && st.dst_l->h[i].offset % 16 == 0;
+        }
+        st.flat = flat;
+        st.unit_size = kChunk;
+        for (int i = 0; i < P->n; ++i) {
+          if (flat) {
+            const int len = sl->h[i].height * sl->h[i].width * 3;
+            for (int c = 0; c * kChunk < len; ++c) st.units.push_back(make_int2(i, c));
+          } else {
+            for (int y = 0; y < sl->h[i].height; ++y) st.units.push_back(make_int2(i, y));
+          }
+        }
+        break;
+      }
+      case SK_RESAMPLE:
+      case SK_AFFINE: {
+        st.unit_size = kStageWords;
+        for (int i = 0; i < P->n; ++i) {
+          const int H = dims[i][st.slot1].first;
+          for (int y = 0, b = 0; y < H; y += 16, ++b) st.units.push_back(make_int2(i, b));
+        }
+        if (st.kind == SK_RESAMPLE) {
+          for (int i = 0; i < P->n; ++i)
+            if (dims[i][st.slot1].second > 2048) return fail(ALB_E_UNSUPPORTED, "resize output wider than 2048");
+        }
+        break;
+      }
+    }
+    total_units += st.units.size() + st.munits.size();
+  }
+  if (total_units) {
+    std::vector<int2> all;
+    all.reserve(total_units);
+    for (auto& st : steps) {
+      st.units_off = all.size();
+      all.insert(all.end(), st.units.begin(), st.units.end());
+      st.munits_off = all.size();
+      all.insert(all.end(), st.munits.begin(), st.munits.end());
+    }
+    CUDA_TRY(cudaMalloc(&P->d_units, sizeof(int2) * all.size()));
+    CUDA_TRY(cudaMemcpy(P->d_units, all.data(), sizeof(int2) * all.size(), cudaMemcpyHostToDevice));
+  }
+  if (n_ops > 0) {
+    CUDA_TRY(cudaMalloc(&P->d_ops, sizeof(alb_op) * n_ops));
+    CUDA_TRY(cudaMemcpy(P->d_ops, P->ops.data(), sizeof(alb_op) * n_ops, cudaMemcpyHostToDevice));
+  }
+  // ------------------------------------------------------------ workspace
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+  const size_t nn = (size_t)std::max(P->n, 1);
+  const size_t nops = (size_t)std::max(n_ops, 1);
+  P->off_params = take(nn * nops * kMaxParams * sizeof(double));
+  P->off_fired = take(nn * nops);
+  P->off_dims = take(nn * (n_ops + 1) * 2 * sizeof(int32_t));
+  P->off_luts = take(nn * std::max(P->n_luts, 1) * 768);
+  P->off_norm = take(768 * sizeof(float));
+  P->off_eqh = take(P->has_eq ? nn * 768 * sizeof(uint32_t) : 0);
+  P->off_eql = take(P->has_eq ? nn * 768 : 0);
+  P->off_buf[0] = take(max_inter + 64);
+  P->off_buf[1] = take(max_inter + 64);
+  P->off_mbuf[0] = take(max_minter + 64);
+  P->off_mbuf[1] = take(max_minter + 64);
+  P->ws_bytes = off;
+  // launches per apply
+  int L = 1;  // prep
+  for (auto& st : steps) {
+    if (st.kind == SK_ROW) L += (st.has_image ? 1 : 0) + (st.has_mask ? 1 : 0);
+    else if (st.kind == SK_EQ) L += 2;
+    else L += 1;
+  }
+  if (max_boxes > 0) L += 1;
+  P->n_launches = L;
+  *plan_out = P.release();
+  return ALB_OK;
+}
+
+void alb_plan_destroy(alb_plan* plan) { delete plan; }
+
+alb_status alb_plan_workspace_size(const alb_plan* plan, size_t* bytes) {
+  if (!plan || !bytes) return fail(ALB_E_INVALID_ARG, "null argument");
+  *bytes = plan->ws_bytes;
+  return ALB_OK;
+}
+
+int32_t alb_plan_num_launches(const alb_plan* plan) { return plan ? plan->n_launches : 0; }
+
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return na && nb && x < y + nb && y < x + na;
+}
+
+alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_index,
+                     const uint8_t* img_in, uint8_t* img_out, float* out_nchw,
+                     const uint8_t* mask_in, uint8_t* mask_out,
+                     const float* boxes_in, const int32_t* labels_in, const int32_t* count_in,
+                     float* boxes_out, int32_t* labels_out, int32_t* count_out,
+                     void* workspace, size_t workspace_bytes, void* stream_) {
+  if (!P) return fail(ALB_E_INVALID_ARG, "null plan");
+  if (P->n == 0) return ALB_OK;
+  if (!img_in) return fail(ALB_E_INVALID_ARG, "null img_in");
+  const bool ends_norm = P->norm_slot >= 0;
+  if (ends_norm ? !out_nchw : !img_out) return fail(ALB_E_INVALID_ARG, "null output");
+  if (P->min && (!mask_in || !mask_out)) return fail(ALB_E_INVALID_ARG, "plan has masks: mask pointers required");
+  if (P->max_boxes > 0 && (!boxes_in || !count_in || !boxes_out || !count_out))
+    return fail(ALB_E_INVALID_ARG, "plan has boxes: box pointers required");
+  if (!workspace || workspace_bytes < P->ws_bytes) return fail(ALB_E_WORKSPACE, "workspace too small");
+  if (((uintptr_t)workspace & 255) != 0) return fail(ALB_E_WORKSPACE, "workspace must be 256-byte aligned");
+  if (first_image_index + (uint64_t)P->n > (1ull << 32)) return fail(ALB_E_INVALID_ARG, "image index >= 2^32");
+  if (!ends_norm && overlap(img_in, P->in->span, img_out, P->out->span))
+    return fail(ALB_E_INVALID_ARG, "img_in and img_out overlap");
+  if (ends_norm && overlap(img_in, P->in->span, out_nchw, (size_t)P->n * 3 * P->out_h * P->out_w * 4))
+    return fail(ALB_E_INVALID_ARG, "img_in and out_nchw overlap");
+  if (P->min && overlap(mask_in, P->min->span, mask_out, P->mout->span))
+    return fail(ALB_E_INVALID_ARG, "mask_in and mask_out overlap");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  uint8_t* ws = (uint8_t*)workspace;
+  const int n_ops = (int)P->ops.size();
+
+  Tables tab{};
+  tab.params = (const double*)(ws + P->off_params);
+  tab.fired = ws + P->off_fired;
+  tab.dims = (const int32_t*)(ws + P->off_dims);
+  tab.luts = ws + P->off_luts;
+  tab.norm_lut = (const float*)(ws + P->off_norm);
+  tab.eq_luts = ws + P->off_eql;
+  tab.n_ops = n_ops;
+  tab.n_luts = P->n_luts;
+
+  PrepArgs pa{};
+  pa.ops = P->d_ops;
+  pa.n_ops = n_ops;
+  pa.n = P->n;
+  pa.seed = seed;
+  pa.first_image = (uint32_t)first_image_index;
+  pa.in_desc = P->in->d;
+  pa.params = (double*)(ws + P->off_params);
+  pa.fired = ws + P->off_fired;
+  pa.dims = (int32_t*)(ws + P->off_dims);
+  pa.luts = ws + P->off_luts;
+  pa.n_luts = P->n_luts;
+  for (int s = 0; s < P->n_luts; ++s) { pa.lut_k0[s] = P->lut_k0[s]; pa.lut_k1[s] = P->lut_k1[s]; }
+  pa.norm_lut = (float*)(ws + P->off_norm);
+  pa.norm_slot = P->norm_slot;
+  launch_prep(pa, stream);
+
+  auto img_buf = [&](int id) -> uint8_t* {
+    switch (id) {
+      case B_IN: return const_cast<uint8_t*>(img_in);
+      case B_OUT: return img_out;
+      case B_WS0: return ws + P->off_buf[0];
+      case B_WS1: return ws + P->off_buf[1];
+      default: return nullptr;
+    }
+  };
+  auto mask_buf = [&](int id) -> uint8_t* {
+    switch (id) {
+      case B_IN: return const_cast<uint8_t*>(mask_in);
+      case B_OUT: return mask_out;
+      case B_WS0: return ws + P->off_mbuf[0];
+      case B_WS1: return ws + P->off_mbuf[1];
+      default: return nullptr;
+    }
+  };
+
+  for (const PlanStep& st : P->steps) {
+    StepArgs a{};
+    a.src = img_buf(st.src);
+    a.sdesc = st.src_l ? st.src_l->d : nullptr;
+    a.dst = img_buf(st.dst);
+    a.ddesc = st.dst_l ? st.dst_l->d : nullptr;
+    a.nchw = st.normalize ? out_nchw : nullptr;
+    a.out_h = P->out_h;
+    a.out_w = P->out_w;
+    a.msrc = st.has_mask ? mask_buf(st.msrc) : nullptr;
+    a.msdesc = st.has_mask ? st.msrc_l->d : nullptr;
+    a.mdst = st.has_mask ? mask_buf(st.mdst) : nullptr;
+    a.mddesc = st.has_mask ? st.mdst_l->d : nullptr;
+    a.units = P->d_units + st.units_off;
+    a.n_units = (int)st.units.size();
+    a.unit_size = st.unit_size;
+    a.slot0 = st.slot0;
+    a.slot1 = st.slot1;
+    a.n_stages = (int)st.stages.size();
+    for (int s = 0; s < a.n_stages; ++s) a.stages[s] = st.stages[s];
+    a.normalize = st.normalize ? 1 : 0;
+    a.flat = st.flat ? 1 : 0;
+    a.fill = st.fill;
+    a.mask_fill = st.mask_fill;
+    a.interp = st.interp;
+    a.border = st.border;
+    a.tab = tab;
+    a.ops = P->d_ops;
+    switch (st.kind) {
+      case SK_ROW:
+        if (st.has_image) {
+          a.channels = 3;
+          launch_rowgather(a, stream);
+        }
+        if (st.has_mask) {
+          a.channels = 1;
+          a.units = P->d_units + st.munits_off;
+          a.n_units = (int)st.munits.size();
+          a.unit_size = st.munit_size;
+          launch_rowgather(a, stream);
+        }
+        break;
+      case SK_POINT: {
+        // 16-byte co-alignment of source and destination segments
+        bool vec = true;
+        if (a.dst) {
+          for (int i = 0; i < P->n && vec; ++i) {
+            const uintptr_t s = (uintptr_t)a.src + st.src_l->h[i].offset;
+            const uintptr_t d = (uintptr_t)a.dst + st.dst_l->h[i].offset;
+            vec = ((s ^ d) & 15) == 0 && (st.flat || ((st.src_l->h[i].pitch - st.dst_l->h[i].pitch) % 16) == 0);
+          }
+        }
+        a.vec_ok = vec ? 1 : 0;
+        launch_point(a, stream);
+        break;
+      }
+      case SK_RESAMPLE: launch_resample(a, stream); break;
+      case SK_AFFINE: launch_affine(a, stream); break;
+      case SK_EQ: {
+        EqArgs e{};
+        e.src = a.src;
+        e.sdesc = a.sdesc;
+        e.hist = (uint32_t*)(ws + P->off_eqh);
+        e.lut = ws + P->off_eql;
+        e.units = a.units;
+        e.n_units = a.n_units;
+        e.unit_size = st.flat ? st.unit_size : 0;
+        e.n = P->n;
+        e.slot = st.eq_slot;
+        e.tab = tab;
+        CUDA_TRY(cudaMemsetAsync(e.hist, 0, (size_t)P->n * 768 * sizeof(uint32_t), stream));
+        launch_eq_hist(e, stream);
+        launch_eq_lut(e, stream);
+        break;
+      }
+    }
+  }
+  if (P->max_boxes > 0) {
+    BoxArgs b{};
+    b.boxes_in = boxes_in;
+    b.labels_in = labels_in;
+    b.count_in = count_in;
+    b.boxes_out = boxes_out;
+    b.labels_out = labels_out;
+    b.count_out = count_out;
+    b.max_boxes = P->max_boxes;
+    b.min_visibility = P->min_vis;
+    b.n = P->n;
+    b.tab = tab;
+    b.ops = P->d_ops;
+    launch_boxes(b, stream);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ALB_E_CUDA, std::string("launch failed: ") + cudaGetErrorString(e));
+  return ALB_OK;
+}
+
+alb_status alb_apply_host(const alb_plan* P, uint64_t seed, uint64_t first_image_index,
+                          const uint8_t* host_in, size_t in_bytes, uint8_t* dev_in,
+                          void* host_out, size_t out_bytes, void* dev_out, void* workspace,
+                          size_t workspace_bytes, void* stream_) {
+  if (!P || !host_in || !dev_in || !host_out || !dev_out) return fail(ALB_E_INVALID_ARG, "null argument");
+  if (P->min || P->max_boxes > 0) return fail(ALB_E_UNSUPPORTED, "alb_apply_host carries images only");
+  if (in_bytes < P->in->span) return fail(ALB_E_INVALID_ARG, "in_bytes smaller than the input layout");
+  const bool ends_norm = P->norm_slot >= 0;
+  const size_t need = ends_norm ? (size_t)P->n * 3 * P->out_h * P->out_w * 4 : P->out->span;
+  if (out_bytes < need) return fail(ALB_E_INVALID_ARG, "out_bytes smaller than the output");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CUDA_TRY(cudaMemcpyAsync(dev_in, host_in, in_bytes, cudaMemcpyHostToDevice, stream));
+  alb_status s = alb_apply(P, seed, first_image_index, dev_in, ends_norm ? nullptr : (uint8_t*)dev_out,
+                           ends_norm ? (float*)dev_out : nullptr, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, nullptr, nullptr, nullptr, workspace, workspace_bytes, stream_);
+  if (s) return s;
+  CUDA_TRY(cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, stream));
+  return ALB_OK;
+}
+
+alb_status alb_sample_params(const alb_pipeline* p, uint64_t seed, uint64_t first_image_index,
+                             const int32_t* in_hw, int32_t n, double* params_out,
+                             uint8_t* fired_out) {
+  if (!p || n < 0 || (n > 0 && (!in_hw || !params_out || !fired_out)))
+    return fail(ALB_E_INVALID_ARG, "null argument");
+  if (n == 0) return ALB_OK;
+  const int n_ops = (int)p->ops.size();
+  std::vector<alb_image_desc> desc(n);
+  for (int i = 0; i < n; ++i) {
+    std::vector<std::pair<int, int>> dims;
+    if (in_hw[2 * i] < 1 || in_hw[2 * i + 1] < 1) return fail(ALB_E_SHAPE, "image dims < 1");
+    alb_status s = track_dims(p->ops, in_hw[2 * i], in_hw[2 * i + 1], dims);
+    if (s) return s;
+    desc[i] = alb_image_desc{0, in_hw[2 * i], in_hw[2 * i + 1], in_hw[2 * i + 1] * 3, 0};
+  }
+  if (n_ops == 0) return ALB_OK;
+  alb_op* d_ops = nullptr;
+  alb_image_desc* d_desc = nullptr;
+  uint8_t* d_tab = nullptr;
+  const size_t pb = (size_t)n * n_ops * kMaxParams * sizeof(double);
+  const size_t fb = (size_t)n * n_ops;
+  const size_t db = (size_t)n * (n_ops + 1) * 2 * sizeof(int32_t);
+  alb_status st = ALB_OK;
+  cudaError_t e = cudaSuccess;
+  do {
+    if ((e = cudaMalloc(&d_ops, sizeof(alb_op) * n_ops))) break;
+    if ((e = cudaMalloc(&d_desc, sizeof(alb_image_desc) * n))) break;
+    if ((e = cudaMalloc(&d_tab, pb + fb + db + 1024))) break;
+    if ((e = cudaMemcpy(d_ops, p->ops.data(), sizeof(alb_op) * n_ops, cudaMemcpyHostToDevice))) break;
+    if ((e = cudaMemcpy(d_desc, desc.data(), sizeof(alb_image_desc) * n, cudaMemcpyHostToDevice))) break;
+    PrepArgs pa{};
+    pa.ops = d_ops;
+    pa.n_ops = n_ops;
+    pa.n = n;
+    pa.seed = seed;
+    pa.first_image = (uint32_t)first_image_index;
+    pa.in_desc = d_desc;
+    pa.params = (double*)d_tab;
+    pa.fired = d_tab + pb;
+    pa.dims = (int32_t*)(d_tab + align_up(pb + fb, 256));
+    pa.n_luts = 0;
+    pa.norm_slot = -1;
+    launch_prep(pa, 0);
+    if ((e = cudaGetLastError())) break;
+    if ((e = cudaMemcpy(params_out, d_tab, pb, cudaMemcpyDeviceToHost))) break;
+    if ((e = cudaMemcpy(fired_out, d_tab + pb, fb, cudaMemcpyDeviceToHost))) break;
+  } while (0);
+  if (e != cudaSuccess) st = fail(ALB_E_CUDA, std::string("alb_sample_params: ") + cudaGetErrorString(e));
+  cudaFree(d_ops);
+  cudaFree(d_desc);
+  cudaFree(d_tab);
+  return st;
+}
+
+}  // extern "C"

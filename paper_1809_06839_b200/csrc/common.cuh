@@ -1,0 +1,215 @@
+// common.cuh -- device helpers shared by the sm_100a kernels of the hot path.
+// (No code is shared with oracle/; the formulas are re-derived from DESIGN.md.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/alb_b200.h"
+
+namespace alb {
+
+constexpr int kMaxOps = ALB_MAX_OPS;
+constexpr int kMaxParams = ALB_MAX_PARAMS;
+constexpr int kMaxStages = 8;
+
+// ---------------------------------------------------------------- O1 Philox
+// Philox4x32-10 (Salmon et al. SC'11).  Counter (image, slot, block, tag=0),
+// key (seed lo, seed hi); draw j uses block j>>1, words 2(j&1), 2(j&1)+1.
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+__host__ __device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = mulhi32(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = mulhi32(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+// exact 53-bit double in [0,1): ((a>>5)*2^26 + (b>>6)) * 2^-53
+__device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
+  return __dmul_rn(__dadd_rn(__dmul_rn((double)(a >> 5), 67108864.0), (double)(b >> 6)),
+                   1.0 / 9007199254740992.0);
+}
+
+__device__ __forceinline__ double draw_u(uint64_t seed, uint32_t img, int slot, int j) {
+  const uint4 o = philox10(make_uint4(img, (uint32_t)slot, (uint32_t)(j >> 1), 0u),
+                           make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  return (j & 1) ? u53(o.z, o.w) : u53(o.x, o.y);
+}
+
+// lo + (hi - lo) * u, no contraction
+__device__ __forceinline__ double urange(double lo, double hi, double u) {
+  return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u));
+}
+
+// floor(u * n), clamped to n - 1
+__device__ __forceinline__ int uint_draw(double u, int n) {
+  int k = (int)floor(__dmul_rn(u, (double)n));
+  return k > n - 1 ? n - 1 : k;
+}
+
+// round half up + clamp to [0,255], in double
+__device__ __forceinline__ int clip_round_d(double v) {
+  double r = floor(__dadd_rn(v, 0.5));
+  r = r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r);
+  return (int)r;
+}
+
+__host__ __device__ __forceinline__ int reflect101(int i, int n) {
+  if (n == 1) return 0;
+  const int period = 2 * n - 2;
+  int k = i < 0 ? -i : i;
+  k = k % period;
+  return k >= n ? period - k : k;
+}
+
+__host__ __device__ __forceinline__ bool is_lut_kind(int k) {
+  return k == ALB_BRIGHTNESS || k == ALB_CONTRAST || k == ALB_BRIGHTNESS_CONTRAST ||
+         k == ALB_GAMMA || k == ALB_SHIFT_RGB;
+}
+
+// ------------------------------------------------------- pointwise stages
+enum StageType : int32_t { ST_LUT = 0, ST_HSV = 1, ST_GRAY = 2, ST_EQ = 3 };
+
+struct Stage {
+  int32_t type;
+  int32_t slot;   // op slot (HSV/GRAY: gate + params)
+  int32_t lut;    // LUT table index (ST_LUT)
+  int32_t pad;
+};
+
+// per-apply tables in the workspace
+struct Tables {
+  const double* params;   // [n][n_ops][8]
+  const uint8_t* fired;   // [n][n_ops]
+  const int32_t* dims;    // [n][n_ops+1][2] (h, w) each slot sees
+  const uint8_t* luts;    // [n][n_luts][768]
+  const float* norm_lut;  // [3][256]
+  const uint8_t* eq_luts; // [n][768] (Equalize, R15)
+  int32_t n_ops;
+  int32_t n_luts;
+};
+
+__device__ __forceinline__ const double* prm_of(const Tables& t, int img, int slot) {
+  return t.params + ((size_t)img * t.n_ops + slot) * kMaxParams;
+}
+__device__ __forceinline__ bool fired_of(const Tables& t, int img, int slot) {
+  return t.fired[(size_t)img * t.n_ops + slot] != 0;
+}
+
+// ---------------------------------------------------------------- HSV (fp32)
+// hexcone RGB->HSV, shift (h mod 360, s/v clamped), HSV->RGB, round half up.
+__device__ __forceinline__ void hsv_shift_px(float dh, float ds, float dv, uint32_t& r,
+                                             uint32_t& g, uint32_t& b) {
+  const float fr = (float)r, fg = (float)g, fb = (float)b;
+  const float mx = fmaxf(fr, fmaxf(fg, fb));
+  const float mn = fminf(fr, fminf(fg, fb));
+  const float d = mx - mn;
+  float h;
+  if (d == 0.f) {
+    h = 0.f;
+  } else {
+    const float inv = __frcp_rn(d);
+    if (mx == fr) {
+      h = (fg - fb) * inv;
+      if (h < 0.f) h += 6.f;
+    } else if (mx == fg) {
+      h = (fb - fr) * inv + 2.f;
+    } else {
+      h = (fr - fg) * inv + 4.f;
+    }
+    h *= 60.f;
+  }
+  float s = mx > 0.f ? d / mx : 0.f;
+  float v = mx * (1.f / 255.f);
+  h = h + dh;
+  h = h - 360.f * floorf(h * (1.f / 360.f));
+  if (h >= 360.f) h -= 360.f;
+  if (h < 0.f) h = 0.f;
+  s = fminf(fmaxf(s + ds, 0.f), 1.f);
+  v = fminf(fmaxf(v + dv, 0.f), 1.f);
+  const float C = v * s;
+  const float hp = h * (1.f / 60.f);
+  const float m2 = hp - 2.f * floorf(hp * 0.5f);
+  const float X = C * (1.f - fabsf(m2 - 1.f));
+  const float m = v - C;
+  int sec = (int)floorf(hp);
+  sec = sec >= 6 ? sec - 6 : sec;
+  float r1, g1, b1;
+  switch (sec) {
+    case 0: r1 = C; g1 = X; b1 = 0.f; break;
+    case 1: r1 = X; g1 = C; b1 = 0.f; break;
+    case 2: r1 = 0.f; g1 = C; b1 = X; break;
+    case 3: r1 = 0.f; g1 = X; b1 = C; break;
+    case 4: r1 = X; g1 = 0.f; b1 = C; break;
+    default: r1 = C; g1 = 0.f; b1 = X; break;
+  }
+  r = (uint32_t)min(255, max(0, (int)floorf(255.f * (r1 + m) + 0.5f)));
+  g = (uint32_t)min(255, max(0, (int)floorf(255.f * (g1 + m) + 0.5f)));
+  b = (uint32_t)min(255, max(0, (int)floorf(255.f * (b1 + m) + 0.5f)));
+}
+
+// exact BT.601 luma (299R + 587G + 114B + 500) / 1000
+__device__ __forceinline__ uint32_t gray_px(uint32_t r, uint32_t g, uint32_t b) {
+  return (299u * r + 587u * g + 114u * b + 500u) / 1000u;
+}
+
+// ------------------------------------------------------------- byte windows
+// Load NW words = bytes [p, p + 4*NW) at arbitrary alignment using 16-byte
+// aligned vector loads; only vectors intersecting [lo, hi) are read (the rest
+// stay zero), so reads never leave the 16-byte blocks of valid data.
+template <int NW>
+__device__ __forceinline__ void load_window(const uint8_t* __restrict__ p, const uint8_t* lo,
+                                            const uint8_t* hi, uint32_t (&w)[NW]) {
+  constexpr int NV = (NW + 4 + 3) / 4;
+  const uintptr_t a = (uintptr_t)p;
+  const uint8_t* base = (const uint8_t*)(a & ~(uintptr_t)15);
+  const int sh = (int)(a & 15);
+  uint32_t r[NV * 4];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const uint8_t* q = base + 16 * v;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (q < hi && q + 16 > lo) x = __ldg(reinterpret_cast<const uint4*>(q));
+    r[4 * v + 0] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
+  }
+  const int qw = sh >> 2, kb = (sh & 3) * 8;
+  uint32_t t1[NV * 4 - 1];
+#pragma unroll
+  for (int i = 0; i < NV * 4 - 1; ++i) t1[i] = (qw & 1) ? r[i + 1] : r[i];
+  uint32_t t2[NW + 1];
+#pragma unroll
+  for (int i = 0; i < NW + 1; ++i) t2[i] = (qw & 2) ? t1[i + 2] : t1[i];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) w[i] = __funnelshift_r(t2[i], t2[i + 1], kb);
+}
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int j) {
+  return (w[j >> 2] >> ((j & 3) * 8)) & 0xffu;
+}
+
+// First offset a0 in [0, 16*C) with (addr + a0) % 16 == 0 and a0 % C == 0.
+template <int C>
+__device__ __forceinline__ int first_aligned_px_offset(uintptr_t addr) {
+  int a0 = (int)((16 - (addr & 15)) & 15);
+  if (C == 3) {
+    while (a0 % 3) a0 += 16;
+  }
+  return a0;
+}
+
+__device__ __forceinline__ int ld_desc_h(const alb_image_desc* d) { return d->height; }
+
+}  // namespace alb

@@ -1,0 +1,142 @@
+// kernels.cuh -- launch-argument structs shared between the planner (abi.cu)
+// and the sm_100a kernels.
+#pragma once
+#include "common.cuh"
+
+namespace alb {
+
+// Prep (K0): per image, draws gate + params of every slot, tracks the dims
+// each slot sees, builds the composed LUT of every LUT stage and the
+// Normalize LUT.
+struct PrepArgs {
+  const alb_op* ops;
+  int32_t n_ops;
+  int32_t n;
+  uint64_t seed;
+  uint32_t first_image;
+  const alb_image_desc* in_desc;
+  double* params;
+  uint8_t* fired;
+  int32_t* dims;
+  uint8_t* luts;
+  int32_t n_luts;
+  int32_t lut_k0[kMaxStages], lut_k1[kMaxStages];
+  float* norm_lut;
+  int32_t norm_slot;
+};
+
+// One geometric / pointwise kernel launch.
+struct StepArgs {
+  const uint8_t* src;
+  const alb_image_desc* sdesc;
+  uint8_t* dst;
+  const alb_image_desc* ddesc;
+  float* nchw;
+  int32_t out_h, out_w;
+  const uint8_t* msrc;
+  const alb_image_desc* msdesc;
+  uint8_t* mdst;
+  const alb_image_desc* mddesc;
+  const int2* units;
+  int32_t n_units;
+  int32_t unit_size;  // rows per unit (row kernels) / bytes per unit (flat kernels)
+  int32_t slot0, slot1;
+  int32_t n_stages;
+  Stage stages[kMaxStages];
+  int32_t normalize;
+  int32_t flat;       // pointwise: 1 = whole image is one segment
+  int32_t vec_ok;     // src/dst 16-byte co-aligned per segment
+  int32_t channels;   // rowgather: 3 (image) or 1 (mask)
+  uint32_t fill;      // constant fill, packed RGB (pad / constant border)
+  uint32_t mask_fill;
+  int32_t interp, border;  // resampling op settings
+  Tables tab;
+  const alb_op* ops;
+};
+
+// Equalize (R15): histogram + LUT.
+struct EqArgs {
+  const uint8_t* src;
+  const alb_image_desc* sdesc;
+  uint32_t* hist;     // [n][3][256]
+  uint8_t* lut;       // [n][768]
+  const int2* units;
+  int32_t n_units;
+  int32_t unit_size;
+  int32_t n;
+  int32_t slot;
+  Tables tab;
+};
+
+// Boxes (K11)
+struct BoxArgs {
+  const float* boxes_in;
+  const int32_t* labels_in;
+  const int32_t* count_in;
+  float* boxes_out;
+  int32_t* labels_out;
+  int32_t* count_out;
+  int32_t max_boxes;
+  float min_visibility;
+  int32_t n;
+  Tables tab;
+  const alb_op* ops;
+};
+
+// ±1 affine integer map output -> input with a valid output rectangle.
+struct Map1 {
+  int ax, bx, ay, by;
+  int vx0, vx1, vy0, vy1;
+};
+
+// Exact ops slots [k_begin, k_end) composed into one map from the output of
+// slot k_end-1 back to the input of slot k_begin (O2-O4).  Resize
+// whose input dims equal its output dims is the identity (x_s == x_d exactly).
+__device__ __forceinline__ Map1 compose_exact(const alb_op* ops, const Tables& t, int img,
+                                              int k_begin, int k_end, int out_w, int out_h) {
+  Map1 m{1, 0, 1, 0, 0, out_w, 0, out_h};
+  for (int k = k_end - 1; k >= k_begin; --k) {
+    if (!fired_of(t, img, k)) continue;
+    const alb_op& o = ops[k];
+    const int hin = t.dims[((size_t)img * (t.n_ops + 1) + k) * 2 + 0];
+    const int win = t.dims[((size_t)img * (t.n_ops + 1) + k) * 2 + 1];
+    const double* q = prm_of(t, img, k);
+    switch (o.kind) {
+      case ALB_HFLIP: m.ax = -m.ax; m.bx = win - 1 - m.bx; break;
+      case ALB_VFLIP: m.ay = -m.ay; m.by = hin - 1 - m.by; break;
+      case ALB_CROP:
+      case ALB_RANDOM_CROP: m.bx += (int)q[0]; m.by += (int)q[1]; break;
+      case ALB_PAD_TO_SIZE: {
+        const int left = (o.out_w - win) / 2, top = (o.out_h - hin) / 2;
+        m.bx -= left; m.by -= top;
+        int lo, hi;
+        if (m.ax > 0) { lo = -m.bx; hi = win - m.bx; } else { lo = m.bx - win + 1; hi = m.bx + 1; }
+        m.vx0 = max(m.vx0, lo); m.vx1 = min(m.vx1, hi);
+        if (m.ay > 0) { lo = -m.by; hi = hin - m.by; } else { lo = m.by - hin + 1; hi = m.by + 1; }
+        m.vy0 = max(m.vy0, lo); m.vy1 = min(m.vy1, hi);
+        break;
+      }
+      default: break;  // identity resize
+    }
+  }
+  return m;
+}
+
+__device__ __forceinline__ int dim_h(const Tables& t, int img, int k) {
+  return t.dims[((size_t)img * (t.n_ops + 1) + k) * 2 + 0];
+}
+__device__ __forceinline__ int dim_w(const Tables& t, int img, int k) {
+  return t.dims[((size_t)img * (t.n_ops + 1) + k) * 2 + 1];
+}
+
+// kernel entry points (launch helpers live next to each kernel)
+void launch_prep(const PrepArgs& a, cudaStream_t s);
+void launch_point(const StepArgs& a, cudaStream_t s);
+void launch_rowgather(const StepArgs& a, cudaStream_t s);
+void launch_resample(const StepArgs& a, cudaStream_t s);
+void launch_affine(const StepArgs& a, cudaStream_t s);
+void launch_eq_hist(const EqArgs& a, cudaStream_t s);
+void launch_eq_lut(const EqArgs& a, cudaStream_t s);
+void launch_boxes(const BoxArgs& a, cudaStream_t s);
+
+}  // namespace alb

@@ -1,0 +1,108 @@
+// prep.cu -- K0, the parameter sampler (O1) and the per-image LUT
+// builder (O8, O12).  One CTA per image: thread 0 walks the op list drawing
+// gate + params from Philox4x32-10 and tracking dims; then 256 threads build
+// the composed LUT of each LUT stage in fp64 without FMA contraction.
+#include "kernels.cuh"
+
+namespace alb {
+
+__device__ int lut_entry(int kind, const double* q, int c, int x) {
+  const double v = (double)x;
+  switch (kind) {
+    case ALB_BRIGHTNESS: return clip_round_d(__dmul_rn(v, q[0]));
+    case ALB_CONTRAST: return clip_round_d(__dadd_rn(127.5, __dmul_rn(__dsub_rn(v, 127.5), q[0])));
+    case ALB_BRIGHTNESS_CONTRAST: {
+      const double t = (double)clip_round_d(__dmul_rn(v, q[0]));
+      return clip_round_d(__dadd_rn(127.5, __dmul_rn(__dsub_rn(t, 127.5), q[1])));
+    }
+    case ALB_GAMMA: return clip_round_d(__dmul_rn(255.0, pow(__ddiv_rn(v, 255.0), q[0])));
+    case ALB_SHIFT_RGB: return clip_round_d(__dadd_rn(v, q[c]));
+    default: return x;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
+  const int i = blockIdx.x;
+  __shared__ double s_prm[kMaxOps][kMaxParams];
+  __shared__ uint8_t s_fired[kMaxOps];
+  if (threadIdx.x == 0) {
+    const uint32_t gi = a.first_image + (uint32_t)i;
+    int h = a.in_desc[i].height, w = a.in_desc[i].width;
+    for (int k = 0; k < a.n_ops; ++k) {
+      const alb_op& o = a.ops[k];
+      double* q = s_prm[k];
+#pragma unroll
+      for (int j = 0; j < kMaxParams; ++j) q[j] = 0.0;
+      const bool fired = draw_u(a.seed, gi, k, 0) < o.p;  // gate: draw 0, always drawn
+      a.dims[((size_t)i * (a.n_ops + 1) + k) * 2 + 0] = h;
+      a.dims[((size_t)i * (a.n_ops + 1) + k) * 2 + 1] = w;
+      int nh = h, nw = w;
+      switch (o.kind) {
+        case ALB_ROTATE: case ALB_BRIGHTNESS: case ALB_CONTRAST: case ALB_GAMMA:
+          q[0] = urange(o.lo[0], o.hi[0], draw_u(a.seed, gi, k, 1));
+          break;
+        case ALB_BRIGHTNESS_CONTRAST:
+          for (int j = 0; j < 2; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(a.seed, gi, k, 1 + j));
+          break;
+        case ALB_SHIFT_RGB: case ALB_SHIFT_HSV:
+          for (int j = 0; j < 3; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(a.seed, gi, k, 1 + j));
+          break;
+        case ALB_SHIFT_SCALE_ROTATE:
+          for (int j = 0; j < 4; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(a.seed, gi, k, 1 + j));
+          break;
+        case ALB_RANDOM_CROP:
+          q[0] = (double)uint_draw(draw_u(a.seed, gi, k, 1), w - o.out_w + 1);
+          q[1] = (double)uint_draw(draw_u(a.seed, gi, k, 2), h - o.out_h + 1);
+          nh = o.out_h; nw = o.out_w;
+          break;
+        case ALB_CROP:
+          q[0] = (double)o.crop_x; q[1] = (double)o.crop_y;
+          nh = o.out_h; nw = o.out_w;
+          break;
+        case ALB_RANDOM_SIZED_CROP: {
+          const int ms = h < w ? h : w;
+          const int hi = o.max_side < ms ? o.max_side : ms;
+          const int side = o.min_side + uint_draw(draw_u(a.seed, gi, k, 1), hi - o.min_side + 1);
+          q[0] = (double)side;
+          q[1] = (double)uint_draw(draw_u(a.seed, gi, k, 2), w - side + 1);
+          q[2] = (double)uint_draw(draw_u(a.seed, gi, k, 3), h - side + 1);
+          nh = o.out_h; nw = o.out_w;
+          break;
+        }
+        case ALB_PAD_TO_SIZE: case ALB_RESIZE:
+          nh = o.out_h; nw = o.out_w;
+          break;
+        default: break;
+      }
+      s_fired[k] = fired ? 1 : 0;
+      double* dst = a.params + ((size_t)i * a.n_ops + k) * kMaxParams;
+      for (int j = 0; j < kMaxParams; ++j) dst[j] = q[j];
+      a.fired[(size_t)i * a.n_ops + k] = s_fired[k];
+      if (fired) { h = nh; w = nw; }
+    }
+    a.dims[((size_t)i * (a.n_ops + 1) + a.n_ops) * 2 + 0] = h;
+    a.dims[((size_t)i * (a.n_ops + 1) + a.n_ops) * 2 + 1] = w;
+  }
+  __syncthreads();
+  const int v = threadIdx.x;
+  for (int s = 0; s < a.n_luts; ++s) {
+    for (int c = 0; c < 3; ++c) {
+      int x = v;
+      for (int k = a.lut_k0[s]; k < a.lut_k1[s]; ++k)
+        if (s_fired[k]) x = lut_entry(a.ops[k].kind, s_prm[k], c, x);
+      a.luts[((size_t)i * a.n_luts + s) * 768 + c * 256 + v] = (uint8_t)x;
+    }
+  }
+  if (a.norm_slot >= 0 && i == 0) {
+    const alb_op& o = a.ops[a.norm_slot];
+    for (int c = 0; c < 3; ++c)
+      a.norm_lut[c * 256 + v] =
+          (float)__ddiv_rn(__dsub_rn(__ddiv_rn((double)v, 255.0), o.mean[c]), o.std[c]);
+  }
+}
+
+void launch_prep(const PrepArgs& a, cudaStream_t s) {
+  if (a.n > 0) k_prep<<<a.n, 256, 0, s>>>(a);
+}
+
+}  // namespace alb

@@ -1,0 +1,108 @@
+"""Shared test helpers: run a pipeline through the C ABI on the GPU and through
+the oracle on the CPU, and compare at the DESIGN.md tolerances."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from synth import gen
+
+
+def to_device_batch(images, channels=3, pitch_pad=0, align=256, shift=0, device="cuda"):
+    """Pack numpy images into one flat device buffer.  shift moves every image
+    by `shift` bytes (to test unaligned offsets)."""
+    sizes = [im.shape[:2] for im in images]
+    desc, total = gen.layout(sizes, channels, align, pitch_pad)
+    desc[:, 0] += shift
+    buf = torch.zeros(total + shift + 64, dtype=torch.uint8)
+    for i, im in enumerate(images):
+        off, h, w, pitch = [int(v) for v in desc[i]]
+        v = buf[off:off + h * pitch].view(h, pitch)
+        v[:, :w * channels] = torch.from_numpy(np.ascontiguousarray(im).reshape(h, w * channels))
+    return gen.Batch(buf.to(device), desc, channels)
+
+
+def out_batch(sizes, channels=3, device="cuda", align=256, pitch_pad=0, shift=0, fill=0xAB):
+    desc, total = gen.layout(sizes, channels, align, pitch_pad)
+    desc[:, 0] += shift
+    buf = torch.full((total + shift + 64,), fill, dtype=torch.uint8, device=device)
+    return gen.Batch(buf, desc, channels)
+
+
+def run_gpu(specs, batch, seed=0, first=0, masks=None, boxes=None, labels=None, count=None,
+            max_boxes=0, min_visibility=0.0, out_pitch_pad=0, out_shift=0, return_plan=False):
+    from paper_1809_06839_b200 import Layout, Pipeline, Plan
+    pipe = Pipeline(specs)
+    n = batch.n
+    in_l = Layout(batch.desc, 3)
+    sizes = [pipe.output_shape(int(h), int(w)) for _, h, w, _ in batch.desc]
+    ends_norm = len(specs) > 0 and specs[-1]["kind"] == "Normalize"
+    out = out_l = nchw = None
+    if ends_norm:
+        oh, ow = sizes[0]
+        nchw = torch.full((n, 3, oh, ow), float("nan"), dtype=torch.float32, device="cuda")
+    else:
+        out = out_batch(sizes, 3, pitch_pad=out_pitch_pad, shift=out_shift)
+        out_l = Layout(out.desc, 3)
+    mi_l = mo_l = mout = None
+    if masks is not None:
+        mi_l = Layout(masks.desc, 1)
+        mout = out_batch(sizes, 1)
+        mo_l = Layout(mout.desc, 1)
+    bo = lo = co = bi = li = ci = None
+    if max_boxes:
+        bi = torch.from_numpy(boxes).cuda()
+        li = torch.from_numpy(labels).cuda()
+        ci = torch.from_numpy(count).cuda()
+        bo = torch.full_like(bi, -1.0)
+        lo = torch.full_like(li, -1)
+        co = torch.full_like(ci, -1)
+    plan = Plan(pipe, in_l, out_l, mi_l, mo_l, max_boxes, min_visibility)
+    plan.apply(seed, first, batch.buf, None if out is None else out.buf, nchw,
+               None if masks is None else masks.buf, None if mout is None else mout.buf,
+               bi, li, ci, bo, lo, co)
+    torch.cuda.synchronize()
+    res = {"images": None if out is None else [out.image(i) for i in range(n)],
+           "nchw": None if nchw is None else nchw.cpu().numpy(),
+           "masks": None if mout is None else [mout.image(i) for i in range(n)],
+           "out_batch": out, "mask_batch": mout}
+    if max_boxes:
+        res["boxes"] = bo.cpu().numpy()
+        res["labels"] = lo.cpu().numpy()
+        res["count"] = co.cpu().numpy()
+    if return_plan:
+        res["plan"] = plan
+    return res
+
+
+def run_oracle(specs, images, seed=0, first=0, masks=None, boxes=None, labels=None, count=None,
+               min_visibility=0.0, threads=8):
+    from oracle import albref as A
+    bl = None if boxes is None else [boxes[i, :count[i]] for i in range(len(images))]
+    ll = None if labels is None else [labels[i, :count[i]] for i in range(len(images))]
+    return A.apply_batch(specs, seed, first, images, masks, bl, ll, min_visibility, threads)
+
+
+def cmp_interp(gpu, ref, min_exact=0.999, max_abs=1):
+    """Interpolating/HSV tolerance: max |d| <= 1 and >= 99.9% exact (per batch)."""
+    tot = eq = 0
+    worst = 0
+    for g, r in zip(gpu, ref):
+        assert g.shape == r.shape, (g.shape, r.shape)
+        d = np.abs(g.astype(np.int32) - r.astype(np.int32))
+        worst = max(worst, int(d.max()) if d.size else 0)
+        tot += d.size
+        eq += int((d == 0).sum())
+    frac = eq / max(1, tot)
+    assert worst <= max_abs, "max abs diff %d > %d" % (worst, max_abs)
+    assert frac >= min_exact, "exact fraction %.6f < %.4f" % (frac, min_exact)
+    return frac, worst
+
+
+def cmp_exact(gpu, ref):
+    for i, (g, r) in enumerate(zip(gpu, ref)):
+        assert g.shape == r.shape, (i, g.shape, r.shape)
+        if not np.array_equal(g, r):
+            bad = np.argwhere(g != r)
+            raise AssertionError("image %d differs at %d positions, first %s: gpu %s ref %s" % (
+                i, len(bad), bad[0].tolist(), g[tuple(bad[0])], r[tuple(bad[0])]))
