@@ -80,7 +80,7 @@ struct PlanStep {
   const alb_layout* mdst_l = nullptr;
   std::vector<int2> units, munits;
   size_t units_off = 0, munits_off = 0;  // into the plan's device unit table
-  int unit_size = 0, munit_size = 0;
+  int unit_size = 0, munit_size = 0, unit_rows = 0;
   bool flat = false;
   uint32_t fill = 0, mask_fill = 0;
   int interp = 1, border = 0;
@@ -103,7 +103,7 @@ struct alb_plan {
   std::vector<std::unique_ptr<alb_layout>> inter;  // intermediate layouts
   std::vector<PlanStep> steps;
   int n_luts = 0;
-  int lut_k0[kMaxStages], lut_k1[kMaxStages];
+  int lut_k0[kMaxLuts], lut_k1[kMaxLuts];
   int norm_slot = -1;
   int out_h = 0, out_w = 0;  // NCHW dims
   int max_boxes = 0;
@@ -415,7 +415,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       if (is_lut_kind(kind)) {
         int j = k;
         while (j < n_ops && is_lut_kind(P->ops[j].kind)) ++j;
-        if (P->n_luts >= kMaxStages) return fail(ALB_E_UNSUPPORTED, "too many LUT stages");
+        if (P->n_luts >= kMaxLuts) return fail(ALB_E_UNSUPPORTED, "too many LUT stages");
         sg.type = ST_LUT;
         sg.lut = P->n_luts;
         P->lut_k0[P->n_luts] = k;
@@ -551,16 +551,31 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
         }
         break;
       }
-      case SK_RESAMPLE:
       case SK_AFFINE: {
         st.unit_size = kStageWords;
+        for (int i = 0; i < P->n; ++i) {  // 64x64 output tiles
+          const int H = dims[i][st.slot1].first, W = dims[i][st.slot1].second;
+          const int ntile = ((W + 63) / 64) * ((H + 63) / 64);
+          for (int t = 0; t < ntile; ++t) st.units.push_back(make_int2(i, t));
+        }
+        break;
+      }
+      case SK_RESAMPLE: {
+        st.unit_size = kStageWords;
+        const alb_op& o = P->ops[st.slot0];
+        int R = 64;
+        for (int i = 0; i < P->n; ++i) {
+          if (dims[i][st.slot1].second > 2048) return fail(ALB_E_UNSUPPORTED, "resize output wider than 2048");
+          int wh = dims[i][st.slot0].first, ww = dims[i][st.slot0].second;
+          if (o.kind == ALB_RANDOM_SIZED_CROP) wh = ww = std::min(o.max_side, std::min(wh, ww));
+          const double rows = (double)kStageWords / ww - 2.0;  // staged window rows that fit
+          R = std::min(R, std::max(1, (int)(rows * o.out_h / wh)));
+        }
+        R = std::max(1, std::min(R, 32));
+        st.unit_rows = R;
         for (int i = 0; i < P->n; ++i) {
           const int H = dims[i][st.slot1].first;
-          for (int y = 0, b = 0; y < H; y += 16, ++b) st.units.push_back(make_int2(i, b));
-        }
-        if (st.kind == SK_RESAMPLE) {
-          for (int i = 0; i < P->n; ++i)
-            if (dims[i][st.slot1].second > 2048) return fail(ALB_E_UNSUPPORTED, "resize output wider than 2048");
+          for (int y = 0, b = 0; y < H; y += R, ++b) st.units.push_back(make_int2(i, b));
         }
         break;
       }
@@ -718,6 +733,7 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
     a.units = P->d_units + st.units_off;
     a.n_units = (int)st.units.size();
     a.unit_size = st.unit_size;
+    a.unit_rows = st.unit_rows;
     a.slot0 = st.slot0;
     a.slot1 = st.slot1;
     a.n_stages = (int)st.stages.size();

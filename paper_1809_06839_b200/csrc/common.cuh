@@ -10,7 +10,8 @@ namespace alb {
 
 constexpr int kMaxOps = ALB_MAX_OPS;
 constexpr int kMaxParams = ALB_MAX_PARAMS;
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 4;   // pointwise stages fused into one kernel
+constexpr int kMaxLuts = 8;     // LUT stages per pipeline
 
 // ---------------------------------------------------------------- O1 Philox
 // Philox4x32-10 (Salmon et al. SC'11).  Counter (image, slot, block, tag=0),

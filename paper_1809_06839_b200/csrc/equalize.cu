@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(kEqThreads) k_eq_hist(EqArgs a) {
   const alb_image_desc sd = a.sdesc[img];
   const int W = sd.width, H = sd.height;
   uint32_t* hw = h[warp];
-  const bool flat = sd.pitch == W * 3;
+  const bool flat = a.unit_size > 0;  // plan: whole image one segment, unit = byte chunk
   const int rows = flat ? 1 : H;
   const int seg = flat ? H * W * 3 : W * 3;
   for (int r = 0; r < rows; ++r) {

@@ -20,7 +20,7 @@ struct PrepArgs {
   int32_t* dims;
   uint8_t* luts;
   int32_t n_luts;
-  int32_t lut_k0[kMaxStages], lut_k1[kMaxStages];
+  int32_t lut_k0[kMaxLuts], lut_k1[kMaxLuts];
   float* norm_lut;
   int32_t norm_slot;
 };
@@ -39,7 +39,9 @@ struct StepArgs {
   const alb_image_desc* mddesc;
   const int2* units;
   int32_t n_units;
-  int32_t unit_size;  // rows per unit (row kernels) / bytes per unit (flat kernels)
+  int32_t unit_size;  // rows per unit (rowgather) / bytes per unit (flat pointwise) /
+                      // shared-memory staging capacity in words (resample, affine)
+  int32_t unit_rows;  // resample: output rows per unit
   int32_t slot0, slot1;
   int32_t n_stages;
   Stage stages[kMaxStages];

@@ -3,22 +3,24 @@
 // chain (HSV / LUT / gray) and Normalize-to-fp32-NCHW output (K9, cfg4).
 //
 // Half-pixel bilinear: x_s = (x_d + 0.5) * ww / nw - 0.5, clamped to the
-// window [0, ww-1] (replicate border at the WINDOW edge, R9).  The column and
-// row tables (x0, x1, fx) are computed once per CTA in fp64 exactly as the
-// definition orders the operations, so coordinates match the oracle to the
-// last bit; the blend runs in fp32.  Masks: nearest, round_half_up(x_s).
+// window [0, ww-1] (replicate border at the WINDOW edge, R9).  Column and row
+// tables (x0, fx, nearest) are computed in fp64 in the definition's operation
+// order, so the coordinates equal the oracle's bit for bit; the blend runs in
+// fp32.  Masks: nearest, round_half_up(x_s).
 //
-// Work unit = (image, band of output rows).  The source window's rows are
-// staged into shared memory as RGBx words (one 32-bit word per pixel) with
-// 16-byte vector loads, then every output pixel reads its 4 taps from shared
-// memory.  Each thread produces one aligned 16-pixel block.
+// Work unit = (image, band of `unit_rows` output rows); persistent grid over
+// contiguous unit ranges; the column table is rebuilt only when the image
+// changes.  Per band, the window rows it needs are staged in shared memory as
+// RGBx words (16-byte loads + byte permutes); each lane then computes one
+// output pixel per (row, 32-pixel segment) from 4 shared-memory taps and the
+// warp writes the segment with shuffled 4-byte stores.
 #include "stages.cuh"
 
 namespace alb {
 
 constexpr int kRsThreads = 256;
-constexpr int kRsMaxCols = 2048;   // output width limit of the table path
-constexpr int kRsBand = 16;        // output rows per unit
+constexpr int kRsMaxCols = 2048;
+constexpr int kRsMaxBand = 64;
 
 struct RsGeom {
   int wx0, wy0, ww, wh;  // source window
@@ -51,159 +53,174 @@ __device__ __forceinline__ double rs_coord(int d, int n_src, int n_dst) {
   return s;
 }
 
+struct ColEnt {
+  int x0;      // tap 0 column (window frame); tap 1 = min(x0+1, ww-1)
+  float fx;
+  int xn;      // nearest column
+  int x1;
+};
+
 __global__ void __launch_bounds__(kRsThreads) k_resample(StepArgs a) {
   extern __shared__ uint32_t sm[];
-  const int2 unit = a.units[blockIdx.x];
-  const int img = unit.x;
-  const int lane = threadIdx.x & 31;
-  const alb_image_desc sd = a.sdesc[img];
-  const int Wo = a.normalize ? a.out_w : a.ddesc[img].width;
-  const int Ho = a.normalize ? a.out_h : a.ddesc[img].height;
-  const RsGeom g = rs_geom(a, img);
-  const Map1 m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, Wo, Ho);
-  const int y0 = unit.y * kRsBand;
-  const int y1 = min(Ho, y0 + kRsBand);
-
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   StageCtx x;
-  load_stages(a, img, sm, x, kRsThreads);
-  uint32_t* smx = sm + x.n_lut * kLutWords;
-  int* col_x0 = reinterpret_cast<int*>(smx);            // [Wo] source column of tap 0 (window frame)
-  float* col_fx = reinterpret_cast<float*>(col_x0 + kRsMaxCols);
-  int* col_xn = reinterpret_cast<int*>(col_fx + kRsMaxCols);  // nearest (masks)
-  int* row_y0 = col_xn + kRsMaxCols;                    // [band]
-  float* row_fy = reinterpret_cast<float*>(row_y0 + kRsBand);
-  int* row_yn = reinterpret_cast<int*>(row_fy + kRsBand);
-  uint32_t* stage = reinterpret_cast<uint32_t*>(row_yn + kRsBand);  // staged source rows (RGBx)
+  init_stages(a, x);
+  ColEnt* col = reinterpret_cast<ColEnt*>(sm + x.n_lut * kLutWords);
+  int* row_y0 = reinterpret_cast<int*>(col + kRsMaxCols);
+  float* row_fy = reinterpret_cast<float*>(row_y0 + kRsMaxBand);
+  int* row_yn = reinterpret_cast<int*>(row_fy + kRsMaxBand);
+  int* s_geom = row_yn + kRsMaxBand;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(s_geom + 8);
+  const bool nearest = a.interp == ALB_INTERP_NEAREST;
+  const bool has_mask = a.mdst != nullptr;
+  const int R = a.unit_rows;
 
-  for (int xo = threadIdx.x; xo < Wo; xo += kRsThreads) {
-    const int xr = m.ax * xo + m.bx;  // resize-output column
-    const double s = rs_coord(xr, g.ww, g.nw);
-    const double f = floor(s);
-    col_x0[xo] = (int)f;
-    col_fx[xo] = (float)__dsub_rn(s, f);
-    col_xn[xo] = (int)floor(__dadd_rn(s, 0.5));
-  }
-  // source rows needed by this band
-  int sy_lo = 1 << 30, sy_hi = -1;
-  for (int yy = y0; yy < y1; ++yy) {
-    const int yr = m.ay * yy + m.by;
-    const double s = rs_coord(yr, g.wh, g.nh);
-    const int f = (int)floor(s);
-    sy_lo = min(sy_lo, f);
-    sy_hi = max(sy_hi, min(f + 1, g.wh - 1));
-    if (threadIdx.x == 0) {
-      row_y0[yy - y0] = f;
-      row_fy[yy - y0] = (float)__dsub_rn(s, floor(s));
-      row_yn[yy - y0] = (int)floor(__dadd_rn(s, 0.5));
-    }
-  }
-  const int nrows = sy_hi - sy_lo + 1;
-  const int stride = g.ww;  // words per staged row
-  const bool staged = a.unit_size > 0 && nrows * stride <= a.unit_size;
-  if (staged) {
-    // stage window rows [sy_lo, sy_hi] x [wx0, wx0+ww) as RGBx words; 16 px per item
-    const int per_row = (g.ww + 15) / 16;
-    for (int it = threadIdx.x; it < nrows * per_row; it += kRsThreads) {
-      const int r = it / per_row, c16 = (it % per_row) * 16;
-      const uint8_t* srow = a.src + sd.offset + (size_t)(g.wy0 + sy_lo + r) * sd.pitch;
-      uint32_t w[12];
-      load_window<12>(srow + (size_t)(g.wx0 + c16) * 3, srow, srow + (size_t)sd.width * 3, w);
-      uint32_t* d = stage + r * stride + c16;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (c16 + i < g.ww)
-          d[i] = byte_of(w, 3 * i) | (byte_of(w, 3 * i + 1) << 8) | (byte_of(w, 3 * i + 2) << 16);
+  int u0, u1;
+  unit_range(a.n_units, u0, u1);
+  int cur_img = -1;
+  RsGeom g{};
+  Map1 m{};
+  int Wo = 0, Ho = 0;
+  for (int u = u0; u < u1; ++u) {
+    const int2 unit = a.units[u];
+    const int img = unit.x;
+    __syncthreads();
+    if (img != cur_img) {
+      load_stages(a, img, sm, x, kRsThreads);
+      g = rs_geom(a, img);
+      Wo = a.normalize ? a.out_w : a.ddesc[img].width;
+      Ho = a.normalize ? a.out_h : a.ddesc[img].height;
+      m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, Wo, Ho);
+      for (int xo = threadIdx.x; xo < Wo; xo += kRsThreads) {
+        const int xr = m.ax * xo + m.bx;
+        const double s = rs_coord(xr, g.ww, g.nw);
+        const double f = floor(s);
+        ColEnt e;
+        e.x0 = (int)f;
+        e.x1 = min(e.x0 + 1, g.ww - 1);
+        e.fx = (float)__dsub_rn(s, f);
+        e.xn = (int)floor(__dadd_rn(s, 0.5));
+        col[xo] = e;
       }
+      cur_img = img;
     }
-  }
-  __syncthreads();
-
-  const uint8_t* wbase = a.src + sd.offset + (size_t)g.wy0 * sd.pitch + (size_t)g.wx0 * 3;
-  const int nbmax = 2 + Wo / 16;
-  const int items = (y1 - y0) * nbmax;
-  for (int it = threadIdx.x; it < items; it += kRsThreads) {
-    const int yy = y0 + it / nbmax;
-    const int k = it % nbmax - 1;
-    int xb;
-    uint8_t* drow = nullptr;
-    if (a.normalize) {
-      xb = 16 * k;
-    } else {
-      const alb_image_desc dd = a.ddesc[img];
-      drow = a.dst + dd.offset + (size_t)yy * dd.pitch;
-      xb = first_aligned_px_offset<3>((uintptr_t)drow) / 3 + 16 * k;
+    const int y0 = unit.y * R, y1 = min(Ho, y0 + R);
+    if (threadIdx.x < y1 - y0) {
+      const int yr = m.ay * (y0 + threadIdx.x) + m.by;
+      const double s = rs_coord(yr, g.wh, g.nh);
+      const double f = floor(s);
+      row_y0[threadIdx.x] = (int)f;
+      row_fy[threadIdx.x] = (float)__dsub_rn(s, f);
+      row_yn[threadIdx.x] = (int)floor(__dadd_rn(s, 0.5));
     }
-    if (xb + 16 <= 0 || xb >= Wo) continue;
-    const int ry0 = row_y0[yy - y0];
-    const int ry1 = min(ry0 + 1, g.wh - 1);
-    const float fy = row_fy[yy - y0];
-    uint32_t px[48];
+    __syncthreads();
+    // rows of the window this band needs (monotone in y up to the flip)
+    int ra = row_y0[0], rb = row_y0[y1 - y0 - 1];
+    const int sy_lo = min(ra, rb);
+    const int sy_hi = min(max(ra, rb) + 1, g.wh - 1);
+    const int nrows = sy_hi - sy_lo + 1;
+    const int S = g.ww;
+    const bool staged = (long long)nrows * S <= a.unit_size;
+    const alb_image_desc sd = a.sdesc[img];
+    const uint8_t* wbase = a.src + sd.offset + (size_t)g.wy0 * sd.pitch + (size_t)g.wx0 * 3;
+    if (staged) {
+      const int per_row = (g.ww + 15) / 16;
+      for (int it = threadIdx.x; it < nrows * per_row; it += kRsThreads) {
+        const int r = it / per_row, c16 = (it % per_row) * 16;
+        const uint8_t* srow = a.src + sd.offset + (size_t)(g.wy0 + sy_lo + r) * sd.pitch;
+        uint32_t w[12];
+        load_window<12>(srow + (size_t)(g.wx0 + c16) * 3, srow, srow + (size_t)sd.width * 3, w);
+        uint32_t* d = stage + r * S + c16;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int xo = min(max(xb + i, 0), Wo - 1);
-      const int cx0 = col_x0[xo];
-      const int cx1 = min(cx0 + 1, g.ww - 1);
-      const float fx = col_fx[xo];
-      uint32_t t00, t10, t01, t11;
-      if (staged) {
-        const uint32_t* r0 = stage + (ry0 - sy_lo) * stride;
-        const uint32_t* r1 = stage + (ry1 - sy_lo) * stride;
-        t00 = r0[cx0]; t10 = r0[cx1]; t01 = r1[cx0]; t11 = r1[cx1];
+        for (int i = 0; i < 16; ++i)
+          if (c16 + i < g.ww) d[i] = rgbx_of(w, i);
+      }
+      __syncthreads();
+    }
+    const int nseg = (Wo + 31) / 32;
+    for (int rs = warp; rs < (y1 - y0) * nseg; rs += kRsThreads / 32) {
+      const int rr = rs / nseg, seg = rs % nseg;
+      const int yo = y0 + rr;
+      const int xo = seg * 32 + lane;
+      const int nvalid = min(32, Wo - seg * 32);
+      const bool act = lane < nvalid;
+      const ColEnt ce = col[act ? xo : 0];
+      uint32_t r, gg, b;
+      if (nearest) {
+        const int yn = row_yn[rr];
+        const uint32_t t = staged ? stage[(yn - sy_lo) * S + ce.xn]
+                                  : (wbase[(size_t)yn * sd.pitch + 3 * ce.xn] |
+                                     (wbase[(size_t)yn * sd.pitch + 3 * ce.xn + 1] << 8) |
+                                     (wbase[(size_t)yn * sd.pitch + 3 * ce.xn + 2] << 16));
+        r = t & 0xff; gg = (t >> 8) & 0xff; b = (t >> 16) & 0xff;
       } else {
-        const uint8_t* p0 = wbase + (size_t)ry0 * sd.pitch;
-        const uint8_t* p1 = wbase + (size_t)ry1 * sd.pitch;
-        t00 = p0[3 * cx0] | (p0[3 * cx0 + 1] << 8) | (p0[3 * cx0 + 2] << 16);
-        t10 = p0[3 * cx1] | (p0[3 * cx1 + 1] << 8) | (p0[3 * cx1 + 2] << 16);
-        t01 = p1[3 * cx0] | (p1[3 * cx0 + 1] << 8) | (p1[3 * cx0 + 2] << 16);
-        t11 = p1[3 * cx1] | (p1[3 * cx1 + 1] << 8) | (p1[3 * cx1 + 2] << 16);
-      }
-      uint32_t ch[3];
+        const int ry0 = row_y0[rr];
+        const int ry1 = min(ry0 + 1, g.wh - 1);
+        const float fy = row_fy[rr];
+        uint32_t t00, t10, t01, t11;
+        if (staged) {
+          const uint32_t* p0 = stage + (ry0 - sy_lo) * S;
+          const uint32_t* p1 = stage + (ry1 - sy_lo) * S;
+          t00 = p0[ce.x0]; t10 = p0[ce.x1]; t01 = p1[ce.x0]; t11 = p1[ce.x1];
+        } else {
+          const uint8_t* q0 = wbase + (size_t)ry0 * sd.pitch;
+          const uint8_t* q1 = wbase + (size_t)ry1 * sd.pitch;
+          t00 = q0[3 * ce.x0] | (q0[3 * ce.x0 + 1] << 8) | (q0[3 * ce.x0 + 2] << 16);
+          t10 = q0[3 * ce.x1] | (q0[3 * ce.x1 + 1] << 8) | (q0[3 * ce.x1 + 2] << 16);
+          t01 = q1[3 * ce.x0] | (q1[3 * ce.x0 + 1] << 8) | (q1[3 * ce.x0 + 2] << 16);
+          t11 = q1[3 * ce.x1] | (q1[3 * ce.x1 + 1] << 8) | (q1[3 * ce.x1 + 2] << 16);
+        }
+        uint32_t ch[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float p00 = (float)((t00 >> (8 * c)) & 0xff), p10 = (float)((t10 >> (8 * c)) & 0xff);
-        const float p01 = (float)((t01 >> (8 * c)) & 0xff), p11 = (float)((t11 >> (8 * c)) & 0xff);
-        const float h0 = (1.f - fx) * p00 + fx * p10;
-        const float h1 = (1.f - fx) * p01 + fx * p11;
-        const float v = (1.f - fy) * h0 + fy * h1;
-        ch[c] = (uint32_t)min(255, (int)floorf(v + 0.5f));
+        for (int c = 0; c < 3; ++c) {
+          const float p00 = (float)((t00 >> (8 * c)) & 0xff), p10 = (float)((t10 >> (8 * c)) & 0xff);
+          const float p01 = (float)((t01 >> (8 * c)) & 0xff), p11 = (float)((t11 >> (8 * c)) & 0xff);
+          const float h0 = fmaf(ce.fx, p10 - p00, p00);
+          const float h1 = fmaf(ce.fx, p11 - p01, p01);
+          const float v = fmaf(fy, h1 - h0, h0);
+          ch[c] = (uint32_t)(v + 0.5f);
+        }
+        r = ch[0]; gg = ch[1]; b = ch[2];
       }
-      apply_stages(a, x, sm, lane, ch[0], ch[1], ch[2]);
-      px[3 * i] = ch[0]; px[3 * i + 1] = ch[1]; px[3 * i + 2] = ch[2];
-    }
-    if (a.normalize) {
-      store_nchw(a, img, yy, xb, px, Wo, Ho);
-    } else {
-      uint32_t w[12];
-#pragma unroll
-      for (int q = 0; q < 12; ++q)
-        w[q] = px[4 * q] | (px[4 * q + 1] << 8) | (px[4 * q + 2] << 16) | (px[4 * q + 3] << 24);
-      store_block<3>(drow, xb, Wo, w);
-    }
-  }
-
-  // mask (nearest), byte-wise
-  if (a.mdst) {
-    const alb_image_desc msd = a.msdesc[img];
-    const alb_image_desc mdd = a.mddesc[img];
-    const uint8_t* mw = a.msrc + msd.offset + (size_t)g.wy0 * msd.pitch + g.wx0;
-    for (int it = threadIdx.x; it < (y1 - y0) * Wo; it += kRsThreads) {
-      const int yy = y0 + it / Wo, xo = it % Wo;
-      a.mdst[mdd.offset + (size_t)yy * mdd.pitch + xo] =
-          mw[(size_t)row_yn[yy - y0] * msd.pitch + col_xn[xo]];
+      apply_stages(x, sm, lane, r, gg, b);
+      if (a.normalize) {
+        if (act) {
+          const size_t plane = (size_t)Ho * Wo;
+          float* o = a.nchw + (size_t)img * 3 * plane + (size_t)yo * Wo + xo;
+          const float* nl = a.tab.norm_lut;
+          __stcs(o, nl[r]);
+          __stcs(o + plane, nl[256 + gg]);
+          __stcs(o + 2 * plane, nl[512 + b]);
+        }
+      } else {
+        const alb_image_desc dd = a.ddesc[img];
+        uint8_t* drow = a.dst + dd.offset + (size_t)yo * dd.pitch + (size_t)seg * 32 * 3;
+        warp_store_rgb(drow, nvalid, r | (gg << 8) | (b << 16), lane);
+      }
+      if (has_mask && act) {
+        const alb_image_desc msd = a.msdesc[img];
+        const alb_image_desc mdd = a.mddesc[img];
+        const uint8_t* mw = a.msrc + msd.offset + (size_t)g.wy0 * msd.pitch + g.wx0;
+        a.mdst[mdd.offset + (size_t)yo * mdd.pitch + xo] = mw[(size_t)row_yn[rr] * msd.pitch + ce.xn];
+      }
     }
   }
 }
 
 size_t resample_smem(const StepArgs& a) {
-  return (size_t)count_lut_stages(a) * kLutWords * 4 + (size_t)kRsMaxCols * 12 + kRsBand * 12 +
-         (size_t)a.unit_size * 4;
+  return (size_t)count_lut_stages(a) * kLutWords * 4 + sizeof(ColEnt) * kRsMaxCols +
+         kRsMaxBand * 12 + 32 + (size_t)a.unit_size * 4;
 }
 
 void launch_resample(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
   const size_t smem = resample_smem(a);
   cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_resample<<<a.n_units, kRsThreads, smem, s>>>(a);
+  int occ = 1, sms = 148, dev = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_resample, kRsThreads, smem);
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(a.n_units, sms * std::max(occ, 1));
+  k_resample<<<grid, kRsThreads, smem, s>>>(a);
 }
 
 }  // namespace alb

@@ -1,6 +1,7 @@
 // stages.cuh -- pointwise stage chain (LUT / Equalize LUT / HSV / gray) shared
 // by the pointwise, resample and affine kernels so fused and unfused paths
-// execute the same arithmetic.
+// execute the same arithmetic.  At most kMaxStages stages per kernel; the
+// chain is unrolled so per-stage state lives in registers.
 #pragma once
 #include "kernels.cuh"
 
@@ -8,13 +9,12 @@ namespace alb {
 
 constexpr int kLutWords = 3 * 64 * 32;  // one lane-replicated LUT stage (24 KB)
 
-struct StageData {
-  float dh, ds, dv;
-  int on;
-};
-
 struct StageCtx {
-  StageData sd[kMaxStages];
+  int type[kMaxStages];
+  int on[kMaxStages];
+  int smb[kMaxStages];  // shared-memory word offset of the stage's LUT
+  float dh[kMaxStages], ds[kMaxStages], dv[kMaxStages];
+  int n;
   int n_lut;
 };
 
@@ -31,54 +31,62 @@ __host__ __device__ inline int count_lut_stages(const StepArgs& a) {
   return n;
 }
 
-// Stage this image's LUTs into shared memory (replicated per lane so the 32
-// lookups of a warp hit 32 distinct banks) and fetch per-stage params.
-// Must be followed by __syncthreads().
-__device__ __forceinline__ void load_stages(const StepArgs& a, int img, uint32_t* sm,
-                                            StageCtx& x, int nthreads) {
+// Static part of the context (types, LUT slots) -- no memory traffic.
+__device__ __forceinline__ void init_stages(const StepArgs& a, StageCtx& x) {
+  x.n = a.n_stages;
   int li = 0;
-  for (int s = 0; s < a.n_stages; ++s) {
-    const Stage st = a.stages[s];
-    x.sd[s].on = 0;
-    x.sd[s].dh = x.sd[s].ds = x.sd[s].dv = 0.f;
-    if (st.type == ST_LUT || st.type == ST_EQ) {
-      const uint8_t* tab = st.type == ST_EQ
-                               ? a.tab.eq_luts + (size_t)img * 768
-                               : a.tab.luts + ((size_t)img * a.tab.n_luts + st.lut) * 768;
-      const uint32_t* t32 = reinterpret_cast<const uint32_t*>(tab);
-      uint32_t* dst = sm + li * kLutWords;
-      for (int idx = threadIdx.x; idx < kLutWords; idx += nthreads) dst[idx] = __ldg(t32 + (idx >> 5));
-      ++li;
-    } else {
-      x.sd[s].on = fired_of(a.tab, img, st.slot) ? 1 : 0;
-      if (st.type == ST_HSV) {
-        const double* q = prm_of(a.tab, img, st.slot);
-        x.sd[s].dh = (float)q[0];
-        x.sd[s].ds = (float)q[1];
-        x.sd[s].dv = (float)q[2];
-      }
-    }
+#pragma unroll
+  for (int s = 0; s < kMaxStages; ++s) {
+    x.type[s] = s < a.n_stages ? a.stages[s].type : -1;
+    x.on[s] = 0;
+    x.dh[s] = x.ds[s] = x.dv[s] = 0.f;
+    x.smb[s] = li * kLutWords;
+    if (x.type[s] == ST_LUT || x.type[s] == ST_EQ) ++li;
   }
   x.n_lut = li;
 }
 
-__device__ __forceinline__ void apply_stages(const StepArgs& a, const StageCtx& x,
-                                             const uint32_t* sm, int lane, uint32_t& r,
-                                             uint32_t& g, uint32_t& b) {
-  int li = 0;
-#pragma unroll 1
-  for (int s = 0; s < a.n_stages; ++s) {
-    const int t = a.stages[s].type;
+// Stage image `img`'s LUTs into shared memory (replicated per lane so a
+// warp's 32 lookups hit 32 distinct banks) and fetch per-stage params.
+// Caller brackets with __syncthreads().
+__device__ __forceinline__ void load_stages(const StepArgs& a, int img, uint32_t* sm, StageCtx& x,
+                                            int nthreads) {
+#pragma unroll
+  for (int s = 0; s < kMaxStages; ++s) {
+    const int t = x.type[s];
     if (t == ST_LUT || t == ST_EQ) {
-      const uint32_t* L = sm + li * kLutWords;
+      const uint8_t* tab = t == ST_EQ
+                               ? a.tab.eq_luts + (size_t)img * 768
+                               : a.tab.luts + ((size_t)img * a.tab.n_luts + a.stages[s].lut) * 768;
+      const uint32_t* t32 = reinterpret_cast<const uint32_t*>(tab);
+      uint32_t* dst = sm + x.smb[s];
+      for (int idx = threadIdx.x; idx < kLutWords; idx += nthreads) dst[idx] = __ldg(t32 + (idx >> 5));
+    } else if (t == ST_HSV || t == ST_GRAY) {
+      x.on[s] = fired_of(a.tab, img, a.stages[s].slot) ? 1 : 0;
+      if (t == ST_HSV) {
+        const double* q = prm_of(a.tab, img, a.stages[s].slot);
+        x.dh[s] = (float)q[0];
+        x.ds[s] = (float)q[1];
+        x.dv[s] = (float)q[2];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void apply_stages(const StageCtx& x, const uint32_t* sm, int lane,
+                                             uint32_t& r, uint32_t& g, uint32_t& b) {
+#pragma unroll
+  for (int s = 0; s < kMaxStages; ++s) {
+    const int t = x.type[s];
+    if (t == ST_LUT || t == ST_EQ) {
+      const uint32_t* L = sm + x.smb[s];
       r = lut_look(L, 0, r, lane);
       g = lut_look(L, 2048, g, lane);
       b = lut_look(L, 4096, b, lane);
-      ++li;
     } else if (t == ST_HSV) {
-      if (x.sd[s].on) hsv_shift_px(x.sd[s].dh, x.sd[s].ds, x.sd[s].dv, r, g, b);
-    } else {
-      if (x.sd[s].on) {
+      if (x.on[s]) hsv_shift_px(x.dh[s], x.ds[s], x.dv[s], r, g, b);
+    } else if (t == ST_GRAY) {
+      if (x.on[s]) {
         const uint32_t y = gray_px(r, g, b);
         r = g = b = y;
       }
@@ -108,7 +116,7 @@ __device__ __forceinline__ void store_block(uint8_t* drow, int xb, int W, const 
   }
 }
 
-// Store 16 pixels (r,g,b in p[3*i..]) as Normalize fp32 NCHW (O12), the 3x256
+// Store 16 pixels (r,g,b in px[3*i..]) as Normalize fp32 NCHW (O12), the 3x256
 // fp32 LUT built by K0 in fp64.
 __device__ __forceinline__ void store_nchw(const StepArgs& a, int img, int y, int xb,
                                            const uint32_t* px, int W, int H) {
@@ -135,6 +143,50 @@ __device__ __forceinline__ void store_nchw(const StepArgs& a, int img, int y, in
       }
     }
   }
+}
+
+// Warp-cooperative store of a row segment: lane l holds pixel l (R | G<<8 |
+// B<<16); pixels l < nvalid are written to base[3l .. 3l+2].  The 3*nvalid
+// bytes are regrouped with two shuffles + one byte permute per lane into
+// 4-byte-aligned words (coalesced STG.32); only the partial first/last words
+// fall back to byte stores.  All 32 lanes must call it.
+__device__ __forceinline__ void warp_store_rgb(uint8_t* base, int nvalid, uint32_t px, int lane) {
+  const int off = (int)((uintptr_t)base & 3);
+  uint8_t* wb = base - off;
+  const int k0 = 4 * lane - off;             // first segment byte of word `lane`
+  const int qa = k0 >= 0 ? k0 / 3 : -1;      // pixel holding byte k0
+  const int r = k0 - 3 * qa;                 // 0..2
+  const uint32_t pa = __shfl_sync(0xffffffffu, px, qa < 0 ? 0 : qa);
+  const uint32_t pb = __shfl_sync(0xffffffffu, px, qa + 1 > 31 ? 31 : qa + 1);
+  const uint32_t sel = r == 0 ? 0x4210u : (r == 1 ? 0x5421u : 0x6542u);
+  const uint32_t w = __byte_perm(pa, pb, sel);
+  const int nbytes = 3 * nvalid;
+  if (k0 >= 0 && k0 + 4 <= nbytes) {
+    *reinterpret_cast<uint32_t*>(wb + 4 * lane) = w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = k0 + j;
+      if (k >= 0 && k < nbytes) wb[4 * lane + j] = (uint8_t)(w >> (8 * j));
+    }
+  }
+  // words beyond lane 31 (segment of 32 px spans up to 25 words: never)
+}
+
+// Pixel i (0..15) of a 48-byte window as an RGBx word (one byte permute).
+__device__ __forceinline__ uint32_t rgbx_of(const uint32_t (&w)[12], int i) {
+  const int q = (3 * i) >> 2, k = (3 * i) & 3;
+  const uint32_t hi = w[q + 1 < 12 ? q + 1 : 11];
+  return __byte_perm(w[q], hi, (uint32_t)k * 0x111u + 0x210u) & 0xffffffu;
+}
+
+// Contiguous range of units for CTA b of G (persistent kernels): consecutive
+// units belong mostly to the same image, so per-image state is reloaded only
+// when the image changes.
+__device__ __forceinline__ void unit_range(int n_units, int& u0, int& u1) {
+  const long long G = gridDim.x, b = blockIdx.x;
+  u0 = (int)(b * n_units / G);
+  u1 = (int)((b + 1) * n_units / G);
 }
 
 }  // namespace alb
