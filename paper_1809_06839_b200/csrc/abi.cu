@@ -88,7 +88,7 @@ struct PlanStep {
 };
 
 constexpr int kChunk = 48 * 512;         // pointwise / histogram bytes per unit
-constexpr int kStageWords = 16 * 1024;   // resample/affine staging capacity (64 KB)
+constexpr int kStageWords = 10 * 1024;   // resample staging capacity (40 KB)
 
 }  // namespace
 
@@ -552,16 +552,16 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
         break;
       }
       case SK_AFFINE: {
-        st.unit_size = kStageWords;
+        st.unit_size = 10 * 1024;  // 40 KB: a 64x32 tile at 45 deg / scale 0.9 needs ~8.7K words
         for (int i = 0; i < P->n; ++i) {  // 64x64 output tiles
           const int H = dims[i][st.slot1].first, W = dims[i][st.slot1].second;
-          const int ntile = ((W + 63) / 64) * ((H + 63) / 64);
+          const int ntile = ((W + 63) / 64) * ((H + 31) / 32);  // 64 x 32 tiles
           for (int t = 0; t < ntile; ++t) st.units.push_back(make_int2(i, t));
         }
         break;
       }
       case SK_RESAMPLE: {
-        st.unit_size = kStageWords;
+        st.unit_size = kStageWords;  // 40 KB of staged window rows per band
         const alb_op& o = P->ops[st.slot0];
         int R = 64;
         for (int i = 0; i < P->n; ++i) {

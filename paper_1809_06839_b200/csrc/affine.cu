@@ -10,22 +10,26 @@
 // error ~2e-6 px, and a pixel's value depends only on its warp-output
 // coordinates, so the fused cfg5 kernel equals the unfused kernel bit for bit.
 //
-// Work unit = (image, 64x64 output tile); the grid is persistent over
+// Work unit = (image, 64x32 output tile); the grid is persistent over
 // contiguous unit ranges.  Per tile the source footprint (+ bilinear halo) is
 // staged in shared memory as RGBx words with the border resolved per staged
-// pixel (reflect-101 or constant fill), so the hot loop has no border logic.
-// The staged row stride S is = +-1 (mod 32), picked from the rotation so the
-// 32 lanes of a warp (32 consecutive output pixels) hit distinct banks.
-// Each lane computes one pixel per row; rows are written with warp-shuffled
-// 4-byte stores (warp_store_rgb).  Footprints larger than the staging
-// capacity fall back to per-tap global loads.
+// pixel (reflect-101 or constant fill): interior runs of 16 pixels with
+// 16-byte loads, border pixels one per thread, so the hot loop has no border
+// logic.  The staged row stride S is = +-1 (mod 32), picked from the rotation
+// so 32 consecutive output pixels hit distinct banks.  Each warp owns 4 output
+// rows (lane = column, 2 pixels per lane per row); RGB bytes go to a per-warp
+// row buffer that the warp writes out with aligned 16-byte stores.
+// Footprints larger than the staging capacity fall back to per-tap loads.
+#include <algorithm>
+
 #include "stages.cuh"
 
 namespace alb {
 
 constexpr int kAfThreads = 256;
-constexpr int kTile = 64;
-constexpr int kCells = 5;  // 16x16 anchor cells per tile axis (64 px unaligned -> <= 5)
+constexpr int kAfWarps = kAfThreads / 32;
+constexpr int kTileW = 64, kTileH = 32;
+constexpr int kRowsPerWarp = kTileH / kAfWarps;
 
 struct AfCoef {
   double A[6];
@@ -66,19 +70,38 @@ __device__ __forceinline__ uint32_t fetch_rgb(const uint8_t* row, int x) {
   return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
 }
 
-struct Anchor {
-  int ix, iy;
-  float fx, fy;
+// border index: one reflection without modulo (the common case), else general
+__device__ __forceinline__ int border_idx(int i, int n, bool reflect, bool& in) {
+  if (i >= 0 && i < n) { in = true; return i; }
+  if (!reflect) { in = false; return 0; }
+  in = true;
+  int k = i < 0 ? -i : i;
+  if (k >= n) k = 2 * n - 2 - k;
+  return (k >= 0 && k < n) ? k : reflect101(i, n);
+}
+
+struct TileGeom {
+  int fx0, fy0, S, fw, fh, staged, Sm, ci0, ci1, pad[3];
 };
 
-__global__ void __launch_bounds__(kAfThreads) k_affine(StepArgs a) {
+struct ImgState {
+  double A[6];
+  float Af[4];
+  Map1 m;
+  int Wo, Ho, tiles_x, pad;
+};
+
+template <int kOne>
+__global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   StageCtx x;
   init_stages(a, x);
-  Anchor* anc = reinterpret_cast<Anchor*>(sm + x.n_lut * kLutWords);
-  int* s_geom = reinterpret_cast<int*>(anc + kCells * kCells);  // fx0, fy0, S, fw, fh, staged, cx0, cy0, Sm
-  uint32_t* stage = reinterpret_cast<uint32_t*>(s_geom + 16);
+  ImgState* is = reinterpret_cast<ImgState*>(sm + x.n_lut * kLutWords);
+  TileGeom* tg = reinterpret_cast<TileGeom*>(is + 1);
+  uint8_t* rowbuf = reinterpret_cast<uint8_t*>(tg + 1) + warp * (kTileW * 3 + 32);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tg + 1) +
+                                                kAfWarps * (kTileW * 3 + 32));
   uint8_t* mstage = reinterpret_cast<uint8_t*>(stage + a.unit_size);
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
   const bool nearest = a.interp == ALB_INTERP_NEAREST;
@@ -87,215 +110,254 @@ __global__ void __launch_bounds__(kAfThreads) k_affine(StepArgs a) {
   int u0, u1;
   unit_range(a.n_units, u0, u1);
   int cur_img = -1;
-  AfCoef cf;
-  Map1 m;
-  int Wo = 0, Ho = 0, tiles_x = 1;
   for (int u = u0; u < u1; ++u) {
     const int2 unit = a.units[u];
     const int img = unit.x;
     __syncthreads();  // previous tile fully consumed
     if (img != cur_img) {
       load_stages(a, img, sm, x, kAfThreads);
-      cf = af_coef(a, img);
-      Wo = a.normalize ? a.out_w : a.ddesc[img].width;
-      Ho = a.normalize ? a.out_h : a.ddesc[img].height;
-      m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, Wo, Ho);
-      tiles_x = (Wo + kTile - 1) / kTile;
+      if (threadIdx.x == 0) {
+        const AfCoef cf = af_coef(a, img);
+        ImgState s;
+        for (int k = 0; k < 6; ++k) s.A[k] = cf.A[k];
+        s.Af[0] = (float)cf.A[0]; s.Af[1] = (float)cf.A[1];
+        s.Af[2] = (float)cf.A[3]; s.Af[3] = (float)cf.A[4];
+        s.Wo = a.normalize ? a.out_w : a.ddesc[img].width;
+        s.Ho = a.normalize ? a.out_h : a.ddesc[img].height;
+        s.m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, s.Wo, s.Ho);
+        s.tiles_x = (s.Wo + kTileW - 1) / kTileW;
+        *is = s;
+      }
       cur_img = img;
+      __syncthreads();
     }
     const alb_image_desc sd = a.sdesc[img];
     const int Ws = sd.width, Hs = sd.height;
-    const int tx0 = (unit.y % tiles_x) * kTile, ty0 = (unit.y / tiles_x) * kTile;
-    const int tw = min(kTile, Wo - tx0), th = min(kTile, Ho - ty0);
-    // warp-output rectangle of the tile
-    const int xwa = m.ax * tx0 + m.bx, xwb = m.ax * (tx0 + tw - 1) + m.bx;
-    const int ywa = m.ay * ty0 + m.by, ywb = m.ay * (ty0 + th - 1) + m.by;
-    const int xw0 = min(xwa, xwb), xw1 = max(xwa, xwb), yw0 = min(ywa, ywb), yw1 = max(ywa, ywb);
+    const int Wo = is->Wo, Ho = is->Ho;
+    const Map1 m = is->m;
+    const int tx0 = (unit.y % is->tiles_x) * kTileW, ty0 = (unit.y / is->tiles_x) * kTileH;
+    const int tw = min(kTileW, Wo - tx0), th = min(kTileH, Ho - ty0);
     if (threadIdx.x == 0) {
+      const int xwa = m.ax * tx0 + m.bx, xwb = m.ax * (tx0 + tw - 1) + m.bx;
+      const int ywa = m.ay * ty0 + m.by, ywb = m.ay * (ty0 + th - 1) + m.by;
+      const double xw0 = min(xwa, xwb), xw1 = max(xwa, xwb), yw0 = min(ywa, ywb), yw1 = max(ywa, ywb);
+      const double* A = is->A;
       double lx = 1e300, hx = -1e300, ly = 1e300, hy = -1e300;
       for (int c = 0; c < 4; ++c) {
         const double xw = (c & 1) ? xw1 : xw0, yw = (c & 2) ? yw1 : yw0;
-        const double sx = fma(cf.A[0], xw, fma(cf.A[1], yw, cf.A[2]));
-        const double sy = fma(cf.A[3], xw, fma(cf.A[4], yw, cf.A[5]));
+        const double sx = fma(A[0], xw, fma(A[1], yw, A[2]));
+        const double sy = fma(A[3], xw, fma(A[4], yw, A[5]));
         lx = fmin(lx, sx); hx = fmax(hx, sx); ly = fmin(ly, sy); hy = fmax(hy, sy);
       }
-      const int fx0 = (int)floor(lx) - 1, fx1 = (int)floor(hx) + 2;
-      const int fy0 = (int)floor(ly) - 1, fy1 = (int)floor(hy) + 2;
-      const int fw = fx1 - fx0 + 1, fh = fy1 - fy0 + 1;
-      // bank-friendly stride: lane step is +-(A0 + S*A3) words
-      const int want = fabs(cf.A[0] + cf.A[3]) >= fabs(cf.A[0] - cf.A[3]) ? 1 : 31;
-      int S = fw + ((want - fw % 32) + 32) % 32;
-      const int Sm = (fw + 3) & ~3;
-      const bool staged = (long long)S * fh <= a.unit_size && (long long)Sm * fh <= 4LL * a.unit_size / 4;
-      s_geom[0] = fx0; s_geom[1] = fy0; s_geom[2] = S; s_geom[3] = fw; s_geom[4] = fh;
-      s_geom[5] = staged ? 1 : 0; s_geom[6] = xw0 >> 4; s_geom[7] = yw0 >> 4; s_geom[8] = Sm;
-    }
-    if (threadIdx.x < kCells * kCells) {
-      const int cxa = (xw0 >> 4) + threadIdx.x % kCells, cya = (yw0 >> 4) + threadIdx.x / kCells;
-      const double xa = (double)(cxa * 16), ya = (double)(cya * 16);
-      const double sx = fma(cf.A[0], xa, fma(cf.A[1], ya, cf.A[2]));
-      const double sy = fma(cf.A[3], xa, fma(cf.A[4], ya, cf.A[5]));
-      const double fx = floor(sx), fy = floor(sy);
-      Anchor an;
-      an.ix = (int)fx; an.iy = (int)fy;
-      an.fx = (float)(sx - fx); an.fy = (float)(sy - fy);
-      anc[threadIdx.x] = an;
+      TileGeom t;
+      t.fx0 = (int)floor(lx) - 1;
+      t.fy0 = (int)floor(ly) - 1;
+      t.fw = (int)floor(hx) + 2 - t.fx0 + 1;
+      t.fh = (int)floor(hy) + 2 - t.fy0 + 1;
+      const int want = fabs(A[0] + A[3]) >= fabs(A[0] - A[3]) ? 1 : 31;  // lane step +-(A0 + S*A3)
+      t.S = t.fw + ((want - t.fw % 32) + 32) % 32;
+      t.Sm = (t.fw + 3) & ~3;
+      t.staged = (long long)t.S * t.fh <= a.unit_size &&
+                 (!has_mask || (long long)t.Sm * t.fh <= a.unit_size);
+      t.ci0 = min(max(-t.fx0, 0), t.fw);
+      t.ci1 = min(max(Ws - t.fx0, 0), t.fw);
+      *tg = t;
     }
     __syncthreads();
-    const int fx0 = s_geom[0], fy0 = s_geom[1], S = s_geom[2], fw = s_geom[3], fh = s_geom[4];
-    const bool staged = s_geom[5] != 0;
-    const int cx0 = s_geom[6], cy0 = s_geom[7], Sm = s_geom[8];
+    const TileGeom t = *tg;
     const uint8_t* simg = a.src + sd.offset;
-    const uint8_t* smk = has_mask ? a.msrc + a.msdesc[img].offset : nullptr;
-    const int mpitch = has_mask ? a.msdesc[img].pitch : 0;
-    if (staged) {
-      const int per_row = (fw + 15) / 16;
-      for (int it = threadIdx.x; it < fh * per_row; it += kAfThreads) {
-        const int r = it / per_row, c16 = (it % per_row) * 16;
-        const int sy = fy0 + r;
-        int ry = sy;
-        bool row_in = sy >= 0 && sy < Hs;
-        if (!row_in && reflect) { ry = reflect101(sy, Hs); row_in = true; }
-        const int sx0 = fx0 + c16;
-        uint32_t* d = stage + r * S + c16;
-        const uint8_t* srow = simg + (size_t)ry * sd.pitch;
-        if (row_in && sx0 >= 0 && sx0 + 16 <= Ws) {
-          uint32_t w[12];
-          load_window<12>(srow + (size_t)sx0 * 3, srow, srow + (size_t)Ws * 3, w);
+    if (t.staged) {
+      // pass A: 16-pixel interior runs with 16-byte loads
+      const int nvi = (t.ci1 - t.ci0) >> 4;
+      if (nvi > 0) {
+        const uint32_t magic = 0xffffffffu / (uint32_t)nvi + 1u;
+        for (int it = threadIdx.x; it < t.fh * nvi; it += kAfThreads) {
+          const int r = nvi == 1 ? it : (int)__umulhi((uint32_t)it, magic);
+          const int c = t.ci0 + ((it - r * nvi) << 4);
+          bool row_in;
+          const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+          uint32_t* d = stage + r * t.S + c;
+          if (row_in) {
+            const uint8_t* srow = simg + (size_t)ry * sd.pitch;
+            uint32_t w[12];
+            load_window<12>(srow + (size_t)(t.fx0 + c) * 3, srow, srow + (size_t)Ws * 3, w);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c16 + i < fw) d[i] = rgbx_of(w, i);
-        } else {
-          for (int i = 0; i < 16 && c16 + i < fw; ++i) {
-            const int sx = sx0 + i;
-            uint32_t v = a.fill;
-            if (row_in) {
-              if (sx >= 0 && sx < Ws) v = fetch_rgb(srow, sx);
-              else if (reflect) v = fetch_rgb(srow, reflect101(sx, Ws));
-            }
-            d[i] = v;
+            for (int i = 0; i < 16; ++i) d[i] = rgbx_of(w, i);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) d[i] = a.fill;
           }
         }
-        if (has_mask) {
-          const uint8_t* mrow = smk + (size_t)ry * mpitch;
-          uint8_t* md = mstage + r * Sm + c16;
-          for (int i = 0; i < 16 && c16 + i < fw; ++i) {
-            const int sx = sx0 + i;
-            uint8_t v = (uint8_t)a.mask_fill;
-            if (row_in) {
-              if (sx >= 0 && sx < Ws) v = mrow[sx];
-              else if (reflect) v = mrow[reflect101(sx, Ws)];
-            }
-            md[i] = v;
-          }
+      }
+      // pass B: border columns + the interior tail, one pixel per thread
+      const int tail = (t.ci1 - t.ci0) & 15;
+      const int P = t.ci0 + tail + (t.fw - t.ci1);
+      if (P > 0) {
+        const uint32_t magic = 0xffffffffu / (uint32_t)P + 1u;
+        for (int it = threadIdx.x; it < t.fh * P; it += kAfThreads) {
+          const int r = P == 1 ? it : (int)__umulhi((uint32_t)it, magic);
+          const int j = it - r * P;
+          const int c = j < t.ci0 ? j : (j < t.ci0 + tail ? t.ci0 + 16 * nvi + (j - t.ci0)
+                                                          : t.ci1 + (j - t.ci0 - tail));
+          bool row_in, col_in;
+          const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+          const int rx = border_idx(t.fx0 + c, Ws, reflect, col_in);
+          stage[r * t.S + c] = (row_in && col_in) ? fetch_rgb(simg + (size_t)ry * sd.pitch, rx) : a.fill;
+        }
+      }
+      if (has_mask) {
+        const uint8_t* smk = a.msrc + a.msdesc[img].offset;
+        const int mpitch = a.msdesc[img].pitch;
+        const uint32_t magic = 0xffffffffu / (uint32_t)t.fw + 1u;
+        for (int it = threadIdx.x; it < t.fh * t.fw; it += kAfThreads) {
+          const int r = t.fw == 1 ? it : (int)__umulhi((uint32_t)it, magic);
+          const int c = it - r * t.fw;
+          bool row_in, col_in;
+          const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+          const int rx = border_idx(t.fx0 + c, Ws, reflect, col_in);
+          mstage[r * t.Sm + c] = (row_in && col_in) ? smk[(size_t)ry * mpitch + rx] : (uint8_t)a.mask_fill;
         }
       }
       __syncthreads();
     }
-    // ---- compute: warp w handles (row, 32-px segment) pairs
-    const int nseg = (tw + 31) / 32;
-    const float A0f = (float)cf.A[0], A1f = (float)cf.A[1], A3f = (float)cf.A[3], A4f = (float)cf.A[4];
-    for (int rs = warp; rs < th * nseg; rs += kAfThreads / 32) {
-      const int row = rs / nseg, seg = rs % nseg;
-      const int yo = ty0 + row;
-      const int xo = tx0 + seg * 32 + lane;
-      const int nvalid = min(32, tw - seg * 32);
-      const bool act = lane < nvalid;
-      const int xw = m.ax * min(xo, Wo - 1) + m.bx, yw = m.ay * yo + m.by;
-      const Anchor an = anc[((xw >> 4) - cx0) + kCells * ((yw >> 4) - cy0)];
-      const float dxl = (float)(xw & 15), dyl = (float)(yw & 15);
-      const float lx = fmaf(A0f, dxl, fmaf(A1f, dyl, an.fx));
-      const float ly = fmaf(A3f, dxl, fmaf(A4f, dyl, an.fy));
-      uint32_t r, g, b;
-      if (nearest) {
-        const int tx = an.ix + (int)floorf(lx + 0.5f), ty = an.iy + (int)floorf(ly + 0.5f);
-        uint32_t t;
-        if (staged) {
-          t = stage[(ty - fy0) * S + (tx - fx0)];
-        } else if (tx >= 0 && tx < Ws && ty >= 0 && ty < Hs) {
-          t = fetch_rgb(simg + (size_t)ty * sd.pitch, tx);
-        } else if (reflect) {
-          t = fetch_rgb(simg + (size_t)reflect101(ty, Hs) * sd.pitch, reflect101(tx, Ws));
-        } else {
-          t = a.fill;
-        }
-        r = t & 0xff; g = (t >> 8) & 0xff; b = (t >> 16) & 0xff;
-      } else {
-        const float flx = floorf(lx), fly = floorf(ly);
-        const float fx = lx - flx, fy = ly - fly;
-        const int tx = an.ix + (int)flx, ty = an.iy + (int)fly;
-        uint32_t t00, t10, t01, t11;
-        if (staged) {
-          const uint32_t* p = stage + (ty - fy0) * S + (tx - fx0);
-          t00 = p[0]; t10 = p[1]; t01 = p[S]; t11 = p[S + 1];
-        } else {
-          auto tap = [&](int qx, int qy) -> uint32_t {
-            if (qx >= 0 && qx < Ws && qy >= 0 && qy < Hs) return fetch_rgb(simg + (size_t)qy * sd.pitch, qx);
-            if (!reflect) return a.fill;
-            return fetch_rgb(simg + (size_t)reflect101(qy, Hs) * sd.pitch, reflect101(qx, Ws));
-          };
-          t00 = tap(tx, ty); t10 = tap(tx + 1, ty); t01 = tap(tx, ty + 1); t11 = tap(tx + 1, ty + 1);
-        }
-        uint32_t ch[3];
+    // ---- compute: warp owns kRowsPerWarp rows; lane = columns lane, lane + 32
+    const float A0f = is->Af[0], A1f = is->Af[1], A3f = is->Af[2], A4f = is->Af[3];
+    const double* A = is->A;
+    uint8_t* dbase = nullptr;
+    int dpitch = 0;
+    if (!a.normalize) {
+      const alb_image_desc dd = a.ddesc[img];
+      dbase = a.dst + dd.offset;
+      dpitch = dd.pitch;
+    }
+    int xw[2];
+    float dxl[2];
+    int cur_cy[2] = {-0x7fffffff, -0x7fffffff};
+    int aix[2] = {0, 0}, aiy[2] = {0, 0};
+    float afx[2] = {0.f, 0.f}, afy[2] = {0.f, 0.f};
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const float p00 = (float)((t00 >> (8 * c)) & 0xff), p10 = (float)((t10 >> (8 * c)) & 0xff);
-          const float p01 = (float)((t01 >> (8 * c)) & 0xff), p11 = (float)((t11 >> (8 * c)) & 0xff);
-          const float h0 = fmaf(fx, p10 - p00, p00);
-          const float h1 = fmaf(fx, p11 - p01, p01);
-          const float v = fmaf(fy, h1 - h0, h0);
-          ch[c] = (uint32_t)(v + 0.5f);
+    for (int j = 0; j < 2; ++j) {
+      xw[j] = m.ax * min(tx0 + lane + 32 * j, Wo - 1) + m.bx;
+      dxl[j] = (float)(xw[j] & 15);
+    }
+    for (int i = 0; i < kRowsPerWarp; ++i) {
+      const int row = warp * kRowsPerWarp + i;
+      if (row >= th) break;
+      const int yo = ty0 + row;
+      const int yw = m.ay * yo + m.by;
+      const float dyl = (float)(yw & 15);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = lane + 32 * j;
+        if (c >= tw) continue;
+        if ((yw >> 4) != cur_cy[j]) {  // fp64 anchor of this column's 16x16 cell
+          cur_cy[j] = yw >> 4;
+          const double xa = (double)((xw[j] >> 4) * 16), ya = (double)(cur_cy[j] * 16);
+          const double sx = fma(A[0], xa, fma(A[1], ya, A[2]));
+          const double sy = fma(A[3], xa, fma(A[4], ya, A[5]));
+          const double flx = floor(sx), fly = floor(sy);
+          aix[j] = (int)flx; aiy[j] = (int)fly;
+          afx[j] = (float)(sx - flx); afy[j] = (float)(sy - fly);
         }
-        r = ch[0]; g = ch[1]; b = ch[2];
-      }
-      apply_stages(x, sm, lane, r, g, b);
-      if (a.normalize) {
-        if (act) {
-          const size_t plane = (size_t)Ho * Wo;
-          float* o = a.nchw + (size_t)img * 3 * plane + (size_t)yo * Wo + xo;
-          const float* nl = a.tab.norm_lut;
-          o[0] = nl[r]; o[plane] = nl[256 + g]; o[2 * plane] = nl[512 + b];
-        }
-      } else {
-        const alb_image_desc dd = a.ddesc[img];
-        uint8_t* drow = a.dst + dd.offset + (size_t)yo * dd.pitch + (size_t)(tx0 + seg * 32) * 3;
-        warp_store_rgb(drow, nvalid, r | (g << 8) | (b << 16), lane);
-      }
-      if (has_mask) {
-        const int tx = an.ix + (int)floorf(lx + 0.5f), ty = an.iy + (int)floorf(ly + 0.5f);
-        uint8_t v;
-        if (staged) {
-          v = mstage[(ty - fy0) * Sm + (tx - fx0)];
-        } else if (tx >= 0 && tx < Ws && ty >= 0 && ty < Hs) {
-          v = smk[(size_t)ty * mpitch + tx];
-        } else if (reflect) {
-          v = smk[(size_t)reflect101(ty, Hs) * mpitch + reflect101(tx, Ws)];
+        const float lx = fmaf(A0f, dxl[j], fmaf(A1f, dyl, afx[j]));
+        const float ly = fmaf(A3f, dxl[j], fmaf(A4f, dyl, afy[j]));
+        uint32_t r, g, b;
+        if (nearest) {
+          const int qx = aix[j] + (int)floorf(lx + 0.5f), qy = aiy[j] + (int)floorf(ly + 0.5f);
+          uint32_t tt;
+          if (t.staged) {
+            tt = stage[(qy - t.fy0) * t.S + (qx - t.fx0)];
+          } else {
+            bool ri, ci;
+            const int yy = border_idx(qy, Hs, reflect, ri), xx = border_idx(qx, Ws, reflect, ci);
+            tt = (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
+          }
+          r = tt & 0xff; g = (tt >> 8) & 0xff; b = (tt >> 16) & 0xff;
         } else {
-          v = (uint8_t)a.mask_fill;
+          const float flx = floorf(lx), fly = floorf(ly);
+          const float fx = lx - flx, fy = ly - fly;
+          const int qx = aix[j] + (int)flx, qy = aiy[j] + (int)fly;
+          uint32_t t00, t10, t01, t11;
+          if (t.staged) {
+            const uint32_t* p = stage + (qy - t.fy0) * t.S + (qx - t.fx0);
+            t00 = p[0]; t10 = p[1]; t01 = p[t.S]; t11 = p[t.S + 1];
+          } else {
+            auto tap = [&](int px, int py) -> uint32_t {
+              bool ri, ci;
+              const int yy = border_idx(py, Hs, reflect, ri), xx = border_idx(px, Ws, reflect, ci);
+              return (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
+            };
+            t00 = tap(qx, qy); t10 = tap(qx + 1, qy); t01 = tap(qx, qy + 1); t11 = tap(qx + 1, qy + 1);
+          }
+          uint32_t ch[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const float a00 = (float)((t00 >> (8 * k)) & 0xff), a10 = (float)((t10 >> (8 * k)) & 0xff);
+            const float a01 = (float)((t01 >> (8 * k)) & 0xff), a11 = (float)((t11 >> (8 * k)) & 0xff);
+            const float h0 = fmaf(fx, a10 - a00, a00);
+            const float h1 = fmaf(fx, a11 - a01, a01);
+            ch[k] = (uint32_t)(fmaf(fy, h1 - h0, h0) + 0.5f);
+          }
+          r = ch[0]; g = ch[1]; b = ch[2];
         }
-        if (act) {
+        apply_stages_t<kOne>(x, sm, lane, r, g, b);
+        if (a.normalize) {
+          const size_t plane = (size_t)Ho * Wo;
+          float* o = a.nchw + (size_t)img * 3 * plane + (size_t)yo * Wo + tx0 + c;
+          const float* nl = a.tab.norm_lut;
+          __stcs(o, nl[r]);
+          __stcs(o + plane, nl[256 + g]);
+          __stcs(o + 2 * plane, nl[512 + b]);
+        } else {
+          rowbuf[3 * c] = (uint8_t)r;
+          rowbuf[3 * c + 1] = (uint8_t)g;
+          rowbuf[3 * c + 2] = (uint8_t)b;
+        }
+        if (has_mask) {
+          const int qx = aix[j] + (int)floorf(lx + 0.5f), qy = aiy[j] + (int)floorf(ly + 0.5f);
+          uint8_t v;
+          if (t.staged) {
+            v = mstage[(qy - t.fy0) * t.Sm + (qx - t.fx0)];
+          } else {
+            bool ri, ci;
+            const int yy = border_idx(qy, Hs, reflect, ri), xx = border_idx(qx, Ws, reflect, ci);
+            v = (ri && ci) ? a.msrc[a.msdesc[img].offset + (size_t)yy * a.msdesc[img].pitch + xx]
+                           : (uint8_t)a.mask_fill;
+          }
           const alb_image_desc mdd = a.mddesc[img];
-          a.mdst[mdd.offset + (size_t)yo * mdd.pitch + xo] = v;
+          a.mdst[mdd.offset + (size_t)yo * mdd.pitch + tx0 + c] = v;
         }
+      }
+      if (!a.normalize) {
+        __syncwarp();
+        warp_copy_row(dbase + (size_t)yo * dpitch + (size_t)tx0 * 3, rowbuf, 3 * tw, lane);
+        __syncwarp();
       }
     }
   }
 }
 
-size_t affine_smem(const StepArgs& a) {
-  return (size_t)count_lut_stages(a) * kLutWords * 4 + sizeof(Anchor) * kCells * kCells + 64 +
-         (size_t)a.unit_size * 4 + (size_t)a.unit_size;
+static size_t affine_smem(const StepArgs& a) {
+  return (size_t)count_lut_stages(a) * kLutWords * 4 + sizeof(ImgState) + sizeof(TileGeom) +
+         kAfWarps * (kTileW * 3 + 32) + (size_t)a.unit_size * 4 +
+         (a.mdst ? (size_t)a.unit_size : 0);
+}
+
+template <int kOne>
+static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
+  cudaFuncSetAttribute(k_affine<kOne>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1, sms = 148, dev = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_affine<kOne>, kAfThreads, smem);
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(a.n_units, sms * std::max(occ, 1));
+  k_affine<kOne><<<grid, kAfThreads, smem, s>>>(a);
 }
 
 void launch_affine(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
   const size_t smem = affine_smem(a);
-  cudaFuncSetAttribute(k_affine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1, sms = 148, dev = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_affine, kAfThreads, smem);
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(a.n_units, sms * std::max(occ, 1));
-  k_affine<<<grid, kAfThreads, smem, s>>>(a);
+  const int mode = stage_mode(a);
+  ALB_DISPATCH_STAGES(mode, launch_affine_t, a, smem, s)
 }
 
 }  // namespace alb

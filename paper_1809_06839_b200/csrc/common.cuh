@@ -112,54 +112,42 @@ __device__ __forceinline__ bool fired_of(const Tables& t, int img, int slot) {
 
 // ---------------------------------------------------------------- HSV (fp32)
 // hexcone RGB->HSV, shift (h mod 360, s/v clamped), HSV->RGB, round half up.
-__device__ __forceinline__ void hsv_shift_px(float dh, float ds, float dv, uint32_t& r,
+// Branch-free (no lane divergence): hue in sixths h6 in [0,6) selected by the
+// dominant channel (ties r > g > b), and the hexcone inverse written as
+//   channel(n) = v - v*s*clamp(min(k, 4-k), 0, 1),  k = (n + h6) mod 6,
+// n = 5, 3, 1 for R, G, B -- algebraically the sector table of SPEC.md:419.
+// dh6 = dh/60 (hue shift in sixths).
+__device__ __forceinline__ void hsv_shift_px(float dh6, float ds, float dv, uint32_t& r,
                                              uint32_t& g, uint32_t& b) {
   const float fr = (float)r, fg = (float)g, fb = (float)b;
   const float mx = fmaxf(fr, fmaxf(fg, fb));
   const float mn = fminf(fr, fminf(fg, fb));
   const float d = mx - mn;
-  float h;
-  if (d == 0.f) {
-    h = 0.f;
-  } else {
-    const float inv = __frcp_rn(d);
-    if (mx == fr) {
-      h = (fg - fb) * inv;
-      if (h < 0.f) h += 6.f;
-    } else if (mx == fg) {
-      h = (fb - fr) * inv + 2.f;
-    } else {
-      h = (fr - fg) * inv + 4.f;
-    }
-    h *= 60.f;
-  }
-  float s = mx > 0.f ? d / mx : 0.f;
-  float v = mx * (1.f / 255.f);
-  h = h + dh;
-  h = h - 360.f * floorf(h * (1.f / 360.f));
-  if (h >= 360.f) h -= 360.f;
-  if (h < 0.f) h = 0.f;
-  s = fminf(fmaxf(s + ds, 0.f), 1.f);
-  v = fminf(fmaxf(v + dv, 0.f), 1.f);
-  const float C = v * s;
-  const float hp = h * (1.f / 60.f);
-  const float m2 = hp - 2.f * floorf(hp * 0.5f);
-  const float X = C * (1.f - fabsf(m2 - 1.f));
-  const float m = v - C;
-  int sec = (int)floorf(hp);
-  sec = sec >= 6 ? sec - 6 : sec;
-  float r1, g1, b1;
-  switch (sec) {
-    case 0: r1 = C; g1 = X; b1 = 0.f; break;
-    case 1: r1 = X; g1 = C; b1 = 0.f; break;
-    case 2: r1 = 0.f; g1 = C; b1 = X; break;
-    case 3: r1 = 0.f; g1 = X; b1 = C; break;
-    case 4: r1 = X; g1 = 0.f; b1 = C; break;
-    default: r1 = C; g1 = 0.f; b1 = X; break;
-  }
-  r = (uint32_t)min(255, max(0, (int)floorf(255.f * (r1 + m) + 0.5f)));
-  g = (uint32_t)min(255, max(0, (int)floorf(255.f * (g1 + m) + 0.5f)));
-  b = (uint32_t)min(255, max(0, (int)floorf(255.f * (b1 + m) + 0.5f)));
+  const bool isr = mx == fr;
+  const bool isg = !isr && mx == fg;
+  const float num = isr ? fg - fb : (isg ? fb - fr : fr - fg);
+  const float off = isr ? 0.f : (isg ? 2.f : 4.f);
+  float h6 = d > 0.f ? __fdividef(num, d) + off : 0.f;
+  h6 = h6 < 0.f ? h6 + 6.f : h6;
+  h6 += dh6;
+  h6 -= 6.f * floorf(h6 * (1.f / 6.f));
+  h6 = h6 >= 6.f ? h6 - 6.f : h6;
+  h6 = fmaxf(h6, 0.f);
+  const float s = __saturatef((mx > 0.f ? __fdividef(d, mx) : 0.f) + ds);
+  const float v = __saturatef(fmaf(mx, 1.f / 255.f, dv));
+  const float vs = v * s;
+  float k = h6 + 5.f;
+  k = k >= 6.f ? k - 6.f : k;
+  const float tr = __saturatef(fminf(k, 4.f - k));
+  k = h6 + 3.f;
+  k = k >= 6.f ? k - 6.f : k;
+  const float tg = __saturatef(fminf(k, 4.f - k));
+  k = h6 + 1.f;
+  k = k >= 6.f ? k - 6.f : k;
+  const float tb = __saturatef(fminf(k, 4.f - k));
+  r = (uint32_t)fmaf(255.f, fmaf(-vs, tr, v), 0.5f);
+  g = (uint32_t)fmaf(255.f, fmaf(-vs, tg, v), 0.5f);
+  b = (uint32_t)fmaf(255.f, fmaf(-vs, tb, v), 0.5f);
 }
 
 // exact BT.601 luma (299R + 587G + 114B + 500) / 1000

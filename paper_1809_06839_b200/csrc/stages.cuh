@@ -65,7 +65,7 @@ __device__ __forceinline__ void load_stages(const StepArgs& a, int img, uint32_t
       x.on[s] = fired_of(a.tab, img, a.stages[s].slot) ? 1 : 0;
       if (t == ST_HSV) {
         const double* q = prm_of(a.tab, img, a.stages[s].slot);
-        x.dh[s] = (float)q[0];
+        x.dh[s] = (float)(q[0] / 60.0);  // hue shift in sixths of a turn
         x.ds[s] = (float)q[1];
         x.dv[s] = (float)q[2];
       }
@@ -93,6 +93,48 @@ __device__ __forceinline__ void apply_stages(const StageCtx& x, const uint32_t* 
     }
   }
 }
+
+// Compile-time stage program: kOne = -2 no stages, -1 generic chain, or the
+// type of the single stage (its LUT, if any, sits at shared word 0).
+constexpr int kStagesNone = -2, kStagesGeneric = -1;
+
+template <int kOne>
+__device__ __forceinline__ void apply_stages_t(const StageCtx& x, const uint32_t* sm, int lane,
+                                               uint32_t& r, uint32_t& g, uint32_t& b) {
+  if constexpr (kOne == kStagesNone) {
+    return;
+  } else if constexpr (kOne == ST_LUT || kOne == ST_EQ) {
+    r = lut_look(sm, 0, r, lane);
+    g = lut_look(sm, 2048, g, lane);
+    b = lut_look(sm, 4096, b, lane);
+  } else if constexpr (kOne == ST_HSV) {
+    if (x.on[0]) hsv_shift_px(x.dh[0], x.ds[0], x.dv[0], r, g, b);
+  } else if constexpr (kOne == ST_GRAY) {
+    if (x.on[0]) {
+      const uint32_t y = gray_px(r, g, b);
+      r = g = b = y;
+    }
+  } else {
+    apply_stages(x, sm, lane, r, g, b);
+  }
+}
+
+inline int stage_mode(const StepArgs& a) {
+  if (a.n_stages == 0) return kStagesNone;
+  if (a.n_stages == 1) return a.stages[0].type;
+  return kStagesGeneric;
+}
+
+// Launch helper: instantiate kernel template K<mode> for the step's stage program.
+#define ALB_DISPATCH_STAGES(mode, KERNEL, ...)                 \
+  switch (mode) {                                               \
+    case kStagesNone: KERNEL<kStagesNone>(__VA_ARGS__); break;  \
+    case ST_LUT: KERNEL<ST_LUT>(__VA_ARGS__); break;            \
+    case ST_EQ: KERNEL<ST_EQ>(__VA_ARGS__); break;              \
+    case ST_HSV: KERNEL<ST_HSV>(__VA_ARGS__); break;            \
+    case ST_GRAY: KERNEL<ST_GRAY>(__VA_ARGS__); break;          \
+    default: KERNEL<kStagesGeneric>(__VA_ARGS__); break;        \
+  }
 
 // Store one 16-pixel output block of a u8 row: vector stores when the block is
 // fully inside [0, W) (the caller guarantees the block start is 16-byte
@@ -171,6 +213,39 @@ __device__ __forceinline__ void warp_store_rgb(uint8_t* base, int nvalid, uint32
     }
   }
   // words beyond lane 31 (segment of 32 px spans up to 25 words: never)
+}
+
+// Warp-cooperative copy of n bytes from a 16-byte-aligned shared buffer to a
+// global address of any alignment: 16-byte aligned STG.128 for the body
+// (source realigned from two LDS.128 with a funnel shift), byte stores for the
+// unaligned head/tail.  Caller brackets with __syncwarp().
+__device__ __forceinline__ void warp_copy_row(uint8_t* dst, const uint8_t* src, int n, int lane) {
+  const int head = min(n, (int)((16 - ((uintptr_t)dst & 15)) & 15));
+  if (lane < head) dst[lane] = src[lane];
+  const int nb = (n - head) >> 4;
+  const int sh = head & 15;  // source misalignment of every body block
+  const int qw = sh >> 2, kb = (sh & 3) * 8;
+  for (int k = lane; k < nb; k += 32) {
+    const int so = head + 16 * k;
+    const uint4* p = reinterpret_cast<const uint4*>(src + (so & ~15));
+    const uint4 v0 = p[0];
+    uint4 v1 = make_uint4(0, 0, 0, 0);
+    if (sh) v1 = p[1];
+    const uint32_t r[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t t1[7], w[5];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) t1[i] = (qw & 1) ? r[i + 1] : r[i];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) w[i] = (qw & 2) ? t1[i + 2] : t1[i];
+    uint4 o;
+    o.x = __funnelshift_r(w[0], w[1], kb);
+    o.y = __funnelshift_r(w[1], w[2], kb);
+    o.z = __funnelshift_r(w[2], w[3], kb);
+    o.w = __funnelshift_r(w[3], w[4], kb);
+    __stcs(reinterpret_cast<uint4*>(dst + so), o);
+  }
+  const int t0 = head + 16 * nb;
+  for (int b = t0 + lane; b < n; b += 32) dst[b] = src[b];
 }
 
 // Pixel i (0..15) of a 48-byte window as an RGBx word (one byte permute).
