@@ -30,6 +30,7 @@ constexpr int kAfThreads = 256;
 constexpr int kAfWarps = kAfThreads / 32;
 constexpr int kTileW = 64, kTileH = 32;
 constexpr int kRowsPerWarp = kTileH / kAfWarps;
+constexpr int kTilePitch = kTileW * 3 + 16;  // output tile row pitch in shared memory (16-aligned)
 
 struct AfCoef {
   double A[6];
@@ -91,7 +92,9 @@ struct ImgState {
   int Wo, Ho, tiles_x, pad;
 };
 
-template <int kOne>
+// kGeneric = false: bilinear, no mask, u8 output (the single-op and cfg5-image
+// fast path) -- the uniform mode branches compile away.
+template <int kOne, bool kGeneric>
 __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -99,13 +102,13 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
   init_stages(a, x);
   ImgState* is = reinterpret_cast<ImgState*>(sm + x.n_lut * kLutWords);
   TileGeom* tg = reinterpret_cast<TileGeom*>(is + 1);
-  uint8_t* rowbuf = reinterpret_cast<uint8_t*>(tg + 1) + warp * (kTileW * 3 + 32);
-  uint32_t* stage = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tg + 1) +
-                                                kAfWarps * (kTileW * 3 + 32));
+  uint8_t* tilebuf = reinterpret_cast<uint8_t*>(tg + 1);  // output tile, RGB bytes
+  uint32_t* stage = reinterpret_cast<uint32_t*>(tilebuf + kTileH * kTilePitch + 16);
   uint8_t* mstage = reinterpret_cast<uint8_t*>(stage + a.unit_size);
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
-  const bool nearest = a.interp == ALB_INTERP_NEAREST;
-  const bool has_mask = a.mdst != nullptr;
+  const bool nearest = kGeneric && a.interp == ALB_INTERP_NEAREST;
+  const bool has_mask = kGeneric && a.mdst != nullptr;
+  const bool normalize = kGeneric && a.normalize;
 
   int u0, u1;
   unit_range(a.n_units, u0, u1);
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
     const double* A = is->A;
     uint8_t* dbase = nullptr;
     int dpitch = 0;
-    if (!a.normalize) {
+    if (!normalize) {
       const alb_image_desc dd = a.ddesc[img];
       dbase = a.dst + dd.offset;
       dpitch = dd.pitch;
@@ -289,19 +292,11 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
             };
             t00 = tap(qx, qy); t10 = tap(qx + 1, qy); t01 = tap(qx, qy + 1); t11 = tap(qx + 1, qy + 1);
           }
-          uint32_t ch[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const float a00 = (float)((t00 >> (8 * k)) & 0xff), a10 = (float)((t10 >> (8 * k)) & 0xff);
-            const float a01 = (float)((t01 >> (8 * k)) & 0xff), a11 = (float)((t11 >> (8 * k)) & 0xff);
-            const float h0 = fmaf(fx, a10 - a00, a00);
-            const float h1 = fmaf(fx, a11 - a01, a01);
-            ch[k] = (uint32_t)(fmaf(fy, h1 - h0, h0) + 0.5f);
-          }
-          r = ch[0]; g = ch[1]; b = ch[2];
+          const uint32_t px = bilerp_rgbx(t00, t10, t01, t11, fx, fy);
+          r = px & 0xff; g = (px >> 8) & 0xff; b = (px >> 16) & 0xff;
         }
         apply_stages_t<kOne>(x, sm, lane, r, g, b);
-        if (a.normalize) {
+        if (normalize) {
           const size_t plane = (size_t)Ho * Wo;
           float* o = a.nchw + (size_t)img * 3 * plane + (size_t)yo * Wo + tx0 + c;
           const float* nl = a.tab.norm_lut;
@@ -309,9 +304,10 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
           __stcs(o + plane, nl[256 + g]);
           __stcs(o + 2 * plane, nl[512 + b]);
         } else {
-          rowbuf[3 * c] = (uint8_t)r;
-          rowbuf[3 * c + 1] = (uint8_t)g;
-          rowbuf[3 * c + 2] = (uint8_t)b;
+          uint8_t* tb = tilebuf + row * kTilePitch + 3 * c;
+          tb[0] = (uint8_t)r;
+          tb[1] = (uint8_t)g;
+          tb[2] = (uint8_t)b;
         }
         if (has_mask) {
           const int qx = aix[j] + (int)floorf(lx + 0.5f), qy = aiy[j] + (int)floorf(ly + 0.5f);
@@ -328,29 +324,36 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
           a.mdst[mdd.offset + (size_t)yo * mdd.pitch + tx0 + c] = v;
         }
       }
-      if (!a.normalize) {
-        __syncwarp();
-        warp_copy_row(dbase + (size_t)yo * dpitch + (size_t)tx0 * 3, rowbuf, 3 * tw, lane);
-        __syncwarp();
-      }
+    }
+    if (!normalize) {  // the whole tile, aligned 16-byte stores
+      __syncthreads();
+      cta_copy_rows(dbase + (size_t)ty0 * dpitch + (size_t)tx0 * 3, dpitch, tilebuf, kTilePitch, th,
+                    3 * tw, kAfThreads);
     }
   }
 }
 
 static size_t affine_smem(const StepArgs& a) {
   return (size_t)count_lut_stages(a) * kLutWords * 4 + sizeof(ImgState) + sizeof(TileGeom) +
-         kAfWarps * (kTileW * 3 + 32) + (size_t)a.unit_size * 4 +
+         kTileH * kTilePitch + 16 + (size_t)a.unit_size * 4 +
          (a.mdst ? (size_t)a.unit_size : 0);
+}
+
+template <int kOne, bool kGeneric>
+static void launch_affine_v(const StepArgs& a, size_t smem, cudaStream_t s) {
+  cudaFuncSetAttribute(k_affine<kOne, kGeneric>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1, sms = 148, dev = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_affine<kOne, kGeneric>, kAfThreads, smem);
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(a.n_units, sms * std::max(occ, 1));
+  k_affine<kOne, kGeneric><<<grid, kAfThreads, smem, s>>>(a);
 }
 
 template <int kOne>
 static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
-  cudaFuncSetAttribute(k_affine<kOne>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1, sms = 148, dev = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_affine<kOne>, kAfThreads, smem);
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(a.n_units, sms * std::max(occ, 1));
-  k_affine<kOne><<<grid, kAfThreads, smem, s>>>(a);
+  const bool generic = a.interp == ALB_INTERP_NEAREST || a.mdst != nullptr || a.normalize;
+  if (generic) launch_affine_v<kOne, true>(a, smem, s);
+  else launch_affine_v<kOne, false>(a, smem, s);
 }
 
 void launch_affine(const StepArgs& a, cudaStream_t s) {

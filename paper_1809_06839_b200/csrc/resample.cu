@@ -197,16 +197,8 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
               t01 = q1[3 * x0] | (q1[3 * x0 + 1] << 8) | (q1[3 * x0 + 2] << 16);
               t11 = q1[3 * x1] | (q1[3 * x1 + 1] << 8) | (q1[3 * x1 + 2] << 16);
             }
-            uint32_t ch[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              const float a00 = (float)((t00 >> (8 * k)) & 0xff), a10 = (float)((t10 >> (8 * k)) & 0xff);
-              const float a01 = (float)((t01 >> (8 * k)) & 0xff), a11 = (float)((t11 >> (8 * k)) & 0xff);
-              const float h0 = fmaf(ce.fx, a10 - a00, a00);
-              const float h1 = fmaf(ce.fx, a11 - a01, a01);
-              ch[k] = (uint32_t)(fmaf(fy, h1 - h0, h0) + 0.5f);
-            }
-            r = ch[0]; gg = ch[1]; b = ch[2];
+            const uint32_t px = bilerp_rgbx(t00, t10, t01, t11, ce.fx, fy);
+            r = px & 0xff; gg = (px >> 8) & 0xff; b = (px >> 16) & 0xff;
           }
           apply_stages_t<kOne>(x, sm, lane, r, gg, b);
           if (a.normalize) {

@@ -248,6 +248,77 @@ __device__ __forceinline__ void warp_copy_row(uint8_t* dst, const uint8_t* src, 
   for (int b = t0 + lane; b < n; b += 32) dst[b] = src[b];
 }
 
+// CTA-cooperative copy of `rows` rows of n bytes from shared memory (row
+// pitch spitch, 16-byte aligned) to global rows of any alignment: per row one
+// item per aligned 16-byte block plus one item each for the unaligned head
+// and tail bytes.
+__device__ __forceinline__ void cta_copy_rows(uint8_t* dst0, int dpitch, const uint8_t* src0,
+                                              int spitch, int rows, int n, int nthreads) {
+  const int npr = (n >> 4) + 2;
+  const uint32_t magic = 0xffffffffu / (uint32_t)npr + 1u;
+  for (int it = threadIdx.x; it < rows * npr; it += nthreads) {
+    const int r = (int)__umulhi((uint32_t)it, magic);
+    const int k = it - r * npr;
+    uint8_t* dst = dst0 + (size_t)r * dpitch;
+    const uint8_t* src = src0 + r * spitch;
+    const int head = min(n, (int)((16 - ((uintptr_t)dst & 15)) & 15));
+    const int nb = (n - head) >> 4;
+    if (k < nb) {
+      const int so = head + 16 * k;
+      const int sh = head & 15, qw = sh >> 2, kb = (sh & 3) * 8;
+      const uint4* p = reinterpret_cast<const uint4*>(src + (so & ~15));
+      const uint4 v0 = p[0];
+      const uint4 v1 = sh ? p[1] : make_uint4(0, 0, 0, 0);
+      const uint32_t q[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      uint32_t t1[7], w[5];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) t1[i] = (qw & 1) ? q[i + 1] : q[i];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) w[i] = (qw & 2) ? t1[i + 2] : t1[i];
+      __stcs(reinterpret_cast<uint4*>(dst + so),
+             make_uint4(__funnelshift_r(w[0], w[1], kb), __funnelshift_r(w[1], w[2], kb),
+                        __funnelshift_r(w[2], w[3], kb), __funnelshift_r(w[3], w[4], kb)));
+    } else if (k == nb) {
+      for (int b = 0; b < head; ++b) dst[b] = src[b];
+    } else if (k == nb + 1) {
+      for (int b = head + 16 * nb; b < n; ++b) dst[b] = src[b];
+    }
+  }
+}
+
+// Bilinear blend of 4 RGBx taps (O5/O7 weights), fp32, same
+// operation sequence per channel as the scalar form
+//   h0 = fma(fx, p10 - p00, p00); h1 = fma(fx, p11 - p01, p01);
+//   v  = fma(fy, h1 - h0, h0);   out = floor(v + 0.5)
+// Bytes become floats exactly via the 2^23 magic (byte permute + one add),
+// channel pairs run on the paired fp32 pipe (FFMA2/FADD2, sm_100), and the
+// rounded result is read back from the mantissa of floor-rounded (v+0.5)+2^23.
+__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
+
+__device__ __forceinline__ uint32_t bilerp_rgbx(uint32_t t00, uint32_t t10, uint32_t t01,
+                                                uint32_t t11, float fx, float fy) {
+  constexpr uint32_t kM = 0x4B000000u;  // 2^23
+  const float M = 8388608.f;
+  auto f = [](uint32_t t, uint32_t c) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | c)); };
+  // biased (2^23 + byte) values
+  const float2 P00 = mk2(f(t00, 0), f(t00, 1)), P10 = mk2(f(t10, 0), f(t10, 1));
+  const float2 P01 = mk2(f(t01, 0), f(t01, 1)), P11 = mk2(f(t11, 0), f(t11, 1));
+  const float2 B0 = mk2(f(t00, 2), f(t01, 2)), B1 = mk2(f(t10, 2), f(t11, 2));
+  const float2 nM = mk2(-M, -M);
+  const float2 fx2 = mk2(fx, fx);
+  const float2 H0 = __ffma2_rn(fx2, __fadd2_rn(P10, mk2(-P00.x, -P00.y)), __fadd2_rn(P00, nM));
+  const float2 H1 = __ffma2_rn(fx2, __fadd2_rn(P11, mk2(-P01.x, -P01.y)), __fadd2_rn(P01, nM));
+  const float2 HB = __ffma2_rn(fx2, __fadd2_rn(B1, mk2(-B0.x, -B0.y)), __fadd2_rn(B0, nM));
+  const float2 V = __ffma2_rn(mk2(fy, fy), __fadd2_rn(H1, mk2(-H0.x, -H0.y)), H0);
+  const float vb = fmaf(fy, HB.y - HB.x, HB.x);
+  // floor(v + 0.5) + 2^23 has the rounded byte in its low mantissa bits
+  const float2 R2 = __fadd2_rn(V, mk2(0.5f, 0.5f));
+  const uint32_t r = __float_as_uint(__fadd_rd(R2.x, M));
+  const uint32_t g = __float_as_uint(__fadd_rd(R2.y, M));
+  const uint32_t b = __float_as_uint(__fadd_rd(vb + 0.5f, M));
+  return __byte_perm(__byte_perm(r, g, 0x0040u), b, 0x6410u);  // byte 3 <- b.byte2 == 0
+}
+
 // Pixel i (0..15) of a 48-byte window as an RGBx word (one byte permute).
 __device__ __forceinline__ uint32_t rgbx_of(const uint32_t (&w)[12], int i) {
   const int q = (3 * i) >> 2, k = (3 * i) & 3;
