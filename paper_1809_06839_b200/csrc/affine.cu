@@ -341,11 +341,7 @@ static size_t affine_smem(const StepArgs& a) {
 
 template <int kOne, bool kGeneric>
 static void launch_affine_v(const StepArgs& a, size_t smem, cudaStream_t s) {
-  cudaFuncSetAttribute(k_affine<kOne, kGeneric>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1, sms = 148, dev = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_affine<kOne, kGeneric>, kAfThreads, smem);
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(a.n_units, sms * std::max(occ, 1));
+  const int grid = persistent_grid((const void*)k_affine<kOne, kGeneric>, kAfThreads, smem, a.n_units);
   k_affine<kOne, kGeneric><<<grid, kAfThreads, smem, s>>>(a);
 }
 

@@ -131,6 +131,9 @@ __device__ __forceinline__ int dim_w(const Tables& t, int img, int k) {
   return t.dims[((size_t)img * (t.n_ops + 1) + k) * 2 + 1];
 }
 
+// grid of a persistent kernel: min(n_units, SMs x occupancy), cached (launch.cu)
+int persistent_grid(const void* fn, int threads, size_t smem, int n_units);
+
 // kernel entry points (launch helpers live next to each kernel)
 void launch_prep(const PrepArgs& a, cudaStream_t s);
 void launch_point(const StepArgs& a, cudaStream_t s);

@@ -1,0 +1,43 @@
+// launch.cu -- cached launch configuration for the persistent kernels: the
+// dynamic shared-memory attribute is raised once per (kernel, size) and the
+// occupancy / SM count are queried once, so an alb_apply costs only the
+// kernel launches themselves on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
+
+namespace alb {
+
+namespace {
+std::mutex g_mu;
+std::map<std::pair<const void*, size_t>, int> g_occ;
+int g_sms = 0;
+}  // namespace
+
+int persistent_grid(const void* fn, int threads, size_t smem, int n_units) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      g_sms = 148;
+  }
+  const auto key = std::make_pair(fn, smem);
+  auto it = g_occ.find(key);
+  int occ;
+  if (it == g_occ.end()) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+    occ = std::max(occ, 1);
+    g_occ[key] = occ;
+  } else {
+    occ = it->second;
+  }
+  return std::min(n_units, g_sms * occ);
+}
+
+}  // namespace alb

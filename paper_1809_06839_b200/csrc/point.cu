@@ -223,23 +223,16 @@ __global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
   }
 }
 
-static int grid_for(const void* fn, size_t smem, int n_units) {
-  int occ = 1, sms = 148, dev = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return std::min(n_units, sms * std::max(occ, 1));
-}
-
 template <bool kNL1>
 static void launch_lut(const StepArgs& a, size_t smem, cudaStream_t s) {
-  cudaFuncSetAttribute(k_point_lut<kNL1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_point_lut<kNL1><<<grid_for((const void*)k_point_lut<kNL1>, smem, a.n_units), kThreads, smem, s>>>(a);
+  const int grid = persistent_grid((const void*)k_point_lut<kNL1>, kThreads, smem, a.n_units);
+  k_point_lut<kNL1><<<grid, kThreads, smem, s>>>(a);
 }
 
 template <int kOne>
 static void launch_px(const StepArgs& a, size_t smem, cudaStream_t s) {
-  cudaFuncSetAttribute(k_point_px<kOne>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_point_px<kOne><<<grid_for((const void*)k_point_px<kOne>, smem, a.n_units), kThreads, smem, s>>>(a);
+  const int grid = persistent_grid((const void*)k_point_px<kOne>, kThreads, smem, a.n_units);
+  k_point_px<kOne><<<grid, kThreads, smem, s>>>(a);
 }
 
 void launch_point(const StepArgs& a, cudaStream_t s) {

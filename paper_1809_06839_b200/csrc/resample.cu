@@ -237,11 +237,7 @@ static size_t resample_smem(const StepArgs& a) {
 
 template <int kOne>
 static void launch_resample_t(const StepArgs& a, size_t smem, cudaStream_t s) {
-  cudaFuncSetAttribute(k_resample<kOne>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 1, sms = 148, dev = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_resample<kOne>, kRsThreads, smem);
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(a.n_units, sms * std::max(occ, 1));
+  const int grid = persistent_grid((const void*)k_resample<kOne>, kRsThreads, smem, a.n_units);
   k_resample<kOne><<<grid, kRsThreads, smem, s>>>(a);
 }
 
