@@ -85,6 +85,7 @@ struct PlanStep {
   uint32_t fill = 0, mask_fill = 0;
   int interp = 1, border = 0;
   int eq_slot = -1;
+  float min_scale = 1.0f;
 };
 
 constexpr int kChunk = 48 * 512;         // pointwise / histogram bytes per unit
@@ -394,6 +395,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       st.kind = (kind == ALB_ROTATE || kind == ALB_SHIFT_SCALE_ROTATE) ? SK_AFFINE : SK_RESAMPLE;
       st.slot0 = k; st.slot1 = k + 1;
       st.interp = o.interp; st.border = o.border;
+      st.min_scale = kind == ALB_SHIFT_SCALE_ROTATE ? (float)o.lo[2] : 1.0f;
       st.fill = o.fill[0] | (o.fill[1] << 8) | (o.fill[2] << 16);
       st.mask_fill = o.mask_fill;
       steps.push_back(st);
@@ -552,11 +554,12 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
         break;
       }
       case SK_AFFINE: {
-        st.unit_size = 10 * 1024;  // 40 KB: a 64x32 tile at 45 deg / scale 0.9 needs ~8.7K words
-        for (int i = 0; i < P->n; ++i) {  // 64x64 output tiles
+        // 55 KB: a 64x64 tile at scale >= 0.9 needs <= (99 + 5 + 31) x (99 + 5) = 14040 words
+        st.unit_size = 14080;
+        for (int i = 0; i < P->n; ++i) {  // 64x64 output tiles, unit.y = (row << 16) | col
           const int H = dims[i][st.slot1].first, W = dims[i][st.slot1].second;
-          const int ntile = ((W + 63) / 64) * ((H + 31) / 32);  // 64 x 32 tiles
-          for (int t = 0; t < ntile; ++t) st.units.push_back(make_int2(i, t));
+          for (int ty = 0; ty < (H + 63) / 64; ++ty)
+            for (int tx = 0; tx < (W + 63) / 64; ++tx) st.units.push_back(make_int2(i, (ty << 16) | tx));
         }
         break;
       }
@@ -744,6 +747,7 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
     a.mask_fill = st.mask_fill;
     a.interp = st.interp;
     a.border = st.border;
+    a.min_scale = st.min_scale;
     a.tab = tab;
     a.ops = P->d_ops;
     switch (st.kind) {

@@ -10,15 +10,20 @@
 // error ~2e-6 px, and a pixel's value depends only on its warp-output
 // coordinates, so the fused cfg5 kernel equals the unfused kernel bit for bit.
 //
-// Work unit = (image, 64x32 output tile); the grid is persistent over
-// contiguous unit ranges.  Per tile the source footprint (+ bilinear halo) is
-// staged in shared memory as RGBx words with the border resolved per staged
-// pixel (reflect-101 or constant fill): interior runs of 16 pixels with
-// 16-byte loads, border pixels one per thread, so the hot loop has no border
-// logic.  The staged row stride S is = +-1 (mod 32), picked from the rotation
-// so 32 consecutive output pixels hit distinct banks.  Each warp owns 4 output
-// rows (lane = column, 2 pixels per lane per row); RGB bytes go to a per-warp
-// row buffer that the warp writes out with aligned 16-byte stores.
+// Work unit = (image, 64x32 output tile); persistent grid over contiguous
+// unit ranges.  Per tile:
+//  1. thread 0 derives the source footprint, the bank-friendly staged stride
+//     S (= +-1 mod 32 from the rotation, so 32 consecutive output pixels hit
+//     distinct banks) and every division constant of the tile;
+//  2. the footprint (+ bilinear halo) is staged in shared memory as RGBx
+//     words with the border resolved per staged pixel (reflect-101 or
+//     constant): interior runs of 16 pixels with 16-byte loads (two runs in
+//     flight per thread), border pixels one per thread;
+//  3. each warp owns 4 output rows, lane = column, 2 pixels per lane per row:
+//     anchored coordinates, magic-number floor, 4 shared taps, paired-fp32
+//     blend, one RGBx word into the shared output tile;
+//  4. the tile is repacked RGBx -> RGB in shared memory and written with
+//     aligned 16-byte stores.
 // Footprints larger than the staging capacity fall back to per-tap loads.
 #include <algorithm>
 
@@ -28,9 +33,9 @@ namespace alb {
 
 constexpr int kAfThreads = 256;
 constexpr int kAfWarps = kAfThreads / 32;
-constexpr int kTileW = 64, kTileH = 32;
+constexpr int kTileW = 64, kTileH = 64;
 constexpr int kRowsPerWarp = kTileH / kAfWarps;
-constexpr int kTilePitch = kTileW * 3 + 16;  // output tile row pitch in shared memory (16-aligned)
+constexpr int kTilePitch = kTileW * 3 + 16;  // packed RGB tile row pitch (bytes, 16-aligned)
 
 struct AfCoef {
   double A[6];
@@ -81,8 +86,18 @@ __device__ __forceinline__ int border_idx(int i, int n, bool reflect, bool& in) 
   return (k >= 0 && k < n) ? k : reflect101(i, n);
 }
 
+// floor(v) for |v| < 2^22 via round-down add of 1.5*2^23: returns the
+// integer and the exact fraction v - floor(v)
+__device__ __forceinline__ int floor_frac(float v, float& frac) {
+  const float M = 12582912.f;  // 1.5 * 2^23
+  const float t = __fadd_rd(v, M);
+  frac = v - (t - M);
+  return __float_as_int(t) - 0x4B400000;
+}
+
 struct TileGeom {
-  int fx0, fy0, S, fw, fh, staged, Sm, ci0, ci1, pad[3];
+  int fx0, fy0, S, fw, fh, staged, Sm, ci0, ci1, nvi, P, tail;
+  uint32_t m_nvi, m_P, m_fw, m_copy;
 };
 
 struct ImgState {
@@ -92,6 +107,15 @@ struct ImgState {
   int Wo, Ho, tiles_x, pad;
 };
 
+// smem word offsets (from sm + n_lut * kLutWords)
+constexpr int kOffIs = 0;
+constexpr int kOffTg = (int)(sizeof(ImgState) + 15) / 16 * 4;
+constexpr int kOffTile = kOffTg + (int)(sizeof(TileGeom) + 15) / 16 * 4;          // RGBx [32][64]
+constexpr int kOffStage = kOffTile + kTileH * kTileW;
+// the packed RGB output tile [64][208] aliases the stage buffer: it is written
+// only after the compute pass has consumed the staged footprint
+static_assert(kTileH * kTilePitch + 16 <= 14040 * 4, "pack must fit in the stage buffer");
+
 // kGeneric = false: bilinear, no mask, u8 output (the single-op and cfg5-image
 // fast path) -- the uniform mode branches compile away.
 template <int kOne, bool kGeneric>
@@ -100,10 +124,12 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   StageCtx x;
   init_stages(a, x);
-  ImgState* is = reinterpret_cast<ImgState*>(sm + x.n_lut * kLutWords);
-  TileGeom* tg = reinterpret_cast<TileGeom*>(is + 1);
-  uint8_t* tilebuf = reinterpret_cast<uint8_t*>(tg + 1);  // output tile, RGB bytes
-  uint32_t* stage = reinterpret_cast<uint32_t*>(tilebuf + kTileH * kTilePitch + 16);
+  const int base = x.n_lut * kLutWords;
+  ImgState* is = reinterpret_cast<ImgState*>(sm + base + kOffIs);
+  TileGeom* tg = reinterpret_cast<TileGeom*>(sm + base + kOffTg);
+  uint32_t* tile = sm + base + kOffTile;
+  uint32_t* stage = sm + base + kOffStage;
+  uint8_t* pack = reinterpret_cast<uint8_t*>(stage);  // aliases stage (see kOffStage)
   uint8_t* mstage = reinterpret_cast<uint8_t*>(stage + a.unit_size);
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
   const bool nearest = kGeneric && a.interp == ALB_INTERP_NEAREST;
@@ -138,19 +164,24 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
     const int Ws = sd.width, Hs = sd.height;
     const int Wo = is->Wo, Ho = is->Ho;
     const Map1 m = is->m;
-    const int tx0 = (unit.y % is->tiles_x) * kTileW, ty0 = (unit.y / is->tiles_x) * kTileH;
+    const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
     const int tw = min(kTileW, Wo - tx0), th = min(kTileH, Ho - ty0);
-    if (threadIdx.x == 0) {
+    if (warp == 0) {  // tile geometry: corners on lanes 0-3, division constants on lanes 0-3
       const int xwa = m.ax * tx0 + m.bx, xwb = m.ax * (tx0 + tw - 1) + m.bx;
       const int ywa = m.ay * ty0 + m.by, ywb = m.ay * (ty0 + th - 1) + m.by;
       const double xw0 = min(xwa, xwb), xw1 = max(xwa, xwb), yw0 = min(ywa, ywb), yw1 = max(ywa, ywb);
       const double* A = is->A;
-      double lx = 1e300, hx = -1e300, ly = 1e300, hy = -1e300;
-      for (int c = 0; c < 4; ++c) {
-        const double xw = (c & 1) ? xw1 : xw0, yw = (c & 2) ? yw1 : yw0;
-        const double sx = fma(A[0], xw, fma(A[1], yw, A[2]));
-        const double sy = fma(A[3], xw, fma(A[4], yw, A[5]));
-        lx = fmin(lx, sx); hx = fmax(hx, sx); ly = fmin(ly, sy); hy = fmax(hy, sy);
+      const int c = lane & 3;
+      const double xw = (c & 1) ? xw1 : xw0, yw = (c & 2) ? yw1 : yw0;
+      const double sx = fma(A[0], xw, fma(A[1], yw, A[2]));
+      const double sy = fma(A[3], xw, fma(A[4], yw, A[5]));
+      double lx = sx, hx = sx, ly = sy, hy = sy;
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        lx = fmin(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+        hx = fmax(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+        ly = fmin(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+        hy = fmax(hy, __shfl_xor_sync(0xffffffffu, hy, o));
       }
       TileGeom t;
       t.fx0 = (int)floor(lx) - 1;
@@ -164,56 +195,79 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
                  (!has_mask || (long long)t.Sm * t.fh <= a.unit_size);
       t.ci0 = min(max(-t.fx0, 0), t.fw);
       t.ci1 = min(max(Ws - t.fx0, 0), t.fw);
-      *tg = t;
+      t.nvi = (t.ci1 - t.ci0 + 15) >> 4;  // last run of a row may be partial
+      t.tail = 0;
+      t.P = t.ci0 + (t.fw - t.ci1);        // border columns only
+      // one integer division per lane instead of four in a row
+      const uint32_t dv = lane == 0 ? (uint32_t)t.nvi : lane == 1 ? (uint32_t)t.P
+                        : lane == 2 ? (uint32_t)t.fw : (uint32_t)((3 * tw) >> 4) + 2u;
+      const uint32_t mg = magic_of(dv);
+      t.m_nvi = __shfl_sync(0xffffffffu, mg, 0);
+      t.m_P = __shfl_sync(0xffffffffu, mg, 1);
+      t.m_fw = __shfl_sync(0xffffffffu, mg, 2);
+      t.m_copy = __shfl_sync(0xffffffffu, mg, 3);
+      if (lane == 0) *tg = t;
     }
     __syncthreads();
     const TileGeom t = *tg;
     const uint8_t* simg = a.src + sd.offset;
     if (t.staged) {
-      // pass A: 16-pixel interior runs with 16-byte loads
-      const int nvi = (t.ci1 - t.ci0) >> 4;
-      if (nvi > 0) {
-        const uint32_t magic = 0xffffffffu / (uint32_t)nvi + 1u;
-        for (int it = threadIdx.x; it < t.fh * nvi; it += kAfThreads) {
-          const int r = nvi == 1 ? it : (int)__umulhi((uint32_t)it, magic);
-          const int c = t.ci0 + ((it - r * nvi) << 4);
-          bool row_in;
-          const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
-          uint32_t* d = stage + r * t.S + c;
-          if (row_in) {
-            const uint8_t* srow = simg + (size_t)ry * sd.pitch;
-            uint32_t w[12];
-            load_window<12>(srow + (size_t)(t.fx0 + c) * 3, srow, srow + (size_t)Ws * 3, w);
+      // pass A: 16-pixel interior runs with 16-byte loads, two runs in flight
+      const int na = t.fh * t.nvi;
+      for (int it = threadIdx.x; it < na; it += 2 * kAfThreads) {
+        uint32_t w[2][12];
+        int dst[2], nw[2];
+        bool live[2];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) d[i] = rgbx_of(w, i);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) d[i] = a.fill;
+        for (int k = 0; k < 2; ++k) {
+          const int ik = it + k * kAfThreads;
+          live[k] = ik < na;
+          dst[k] = -1;
+          nw[k] = 0;
+          if (live[k]) {
+            const int r = fdiv(ik, t.m_nvi);
+            const int c = t.ci0 + ((ik - r * t.nvi) << 4);
+            nw[k] = min(16, t.ci1 - c);  // partial last run of the row
+            bool row_in;
+            const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+            dst[k] = r * t.S + c;
+            if (row_in) {
+              const uint8_t* srow = simg + (size_t)ry * sd.pitch;
+              load_window<12>(srow + (size_t)(t.fx0 + c) * 3, srow, srow + (size_t)Ws * 3, w[k]);
+            } else {
+              live[k] = false;  // constant-border row
+              for (int i = 0; i < nw[k]; ++i) stage[dst[k] + i] = a.fill;
+            }
           }
         }
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (live[k]) {
+            if (nw[k] == 16) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) stage[dst[k] + i] = rgbx_of(w[k], i);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (i < nw[k]) stage[dst[k] + i] = rgbx_of(w[k], i);
+            }
+          }
       }
-      // pass B: border columns + the interior tail, one pixel per thread
-      const int tail = (t.ci1 - t.ci0) & 15;
-      const int P = t.ci0 + tail + (t.fw - t.ci1);
-      if (P > 0) {
-        const uint32_t magic = 0xffffffffu / (uint32_t)P + 1u;
-        for (int it = threadIdx.x; it < t.fh * P; it += kAfThreads) {
-          const int r = P == 1 ? it : (int)__umulhi((uint32_t)it, magic);
-          const int j = it - r * P;
-          const int c = j < t.ci0 ? j : (j < t.ci0 + tail ? t.ci0 + 16 * nvi + (j - t.ci0)
-                                                          : t.ci1 + (j - t.ci0 - tail));
-          bool row_in, col_in;
-          const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
-          const int rx = border_idx(t.fx0 + c, Ws, reflect, col_in);
-          stage[r * t.S + c] = (row_in && col_in) ? fetch_rgb(simg + (size_t)ry * sd.pitch, rx) : a.fill;
-        }
+      // pass B: border columns, one pixel per thread
+      for (int it = threadIdx.x; it < t.fh * t.P; it += kAfThreads) {
+        const int r = fdiv(it, t.m_P);
+        const int j = it - r * t.P;
+        const int c = j < t.ci0 ? j : t.ci1 + (j - t.ci0);
+        bool row_in, col_in;
+        const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+        const int rx = border_idx(t.fx0 + c, Ws, reflect, col_in);
+        stage[r * t.S + c] = (row_in && col_in) ? fetch_rgb(simg + (size_t)ry * sd.pitch, rx) : a.fill;
       }
       if (has_mask) {
         const uint8_t* smk = a.msrc + a.msdesc[img].offset;
         const int mpitch = a.msdesc[img].pitch;
-        const uint32_t magic = 0xffffffffu / (uint32_t)t.fw + 1u;
         for (int it = threadIdx.x; it < t.fh * t.fw; it += kAfThreads) {
-          const int r = t.fw == 1 ? it : (int)__umulhi((uint32_t)it, magic);
+          const int r = fdiv(it, t.m_fw);
           const int c = it - r * t.fw;
           bool row_in, col_in;
           const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
@@ -226,23 +280,66 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
     // ---- compute: warp owns kRowsPerWarp rows; lane = columns lane, lane + 32
     const float A0f = is->Af[0], A1f = is->Af[1], A3f = is->Af[2], A4f = is->Af[3];
     const double* A = is->A;
-    uint8_t* dbase = nullptr;
-    int dpitch = 0;
-    if (!normalize) {
-      const alb_image_desc dd = a.ddesc[img];
-      dbase = a.dst + dd.offset;
-      dpitch = dd.pitch;
-    }
     int xw[2];
     float dxl[2];
     int cur_cy[2] = {-0x7fffffff, -0x7fffffff};
-    int aix[2] = {0, 0}, aiy[2] = {0, 0};
+    int abase[2] = {0, 0}, aix[2] = {0, 0}, aiy[2] = {0, 0};
     float afx[2] = {0.f, 0.f}, afy[2] = {0.f, 0.f};
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       xw[j] = m.ax * min(tx0 + lane + 32 * j, Wo - 1) + m.bx;
       dxl[j] = (float)(xw[j] & 15);
     }
+    if constexpr (!kGeneric) {
+      // fast path (always staged, bilinear, u8 out): the lane's two pixels are
+      // independent chains interleaved for ILP; columns >= tw compute clamped
+      // garbage that the copy-out never reads.
+      for (int i = 0; i < kRowsPerWarp; ++i) {
+        const int row = warp * kRowsPerWarp + i;
+        if (row >= th) break;
+        const int yw = m.ay * (ty0 + row) + m.by;
+        const float dyl = (float)(yw & 15);
+        if ((yw >> 4) != cur_cy[0]) {  // warp-uniform: both columns share the cell row
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            cur_cy[j] = yw >> 4;
+            const double xa = (double)((xw[j] >> 4) * 16), ya = (double)(cur_cy[j] * 16);
+            const double sx = fma(A[0], xa, fma(A[1], ya, A[2]));
+            const double sy = fma(A[3], xa, fma(A[4], ya, A[5]));
+            const double flx = floor(sx), fly = floor(sy);
+            afx[j] = (float)(sx - flx); afy[j] = (float)(sy - fly);
+            abase[j] = ((int)fly - t.fy0) * t.S + ((int)flx - t.fx0);
+          }
+        }
+        float fx[2], fy[2];
+        int idx[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float lx = fmaf(A0f, dxl[j], fmaf(A1f, dyl, afx[j]));
+          const float ly = fmaf(A3f, dxl[j], fmaf(A4f, dyl, afy[j]));
+          const int qx = floor_frac(lx, fx[j]), qy = floor_frac(ly, fy[j]);
+          idx[j] = abase[j] + qy * t.S + qx;
+        }
+        uint32_t tp[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          tp[j][0] = stage[idx[j]];
+          tp[j][1] = stage[idx[j] + 1];
+          tp[j][2] = stage[idx[j] + t.S];
+          tp[j][3] = stage[idx[j] + t.S + 1];
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          uint32_t px = bilerp_rgbx(tp[j][0], tp[j][1], tp[j][2], tp[j][3], fx[j], fy[j]);
+          if (kOne != kStagesNone) {
+            uint32_t r = px & 0xff, g = (px >> 8) & 0xff, b = (px >> 16) & 0xff;
+            apply_stages_t<kOne>(x, sm, lane, r, g, b);
+            px = r | (g << 8) | (b << 16);
+          }
+          tile[row * kTileW + lane + 32 * j] = px;
+        }
+      }
+    } else
     for (int i = 0; i < kRowsPerWarp; ++i) {
       const int row = warp * kRowsPerWarp + i;
       if (row >= th) break;
@@ -252,7 +349,7 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int c = lane + 32 * j;
-        if (c >= tw) continue;
+        if (j == 1 && tw <= 32) break;
         if ((yw >> 4) != cur_cy[j]) {  // fp64 anchor of this column's 16x16 cell
           cur_cy[j] = yw >> 4;
           const double xa = (double)((xw[j] >> 4) * 16), ya = (double)(cur_cy[j] * 16);
@@ -261,81 +358,96 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
           const double flx = floor(sx), fly = floor(sy);
           aix[j] = (int)flx; aiy[j] = (int)fly;
           afx[j] = (float)(sx - flx); afy[j] = (float)(sy - fly);
+          abase[j] = (aiy[j] - t.fy0) * t.S + (aix[j] - t.fx0);
         }
         const float lx = fmaf(A0f, dxl[j], fmaf(A1f, dyl, afx[j]));
         const float ly = fmaf(A3f, dxl[j], fmaf(A4f, dyl, afy[j]));
-        uint32_t r, g, b;
+        uint32_t px;
         if (nearest) {
-          const int qx = aix[j] + (int)floorf(lx + 0.5f), qy = aiy[j] + (int)floorf(ly + 0.5f);
-          uint32_t tt;
+          float f0, f1;
+          const int qx = floor_frac(lx + 0.5f, f0), qy = floor_frac(ly + 0.5f, f1);
           if (t.staged) {
-            tt = stage[(qy - t.fy0) * t.S + (qx - t.fx0)];
+            px = stage[abase[j] + qy * t.S + qx];
           } else {
             bool ri, ci;
-            const int yy = border_idx(qy, Hs, reflect, ri), xx = border_idx(qx, Ws, reflect, ci);
-            tt = (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
+            const int yy = border_idx(aiy[j] + qy, Hs, reflect, ri);
+            const int xx = border_idx(aix[j] + qx, Ws, reflect, ci);
+            px = (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
           }
-          r = tt & 0xff; g = (tt >> 8) & 0xff; b = (tt >> 16) & 0xff;
         } else {
-          const float flx = floorf(lx), fly = floorf(ly);
-          const float fx = lx - flx, fy = ly - fly;
-          const int qx = aix[j] + (int)flx, qy = aiy[j] + (int)fly;
+          float fx, fy;
+          const int qx = floor_frac(lx, fx), qy = floor_frac(ly, fy);
           uint32_t t00, t10, t01, t11;
-          if (t.staged) {
-            const uint32_t* p = stage + (qy - t.fy0) * t.S + (qx - t.fx0);
-            t00 = p[0]; t10 = p[1]; t01 = p[t.S]; t11 = p[t.S + 1];
+          if (!kGeneric || t.staged) {
+            const int idx = abase[j] + qy * t.S + qx;
+            t00 = stage[idx]; t10 = stage[idx + 1]; t01 = stage[idx + t.S]; t11 = stage[idx + t.S + 1];
           } else {
-            auto tap = [&](int px, int py) -> uint32_t {
+            auto tap = [&](int px_, int py_) -> uint32_t {
               bool ri, ci;
-              const int yy = border_idx(py, Hs, reflect, ri), xx = border_idx(px, Ws, reflect, ci);
+              const int yy = border_idx(py_, Hs, reflect, ri), xx = border_idx(px_, Ws, reflect, ci);
               return (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
             };
-            t00 = tap(qx, qy); t10 = tap(qx + 1, qy); t01 = tap(qx, qy + 1); t11 = tap(qx + 1, qy + 1);
+            const int X = aix[j] + qx, Y = aiy[j] + qy;
+            t00 = tap(X, Y); t10 = tap(X + 1, Y); t01 = tap(X, Y + 1); t11 = tap(X + 1, Y + 1);
           }
-          const uint32_t px = bilerp_rgbx(t00, t10, t01, t11, fx, fy);
-          r = px & 0xff; g = (px >> 8) & 0xff; b = (px >> 16) & 0xff;
+          px = bilerp_rgbx(t00, t10, t01, t11, fx, fy);
         }
-        apply_stages_t<kOne>(x, sm, lane, r, g, b);
+        if (kOne != kStagesNone) {
+          uint32_t r = px & 0xff, g = (px >> 8) & 0xff, b = (px >> 16) & 0xff;
+          apply_stages_t<kOne>(x, sm, lane, r, g, b);
+          px = r | (g << 8) | (b << 16);
+        }
         if (normalize) {
           const size_t plane = (size_t)Ho * Wo;
           float* o = a.nchw + (size_t)img * 3 * plane + (size_t)yo * Wo + tx0 + c;
           const float* nl = a.tab.norm_lut;
-          __stcs(o, nl[r]);
-          __stcs(o + plane, nl[256 + g]);
-          __stcs(o + 2 * plane, nl[512 + b]);
+          __stcs(o, nl[px & 0xff]);
+          __stcs(o + plane, nl[256 + ((px >> 8) & 0xff)]);
+          __stcs(o + 2 * plane, nl[512 + ((px >> 16) & 0xff)]);
         } else {
-          uint8_t* tb = tilebuf + row * kTilePitch + 3 * c;
-          tb[0] = (uint8_t)r;
-          tb[1] = (uint8_t)g;
-          tb[2] = (uint8_t)b;
+          tile[row * kTileW + c] = px;
         }
         if (has_mask) {
-          const int qx = aix[j] + (int)floorf(lx + 0.5f), qy = aiy[j] + (int)floorf(ly + 0.5f);
+          float f0, f1;
+          const int qx = floor_frac(lx + 0.5f, f0), qy = floor_frac(ly + 0.5f, f1);
           uint8_t v;
           if (t.staged) {
-            v = mstage[(qy - t.fy0) * t.Sm + (qx - t.fx0)];
+            v = mstage[(aiy[j] + qy - t.fy0) * t.Sm + (aix[j] + qx - t.fx0)];
           } else {
             bool ri, ci;
-            const int yy = border_idx(qy, Hs, reflect, ri), xx = border_idx(qx, Ws, reflect, ci);
+            const int yy = border_idx(aiy[j] + qy, Hs, reflect, ri);
+            const int xx = border_idx(aix[j] + qx, Ws, reflect, ci);
             v = (ri && ci) ? a.msrc[a.msdesc[img].offset + (size_t)yy * a.msdesc[img].pitch + xx]
                            : (uint8_t)a.mask_fill;
           }
-          const alb_image_desc mdd = a.mddesc[img];
-          a.mdst[mdd.offset + (size_t)yo * mdd.pitch + tx0 + c] = v;
+          if (c < tw) {
+            const alb_image_desc mdd = a.mddesc[img];
+            a.mdst[mdd.offset + (size_t)yo * mdd.pitch + tx0 + c] = v;
+          }
         }
       }
     }
-    if (!normalize) {  // the whole tile, aligned 16-byte stores
+    if (!normalize) {
       __syncthreads();
-      cta_copy_rows(dbase + (size_t)ty0 * dpitch + (size_t)tx0 * 3, dpitch, tilebuf, kTilePitch, th,
-                    3 * tw, kAfThreads);
+      // repack RGBx -> RGB: 4 pixels (one 16-byte read) -> 12 bytes per thread item
+      for (int it = threadIdx.x; it < kTileH * (kTileW / 4); it += kAfThreads) {
+        const int r = it >> 4, q = it & 15;
+        const uint4 v = *reinterpret_cast<const uint4*>(tile + r * kTileW + 4 * q);
+        uint32_t* d = reinterpret_cast<uint32_t*>(pack + r * kTilePitch + 12 * q);
+        d[0] = __byte_perm(v.x, v.y, 0x4210);
+        d[1] = __byte_perm(v.y, v.z, 0x5421);
+        d[2] = __byte_perm(v.z, v.w, 0x6542);
+      }
+      __syncthreads();
+      const alb_image_desc dd = a.ddesc[img];
+      cta_copy_rows(a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3, dd.pitch, pack,
+                    kTilePitch, th, 3 * tw, kAfThreads, t.m_copy);
     }
   }
 }
 
 static size_t affine_smem(const StepArgs& a) {
-  return (size_t)count_lut_stages(a) * kLutWords * 4 + sizeof(ImgState) + sizeof(TileGeom) +
-         kTileH * kTilePitch + 16 + (size_t)a.unit_size * 4 +
+  return ((size_t)count_lut_stages(a) * kLutWords + kOffStage) * 4 + (size_t)a.unit_size * 4 +
          (a.mdst ? (size_t)a.unit_size : 0);
 }
 
@@ -347,7 +459,10 @@ static void launch_affine_v(const StepArgs& a, size_t smem, cudaStream_t s) {
 
 template <int kOne>
 static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
-  const bool generic = a.interp == ALB_INTERP_NEAREST || a.mdst != nullptr || a.normalize;
+  // fast variant always stages: a 64x64 tile's footprint (+halo) is at most
+  // (63*sqrt2/s + 5 + 31) x (63*sqrt2/s + 5) words, <= 14040 <= a.unit_size for s >= 0.9
+  const bool generic = a.interp == ALB_INTERP_NEAREST || a.mdst != nullptr || a.normalize ||
+                       a.min_scale < 0.9f || a.unit_size < 14040;
   if (generic) launch_affine_v<kOne, true>(a, smem, s);
   else launch_affine_v<kOne, false>(a, smem, s);
 }

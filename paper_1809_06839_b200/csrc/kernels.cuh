@@ -52,6 +52,7 @@ struct StepArgs {
   uint32_t fill;      // constant fill, packed RGB (pad / constant border)
   uint32_t mask_fill;
   int32_t interp, border;  // resampling op settings
+  float min_scale;         // affine: smallest scale the op can draw (footprint bound)
   Tables tab;
   const alb_op* ops;
 };

@@ -252,12 +252,20 @@ __device__ __forceinline__ void warp_copy_row(uint8_t* dst, const uint8_t* src, 
 // pitch spitch, 16-byte aligned) to global rows of any alignment: per row one
 // item per aligned 16-byte block plus one item each for the unaligned head
 // and tail bytes.
+// x / d for 0 <= x < 2^20 via a precomputed magic (magic_of(d) == 0 means d == 1)
+__host__ __device__ __forceinline__ uint32_t magic_of(uint32_t d) {
+  return d <= 1 ? 0u : 0xffffffffu / d + 1u;
+}__device__ __forceinline__ int fdiv(int x, uint32_t m) {
+  return m == 0 ? x : (int)__umulhi((uint32_t)x, m);
+}
+
+// magic = magic_of((n >> 4) + 2), precomputed by the caller (one thread)
 __device__ __forceinline__ void cta_copy_rows(uint8_t* dst0, int dpitch, const uint8_t* src0,
-                                              int spitch, int rows, int n, int nthreads) {
+                                              int spitch, int rows, int n, int nthreads,
+                                              uint32_t magic) {
   const int npr = (n >> 4) + 2;
-  const uint32_t magic = 0xffffffffu / (uint32_t)npr + 1u;
   for (int it = threadIdx.x; it < rows * npr; it += nthreads) {
-    const int r = (int)__umulhi((uint32_t)it, magic);
+    const int r = fdiv(it, magic);
     const int k = it - r * npr;
     uint8_t* dst = dst0 + (size_t)r * dpitch;
     const uint8_t* src = src0 + r * spitch;
