@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
   }
 }
 
-// pixel-wise chain (HSV / gray / mixed / Normalize output)
-template <int kOne>
+// pixel-wise chain (HSV / gray / mixed / Normalize output); kNorm is
+// compile-time so the unused output path is not issued per pixel
+template <int kOne, bool kNorm>
 __global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31;
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
           const uint32_t px = rgbx_of(w[k], i);
           uint32_t r = px & 0xff, g = (px >> 8) & 0xff, b = px >> 16;
           apply_stages_t<kOne>(x, sm, lane, r, g, b);
-          if (a.normalize) {
+          if constexpr (kNorm) {
             s.plane0[p0 + i] = nl[r];
             s.plane0[s.plane + p0 + i] = nl[256 + g];
             s.plane0[2 * s.plane + p0 + i] = nl[512 + b];
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
             o[(3 * i + 2) >> 2] |= b << (((3 * i + 2) & 3) * 8);
           }
         }
-        if (!a.normalize) {
+        if constexpr (!kNorm) {
           uint4* d4 = reinterpret_cast<uint4*>(s.dst + s.bA + 48 * gi);
 #pragma unroll
           for (int q = 0; q < 3; ++q)
@@ -229,10 +230,16 @@ static void launch_lut(const StepArgs& a, size_t smem, cudaStream_t s) {
   k_point_lut<kNL1><<<grid, kThreads, smem, s>>>(a);
 }
 
+template <int kOne, bool kNorm>
+static void launch_px_n(const StepArgs& a, size_t smem, cudaStream_t s) {
+  const int grid = persistent_grid((const void*)k_point_px<kOne, kNorm>, kThreads, smem, a.n_units);
+  k_point_px<kOne, kNorm><<<grid, kThreads, smem, s>>>(a);
+}
+
 template <int kOne>
 static void launch_px(const StepArgs& a, size_t smem, cudaStream_t s) {
-  const int grid = persistent_grid((const void*)k_point_px<kOne>, kThreads, smem, a.n_units);
-  k_point_px<kOne><<<grid, kThreads, smem, s>>>(a);
+  if (a.normalize) launch_px_n<kOne, true>(a, smem, s);
+  else launch_px_n<kOne, false>(a, smem, s);
 }
 
 void launch_point(const StepArgs& a, cudaStream_t s) {

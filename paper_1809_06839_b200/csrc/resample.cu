@@ -69,7 +69,9 @@ struct RsState {
   int sy_lo, nrows, staged, pad;
 };
 
-template <int kOne>
+// kGeneric = false: bilinear, u8 output -- the uniform mode branches compile
+// away (a predicated-off Normalize path would otherwise issue per pixel)
+template <int kOne, bool kGeneric>
 __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -83,8 +85,9 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
   uint8_t* rowbuf = reinterpret_cast<uint8_t*>(st + 1) + warp * (kRsChunk * 3 + 32);
   uint32_t* stage = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(st + 1) +
                                                 kRsWarps * (kRsChunk * 3 + 32));
-  const bool nearest = a.interp == ALB_INTERP_NEAREST;
+  const bool nearest = kGeneric && a.interp == ALB_INTERP_NEAREST;
   const bool has_mask = a.mdst != nullptr;
+  const bool normalize = kGeneric && a.normalize;
   const int R = a.unit_rows;
 
   int u0, u1;
@@ -153,13 +156,13 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
     }
     uint8_t* dbase = nullptr;
     int dpitch = 0;
-    if (!a.normalize) {
+    if (!normalize) {
       const alb_image_desc dd = a.ddesc[img];
       dbase = a.dst + dd.offset;
       dpitch = dd.pitch;
     }
     const size_t plane = (size_t)Ho * Wo;
-    float* nbase = a.normalize ? a.nchw + (size_t)img * 3 * plane : nullptr;
+    float* nbase = normalize ? a.nchw + (size_t)img * 3 * plane : nullptr;
     const float* nl = a.tab.norm_lut;
     for (int rr = warp; rr < y1 - y0; rr += kRsWarps) {
       const int yo = y0 + rr;
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
             r = px & 0xff; gg = (px >> 8) & 0xff; b = (px >> 16) & 0xff;
           }
           apply_stages_t<kOne>(x, sm, lane, r, gg, b);
-          if (a.normalize) {
+          if (normalize) {
             float* o = nbase + (size_t)yo * Wo + xo;
             __stcs(o, nl[r]);
             __stcs(o + plane, nl[256 + gg]);
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
             rowbuf[3 * c + 2] = (uint8_t)b;
           }
         }
-        if (!a.normalize) {
+        if (!normalize) {
           __syncwarp();
           warp_copy_row(dbase + (size_t)yo * dpitch + (size_t)cx0 * 3, rowbuf, 3 * cw, lane);
           __syncwarp();
@@ -235,10 +238,16 @@ static size_t resample_smem(const StepArgs& a) {
          (size_t)a.unit_size * 4;
 }
 
+template <int kOne, bool kGeneric>
+static void launch_resample_v(const StepArgs& a, size_t smem, cudaStream_t s) {
+  const int grid = persistent_grid((const void*)k_resample<kOne, kGeneric>, kRsThreads, smem, a.n_units);
+  k_resample<kOne, kGeneric><<<grid, kRsThreads, smem, s>>>(a);
+}
+
 template <int kOne>
 static void launch_resample_t(const StepArgs& a, size_t smem, cudaStream_t s) {
-  const int grid = persistent_grid((const void*)k_resample<kOne>, kRsThreads, smem, a.n_units);
-  k_resample<kOne><<<grid, kRsThreads, smem, s>>>(a);
+  if (a.normalize || a.interp == ALB_INTERP_NEAREST) launch_resample_v<kOne, true>(a, smem, s);
+  else launch_resample_v<kOne, false>(a, smem, s);
 }
 
 void launch_resample(const StepArgs& a, cudaStream_t s) {
