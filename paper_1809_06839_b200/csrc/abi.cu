@@ -112,7 +112,7 @@ struct alb_plan {
   bool has_eq = false;
   // workspace layout
   size_t off_params = 0, off_fired = 0, off_dims = 0, off_luts = 0, off_norm = 0,
-         off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, ws_bytes = 0;
+         off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, off_geo = 0, ws_bytes = 0;
   int2* d_units = nullptr;
   int n_launches = 0;
   ~alb_plan() {
@@ -613,6 +613,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   P->off_norm = take(768 * sizeof(float));
   P->off_eqh = take(P->has_eq ? nn * 768 * sizeof(uint32_t) : 0);
   P->off_eql = take(P->has_eq ? nn * 768 : 0);
+  P->off_geo = take(nn * kGeoBytes);  // per-image affine state (affine steps)
   P->off_buf[0] = take(max_inter + 64);
   P->off_buf[1] = take(max_inter + 64);
   P->off_mbuf[0] = take(max_minter + 64);
@@ -750,6 +751,8 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
     a.min_scale = st.min_scale;
     a.tab = tab;
     a.ops = P->d_ops;
+    a.geo = ws + P->off_geo;
+    a.n_img = P->n;
     switch (st.kind) {
       case SK_ROW:
         if (st.has_image) {

@@ -7,24 +7,31 @@
 // written as x_s = A0*xw + A1*yw + A2 with the coefficients formed in fp64.
 // Coordinates: an fp64 ANCHOR per 16x16 cell of warp-output coordinates
 // (split into integer + fp32 fraction) plus fp32 local offsets (<= 15 px):
-// error ~2e-6 px, and a pixel's value depends only on its warp-output
+//   b = fma(A0f, dxl, frac_anchor)       (per column and cell)
+//   l = fma(A1f, dyl, b)                 (per pixel, both axes in one FFMA2)
+// error ~4e-6 px, and a pixel's value depends only on its warp-output
 // coordinates, so the fused cfg5 kernel equals the unfused kernel bit for bit.
 //
-// Work unit = (image, 64x32 output tile); persistent grid over contiguous
+// Work unit = (image, 64x64 output tile); persistent grid over contiguous
 // unit ranges.  Per tile:
-//  1. thread 0 derives the source footprint, the bank-friendly staged stride
+//  1. warp 0 derives the source footprint, the bank-friendly staged stride
 //     S (= +-1 mod 32 from the rotation, so 32 consecutive output pixels hit
-//     distinct banks) and every division constant of the tile;
+//     ~distinct banks: bank = (x +- y) mod 32) and the division constants;
 //  2. the footprint (+ bilinear halo) is staged in shared memory as RGBx
 //     words with the border resolved per staged pixel (reflect-101 or
-//     constant): interior runs of 16 pixels with 16-byte loads (two runs in
-//     flight per thread), border pixels one per thread;
-//  3. each warp owns 4 output rows, lane = column, 2 pixels per lane per row:
-//     anchored coordinates, magic-number floor, 4 shared taps, paired-fp32
-//     blend, one RGBx word into the shared output tile;
-//  4. the tile is repacked RGBx -> RGB in shared memory and written with
-//     aligned 16-byte stores.
-// Footprints larger than the staging capacity fall back to per-tap loads.
+//     constant).  Interior runs are 16 pixels whose 48 source bytes are
+//     16-byte aligned (x == 11*(-rowaddr) mod 16), so three aligned vector
+//     loads and one byte permute per pixel stage them; consecutive threads
+//     take consecutive footprint ROWS, so their stores hit distinct banks;
+//  3. each warp owns 8 output rows, lane = column (2 columns per lane):
+//     paired-fp32 coordinates, magic-number floor (add.rm.f32x2), 4 shared
+//     taps, paired-fp32 blend, bytes stored straight into a shared output row
+//     buffer that is pre-shifted by the destination row's 16-byte phase;
+//  4. the tile is copied out in 16-byte chunks that are aligned on BOTH
+//     sides; the partial first / last chunk of a row is a separate item that
+//     uses naturally aligned 8/4/2/1-byte pieces (no byte loops).
+// Footprints larger than the staging capacity fall back to per-tap loads
+// (generic variant).
 #include <algorithm>
 
 #include "stages.cuh"
@@ -35,7 +42,13 @@ constexpr int kAfThreads = 256;
 constexpr int kAfWarps = kAfThreads / 32;
 constexpr int kTileW = 64, kTileH = 64;
 constexpr int kRowsPerWarp = kTileH / kAfWarps;
-constexpr int kTilePitch = kTileW * 3 + 16;  // packed RGB tile row pitch (bytes, 16-aligned)
+constexpr int kObPitch = 208;   // output row buffer: 15 (phase) + 3*64, rounded to 16
+constexpr int kObFull = 12;     // full 16-byte chunks per output row (192 bytes)
+constexpr int kMobPitch = 80;   // mask row buffer: 15 + 64, rounded to 16
+constexpr int kMobFull = 4;     // full 16-byte chunks per mask row (64 bytes)
+constexpr int kMStageBytes = 11264;  // staged mask footprint capacity (bytes)
+constexpr float kMagic15 = 12582912.f;  // 1.5 * 2^23: floor via round-down add
+constexpr uint32_t kMagic15Bits = 0x4B400000u;
 
 struct AfCoef {
   double A[6];
@@ -86,54 +99,157 @@ __device__ __forceinline__ int border_idx(int i, int n, bool reflect, bool& in) 
   return (k >= 0 && k < n) ? k : reflect101(i, n);
 }
 
-// floor(v) for |v| < 2^22 via round-down add of 1.5*2^23: returns the
-// integer and the exact fraction v - floor(v)
-__device__ __forceinline__ int floor_frac(float v, float& frac) {
-  const float M = 12582912.f;  // 1.5 * 2^23
-  const float t = __fadd_rd(v, M);
-  frac = v - (t - M);
-  return __float_as_int(t) - 0x4B400000;
+// ---- paired fp32 helpers (sm_100 f32x2 pipe)
+__device__ __forceinline__ unsigned long long f2u(float2 v) {
+  return ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x);
+}
+__device__ __forceinline__ float2 u2f(unsigned long long u) {
+  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
+}
+// round-toward-minus-infinity paired add: floor(v) + 1.5*2^23 for |v| < 2^22
+__device__ __forceinline__ float2 fadd2_rm(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+
+// Per-column cell anchor: fp64 source coordinate of the cell origin, split
+// into integer part (ix, iy) and fp32 fraction, plus the column's fp32 offset.
+struct Anchor {
+  float bx, by;  // fma(A0f, dxl, afx), fma(A3f, dxl, afy)
+  int ix, iy;
+};
+
+__device__ __forceinline__ Anchor cell_anchor(const double* A, float A0f, float A3f, int xw, int cy) {
+  const double xa = (double)((xw >> 4) * 16), ya = (double)(cy * 16);
+  const double sx = fma(A[0], xa, fma(A[1], ya, A[2]));
+  const double sy = fma(A[3], xa, fma(A[4], ya, A[5]));
+  const double flx = floor(sx), fly = floor(sy);
+  const float dxl = (float)(xw & 15);
+  Anchor an;
+  an.bx = fmaf(A0f, dxl, (float)(sx - flx));
+  an.by = fmaf(A3f, dxl, (float)(sy - fly));
+  an.ix = (int)flx;
+  an.iy = (int)fly;
+  return an;
+}
+
+// Bilinear blend of 4 RGBx taps (O5/O7 weights), fp32, per channel
+//   h0 = fma(fx, p10 - p00, p00 + .5); h1 = fma(fx, p11 - p01, p01 + .5);
+//   v  = fma(fy, h1 - h0, h0);   out = floor(v)        (= round_half_up)
+// Bytes become floats via the 2^23 magic (byte permute); channel pairs run
+// on the paired fp32 pipe.  Returns the three rounded channels as the bit
+// patterns of floor(v) + 2^23 (byte in bits 0-7).
+__device__ __forceinline__ void bilerp3(uint32_t t00, uint32_t t10, uint32_t t01, uint32_t t11,
+                                        float2 f, uint32_t& r, uint32_t& g, uint32_t& b) {
+  constexpr uint32_t kM = 0x4B000000u;  // 2^23
+  auto cv = [](uint32_t t, uint32_t c) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | c)); };
+  const float2 P00 = make_float2(cv(t00, 0), cv(t00, 1)), P10 = make_float2(cv(t10, 0), cv(t10, 1));
+  const float2 P01 = make_float2(cv(t01, 0), cv(t01, 1)), P11 = make_float2(cv(t11, 0), cv(t11, 1));
+  const float2 B0 = make_float2(cv(t00, 2), cv(t01, 2)), B1 = make_float2(cv(t10, 2), cv(t11, 2));
+  const float2 nMh = make_float2(-8388607.5f, -8388607.5f);  // -(2^23 - 0.5), exact
+  const float2 fx2 = make_float2(f.x, f.x);
+  const float2 H0 = __ffma2_rn(fx2, __fadd2_rn(P10, make_float2(-P00.x, -P00.y)), __fadd2_rn(P00, nMh));
+  const float2 H1 = __ffma2_rn(fx2, __fadd2_rn(P11, make_float2(-P01.x, -P01.y)), __fadd2_rn(P01, nMh));
+  const float2 HB = __ffma2_rn(fx2, __fadd2_rn(B1, make_float2(-B0.x, -B0.y)), __fadd2_rn(B0, nMh));
+  const float2 V = __ffma2_rn(make_float2(f.y, f.y), __fadd2_rn(H1, make_float2(-H0.x, -H0.y)), H0);
+  const float vb = fmaf(f.y, HB.y - HB.x, HB.x);
+  const float2 R2 = fadd2_rm(V, make_float2(8388608.f, 8388608.f));
+  r = __float_as_uint(R2.x);
+  g = __float_as_uint(R2.y);
+  b = __float_as_uint(__fadd_rd(vb, 8388608.f));
+}
+
+// Copy bytes [lo, hi) of one 16-byte chunk, smem -> global, both 16-aligned:
+// naturally aligned pieces when the range touches an end of the chunk.
+__device__ __forceinline__ void copy_partial(uint8_t* d, const uint8_t* s, int lo, int hi) {
+  if (hi == 16) {
+    int p = lo;
+    if (p & 1) { d[p] = s[p]; p += 1; }
+    if (p & 2) { *reinterpret_cast<uint16_t*>(d + p) = *reinterpret_cast<const uint16_t*>(s + p); p += 2; }
+    if (p & 4) { *reinterpret_cast<uint32_t*>(d + p) = *reinterpret_cast<const uint32_t*>(s + p); p += 4; }
+    if (p & 8) { *reinterpret_cast<uint2*>(d + p) = *reinterpret_cast<const uint2*>(s + p); }
+  } else if (lo == 0) {
+    int p = 0;
+    if (hi & 8) { *reinterpret_cast<uint2*>(d) = *reinterpret_cast<const uint2*>(s); p = 8; }
+    if (hi & 4) { *reinterpret_cast<uint32_t*>(d + p) = *reinterpret_cast<const uint32_t*>(s + p); p += 4; }
+    if (hi & 2) { *reinterpret_cast<uint16_t*>(d + p) = *reinterpret_cast<const uint16_t*>(s + p); p += 2; }
+    if (hi & 1) d[p] = s[p];
+  } else {
+    for (int b = lo; b < hi; ++b) d[b] = s[b];
+  }
+}
+
+// CTA copy of `rows` buffered rows to global.  Row r's n bytes sit in the
+// buffer at [r*pitch + phase, +n) where phase = (global row address) & 15, so
+// every 16-byte chunk is aligned on both sides.  Full chunks first (kFull =
+// max full chunks per row), then one item per partial head / tail chunk.
+template <int kFull, int NT>
+__device__ __forceinline__ void copy_rows_out(uint8_t* g0, int gpitch, const uint8_t* b0, int bpitch,
+                                              int rows, int n) {
+  for (int it = threadIdx.x; it < rows * kFull; it += NT) {
+    const int r = it / kFull, k = it - r * kFull;
+    uint8_t* grow = g0 + (size_t)r * gpitch;
+    const int o = (int)((uintptr_t)grow & 15);
+    const int c = ((o + 15) >> 4) + k;
+    if (16 * c + 16 <= o + n)
+      __stcs(reinterpret_cast<uint4*>(grow - o + 16 * c),
+             *reinterpret_cast<const uint4*>(b0 + r * bpitch + 16 * c));
+  }
+  for (int it = threadIdx.x; it < 2 * rows; it += NT) {
+    const bool head = it < rows;
+    const int r = head ? it : it - rows;
+    uint8_t* grow = g0 + (size_t)r * gpitch;
+    const int o = (int)((uintptr_t)grow & 15);
+    const uint8_t* s = b0 + r * bpitch;
+    uint8_t* d = grow - o;
+    const int e = o + n;
+    if (head) {  // chunk 0 when the row does not start on a chunk boundary
+      if (o > 0) copy_partial(d, s, o, min(e, 16));
+    } else {     // last chunk when the row does not end on a chunk boundary
+      const int c = e >> 4, hi = e & 15;
+      if (hi > 0 && (c > 0 || o == 0)) copy_partial(d + 16 * c, s + 16 * c, 0, hi);
+    }
+  }
 }
 
 struct TileGeom {
-  int fx0, fy0, S, fw, fh, staged, Sm, ci0, ci1, nvi, P, tail;
-  uint32_t m_nvi, m_P, m_fw, m_copy;
+  int fx0, fy0, S, fw, fh, staged, Sm, ci0, ci1, nrun, P, pad;
+  uint32_t m_fh;  // magic of fh (items are row-major across threads)
 };
 
 struct ImgState {
   double A[6];
-  float Af[4];
+  float Af[4];  // A0, A1, A3, A4
   Map1 m;
   int Wo, Ho, tiles_x, pad;
 };
 
-// smem word offsets (from sm + n_lut * kLutWords)
+// shared-memory byte offsets (from the end of the LUT stages)
 constexpr int kOffIs = 0;
-constexpr int kOffTg = (int)(sizeof(ImgState) + 15) / 16 * 4;
-constexpr int kOffTile = kOffTg + (int)(sizeof(TileGeom) + 15) / 16 * 4;          // RGBx [32][64]
-constexpr int kOffStage = kOffTile + kTileH * kTileW;
-// the packed RGB output tile [64][208] aliases the stage buffer: it is written
-// only after the compute pass has consumed the staged footprint
-static_assert(kTileH * kTilePitch + 16 <= 14040 * 4, "pack must fit in the stage buffer");
+constexpr int kOffTg = (int)(sizeof(ImgState) + 15) / 16 * 16;
+constexpr int kOffOb = kOffTg + (int)(sizeof(TileGeom) + 15) / 16 * 16;
+constexpr int kOffStage = kOffOb + kTileH * kObPitch + 16;  // 16 B slack before the stage
+// after the stage (a.unit_size words + 16 B slack): mask row buffer, mask stage
 
-// kGeneric = false: bilinear, no mask, u8 output (the single-op and cfg5-image
-// fast path) -- the uniform mode branches compile away.
-template <int kOne, bool kGeneric>
-__global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
+// kMode: 0 = fast (bilinear image, u8 output, always staged),
+//        1 = generic (runtime nearest / Normalize / unstaged fallback)
+template <int kOne, bool kMask, int kMode>
+__global__ void __launch_bounds__(kAfThreads, kMask ? 2 : 3) k_affine(StepArgs a) {
   extern __shared__ uint32_t sm[];
+  constexpr bool kGeneric = kMode == 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   StageCtx x;
   init_stages(a, x);
-  const int base = x.n_lut * kLutWords;
-  ImgState* is = reinterpret_cast<ImgState*>(sm + base + kOffIs);
-  TileGeom* tg = reinterpret_cast<TileGeom*>(sm + base + kOffTg);
-  uint32_t* tile = sm + base + kOffTile;
-  uint32_t* stage = sm + base + kOffStage;
-  uint8_t* pack = reinterpret_cast<uint8_t*>(stage);  // aliases stage (see kOffStage)
-  uint8_t* mstage = reinterpret_cast<uint8_t*>(stage + a.unit_size);
+  uint8_t* smb = reinterpret_cast<uint8_t*>(sm + x.n_lut * kLutWords);
+  ImgState* is = reinterpret_cast<ImgState*>(smb + kOffIs);
+  TileGeom* tg = reinterpret_cast<TileGeom*>(smb + kOffTg);
+  uint8_t* obuf = smb + kOffOb;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smb + kOffStage);
+  uint8_t* mobuf = reinterpret_cast<uint8_t*>(stage + a.unit_size) + 16;
+  uint8_t* mstage = mobuf + kTileH * kMobPitch;
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
   const bool nearest = kGeneric && a.interp == ALB_INTERP_NEAREST;
-  const bool has_mask = kGeneric && a.mdst != nullptr;
   const bool normalize = kGeneric && a.normalize;
 
   int u0, u1;
@@ -166,7 +282,7 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
     const Map1 m = is->m;
     const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
     const int tw = min(kTileW, Wo - tx0), th = min(kTileH, Ho - ty0);
-    if (warp == 0) {  // tile geometry: corners on lanes 0-3, division constants on lanes 0-3
+    if (warp == 0) {  // tile geometry: corners on lanes 0-3
       const int xwa = m.ax * tx0 + m.bx, xwb = m.ax * (tx0 + tw - 1) + m.bx;
       const int ywa = m.ay * ty0 + m.by, ywb = m.ay * (ty0 + th - 1) + m.by;
       const double xw0 = min(xwa, xwb), xw1 = max(xwa, xwb), yw0 = min(ywa, ywb), yw1 = max(ywa, ywb);
@@ -183,92 +299,112 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
         ly = fmin(ly, __shfl_xor_sync(0xffffffffu, ly, o));
         hy = fmax(hy, __shfl_xor_sync(0xffffffffu, hy, o));
       }
-      TileGeom t;
-      t.fx0 = (int)floor(lx) - 1;
-      t.fy0 = (int)floor(ly) - 1;
-      t.fw = (int)floor(hx) + 2 - t.fx0 + 1;
-      t.fh = (int)floor(hy) + 2 - t.fy0 + 1;
-      const int want = fabs(A[0] + A[3]) >= fabs(A[0] - A[3]) ? 1 : 31;  // lane step +-(A0 + S*A3)
-      t.S = t.fw + ((want - t.fw % 32) + 32) % 32;
-      t.Sm = (t.fw + 3) & ~3;
-      t.staged = (long long)t.S * t.fh <= a.unit_size &&
-                 (!has_mask || (long long)t.Sm * t.fh <= a.unit_size);
-      t.ci0 = min(max(-t.fx0, 0), t.fw);
-      t.ci1 = min(max(Ws - t.fx0, 0), t.fw);
-      t.nvi = (t.ci1 - t.ci0 + 15) >> 4;  // last run of a row may be partial
-      t.tail = 0;
-      t.P = t.ci0 + (t.fw - t.ci1);        // border columns only
-      // one integer division per lane instead of four in a row
-      const uint32_t dv = lane == 0 ? (uint32_t)t.nvi : lane == 1 ? (uint32_t)t.P
-                        : lane == 2 ? (uint32_t)t.fw : (uint32_t)((3 * tw) >> 4) + 2u;
-      const uint32_t mg = magic_of(dv);
-      t.m_nvi = __shfl_sync(0xffffffffu, mg, 0);
-      t.m_P = __shfl_sync(0xffffffffu, mg, 1);
-      t.m_fw = __shfl_sync(0xffffffffu, mg, 2);
-      t.m_copy = __shfl_sync(0xffffffffu, mg, 3);
-      if (lane == 0) *tg = t;
+      if (lane == 0) {
+        TileGeom t;
+        t.fx0 = (int)floor(lx) - 1;
+        t.fy0 = (int)floor(ly) - 1;
+        t.fw = (int)floor(hx) + 2 - t.fx0 + 1;
+        t.fh = (int)floor(hy) + 2 - t.fy0 + 1;
+        // S = +-1 mod 32: bank = (x +- y) mod 32 for staged pixel (x, y)
+        const int want = fabs(A[0] + A[3]) >= fabs(A[0] - A[3]) ? 1 : 31;
+        t.S = t.fw + ((want - t.fw % 32) + 32) % 32;
+        t.Sm = ((t.fw + 3) >> 2) | 1;  // mask pitch = 4 * odd words
+        t.Sm *= 4;
+        t.staged = (long long)t.S * t.fh <= a.unit_size &&
+                   (!kMask || (long long)t.Sm * t.fh <= kMStageBytes);
+        t.ci0 = min(max(-t.fx0, 0), t.fw);
+        t.ci1 = min(max(Ws - t.fx0, 0), t.fw);
+        t.nrun = (t.ci1 - t.ci0 + 30) >> 4;
+        t.P = t.ci0 + (t.fw - t.ci1);  // border columns only
+        t.m_fh = magic_of((uint32_t)t.fh);
+        *tg = t;
+      }
     }
     __syncthreads();
     const TileGeom t = *tg;
     const uint8_t* simg = a.src + sd.offset;
     if (t.staged) {
-      // pass A: 16-pixel interior runs with 16-byte loads, two runs in flight
-      const int na = t.fh * t.nvi;
-      for (int it = threadIdx.x; it < na; it += 2 * kAfThreads) {
-        uint32_t w[2][12];
-        int dst[2], nw[2];
-        bool live[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int ik = it + k * kAfThreads;
-          live[k] = ik < na;
-          dst[k] = -1;
-          nw[k] = 0;
-          if (live[k]) {
-            const int r = fdiv(ik, t.m_nvi);
-            const int c = t.ci0 + ((ik - r * t.nvi) << 4);
-            nw[k] = min(16, t.ci1 - c);  // partial last run of the row
-            bool row_in;
-            const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
-            dst[k] = r * t.S + c;
-            if (row_in) {
-              const uint8_t* srow = simg + (size_t)ry * sd.pitch;
-              load_window<12>(srow + (size_t)(t.fx0 + c) * 3, srow, srow + (size_t)Ws * 3, w[k]);
-            } else {
-              live[k] = false;  // constant-border row
-              for (int i = 0; i < nw[k]; ++i) stage[dst[k] + i] = a.fill;
-            }
-          }
+      // pass A: interior columns, 16-pixel runs with 16-byte aligned sources;
+      // thread -> (row = it % fh, run = it / fh)
+      const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
+      const int na = t.fh * t.nrun;
+      for (int it = threadIdx.x; it < na; it += kAfThreads) {
+        const int k = fdiv(it, t.m_fh), r = it - k * t.fh;
+        bool row_in;
+        const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+        uint32_t* drow = stage + r * t.S - t.fx0;  // indexed by absolute source column
+        if (!row_in) {  // constant-border row
+          const int e = min(X0 + 16 * k + 16, X1);
+          for (int xx = X0 + 16 * k; xx < e; ++xx) drow[xx] = a.fill;
+          continue;
         }
+        const uint8_t* srow = simg + (size_t)ry * sd.pitch;
+        const int xa = (11 * (16 - (int)((uintptr_t)srow & 15))) & 15;
+        const int xs = X0 - ((X0 - xa) & 15) + 16 * k;
+        if (xs >= X1) continue;
+        const uint8_t* p = srow + 3 * (ptrdiff_t)xs;  // 16-byte aligned
+        const uint8_t* lo = srow + 3 * X0;
+        const uint8_t* hi = srow + 3 * X1;
+        uint32_t w[12];
 #pragma unroll
-        for (int k = 0; k < 2; ++k)
-          if (live[k]) {
-            if (nw[k] == 16) {
+        for (int v = 0; v < 3; ++v) {
+          const uint8_t* q = p + 16 * v;
+          uint4 z = make_uint4(0, 0, 0, 0);
+          if (q < hi && q + 16 > lo) z = __ldg(reinterpret_cast<const uint4*>(q));
+          w[4 * v] = z.x; w[4 * v + 1] = z.y; w[4 * v + 2] = z.z; w[4 * v + 3] = z.w;
+        }
+        uint32_t* d = drow + xs;
+        if (xs >= X0 && xs + 16 <= X1) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) stage[dst[k] + i] = rgbx_of(w[k], i);
-            } else {
+          for (int i = 0; i < 16; ++i) d[i] = rgbx_raw(w, i);
+        } else {  // first / last run of the row: valid-pixel bit mask
+          const int lo_i = max(X0 - xs, 0), hi_i = min(X1 - xs, 16);
+          const uint32_t vm = ((1u << hi_i) - 1u) & ~((1u << lo_i) - 1u);
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (i < nw[k]) stage[dst[k] + i] = rgbx_of(w[k], i);
-            }
-          }
+          for (int i = 0; i < 16; ++i)
+            if (vm & (1u << i)) d[i] = rgbx_raw(w, i);
+        }
       }
       // pass B: border columns, one pixel per thread
       for (int it = threadIdx.x; it < t.fh * t.P; it += kAfThreads) {
-        const int r = fdiv(it, t.m_P);
-        const int j = it - r * t.P;
+        const int j = fdiv(it, t.m_fh), r = it - j * t.fh;
         const int c = j < t.ci0 ? j : t.ci1 + (j - t.ci0);
         bool row_in, col_in;
         const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
         const int rx = border_idx(t.fx0 + c, Ws, reflect, col_in);
         stage[r * t.S + c] = (row_in && col_in) ? fetch_rgb(simg + (size_t)ry * sd.pitch, rx) : a.fill;
       }
-      if (has_mask) {
+      if constexpr (kMask) {
         const uint8_t* smk = a.msrc + a.msdesc[img].offset;
         const int mpitch = a.msdesc[img].pitch;
-        for (int it = threadIdx.x; it < t.fh * t.fw; it += kAfThreads) {
-          const int r = fdiv(it, t.m_fw);
-          const int c = it - r * t.fw;
+        const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
+        const int na = t.fh * t.nrun;
+        for (int it = threadIdx.x; it < na; it += kAfThreads) {
+          const int k = fdiv(it, t.m_fh), r = it - k * t.fh;
+          bool row_in;
+          const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+          uint8_t* drow = mstage + r * t.Sm - t.fx0;
+          if (!row_in) {
+            const int e = min(X0 + 16 * k + 16, X1);
+            for (int xx = X0 + 16 * k; xx < e; ++xx) drow[xx] = (uint8_t)a.mask_fill;
+            continue;
+          }
+          const uint8_t* mrow = smk + (size_t)ry * mpitch;
+          const int xa = (16 - (int)((uintptr_t)mrow & 15)) & 15;
+          const int xs = X0 - ((X0 - xa) & 15) + 16 * k;
+          if (xs >= X1) continue;
+          const uint4 z = __ldg(reinterpret_cast<const uint4*>(mrow + xs));  // intersects [X0, X1)
+          const uint32_t w4[4] = {z.x, z.y, z.z, z.w};
+          uint8_t* d = drow + xs;
+          const int lo_i = max(X0 - xs, 0), hi_i = min(X1 - xs, 16);
+          const uint32_t vm = ((1u << hi_i) - 1u) & ~((1u << lo_i) - 1u);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (vm & (1u << i)) d[i] = (uint8_t)(w4[i >> 2] >> (8 * (i & 3)));
+        }
+        for (int it = threadIdx.x; it < t.fh * t.P; it += kAfThreads) {
+          const int j = fdiv(it, t.m_fh), r = it - j * t.fh;
+          const int c = j < t.ci0 ? j : t.ci1 + (j - t.ci0);
           bool row_in, col_in;
           const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
           const int rx = border_idx(t.fx0 + c, Ws, reflect, col_in);
@@ -280,107 +416,84 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
     // ---- compute: warp owns kRowsPerWarp rows; lane = columns lane, lane + 32
     const float A0f = is->Af[0], A1f = is->Af[1], A3f = is->Af[2], A4f = is->Af[3];
     const double* A = is->A;
+    const float2 A14 = make_float2(A1f, A4f);
+    const int ncol = tw > 32 ? 2 : 1;
     int xw[2];
-    float dxl[2];
-    int cur_cy[2] = {-0x7fffffff, -0x7fffffff};
-    int abase[2] = {0, 0}, aix[2] = {0, 0}, aiy[2] = {0, 0};
-    float afx[2] = {0.f, 0.f}, afy[2] = {0.f, 0.f};
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      xw[j] = m.ax * min(tx0 + lane + 32 * j, Wo - 1) + m.bx;
-      dxl[j] = (float)(xw[j] & 15);
+    for (int j = 0; j < 2; ++j) xw[j] = m.ax * min(tx0 + lane + 32 * j, Wo - 1) + m.bx;
+    int cur_cy = -0x7fffffff;
+    float2 bxy[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    uint32_t c0[2] = {0u, 0u}, mc0[2] = {0u, 0u};
+    int aix[2] = {0, 0}, aiy[2] = {0, 0};
+    uint8_t* drow0 = nullptr;
+    int dpitch = 0;
+    if (!normalize) {
+      const alb_image_desc dd = a.ddesc[img];
+      drow0 = a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3;
+      dpitch = dd.pitch;
     }
-    if constexpr (!kGeneric) {
-      // fast path (always staged, bilinear, u8 out): the lane's two pixels are
-      // independent chains interleaved for ILP; columns >= tw compute clamped
-      // garbage that the copy-out never reads.
-      for (int i = 0; i < kRowsPerWarp; ++i) {
-        const int row = warp * kRowsPerWarp + i;
-        if (row >= th) break;
-        const int yw = m.ay * (ty0 + row) + m.by;
-        const float dyl = (float)(yw & 15);
-        if ((yw >> 4) != cur_cy[0]) {  // warp-uniform: both columns share the cell row
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            cur_cy[j] = yw >> 4;
-            const double xa = (double)((xw[j] >> 4) * 16), ya = (double)(cur_cy[j] * 16);
-            const double sx = fma(A[0], xa, fma(A[1], ya, A[2]));
-            const double sy = fma(A[3], xa, fma(A[4], ya, A[5]));
-            const double flx = floor(sx), fly = floor(sy);
-            afx[j] = (float)(sx - flx); afy[j] = (float)(sy - fly);
-            abase[j] = ((int)fly - t.fy0) * t.S + ((int)flx - t.fx0);
-          }
-        }
-        float fx[2], fy[2];
-        int idx[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const float lx = fmaf(A0f, dxl[j], fmaf(A1f, dyl, afx[j]));
-          const float ly = fmaf(A3f, dxl[j], fmaf(A4f, dyl, afy[j]));
-          const int qx = floor_frac(lx, fx[j]), qy = floor_frac(ly, fy[j]);
-          idx[j] = abase[j] + qy * t.S + qx;
-        }
-        uint32_t tp[2][4];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          tp[j][0] = stage[idx[j]];
-          tp[j][1] = stage[idx[j] + 1];
-          tp[j][2] = stage[idx[j] + t.S];
-          tp[j][3] = stage[idx[j] + t.S + 1];
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          uint32_t px = bilerp_rgbx(tp[j][0], tp[j][1], tp[j][2], tp[j][3], fx[j], fy[j]);
-          if (kOne != kStagesNone) {
-            uint32_t r = px & 0xff, g = (px >> 8) & 0xff, b = (px >> 16) & 0xff;
-            apply_stages_t<kOne>(x, sm, lane, r, g, b);
-            px = r | (g << 8) | (b << 16);
-          }
-          tile[row * kTileW + lane + 32 * j] = px;
-        }
-      }
-    } else
+    uint8_t* mrow0 = nullptr;
+    int mdpitch = 0;
+    if constexpr (kMask) {
+      const alb_image_desc mdd = a.mddesc[img];
+      mrow0 = a.mdst + mdd.offset + (size_t)ty0 * mdd.pitch + tx0;
+      mdpitch = mdd.pitch;
+    }
+    const uint32_t* stg = stage;
     for (int i = 0; i < kRowsPerWarp; ++i) {
       const int row = warp * kRowsPerWarp + i;
       if (row >= th) break;
-      const int yo = ty0 + row;
-      const int yw = m.ay * yo + m.by;
+      const int yw = m.ay * (ty0 + row) + m.by;
+      if ((yw >> 4) != cur_cy) {  // warp-uniform: fp64 anchors of this cell row
+        cur_cy = yw >> 4;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j < ncol) {
+            const Anchor an = cell_anchor(A, A0f, A3f, xw[j], cur_cy);
+            bxy[j] = make_float2(an.bx, an.by);
+            aix[j] = an.ix; aiy[j] = an.iy;
+            const int base = (an.iy - t.fy0) * t.S + (an.ix - t.fx0);
+            c0[j] = (uint32_t)base - kMagic15Bits * (uint32_t)(t.S + 1);
+            if constexpr (kMask) {
+              const int mb = (an.iy - t.fy0) * t.Sm + (an.ix - t.fx0);
+              mc0[j] = (uint32_t)mb - kMagic15Bits * (uint32_t)(t.Sm + 1);
+            }
+          }
+        }
+      }
       const float dyl = (float)(yw & 15);
+      uint8_t* orow = obuf + row * kObPitch + (int)((uintptr_t)(drow0 + (size_t)row * dpitch) & 15);
+      uint8_t* morow = nullptr;
+      if constexpr (kMask) morow = mobuf + row * kMobPitch + (int)((uintptr_t)(mrow0 + (size_t)row * mdpitch) & 15);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
+        if (j >= ncol) break;
         const int c = lane + 32 * j;
-        if (j == 1 && tw <= 32) break;
-        if ((yw >> 4) != cur_cy[j]) {  // fp64 anchor of this column's 16x16 cell
-          cur_cy[j] = yw >> 4;
-          const double xa = (double)((xw[j] >> 4) * 16), ya = (double)(cur_cy[j] * 16);
-          const double sx = fma(A[0], xa, fma(A[1], ya, A[2]));
-          const double sy = fma(A[3], xa, fma(A[4], ya, A[5]));
-          const double flx = floor(sx), fly = floor(sy);
-          aix[j] = (int)flx; aiy[j] = (int)fly;
-          afx[j] = (float)(sx - flx); afy[j] = (float)(sy - fly);
-          abase[j] = (aiy[j] - t.fy0) * t.S + (aix[j] - t.fx0);
-        }
-        const float lx = fmaf(A0f, dxl[j], fmaf(A1f, dyl, afx[j]));
-        const float ly = fmaf(A3f, dxl[j], fmaf(A4f, dyl, afy[j]));
-        uint32_t px;
-        if (nearest) {
-          float f0, f1;
-          const int qx = floor_frac(lx + 0.5f, f0), qy = floor_frac(ly + 0.5f, f1);
-          if (t.staged) {
-            px = stage[abase[j] + qy * t.S + qx];
-          } else {
-            bool ri, ci;
-            const int yy = border_idx(aiy[j] + qy, Hs, reflect, ri);
-            const int xx = border_idx(aix[j] + qx, Ws, reflect, ci);
-            px = (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
-          }
+        const float2 l = __ffma2_rn(A14, make_float2(dyl, dyl), bxy[j]);
+        const float2 tq = fadd2_rm(l, make_float2(kMagic15, kMagic15));  // floor + 1.5*2^23
+        const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
+        const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));     // fractions
+        const uint32_t qxb = __float_as_uint(tq.x), qyb = __float_as_uint(tq.y);
+        uint32_t r, g, b;
+        if (!kGeneric || (!nearest && t.staged)) {
+          const uint32_t idx = qyb * (uint32_t)t.S + qxb + c0[j];
+          const uint32_t* p0 = stg + idx;
+          const uint32_t* p1 = p0 + t.S;
+          bilerp3(p0[0], p0[1], p1[0], p1[1], fr, r, g, b);
         } else {
-          float fx, fy;
-          const int qx = floor_frac(lx, fx), qy = floor_frac(ly, fy);
-          uint32_t t00, t10, t01, t11;
-          if (!kGeneric || t.staged) {
-            const int idx = abase[j] + qy * t.S + qx;
-            t00 = stage[idx]; t10 = stage[idx + 1]; t01 = stage[idx + t.S]; t11 = stage[idx + t.S + 1];
+          const int qx = (int)(qxb - kMagic15Bits), qy = (int)(qyb - kMagic15Bits);
+          if (nearest) {
+            const int nx = qx + (fr.x >= 0.5f), ny = qy + (fr.y >= 0.5f);
+            uint32_t px;
+            if (t.staged) {
+              px = stg[(aiy[j] + ny - t.fy0) * t.S + (aix[j] + nx - t.fx0)];
+            } else {
+              bool ri, ci;
+              const int yy = border_idx(aiy[j] + ny, Hs, reflect, ri);
+              const int xx = border_idx(aix[j] + nx, Ws, reflect, ci);
+              px = (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
+            }
+            r = px & 0xff; g = (px >> 8) & 0xff; b = (px >> 16) & 0xff;
           } else {
             auto tap = [&](int px_, int py_) -> uint32_t {
               bool ri, ci;
@@ -388,83 +501,436 @@ __global__ void __launch_bounds__(kAfThreads, 3) k_affine(StepArgs a) {
               return (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
             };
             const int X = aix[j] + qx, Y = aiy[j] + qy;
-            t00 = tap(X, Y); t10 = tap(X + 1, Y); t01 = tap(X, Y + 1); t11 = tap(X + 1, Y + 1);
+            bilerp3(tap(X, Y), tap(X + 1, Y), tap(X, Y + 1), tap(X + 1, Y + 1), fr, r, g, b);
           }
-          px = bilerp_rgbx(t00, t10, t01, t11, fx, fy);
         }
-        if (kOne != kStagesNone) {
-          uint32_t r = px & 0xff, g = (px >> 8) & 0xff, b = (px >> 16) & 0xff;
+        if constexpr (kOne != kStagesNone) {
+          r &= 0xffu; g &= 0xffu; b &= 0xffu;
           apply_stages_t<kOne>(x, sm, lane, r, g, b);
-          px = r | (g << 8) | (b << 16);
         }
         if (normalize) {
-          const size_t plane = (size_t)Ho * Wo;
-          float* o = a.nchw + (size_t)img * 3 * plane + (size_t)yo * Wo + tx0 + c;
-          const float* nl = a.tab.norm_lut;
-          __stcs(o, nl[px & 0xff]);
-          __stcs(o + plane, nl[256 + ((px >> 8) & 0xff)]);
-          __stcs(o + 2 * plane, nl[512 + ((px >> 16) & 0xff)]);
+          if (c < tw) {
+            const size_t plane = (size_t)Ho * Wo;
+            float* o = a.nchw + (size_t)img * 3 * plane + (size_t)(ty0 + row) * Wo + tx0 + c;
+            const float* nl = a.tab.norm_lut;
+            __stcs(o, nl[r & 0xff]);
+            __stcs(o + plane, nl[256 + (g & 0xff)]);
+            __stcs(o + 2 * plane, nl[512 + (b & 0xff)]);
+          }
         } else {
-          tile[row * kTileW + c] = px;
+          orow[3 * c] = (uint8_t)r;
+          orow[3 * c + 1] = (uint8_t)g;
+          orow[3 * c + 2] = (uint8_t)b;
         }
-        if (has_mask) {
-          float f0, f1;
-          const int qx = floor_frac(lx + 0.5f, f0), qy = floor_frac(ly + 0.5f, f1);
+        if constexpr (kMask) {
+          const uint32_t nxb = qxb + (fr.x >= 0.5f ? 1u : 0u), nyb = qyb + (fr.y >= 0.5f ? 1u : 0u);
           uint8_t v;
           if (t.staged) {
-            v = mstage[(aiy[j] + qy - t.fy0) * t.Sm + (aix[j] + qx - t.fx0)];
+            v = mstage[nyb * (uint32_t)t.Sm + nxb + mc0[j]];
           } else {
             bool ri, ci;
-            const int yy = border_idx(aiy[j] + qy, Hs, reflect, ri);
-            const int xx = border_idx(aix[j] + qx, Ws, reflect, ci);
+            const int yy = border_idx(aiy[j] + (int)(nyb - kMagic15Bits), Hs, reflect, ri);
+            const int xx = border_idx(aix[j] + (int)(nxb - kMagic15Bits), Ws, reflect, ci);
             v = (ri && ci) ? a.msrc[a.msdesc[img].offset + (size_t)yy * a.msdesc[img].pitch + xx]
                            : (uint8_t)a.mask_fill;
           }
-          if (c < tw) {
-            const alb_image_desc mdd = a.mddesc[img];
-            a.mdst[mdd.offset + (size_t)yo * mdd.pitch + tx0 + c] = v;
+          morow[c] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (!normalize)
+      copy_rows_out<kObFull, kAfThreads>(drow0, dpitch, obuf, kObPitch, th, 3 * tw);
+    if constexpr (kMask)
+      copy_rows_out<kMobFull, kAfThreads>(mrow0, mdpitch, mobuf, kMobPitch, th, tw);
+  }
+}
+
+
+// ===================================================== pipelined fast path
+// Bilinear, no mask, u8 output, scale >= 0.9 (the single-op Rotate / SSR
+// path and any fused post crop / flip).  The footprint rows of tile t+1 are
+// fetched by the TMA engine (cp.async.bulk, one 16-byte aligned row range
+// per footprint row, completion on an mbarrier) into a RAW byte buffer while
+// the CTA computes tile t, so no warp waits on global loads.  Warps 0-10
+// compute, warp 11 is the producer.  Per tile t:
+//   P: compute warps: wait raw(t); raw RGB -> RGBx stage (aligned 16-pixel
+//      runs, 3 LDS.128 + 16 byte permutes); border columns; anchor table
+//      (fp64 anchor per column x cell row); copy-out of tile t-1.
+//      producer: geometry of tile t+1 (per-image state precomputed by
+//      k_affine_setup).                                        -- barrier
+//   C: compute warps: tile t, two rows x two columns per lane in flight.
+//      producer: TMA row copies of tile t+1 into the (now free) raw buffer.
+//                                                              -- barrier
+constexpr int kPThreads = 384;
+constexpr int kPWarps = kPThreads / 32;
+constexpr int kCW = kPWarps - 1;      // compute warps
+constexpr int kCThreads = kCW * 32;
+constexpr int kRawPitch = 368;        // >= 3*103 + 30 bytes; pitch/16 odd (LDS.128 banks)
+constexpr int kRawRows = 104;
+constexpr int kRawSlack = 64;
+constexpr int kPStageWords = 13416;   // S <= 129, fh <= 104 at scale >= 0.9
+constexpr int kAnCells = 5;           // cell rows a 64-row tile spans
+
+struct AnEnt {
+  float bx, by;
+  uint32_t c0;
+  int pad;
+};
+
+struct TileCtx {
+  ImgState is;
+  TileGeom t;
+  uint8_t* drow0;
+  int img, tx0, ty0, tw, th, cy0, ncy, dpitch;
+};
+
+static_assert(sizeof(ImgState) <= kGeoBytes, "ImgState must fit the per-image scratch");
+
+constexpr int kPOffCtx = 0;                                            // 3 x TileCtx
+constexpr int kPCtxBytes = (int)(sizeof(TileCtx) + 15) / 16 * 16;
+constexpr int kPOffBar = 3 * kPCtxBytes;                               // mbarrier
+constexpr int kPOffAn = kPOffBar + 16;                                 // AnEnt[kAnCells][64]
+constexpr int kPOffOb = kPOffAn + kAnCells * 64 * (int)sizeof(AnEnt);  // output rows
+constexpr int kPOffRaw = kPOffOb + kTileH * kObPitch + kRawSlack;      // raw rows
+constexpr int kPOffStage = kPOffRaw + kRawRows * kRawPitch + kRawSlack;
+constexpr int kPSmem = kPOffStage + kPStageWords * 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+// Per-image state of the affine step (one thread per image), read by the
+// producer warp whenever a tile starts a new image.
+__global__ void k_affine_setup(StepArgs a) {
+  const int img = blockIdx.x * blockDim.x + threadIdx.x;
+  if (img >= a.n_img) return;
+  const AfCoef cf = af_coef(a, img);
+  ImgState s;
+  for (int k = 0; k < 6; ++k) s.A[k] = cf.A[k];
+  s.Af[0] = (float)cf.A[0]; s.Af[1] = (float)cf.A[1];
+  s.Af[2] = (float)cf.A[3]; s.Af[3] = (float)cf.A[4];
+  s.Wo = a.ddesc[img].width;
+  s.Ho = a.ddesc[img].height;
+  s.m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, s.Wo, s.Ho);
+  s.tiles_x = (s.Wo + kTileW - 1) / kTileW;
+  s.pad = 0;
+  *reinterpret_cast<ImgState*>(reinterpret_cast<uint8_t*>(a.geo) + (size_t)img * kGeoBytes) = s;
+}
+
+// Producer warp, phase P: geometry of unit u into c.
+__device__ __forceinline__ void pipe_geom(const StepArgs& a, int u, TileCtx* c, const TileCtx* prev, int lane) {
+  const int2 unit = __ldg(a.units + u);
+  const int img = unit.x;
+  if (prev == nullptr || prev->img != img) {
+    constexpr int kW = (int)sizeof(ImgState) / 4;
+    const uint32_t* g = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.geo) +
+                                                          (size_t)img * kGeoBytes);
+    if (lane < kW) reinterpret_cast<uint32_t*>(&c->is)[lane] = __ldcg(g + lane);
+  } else if (lane == 0) {
+    c->is = prev->is;
+  }
+  __syncwarp();
+  const Map1 m = c->is.m;
+  const int Wo = c->is.Wo, Ho = c->is.Ho;
+  const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
+  const int tw = min(kTileW, Wo - tx0), th = min(kTileH, Ho - ty0);
+  const int xwa = m.ax * tx0 + m.bx, xwb = m.ax * (tx0 + tw - 1) + m.bx;
+  const int ywa = m.ay * ty0 + m.by, ywb = m.ay * (ty0 + th - 1) + m.by;
+  const double xw0 = min(xwa, xwb), xw1 = max(xwa, xwb), yw0 = min(ywa, ywb), yw1 = max(ywa, ywb);
+  const double* A = c->is.A;
+  const int cc = lane & 3;
+  const double xw = (cc & 1) ? xw1 : xw0, yw = (cc & 2) ? yw1 : yw0;
+  const double sx = fma(A[0], xw, fma(A[1], yw, A[2]));
+  const double sy = fma(A[3], xw, fma(A[4], yw, A[5]));
+  double lx = sx, hx = sx, ly = sy, hy = sy;
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {
+    lx = fmin(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+    hx = fmax(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+    ly = fmin(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+    hy = fmax(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+  }
+  if (lane == 0) {
+    const int Ws = a.sdesc[img].width;
+    TileGeom t;
+    t.fx0 = (int)floor(lx) - 1;
+    t.fy0 = (int)floor(ly) - 1;
+    t.fw = (int)floor(hx) + 2 - t.fx0 + 1;
+    t.fh = (int)floor(hy) + 2 - t.fy0 + 1;
+    const int want = fabs(A[0] + A[3]) >= fabs(A[0] - A[3]) ? 1 : 31;
+    t.S = t.fw + ((want - t.fw % 32) + 32) % 32;
+    t.Sm = 0;
+    t.staged = 1;
+    t.ci0 = min(max(-t.fx0, 0), t.fw);
+    t.ci1 = min(max(Ws - t.fx0, 0), t.fw);
+    t.nrun = (t.ci1 - t.ci0 + 30) >> 4;
+    t.P = t.ci0 + (t.fw - t.ci1);
+    t.pad = 0;
+    t.m_fh = magic_of((uint32_t)t.fh);
+    c->t = t;
+    c->img = img; c->tx0 = tx0; c->ty0 = ty0; c->tw = tw; c->th = th;
+    c->cy0 = min(ywa, ywb) >> 4;
+    c->ncy = (max(ywa, ywb) >> 4) - c->cy0 + 1;
+    const alb_image_desc dd = a.ddesc[img];
+    c->drow0 = a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3;
+    c->dpitch = dd.pitch;
+  }
+  __syncwarp();
+}
+
+// Producer warp, phase C: TMA row copies of c's footprint, row r ->
+// raw + r * kRawPitch, completion counted on `bar`.
+__device__ __forceinline__ void pipe_issue(const StepArgs& a, const TileCtx* c, uint8_t* raw, uint32_t bar,
+                                           int lane) {
+  const TileGeom t = c->t;
+  const alb_image_desc sd = a.sdesc[c->img];
+  const uint8_t* simg = a.src + sd.offset;
+  const bool reflect = a.border == ALB_BORDER_REFLECT_101;
+  const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
+  uint32_t bytes = 0;
+  if (X1 > X0) {
+    for (int r = lane; r < t.fh; r += 32) {
+      bool row_in;
+      const int ry = border_idx(t.fy0 + r, sd.height, reflect, row_in);
+      if (!row_in) continue;
+      const uintptr_t g0 = (uintptr_t)(simg + (size_t)ry * sd.pitch + 3 * X0);
+      const uintptr_t g1 = (uintptr_t)(simg + (size_t)ry * sd.pitch + 3 * X1);
+      const uintptr_t ga = g0 & ~(uintptr_t)15, gb = (g1 + 15) & ~(uintptr_t)15;
+      const uint32_t nb = (uint32_t)(gb - ga);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              smem_u32(raw + r * kRawPitch)),
+          "l"(ga), "r"(nb), "r"(bar)
+          : "memory");
+      bytes += nb;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+  __syncwarp();
+}
+
+template <int kOne>
+__global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
+  extern __shared__ uint32_t sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool producer = warp == kPWarps - 1;
+  StageCtx x;
+  init_stages(a, x);
+  uint8_t* smb = reinterpret_cast<uint8_t*>(sm + x.n_lut * kLutWords);
+  TileCtx* ctx = reinterpret_cast<TileCtx*>(smb + kPOffCtx);
+  const uint32_t bar = smem_u32(smb + kPOffBar);
+  AnEnt* an = reinterpret_cast<AnEnt*>(smb + kPOffAn);
+  uint8_t* obuf = smb + kPOffOb;
+  uint8_t* raw = smb + kPOffRaw;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smb + kPOffStage);
+  const bool reflect = a.border == ALB_BORDER_REFLECT_101;
+
+  int u0, u1;
+  unit_range(a.n_units, u0, u1);
+  if (u0 >= u1) return;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (producer) {
+    pipe_geom(a, u0, &ctx[0], nullptr, lane);
+    pipe_issue(a, &ctx[0], raw, bar, lane);
+  }
+  __syncthreads();
+  int lut_img = -1;
+  for (int u = u0; u < u1; ++u) {
+    const int it_t = u - u0;
+    const TileCtx& c = ctx[it_t % 3];
+    const TileGeom t = c.t;
+    const int img = c.img;
+    if (kOne != kStagesNone && img != lut_img) {
+      load_stages(a, img, sm, x, kPThreads);  // LUTs are read only in phase C
+      lut_img = img;
+    }
+    // ---------------- phase P
+    if (producer) {
+      if (u + 1 < u1) pipe_geom(a, u + 1, &ctx[(it_t + 1) % 3], &c, lane);
+    } else {
+      const int tid = threadIdx.x;
+      if (it_t > 0) {  // copy-out of the previous tile
+        const TileCtx& p = ctx[(it_t + 2) % 3];
+        copy_rows_out<kObFull, kCThreads>(p.drow0, p.dpitch, obuf, kObPitch, p.th, 3 * p.tw);
+      }
+      {  // anchor table: (cell row q, column) -> fp32 offsets + tap base
+        const double* A = c.is.A;
+        const float A0f = c.is.Af[0], A3f = c.is.Af[2];
+        const Map1 m = c.is.m;
+        for (int e = tid; e < 64 * c.ncy; e += kCThreads) {
+          const int col = e & 63, q = e >> 6;
+          const int xw = m.ax * min(c.tx0 + col, c.is.Wo - 1) + m.bx;
+          const Anchor ae = cell_anchor(A, A0f, A3f, xw, c.cy0 + q);
+          AnEnt en;
+          en.bx = ae.bx;
+          en.by = ae.by;
+          en.c0 = (uint32_t)((ae.iy - t.fy0) * t.S + (ae.ix - t.fx0)) - kMagic15Bits * (uint32_t)(t.S + 1);
+          en.pad = 0;
+          an[e] = en;
+        }
+      }
+      const alb_image_desc sd = a.sdesc[img];
+      const int Ws = sd.width, Hs = sd.height;
+      const uint8_t* simg = a.src + sd.offset;
+      // border columns from global (tiles at the image's left / right edge)
+      for (int it = tid; it < t.fh * t.P; it += kCThreads) {
+        const int j = fdiv(it, t.m_fh), r = it - j * t.fh;
+        const int cc = j < t.ci0 ? j : t.ci1 + (j - t.ci0);
+        bool row_in, col_in;
+        const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+        const int rx = border_idx(t.fx0 + cc, Ws, reflect, col_in);
+        stage[r * t.S + cc] = (row_in && col_in) ? fetch_rgb(simg + (size_t)ry * sd.pitch, rx) : a.fill;
+      }
+      mbar_wait(bar, (uint32_t)(it_t & 1));
+      // raw RGB rows -> RGBx stage; thread -> (row = it % fh, run = it / fh)
+      const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
+      const int na = t.fh * t.nrun;
+      for (int it = tid; it < na; it += kCThreads) {
+        const int k = fdiv(it, t.m_fh), r = it - k * t.fh;
+        bool row_in;
+        const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
+        uint32_t* drow = stage + r * t.S - t.fx0;
+        if (!row_in) {
+          const int e = min(X0 + 16 * k + 16, X1);
+          for (int xx = X0 + 16 * k; xx < e; ++xx) drow[xx] = a.fill;
+          continue;
+        }
+        const uintptr_t srow = (uintptr_t)(simg + (size_t)ry * sd.pitch);
+        const int xa = (11 * (16 - (int)(srow & 15))) & 15;
+        const int xs = X0 - ((X0 - xa) & 15) + 16 * k;
+        if (xs >= X1) continue;
+        const uintptr_t ga = (srow + 3 * X0) & ~(uintptr_t)15;
+        const int off = (int)((intptr_t)(srow + 3 * (intptr_t)xs) - (intptr_t)ga);  // multiple of 16
+        const uint4* q = reinterpret_cast<const uint4*>(raw + r * kRawPitch + off);
+        uint32_t w[12];
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          const uint4 z = q[v];
+          w[4 * v] = z.x; w[4 * v + 1] = z.y; w[4 * v + 2] = z.z; w[4 * v + 3] = z.w;
+        }
+        uint32_t* d = drow + xs;
+        if (xs >= X0 && xs + 16 <= X1) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) d[i] = rgbx_raw(w, i);
+        } else {
+          const int lo_i = max(X0 - xs, 0), hi_i = min(X1 - xs, 16);
+          const uint32_t vm = ((1u << hi_i) - 1u) & ~((1u << lo_i) - 1u);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (vm & (1u << i)) d[i] = rgbx_raw(w, i);
+        }
+      }
+    }
+    __syncthreads();
+    // ---------------- phase C
+    if (producer) {
+      if (u + 1 < u1) pipe_issue(a, &ctx[(it_t + 1) % 3], raw, bar, lane);
+    } else {
+      const float2 A14 = make_float2(c.is.Af[1], c.is.Af[3]);
+      const Map1 m = c.is.m;
+      const int th = c.th, ncol = c.tw > 32 ? 2 : 1;
+      const uint8_t* drow0 = c.drow0;
+      const int dpitch = c.dpitch;
+      // two rows (row, row + kCW) per iteration: 4 independent pixels per lane
+      for (int r0 = warp; r0 < th; r0 += 2 * kCW) {
+        const bool two = r0 + kCW < th;
+        float dyl[2];
+        int q[2];
+        uint8_t* orow[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = two || h == 0 ? r0 + h * kCW : r0;
+          const int yw = m.ay * (c.ty0 + row) + m.by;
+          q[h] = (yw >> 4) - c.cy0;
+          dyl[h] = (float)(yw & 15);
+          orow[h] = obuf + row * kObPitch + (int)((uintptr_t)(drow0 + (size_t)row * dpitch) & 15);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j >= ncol) break;
+          const int col = lane + 32 * j;
+          uint32_t rr[2], gg[2], bb[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const AnEnt e = an[q[h] * 64 + col];
+            const float2 l = __ffma2_rn(A14, make_float2(dyl[h], dyl[h]), make_float2(e.bx, e.by));
+            const float2 tq = fadd2_rm(l, make_float2(kMagic15, kMagic15));
+            const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
+            const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
+            const uint32_t idx = __float_as_uint(tq.y) * (uint32_t)t.S + __float_as_uint(tq.x) + e.c0;
+            const uint32_t* p0 = stage + idx;
+            const uint32_t* p1 = p0 + t.S;
+            bilerp3(p0[0], p0[1], p1[0], p1[1], fr, rr[h], gg[h], bb[h]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t r = rr[h], g = gg[h], b = bb[h];
+            if constexpr (kOne != kStagesNone) {
+              r &= 0xffu; g &= 0xffu; b &= 0xffu;
+              apply_stages_t<kOne>(x, sm, lane, r, g, b);
+            }
+            if (h == 0 || two) {
+              orow[h][3 * col] = (uint8_t)r;
+              orow[h][3 * col + 1] = (uint8_t)g;
+              orow[h][3 * col + 2] = (uint8_t)b;
+            }
           }
         }
       }
     }
-    if (!normalize) {
-      __syncthreads();
-      // repack RGBx -> RGB: 4 pixels (one 16-byte read) -> 12 bytes per thread item
-      for (int it = threadIdx.x; it < kTileH * (kTileW / 4); it += kAfThreads) {
-        const int r = it >> 4, q = it & 15;
-        const uint4 v = *reinterpret_cast<const uint4*>(tile + r * kTileW + 4 * q);
-        uint32_t* d = reinterpret_cast<uint32_t*>(pack + r * kTilePitch + 12 * q);
-        d[0] = __byte_perm(v.x, v.y, 0x4210);
-        d[1] = __byte_perm(v.y, v.z, 0x5421);
-        d[2] = __byte_perm(v.z, v.w, 0x6542);
-      }
-      __syncthreads();
-      const alb_image_desc dd = a.ddesc[img];
-      cta_copy_rows(a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3, dd.pitch, pack,
-                    kTilePitch, th, 3 * tw, kAfThreads, t.m_copy);
-    }
+    __syncthreads();
+  }
+  if (!producer) {
+    const TileCtx& p = ctx[(u1 - 1 - u0) % 3];
+    copy_rows_out<kObFull, kCThreads>(p.drow0, p.dpitch, obuf, kObPitch, p.th, 3 * p.tw);
   }
 }
 
 static size_t affine_smem(const StepArgs& a) {
-  return ((size_t)count_lut_stages(a) * kLutWords + kOffStage) * 4 + (size_t)a.unit_size * 4 +
-         (a.mdst ? (size_t)a.unit_size : 0);
+  return (size_t)count_lut_stages(a) * kLutWords * 4 + kOffStage + (size_t)a.unit_size * 4 + 16 +
+         (a.mdst ? (size_t)(kTileH * kMobPitch + kMStageBytes) : 0);
 }
 
-template <int kOne, bool kGeneric>
+template <int kOne, bool kMask, int kMode>
 static void launch_affine_v(const StepArgs& a, size_t smem, cudaStream_t s) {
-  const int grid = persistent_grid((const void*)k_affine<kOne, kGeneric>, kAfThreads, smem, a.n_units);
-  k_affine<kOne, kGeneric><<<grid, kAfThreads, smem, s>>>(a);
+  const int grid = persistent_grid((const void*)k_affine<kOne, kMask, kMode>, kAfThreads, smem, a.n_units);
+  k_affine<kOne, kMask, kMode><<<grid, kAfThreads, smem, s>>>(a);
 }
 
 template <int kOne>
 static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
-  // fast variant always stages: a 64x64 tile's footprint (+halo) is at most
-  // (63*sqrt2/s + 5 + 31) x (63*sqrt2/s + 5) words, <= 14040 <= a.unit_size for s >= 0.9
-  const bool generic = a.interp == ALB_INTERP_NEAREST || a.mdst != nullptr || a.normalize ||
-                       a.min_scale < 0.9f || a.unit_size < 14040;
-  if (generic) launch_affine_v<kOne, true>(a, smem, s);
-  else launch_affine_v<kOne, false>(a, smem, s);
+  // fast variant always stages: a 64x64 tile's footprint (+halo) at scale
+  // >= 0.9 is at most fw, fh <= 104 and S <= fw + 31, i.e. <= 14040 words
+  const bool generic = a.interp == ALB_INTERP_NEAREST || a.normalize || a.min_scale < 0.9f ||
+                       a.unit_size < 14040;
+  const bool mask = a.mdst != nullptr;
+  if (generic) {
+    if (mask) launch_affine_v<kOne, true, 1>(a, smem, s);
+    else launch_affine_v<kOne, false, 1>(a, smem, s);
+  } else if (mask) {
+    launch_affine_v<kOne, true, 0>(a, smem, s);
+  } else {  // pipelined TMA-staged path
+    k_affine_setup<<<(a.n_img + 127) / 128, 128, 0, s>>>(a);
+    const size_t psmem = (size_t)count_lut_stages(a) * kLutWords * 4 + kPSmem;
+    const int grid = persistent_grid((const void*)k_affine_pipe<kOne>, kPThreads, psmem, a.n_units);
+    k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(a);
+  }
 }
 
 void launch_affine(const StepArgs& a, cudaStream_t s) {

@@ -55,7 +55,11 @@ struct StepArgs {
   float min_scale;         // affine: smallest scale the op can draw (footprint bound)
   Tables tab;
   const alb_op* ops;
+  void* geo;  // workspace scratch: per-image affine state, kGeoBytes each
+  int32_t n_img;  // images in the batch
 };
+
+constexpr int kGeoBytes = 128;
 
 // Equalize (R15): histogram + LUT.
 struct EqArgs {

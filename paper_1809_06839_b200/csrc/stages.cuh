@@ -334,6 +334,13 @@ __device__ __forceinline__ uint32_t rgbx_of(const uint32_t (&w)[12], int i) {
   return __byte_perm(w[q], hi, (uint32_t)k * 0x111u + 0x210u) & 0xffffffu;
 }
 
+// Pixel i (0..15) of a 48-byte window as an RGBx word, byte 3 unspecified.
+__device__ __forceinline__ uint32_t rgbx_raw(const uint32_t (&w)[12], int i) {
+  const int q = (3 * i) >> 2, k = (3 * i) & 3;
+  const uint32_t hi = w[q + 1 < 12 ? q + 1 : 11];
+  return __byte_perm(w[q], hi, (uint32_t)k * 0x111u + 0x210u);
+}
+
 // Contiguous range of units for CTA b of G (persistent kernels): consecutive
 // units belong mostly to the same image, so per-image state is reloaded only
 // when the image changes.
