@@ -86,6 +86,7 @@ struct PlanStep {
   int interp = 1, border = 0;
   int eq_slot = -1;
   float min_scale = 1.0f;
+  int rs_ring = 0, rs_sw = 0, rs_hw = 0;  // separable resample parameters (0 = old kernel)
 };
 
 constexpr int kChunk = 48 * 512;         // pointwise / histogram bytes per unit
@@ -566,6 +567,45 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       case SK_RESAMPLE: {
         st.unit_size = kStageWords;  // 40 KB of staged window rows per band
         const alb_op& o = P->ops[st.slot0];
+        if (st.interp == ALB_INTERP_BILINEAR && !st.has_mask) {
+          // separable kernel: a group of G output rows needs <= ceil(G * ratio) + 1
+          // new window rows (ratio = largest window/output row ratio); strips of
+          // 256 output columns need <= 256 * ww / nw + 3 window columns
+          int max_ww = 0;
+          double ratio = 0.0;
+          for (int i = 0; i < P->n; ++i) {
+            int wh = dims[i][st.slot0].first, ww = dims[i][st.slot0].second;
+            if (o.kind == ALB_RANDOM_SIZED_CROP) wh = ww = std::min(o.max_side, std::min(wh, ww));
+            max_ww = std::max(max_ww, ww);
+            ratio = std::max(ratio, (double)wh / o.out_h);
+          }
+          const double cratio = (double)max_ww / o.out_w;
+          const int sw = (std::min(max_ww, (int)std::ceil(256.0 * cratio) + 3)) | 1;
+          int nl = 0;
+          for (auto& sg : st.stages) nl += (sg.type == ST_LUT || sg.type == ST_EQ);
+          // largest group that keeps >= 4 CTAs (16 warps) per SM, else any that fits
+          for (int lim : {48 * 1024, 100 * 1024}) {
+            for (int G : {16, 8, 4}) {
+              const int ring = (int)std::ceil(G * ratio) + 2;
+              if (ring > 63 || resample_sep_smem(nl, ring, sw, G, st.normalize) > (size_t)lim) continue;
+              st.rs_ring = ring;
+              st.rs_sw = sw;
+              st.rs_hw = G;
+              break;
+            }
+            if (st.rs_ring > 0) break;
+          }
+          if (st.rs_ring > 0) {
+            const int R = 128;
+            st.unit_rows = R;
+            for (int i = 0; i < P->n; ++i) {
+              const int H = dims[i][st.slot1].first, W = st.normalize ? P->out_w : dims[i][st.slot1].second;
+              for (int y = 0, b = 0; y < H; y += R, ++b)
+                for (int x = 0, c = 0; x < W; x += 256, ++c) st.units.push_back(make_int2(i, (b << 8) | c));
+            }
+            break;
+          }
+        }
         int R = 64;
         for (int i = 0; i < P->n; ++i) {
           if (dims[i][st.slot1].second > 2048) return fail(ALB_E_UNSUPPORTED, "resize output wider than 2048");
@@ -753,6 +793,9 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
     a.ops = P->d_ops;
     a.geo = ws + P->off_geo;
     a.n_img = P->n;
+    a.rs_ring = st.rs_ring;
+    a.rs_sw = st.rs_sw;
+    a.rs_hw = st.rs_hw;
     switch (st.kind) {
       case SK_ROW:
         if (st.has_image) {

@@ -99,20 +99,6 @@ __device__ __forceinline__ int border_idx(int i, int n, bool reflect, bool& in) 
   return (k >= 0 && k < n) ? k : reflect101(i, n);
 }
 
-// ---- paired fp32 helpers (sm_100 f32x2 pipe)
-__device__ __forceinline__ unsigned long long f2u(float2 v) {
-  return ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x);
-}
-__device__ __forceinline__ float2 u2f(unsigned long long u) {
-  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
-}
-// round-toward-minus-infinity paired add: floor(v) + 1.5*2^23 for |v| < 2^22
-__device__ __forceinline__ float2 fadd2_rm(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
-  return u2f(r);
-}
-
 // Per-column cell anchor: fp64 source coordinate of the cell origin, split
 // into integer part (ix, iy) and fp32 fraction, plus the column's fp32 offset.
 struct Anchor {
@@ -132,52 +118,6 @@ __device__ __forceinline__ Anchor cell_anchor(const double* A, float A0f, float 
   an.ix = (int)flx;
   an.iy = (int)fly;
   return an;
-}
-
-// Bilinear blend of 4 RGBx taps (O5/O7 weights), fp32, per channel
-//   h0 = fma(fx, p10 - p00, p00 + .5); h1 = fma(fx, p11 - p01, p01 + .5);
-//   v  = fma(fy, h1 - h0, h0);   out = floor(v)        (= round_half_up)
-// Bytes become floats via the 2^23 magic (byte permute); channel pairs run
-// on the paired fp32 pipe.  Returns the three rounded channels as the bit
-// patterns of floor(v) + 2^23 (byte in bits 0-7).
-__device__ __forceinline__ void bilerp3(uint32_t t00, uint32_t t10, uint32_t t01, uint32_t t11,
-                                        float2 f, uint32_t& r, uint32_t& g, uint32_t& b) {
-  constexpr uint32_t kM = 0x4B000000u;  // 2^23
-  auto cv = [](uint32_t t, uint32_t c) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | c)); };
-  const float2 P00 = make_float2(cv(t00, 0), cv(t00, 1)), P10 = make_float2(cv(t10, 0), cv(t10, 1));
-  const float2 P01 = make_float2(cv(t01, 0), cv(t01, 1)), P11 = make_float2(cv(t11, 0), cv(t11, 1));
-  const float2 B0 = make_float2(cv(t00, 2), cv(t01, 2)), B1 = make_float2(cv(t10, 2), cv(t11, 2));
-  const float2 nMh = make_float2(-8388607.5f, -8388607.5f);  // -(2^23 - 0.5), exact
-  const float2 fx2 = make_float2(f.x, f.x);
-  const float2 H0 = __ffma2_rn(fx2, __fadd2_rn(P10, make_float2(-P00.x, -P00.y)), __fadd2_rn(P00, nMh));
-  const float2 H1 = __ffma2_rn(fx2, __fadd2_rn(P11, make_float2(-P01.x, -P01.y)), __fadd2_rn(P01, nMh));
-  const float2 HB = __ffma2_rn(fx2, __fadd2_rn(B1, make_float2(-B0.x, -B0.y)), __fadd2_rn(B0, nMh));
-  const float2 V = __ffma2_rn(make_float2(f.y, f.y), __fadd2_rn(H1, make_float2(-H0.x, -H0.y)), H0);
-  const float vb = fmaf(f.y, HB.y - HB.x, HB.x);
-  const float2 R2 = fadd2_rm(V, make_float2(8388608.f, 8388608.f));
-  r = __float_as_uint(R2.x);
-  g = __float_as_uint(R2.y);
-  b = __float_as_uint(__fadd_rd(vb, 8388608.f));
-}
-
-// Copy bytes [lo, hi) of one 16-byte chunk, smem -> global, both 16-aligned:
-// naturally aligned pieces when the range touches an end of the chunk.
-__device__ __forceinline__ void copy_partial(uint8_t* d, const uint8_t* s, int lo, int hi) {
-  if (hi == 16) {
-    int p = lo;
-    if (p & 1) { d[p] = s[p]; p += 1; }
-    if (p & 2) { *reinterpret_cast<uint16_t*>(d + p) = *reinterpret_cast<const uint16_t*>(s + p); p += 2; }
-    if (p & 4) { *reinterpret_cast<uint32_t*>(d + p) = *reinterpret_cast<const uint32_t*>(s + p); p += 4; }
-    if (p & 8) { *reinterpret_cast<uint2*>(d + p) = *reinterpret_cast<const uint2*>(s + p); }
-  } else if (lo == 0) {
-    int p = 0;
-    if (hi & 8) { *reinterpret_cast<uint2*>(d) = *reinterpret_cast<const uint2*>(s); p = 8; }
-    if (hi & 4) { *reinterpret_cast<uint32_t*>(d + p) = *reinterpret_cast<const uint32_t*>(s + p); p += 4; }
-    if (hi & 2) { *reinterpret_cast<uint16_t*>(d + p) = *reinterpret_cast<const uint16_t*>(s + p); p += 2; }
-    if (hi & 1) d[p] = s[p];
-  } else {
-    for (int b = lo; b < hi; ++b) d[b] = s[b];
-  }
 }
 
 // CTA copy of `rows` buffered rows to global.  Row r's n bytes sit in the
@@ -595,18 +535,6 @@ constexpr int kPOffOb = kPOffAn + kAnCells * 64 * (int)sizeof(AnEnt);  // output
 constexpr int kPOffRaw = kPOffOb + kTileH * kObPitch + kRawSlack;      // raw rows
 constexpr int kPOffStage = kPOffRaw + kRawRows * kRawPitch + kRawSlack;
 constexpr int kPSmem = kPOffStage + kPStageWords * 4;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
-}
 
 // Per-image state of the affine step (one thread per image), read by the
 // producer warp whenever a tile starts a new image.

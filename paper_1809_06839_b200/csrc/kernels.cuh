@@ -57,7 +57,12 @@ struct StepArgs {
   const alb_op* ops;
   void* geo;  // workspace scratch: per-image affine state, kGeoBytes each
   int32_t n_img;  // images in the batch
+  int32_t rs_ring, rs_sw, rs_hw;  // separable resample: ring rows (0 = old kernel), staged row
+                                   // stride (words), output rows per group
 };
+
+// shared memory of the separable resample kernel (resample.cu)
+size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize);
 
 constexpr int kGeoBytes = 128;
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <set>
 #include <utility>
 
 namespace alb {
@@ -14,6 +15,7 @@ namespace alb {
 namespace {
 std::mutex g_mu;
 std::map<std::pair<const void*, size_t>, int> g_occ;
+std::set<const void*> g_fn_set;
 int g_sms = 0;
 }  // namespace
 
@@ -29,7 +31,14 @@ int persistent_grid(const void* fn, int threads, size_t smem, int n_units) {
   auto it = g_occ.find(key);
   int occ;
   if (it == g_occ.end()) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the attribute is per function: raise it to the opt-in maximum once, so
+    // launches of the same kernel with different smem sizes all stay legal
+    if (g_fn_set.insert(fn).second) {
+      int dev = 0, mx = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, mx > 0 ? mx : (int)smem);
+    }
     occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
     occ = std::max(occ, 1);

@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
               t01 = q1[3 * x0] | (q1[3 * x0 + 1] << 8) | (q1[3 * x0 + 2] << 16);
               t11 = q1[3 * x1] | (q1[3 * x1 + 1] << 8) | (q1[3 * x1 + 2] << 16);
             }
-            const uint32_t px = bilerp_rgbx(t00, t10, t01, t11, ce.fx, fy);
-            r = px & 0xff; gg = (px >> 8) & 0xff; b = (px >> 16) & 0xff;
+            bilerp3(t00, t10, t01, t11, make_float2(ce.fx, fy), r, gg, b);
+            r &= 0xffu; gg &= 0xffu; b &= 0xffu;
           }
           apply_stages_t<kOne>(x, sm, lane, r, gg, b);
           if (normalize) {
@@ -232,6 +232,332 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
   }
 }
 
+
+// ============================================================ separable path
+// Bilinear, no mask (Resize512, RandomSizedCrop, the fused cfg4 chain).  The
+// per-channel arithmetic is bilerp3's, split at its natural seam:
+//   H(r, xo) = fma(fx, p(x1, r) - p(x0, r), p(x0, r) + 0.5)    once per (window row, column)
+//   V(yo, xo) = fma(fy, H(y1, xo) - H(y0, xo), H(y0, xo));  out = floor(V)
+// so every output byte equals the non-separable kernel's bit for bit, while
+// each horizontal lerp is shared by all output rows that use the window row.
+// Work unit = (image, band of unit_rows output rows, strip of 256 columns);
+// warp w owns columns [32w, 32w+32) of the strip and walks down the band in
+// increasing window-row order, carrying the two current H rows in REGISTERS
+// (a new H row costs two shared taps; consecutive output rows mostly reuse
+// them).  Per group of G output rows:
+//   1. the window rows the group newly needs arrive by TMA (cp.async.bulk,
+//      one aligned row range each, issued while the previous group computes)
+//      in a raw ring and are unpacked to RGBx words (16-byte aligned 16-pixel
+//      runs) into a second ring; the previous group's output rows are copied
+//      out (aligned 16-byte chunks of pre-shifted row buffers);
+//   2. each warp forms its 32 columns of the G rows (stage chain, then u8
+//      bytes into the row buffers or planar fp32 Normalize stores).
+constexpr int kSepCW = 256;      // strip width (output columns) = 32 x kCols x warps
+constexpr int kSepMaxG = 16;     // output rows per group
+constexpr int kSepMaxBand = 128;
+constexpr int kSepObp = 3 * kSepCW + 16;
+
+struct SepRow {
+  int y0, y1;  // window-frame source rows
+  float fy;
+  int ob;      // byte offset of the row in the output row buffers (incl. 16-byte phase)
+  int yo;      // output row
+  int pad[3];
+};
+struct SepState {
+  RsGeom g;
+  Map1 m;
+  int Wo, Ho;
+};
+
+// raw window row pitch (bytes): 16-byte aligned hull of <= sw pixels
+__host__ __device__ inline int sep_raw_pitch(int sw) { return (3 * sw + 32 + 15) & ~15; }
+
+// kCols output columns per lane: 2 for plain resamples (the per-row control
+// work is shared by two pixels), 1 when a stage chain / Normalize makes each
+// pixel long (more warps hide its latency)
+template <int kOne, bool kNorm, int kCols>
+__global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArgs a) {
+  constexpr int kSepThreads = 256 / kCols;
+  extern __shared__ uint32_t sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  StageCtx x;
+  init_stages(a, x);
+  const int SW = a.rs_sw, K = a.rs_ring, G = a.rs_hw;  // ring rows, staged row stride (words), group rows
+  const int RP = sep_raw_pitch(SW);
+  uint8_t* smb = reinterpret_cast<uint8_t*>(sm + x.n_lut * kLutWords);
+  SepState* st = reinterpret_cast<SepState*>(smb);
+  SepRow* rowt = reinterpret_cast<SepRow*>(smb + 128);
+  uint32_t* mtab = reinterpret_cast<uint32_t*>(rowt + kSepMaxBand);   // magic_of(n), n < 64
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(mtab + 64);
+  uint32_t* src = reinterpret_cast<uint32_t*>(mbar + 2);              // [K][SW] RGBx rows
+  uint8_t* raw = reinterpret_cast<uint8_t*>(src + ((K * SW + 3) & ~3)) + 64;  // [K][RP] raw rows
+  uint8_t* obuf = raw + K * RP + 64;                                  // [G][kSepObp] output rows
+  const uint32_t bar = smem_u32(mbar);
+  const int R = a.unit_rows;
+  const uint32_t mK = magic_of((uint32_t)K);
+  auto slot = [&](int r) { return r - K * fdiv(r, mK); };  // r % K, r >= 0
+  if (tid < 64) mtab[tid] = magic_of((uint32_t)tid);
+  if (tid == 0) mbar_init(bar);
+  uint32_t parity = 0;
+
+  int u0, u1;
+  unit_range(a.n_units, u0, u1);
+  int cur_img = -1;
+  for (int u = u0; u < u1; ++u) {
+    const int2 unit = a.units[u];
+    const int img = unit.x, band = unit.y >> 8, strip = unit.y & 255;
+    __syncthreads();  // previous unit fully consumed
+    if (img != cur_img) {
+      load_stages(a, img, sm, x, kSepThreads);
+      if (tid == 0) {
+        SepState s;
+        s.g = rs_geom(a, img);
+        s.Wo = kNorm ? a.out_w : a.ddesc[img].width;
+        s.Ho = kNorm ? a.out_h : a.ddesc[img].height;
+        s.m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, s.Wo, s.Ho);
+        *st = s;
+      }
+      cur_img = img;
+      __syncthreads();
+    }
+    const RsGeom g = st->g;
+    const Map1 m = st->m;
+    const int Wo = st->Wo, Ho = st->Ho;
+    const int xs0 = strip * kSepCW, cw = min(kSepCW, Wo - xs0);
+    const int y0 = band * R, nr = min(R, Ho - y0);
+    for (int i = tid; i < nr; i += kSepThreads) {  // i-th row in increasing source order
+      const int yo = m.ay > 0 ? y0 + i : y0 + nr - 1 - i;
+      const double sy = rs_coord(m.ay * yo + m.by, g.wh, g.nh);
+      const double f = floor(sy);
+      SepRow e;
+      e.y0 = (int)f;
+      e.y1 = min((int)f + 1, g.wh - 1);
+      e.fy = (float)__dsub_rn(sy, f);
+      e.yo = yo;
+      e.ob = 0;
+      if constexpr (!kNorm) {
+        const alb_image_desc dd = a.ddesc[img];
+        e.ob = (i % G) * kSepObp + (int)((uintptr_t)(a.dst + dd.offset + (size_t)yo * dd.pitch + (size_t)xs0 * 3) & 15);
+      }
+      e.pad[0] = e.pad[1] = e.pad[2] = 0;
+      rowt[i] = e;
+    }
+    // this lane's two columns (fp64, definition order O5) and the strip's window columns
+    const int cb = warp * 32 * kCols + lane;
+    const int xe0 = m.ax * xs0 + m.bx, xe1 = m.ax * (xs0 + cw - 1) + m.bx;
+    const int sxa = (int)floor(rs_coord(min(xe0, xe1), g.ww, g.nw));
+    const int sxb = min((int)floor(rs_coord(max(xe0, xe1), g.ww, g.nw)) + 1, g.ww - 1) + 1;
+    int o0[kCols], o1[kCols];
+    float fx[kCols];
+#pragma unroll
+    for (int q = 0; q < kCols; ++q) {
+      const double sx = rs_coord(m.ax * (xs0 + min(cb + 32 * q, cw - 1)) + m.bx, g.ww, g.nw);
+      const double f = floor(sx);
+      o0[q] = (int)f - sxa;
+      o1[q] = min((int)f + 1, g.ww - 1) - sxa;
+      fx[q] = (float)__dsub_rn(sx, f);
+    }
+    const alb_image_desc sd = a.sdesc[img];
+    const uint8_t* wbase = a.src + sd.offset + (size_t)g.wy0 * sd.pitch;
+    const int X0 = g.wx0 + sxa, X1 = g.wx0 + sxb;  // absolute source columns
+    const int nrun = (X1 - X0 + 30) >> 4;
+    uint8_t* gbase = nullptr;
+    int dpitch = 0;
+    if constexpr (!kNorm) {
+      const alb_image_desc dd = a.ddesc[img];
+      gbase = a.dst + dd.offset + (size_t)xs0 * 3;
+      dpitch = dd.pitch;
+    }
+    __syncthreads();  // row table
+    // TMA row copies of window rows [na, rhi] -> raw ring (thread 0)
+    auto issue = [&](int na, int rhi) {
+      uint32_t bytes = 0;
+      for (int r = na; r <= rhi; ++r) {
+        const uintptr_t row = (uintptr_t)(wbase + (size_t)r * sd.pitch);
+        const uintptr_t ga = (row + 3 * X0) & ~(uintptr_t)15, gb = (row + 3 * X1 + 15) & ~(uintptr_t)15;
+        bulk_g2s(smem_u32(raw + slot(r) * RP), reinterpret_cast<const void*>(ga), (uint32_t)(gb - ga), bar);
+        bytes += (uint32_t)(gb - ga);
+      }
+      mbar_arrive_tx(bar, bytes);
+    };
+    auto copy_out = [&](int gi0, int ng) {  // output rows gi0 .. gi0+ng-1 (source order)
+      if constexpr (!kNorm) {
+        const int n = 3 * cw;
+        constexpr int kFull = kSepCW * 3 / 16;
+        for (int it = tid; it < ng * kFull; it += kSepThreads) {
+          const int j = it / kFull, k = it - j * kFull;
+          uint8_t* grow = gbase + (size_t)rowt[gi0 + j].yo * dpitch;
+          const int o = (int)((uintptr_t)grow & 15);
+          const int cc = ((o + 15) >> 4) + k;
+          if (16 * cc + 16 <= o + n)
+            __stcs(reinterpret_cast<uint4*>(grow - o + 16 * cc),
+                   *reinterpret_cast<const uint4*>(obuf + j * kSepObp + 16 * cc));
+        }
+        for (int it = tid; it < 2 * ng; it += kSepThreads) {
+          const bool head = it < ng;
+          const int j = head ? it : it - ng;
+          uint8_t* grow = gbase + (size_t)rowt[gi0 + j].yo * dpitch;
+          const int o = (int)((uintptr_t)grow & 15);
+          const uint8_t* sb = obuf + j * kSepObp;
+          uint8_t* d = grow - o;
+          const int e = o + n;
+          if (head) {
+            if (o > 0) copy_partial(d, sb, o, min(e, 16));
+          } else {
+            const int cc = e >> 4, hi = e & 15;
+            if (hi > 0 && (cc > 0 || o == 0)) copy_partial(d + 16 * cc, sb + 16 * cc, 0, hi);
+          }
+        }
+      }
+    };
+    int nxt = rowt[0].y0;  // first window row not yet staged
+    if (tid == 0) issue(nxt, rowt[min(G, nr) - 1].y1);
+    // this warp's current two H rows (window rows hr0, hr1), both lane columns
+    float4 h0[kCols], h1[kCols];
+#pragma unroll
+    for (int q = 0; q < kCols; ++q) h0[q] = h1[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int hr0 = -1, hr1 = -1;
+    auto hrow = [&](int r, float4 (&h)[kCols]) {  // horizontal lerps of staged window row r
+      const uint32_t* srow = src + slot(r) * SW;
+#pragma unroll
+      for (int q = 0; q < kCols; ++q) {
+        const uint32_t t0 = srow[o0[q]], t1 = srow[o1[q]];
+        constexpr uint32_t kM = 0x4B000000u;
+        auto cv = [](uint32_t t, uint32_t ch) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | ch)); };
+        const float2 P0 = make_float2(cv(t0, 0), cv(t0, 1)), P1 = make_float2(cv(t1, 0), cv(t1, 1));
+        const float2 nMh = make_float2(-8388607.5f, -8388607.5f);
+        const float2 H = __ffma2_rn(make_float2(fx[q], fx[q]), __fadd2_rn(P1, make_float2(-P0.x, -P0.y)),
+                                    __fadd2_rn(P0, nMh));
+        const float B0 = cv(t0, 2), B1 = cv(t1, 2);
+        h[q] = make_float4(H.x, H.y, fmaf(fx[q], B1 - B0, B0 + -8388607.5f), 0.f);
+      }
+    };
+    uint8_t* olane = obuf + 3 * cb;
+    int prev_gi = -1, prev_ng = 0;
+    for (int gi = 0; gi < nr; gi += G) {
+      const int ng = min(G, nr - gi), gl = gi + ng - 1;
+      const int rhi = rowt[gl].y1;
+      const int na = max(nxt, rowt[gi].y0);
+      const int nn = rhi - na + 1;  // <= K
+      // 1. unpack the group's new window rows; copy out the previous group
+      if (nn > 0) {
+        mbar_wait(bar, parity);
+        parity ^= 1u;
+        const uint32_t mnn = mtab[nn];
+        for (int it = tid; it < nn * nrun; it += kSepThreads) {
+          const int k = fdiv(it, mnn), r = na + (it - k * nn);
+          const uintptr_t srow = (uintptr_t)(wbase + (size_t)r * sd.pitch);
+          const int xa = (11 * (16 - (int)(srow & 15))) & 15;
+          const int xs = X0 - ((X0 - xa) & 15) + 16 * k;
+          if (xs >= X1) continue;
+          const uintptr_t ga = (srow + 3 * X0) & ~(uintptr_t)15;
+          const int sl = slot(r);
+          const uint4* q = reinterpret_cast<const uint4*>(raw + sl * RP +
+                                                          (int)((intptr_t)(srow + 3 * (intptr_t)xs) - (intptr_t)ga));
+          uint32_t w[12];
+#pragma unroll
+          for (int v = 0; v < 3; ++v) {
+            const uint4 z = q[v];
+            w[4 * v] = z.x; w[4 * v + 1] = z.y; w[4 * v + 2] = z.z; w[4 * v + 3] = z.w;
+          }
+          uint32_t* d = src + sl * SW + (xs - X0);
+          if (xs >= X0 && xs + 16 <= X1) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) d[i] = rgbx_raw(w, i);
+          } else {
+            const int lo_i = max(X0 - xs, 0), hi_i = min(X1 - xs, 16);
+            const uint32_t vm = ((1u << hi_i) - 1u) & ~((1u << lo_i) - 1u);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (vm & (1u << i)) d[i] = rgbx_raw(w, i);
+          }
+        }
+        nxt = rhi + 1;
+      }
+      if (prev_gi >= 0) copy_out(prev_gi, prev_ng);
+      __syncthreads();
+      // prefetch the next group's new window rows while this group computes
+      if (tid == 0 && gi + G < nr) {
+        const int gl2 = min(gi + 2 * G, nr) - 1;
+        const int na2 = max(nxt, rowt[gi + G].y0), rhi2 = rowt[gl2].y1;
+        if (rhi2 >= na2) issue(na2, rhi2);
+      }
+      // 2. this warp's 32 x kCols columns of the group's output rows
+      for (int j = 0; j < ng; ++j) {
+        const SepRow rw = rowt[gi + j];
+        if (rw.y0 != hr0) {
+          if (rw.y0 == hr1) {
+#pragma unroll
+            for (int q = 0; q < kCols; ++q) h0[q] = h1[q];
+            hr0 = hr1;
+          }
+          else { hrow(rw.y0, h0); hr0 = rw.y0; }
+        }
+        if (rw.y1 != hr1) {
+          if (rw.y1 == hr0) {
+#pragma unroll
+            for (int q = 0; q < kCols; ++q) h1[q] = h0[q];
+          }
+          else hrow(rw.y1, h1);
+          hr1 = rw.y1;
+        }
+#pragma unroll
+        for (int q = 0; q < kCols; ++q) {
+          const float2 V = __ffma2_rn(make_float2(rw.fy, rw.fy),
+                                      __fadd2_rn(make_float2(h1[q].x, h1[q].y), make_float2(-h0[q].x, -h0[q].y)),
+                                      make_float2(h0[q].x, h0[q].y));
+          const float vb = fmaf(rw.fy, h1[q].z - h0[q].z, h0[q].z);
+          const float2 R2 = fadd2_rm(V, make_float2(8388608.f, 8388608.f));
+          uint32_t r = __float_as_uint(R2.x), gg = __float_as_uint(R2.y), b = __float_as_uint(__fadd_rd(vb, 8388608.f));
+          if constexpr (kOne != kStagesNone || kNorm) {
+            r &= 0xffu; gg &= 0xffu; b &= 0xffu;
+          }
+          apply_stages_t<kOne>(x, sm, lane, r, gg, b);
+          if (cb + 32 * q < cw) {
+            if constexpr (kNorm) {
+              const size_t plane = (size_t)Ho * Wo;
+              float* o = a.nchw + (size_t)img * 3 * plane + (size_t)rw.yo * Wo + xs0 + cb + 32 * q;
+              const float* nl = a.tab.norm_lut;
+              __stcs(o, __ldg(nl + r));
+              __stcs(o + plane, __ldg(nl + 256 + gg));
+              __stcs(o + 2 * plane, __ldg(nl + 512 + b));
+            } else {
+              uint8_t* orow = olane + rw.ob + 96 * q;
+              orow[0] = (uint8_t)r;
+              orow[1] = (uint8_t)gg;
+              orow[2] = (uint8_t)b;
+            }
+          }
+        }
+      }
+      prev_gi = gi;
+      prev_ng = ng;
+      __syncthreads();
+    }
+    copy_out(prev_gi, prev_ng);
+  }
+}
+
+size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize) {
+  return (size_t)n_lut_stages * kLutWords * 4 + 128 + kSepMaxBand * sizeof(SepRow) + 256 + 16 +
+         (size_t)((ring * sw + 3) & ~3) * 4 + 64 + (size_t)ring * sep_raw_pitch(sw) + 64 +
+         (normalize ? 0 : (size_t)g * kSepObp);
+}
+
+template <int kOne, bool kNorm, int kCols>
+static void launch_sep_v(const StepArgs& a, size_t smem, cudaStream_t s) {
+  const int grid = persistent_grid((const void*)k_resample_sep<kOne, kNorm, kCols>, 256 / kCols, smem, a.n_units);
+  k_resample_sep<kOne, kNorm, kCols><<<grid, 256 / kCols, smem, s>>>(a);
+}
+
+template <int kOne>
+static void launch_sep_t(const StepArgs& a, size_t smem, cudaStream_t s) {
+  if (a.normalize) launch_sep_v<kOne, true, 1>(a, smem, s);
+  else if (kOne == kStagesNone) launch_sep_v<kOne, false, 2>(a, smem, s);
+  else launch_sep_v<kOne, false, 1>(a, smem, s);
+}
+
 static size_t resample_smem(const StepArgs& a) {
   return (size_t)count_lut_stages(a) * kLutWords * 4 + sizeof(ColEnt) * kRsMaxCols +
          kRsMaxBand * 12 + sizeof(RsState) + kRsWarps * (kRsChunk * 3 + 32) +
@@ -252,8 +578,13 @@ static void launch_resample_t(const StepArgs& a, size_t smem, cudaStream_t s) {
 
 void launch_resample(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
-  const size_t smem = resample_smem(a);
   const int mode = stage_mode(a);
+  if (a.rs_ring > 0) {  // separable path (planner checked capacity)
+    const size_t smem = resample_sep_smem(count_lut_stages(a), a.rs_ring, a.rs_sw, a.rs_hw, a.normalize != 0);
+    ALB_DISPATCH_STAGES(mode, launch_sep_t, a, smem, s)
+    return;
+  }
+  const size_t smem = resample_smem(a);
   ALB_DISPATCH_STAGES(mode, launch_resample_t, a, smem, s)
 }
 

@@ -294,39 +294,6 @@ __device__ __forceinline__ void cta_copy_rows(uint8_t* dst0, int dpitch, const u
   }
 }
 
-// Bilinear blend of 4 RGBx taps (O5/O7 weights), fp32, same
-// operation sequence per channel as the scalar form
-//   h0 = fma(fx, p10 - p00, p00); h1 = fma(fx, p11 - p01, p01);
-//   v  = fma(fy, h1 - h0, h0);   out = floor(v + 0.5)
-// Bytes become floats exactly via the 2^23 magic (byte permute + one add),
-// channel pairs run on the paired fp32 pipe (FFMA2/FADD2, sm_100), and the
-// rounded result is read back from the mantissa of floor-rounded (v+0.5)+2^23.
-__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
-
-__device__ __forceinline__ uint32_t bilerp_rgbx(uint32_t t00, uint32_t t10, uint32_t t01,
-                                                uint32_t t11, float fx, float fy) {
-  constexpr uint32_t kM = 0x4B000000u;  // 2^23
-  const float M = 8388608.f;
-  auto f = [](uint32_t t, uint32_t c) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | c)); };
-  // biased (2^23 + byte) values
-  const float2 P00 = mk2(f(t00, 0), f(t00, 1)), P10 = mk2(f(t10, 0), f(t10, 1));
-  const float2 P01 = mk2(f(t01, 0), f(t01, 1)), P11 = mk2(f(t11, 0), f(t11, 1));
-  const float2 B0 = mk2(f(t00, 2), f(t01, 2)), B1 = mk2(f(t10, 2), f(t11, 2));
-  const float2 nM = mk2(-M, -M);
-  const float2 fx2 = mk2(fx, fx);
-  const float2 H0 = __ffma2_rn(fx2, __fadd2_rn(P10, mk2(-P00.x, -P00.y)), __fadd2_rn(P00, nM));
-  const float2 H1 = __ffma2_rn(fx2, __fadd2_rn(P11, mk2(-P01.x, -P01.y)), __fadd2_rn(P01, nM));
-  const float2 HB = __ffma2_rn(fx2, __fadd2_rn(B1, mk2(-B0.x, -B0.y)), __fadd2_rn(B0, nM));
-  const float2 V = __ffma2_rn(mk2(fy, fy), __fadd2_rn(H1, mk2(-H0.x, -H0.y)), H0);
-  const float vb = fmaf(fy, HB.y - HB.x, HB.x);
-  // floor(v + 0.5) + 2^23 has the rounded byte in its low mantissa bits
-  const float2 R2 = __fadd2_rn(V, mk2(0.5f, 0.5f));
-  const uint32_t r = __float_as_uint(__fadd_rd(R2.x, M));
-  const uint32_t g = __float_as_uint(__fadd_rd(R2.y, M));
-  const uint32_t b = __float_as_uint(__fadd_rd(vb + 0.5f, M));
-  return __byte_perm(__byte_perm(r, g, 0x0040u), b, 0x6410u);  // byte 3 <- b.byte2 == 0
-}
-
 // Pixel i (0..15) of a 48-byte window as an RGBx word (one byte permute).
 __device__ __forceinline__ uint32_t rgbx_of(const uint32_t (&w)[12], int i) {
   const int q = (3 * i) >> 2, k = (3 * i) & 3;
@@ -339,6 +306,110 @@ __device__ __forceinline__ uint32_t rgbx_raw(const uint32_t (&w)[12], int i) {
   const int q = (3 * i) >> 2, k = (3 * i) & 3;
   const uint32_t hi = w[q + 1 < 12 ? q + 1 : 11];
   return __byte_perm(w[q], hi, (uint32_t)k * 0x111u + 0x210u);
+}
+
+// ---- paired fp32 helpers (sm_100 f32x2 pipe)
+__device__ __forceinline__ unsigned long long f2u(float2 v) {
+  return ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x);
+}
+__device__ __forceinline__ float2 u2f(unsigned long long u) {
+  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
+}
+// round-toward-minus-infinity paired add: floor(v) + 1.5*2^23 for |v| < 2^22
+__device__ __forceinline__ float2 fadd2_rm(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+
+// Bilinear blend of 4 RGBx taps (O5/O7 weights), fp32, per channel
+//   h0 = fma(fx, p10 - p00, p00 + .5); h1 = fma(fx, p11 - p01, p01 + .5);
+//   v  = fma(fy, h1 - h0, h0);   out = floor(v)        (= round_half_up)
+// Bytes become floats via the 2^23 magic (byte permute); channel pairs run
+// on the paired fp32 pipe.  Returns the three rounded channels as the bit
+// patterns of floor(v) + 2^23 (byte in bits 0-7).
+__device__ __forceinline__ void bilerp3(uint32_t t00, uint32_t t10, uint32_t t01, uint32_t t11,
+                                        float2 f, uint32_t& r, uint32_t& g, uint32_t& b) {
+  constexpr uint32_t kM = 0x4B000000u;  // 2^23
+  auto cv = [](uint32_t t, uint32_t c) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | c)); };
+  const float2 P00 = make_float2(cv(t00, 0), cv(t00, 1)), P10 = make_float2(cv(t10, 0), cv(t10, 1));
+  const float2 P01 = make_float2(cv(t01, 0), cv(t01, 1)), P11 = make_float2(cv(t11, 0), cv(t11, 1));
+  const float2 B0 = make_float2(cv(t00, 2), cv(t01, 2)), B1 = make_float2(cv(t10, 2), cv(t11, 2));
+  const float2 nMh = make_float2(-8388607.5f, -8388607.5f);  // -(2^23 - 0.5), exact
+  const float2 fx2 = make_float2(f.x, f.x);
+  const float2 H0 = __ffma2_rn(fx2, __fadd2_rn(P10, make_float2(-P00.x, -P00.y)), __fadd2_rn(P00, nMh));
+  const float2 H1 = __ffma2_rn(fx2, __fadd2_rn(P11, make_float2(-P01.x, -P01.y)), __fadd2_rn(P01, nMh));
+  const float2 HB = __ffma2_rn(fx2, __fadd2_rn(B1, make_float2(-B0.x, -B0.y)), __fadd2_rn(B0, nMh));
+  const float2 V = __ffma2_rn(make_float2(f.y, f.y), __fadd2_rn(H1, make_float2(-H0.x, -H0.y)), H0);
+  const float vb = fmaf(f.y, HB.y - HB.x, HB.x);
+  const float2 R2 = fadd2_rm(V, make_float2(8388608.f, 8388608.f));
+  r = __float_as_uint(R2.x);
+  g = __float_as_uint(R2.y);
+  b = __float_as_uint(__fadd_rd(vb, 8388608.f));
+}
+
+// Copy bytes [lo, hi) of one 16-byte chunk, smem -> global, both 16-aligned:
+// naturally aligned pieces when the range touches an end of the chunk.
+__device__ __forceinline__ void copy_partial(uint8_t* d, const uint8_t* s, int lo, int hi) {
+  if (hi == 16) {
+    int p = lo;
+    if (p & 1) { d[p] = s[p]; p += 1; }
+    if (p & 2) { *reinterpret_cast<uint16_t*>(d + p) = *reinterpret_cast<const uint16_t*>(s + p); p += 2; }
+    if (p & 4) { *reinterpret_cast<uint32_t*>(d + p) = *reinterpret_cast<const uint32_t*>(s + p); p += 4; }
+    if (p & 8) { *reinterpret_cast<uint2*>(d + p) = *reinterpret_cast<const uint2*>(s + p); }
+  } else if (lo == 0) {
+    int p = 0;
+    if (hi & 8) { *reinterpret_cast<uint2*>(d) = *reinterpret_cast<const uint2*>(s); p = 8; }
+    if (hi & 4) { *reinterpret_cast<uint32_t*>(d + p) = *reinterpret_cast<const uint32_t*>(s + p); p += 4; }
+    if (hi & 2) { *reinterpret_cast<uint16_t*>(d + p) = *reinterpret_cast<const uint16_t*>(s + p); p += 2; }
+    if (hi & 1) d[p] = s[p];
+  } else {
+    for (int b = lo; b < hi; ++b) d[b] = s[b];
+  }
+}
+
+// Warp copy of one buffered row to global: the row's n bytes sit in `buf`
+// (16-byte aligned) at [phase, phase + n), phase = (global row address) & 15,
+// so every 16-byte chunk is aligned on both sides.
+__device__ __forceinline__ void warp_copy_row_phased(uint8_t* grow, const uint8_t* buf, int n, int lane) {
+  const int o = (int)((uintptr_t)grow & 15);
+  uint8_t* d = grow - o;
+  const int e = o + n;
+  const int cf = (o + 15) >> 4, ce = e >> 4;
+  for (int c = cf + lane; c < ce; c += 32)
+    __stcs(reinterpret_cast<uint4*>(d + 16 * c), *reinterpret_cast<const uint4*>(buf + 16 * c));
+  if (lane == 0 && o > 0) copy_partial(d, buf, o, min(e, 16));
+  if (lane == 1) {
+    const int hi = e & 15;
+    if (hi > 0 && (ce > 0 || o == 0)) copy_partial(d + 16 * ce, buf + 16 * ce, 0, hi);
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+// TMA bulk copy global -> shared (16-byte aligned, size multiple of 16),
+// completion counted on the mbarrier `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
 
 // Contiguous range of units for CTA b of G (persistent kernels): consecutive
