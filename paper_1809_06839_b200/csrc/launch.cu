@@ -37,7 +37,11 @@ int persistent_grid(const void* fn, int threads, size_t smem, int n_units) {
       int dev = 0, mx = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, mx > 0 ? mx : (int)smem);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, fn);
+      const int lim = (mx > 0 ? mx : (int)smem) - (int)fa.sharedSizeBytes;
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, lim) != cudaSuccess)
+        cudaGetLastError();  // not sticky: the launch reports any real problem
     }
     occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);

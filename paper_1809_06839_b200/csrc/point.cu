@@ -88,11 +88,21 @@ __device__ __forceinline__ void scalar_edges(const StepArgs& a, const Seg& s, co
   for (int p = s.bE / 3 + threadIdx.x; p < s.b1 / 3; p += kThreads) px(p);
 }
 
-// LUT-only chain (kNL1: exactly one LUT stage)
+// LUT-only chain (kNL1: exactly one LUT stage).  Single-stage lookups of
+// byte j of word w (channel table base B_c 8 KB aligned, lane-replicated
+// words: entry v at word (v >> 2) * 32 + lane):
+//   addr  = ((w >> (8j - 5)) & 0x1F80) | (B_c | 4 lane)       SHF + LOP3
+//   word  = LDS(addr)
+// then four looked-up words pack into the output word with PRMT selectors
+// built from (w & 0x03030303) for all four bytes at once.
 template <bool kNL1>
 __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
-  extern __shared__ uint32_t sm[];
+  extern __shared__ uint32_t sm_raw[];
   const int lane = threadIdx.x & 31;
+  // 8 KB-aligned LUT base (the launch reserves 8 KB of slack)
+  const uint32_t raw_addr = (uint32_t)__cvta_generic_to_shared(sm_raw);
+  uint32_t* sm = sm_raw + (((8192u - (raw_addr & 8191u)) & 8191u) >> 2);
+  const uint32_t lb = (uint32_t)__cvta_generic_to_shared(sm) | (4u * lane);
   StageCtx x;
   init_stages(a, x);
   int u0, u1;
@@ -123,27 +133,47 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
       for (int k = 0; k < kU; ++k) {
         const int v = v0 + k * kThreads;
         if (v < nv) {
-          const int ph = v % 3;
-          const int cb0 = ph * 2048;
-          const int cb1 = (ph == 2 ? 0 : ph + 1) * 2048;
-          const int cb2 = (ph == 0 ? 2 : ph - 1) * 2048;
+          const int ph = v % 3;  // channel of byte j is (ph + j) % 3 (segment starts on a pixel)
           uint32_t w[4] = {in[k].x, in[k].y, in[k].z, in[k].w};
+          if constexpr (kNL1) {
+            const uint32_t c0 = lb + (uint32_t)ph * 8192u;
+            const uint32_t c1 = lb + (uint32_t)(ph == 2 ? 0 : ph + 1) * 8192u;
+            const uint32_t c2 = lb + (uint32_t)(ph == 0 ? 2 : ph - 1) * 8192u;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t o = 0;
+            for (int q = 0; q < 4; ++q) {
+              uint32_t r[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int jj = q * 4 + j;
-              const int cb = (jj % 3 == 0) ? cb0 : ((jj % 3 == 1) ? cb1 : cb2);
-              uint32_t val = (w[q] >> (8 * j)) & 0xffu;
-              if (kNL1) {
-                val = lut_look(sm, cb, val, lane);
-              } else {
-                for (int t = 0; t < x.n_lut; ++t) val = lut_look(sm + t * kLutWords, cb, val, lane);
+              for (int j = 0; j < 4; ++j) {
+                const int jj = q * 4 + j;
+                const uint32_t cb = (jj % 3 == 0) ? c0 : ((jj % 3 == 1) ? c1 : c2);
+                const uint32_t t = j == 0 ? (w[q] << 5) : (w[q] >> (8 * j - 5));
+                const uint32_t addr = (t & 0x1F80u) | cb;
+                asm("ld.shared.u32 %0, [%1];" : "=r"(r[j]) : "r"(addr));
               }
-              o |= val << (8 * j);
+              // byte (v & 3) of each looked-up word: selector nibbles from w & 0x03030303
+              const uint32_t xs = w[q] & 0x03030303u;
+              const uint32_t y = xs | (xs >> 4);  // byte k: (v_k & 3) | (v_{k+1} & 3) << 4
+              const uint32_t lo = __byte_perm(r[0], r[1], (y & 0xffu) + 0x40u);
+              const uint32_t hi = __byte_perm(r[2], r[3], ((y >> 16) & 0xffu) + 0x40u);
+              w[q] = __byte_perm(lo, hi, 0x5410u);
             }
-            w[q] = o;
+          } else {
+            const int cb0 = ph * 2048;
+            const int cb1 = (ph == 2 ? 0 : ph + 1) * 2048;
+            const int cb2 = (ph == 0 ? 2 : ph - 1) * 2048;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t o = 0;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int jj = q * 4 + j;
+                const int cb = (jj % 3 == 0) ? cb0 : ((jj % 3 == 1) ? cb1 : cb2);
+                uint32_t val = (w[q] >> (8 * j)) & 0xffu;
+                for (int t = 0; t < x.n_lut; ++t) val = lut_look(sm + t * kLutWords, cb, val, lane);
+                o |= val << (8 * j);
+              }
+              w[q] = o;
+            }
           }
           __stcs(d4 + v, make_uint4(w[0], w[1], w[2], w[3]));
         }
@@ -226,13 +256,17 @@ __global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
 
 template <bool kNL1>
 static void launch_lut(const StepArgs& a, size_t smem, cudaStream_t s) {
+  smem += 8192;  // slack to align the LUT base to 8 KB
   const int grid = persistent_grid((const void*)k_point_lut<kNL1>, kThreads, smem, a.n_units);
   k_point_lut<kNL1><<<grid, kThreads, smem, s>>>(a);
 }
 
 template <int kOne, bool kNorm>
 static void launch_px_n(const StepArgs& a, size_t smem, cudaStream_t s) {
-  const int grid = persistent_grid((const void*)k_point_px<kOne, kNorm>, kThreads, smem, a.n_units);
+  // without LUT stages there is no per-image shared state worth keeping:
+  // one CTA per unit lets the hardware balance the ragged tail
+  const int grid = smem == 0 ? a.n_units
+                             : persistent_grid((const void*)k_point_px<kOne, kNorm>, kThreads, smem, a.n_units);
   k_point_px<kOne, kNorm><<<grid, kThreads, smem, s>>>(a);
 }
 
