@@ -543,11 +543,13 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
             flat = flat && st.dst_l->h[i].pitch == st.dst_l->h[i].width * 3 && st.dst_l->h[i].offset % 16 == 0;
         }
         st.flat = flat;
-        st.unit_size = kChunk;
+        // histogram units are 4x larger: fewer per-unit zero / merge passes
+        const int chunk = st.kind == SK_EQ ? 4 * kChunk : kChunk;
+        st.unit_size = chunk;
         for (int i = 0; i < P->n; ++i) {
           if (flat) {
             const int len = sl->h[i].height * sl->h[i].width * 3;
-            for (int c = 0; c * kChunk < len; ++c) st.units.push_back(make_int2(i, c));
+            for (int c = 0; c * chunk < len; ++c) st.units.push_back(make_int2(i, c));
           } else {
             for (int y = 0; y < sl->h[i].height; ++y) st.units.push_back(make_int2(i, y));
           }
