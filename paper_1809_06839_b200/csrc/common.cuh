@@ -111,43 +111,51 @@ __device__ __forceinline__ bool fired_of(const Tables& t, int img, int slot) {
 }
 
 // ---------------------------------------------------------------- HSV (fp32)
-// hexcone RGB->HSV, shift (h mod 360, s/v clamped), HSV->RGB, round half up.
-// Branch-free (no lane divergence): hue in sixths h6 in [0,6) selected by the
-// dominant channel (ties r > g > b), and the hexcone inverse written as
-//   channel(n) = v - v*s*clamp(min(k, 4-k), 0, 1),  k = (n + h6) mod 6,
-// n = 5, 3, 1 for R, G, B -- algebraically the sector table of SPEC.md:419.
-// dh6 = dh/60 (hue shift in sixths).
-__device__ __forceinline__ void hsv_shift_px(float dh6, float ds, float dv, uint32_t& r,
-                                             uint32_t& g, uint32_t& b) {
-  const float fr = (float)r, fg = (float)g, fb = (float)b;
-  const float mx = fmaxf(fr, fmaxf(fg, fb));
-  const float mn = fminf(fr, fminf(fg, fb));
-  const float d = mx - mn;
-  const bool isr = mx == fr;
-  const bool isg = !isr && mx == fg;
-  const float num = isr ? fg - fb : (isg ? fb - fr : fr - fg);
-  const float off = isr ? 0.f : (isg ? 2.f : 4.f);
-  float h6 = d > 0.f ? __fdividef(num, d) + off : 0.f;
-  h6 = h6 < 0.f ? h6 + 6.f : h6;
-  h6 += dh6;
-  h6 -= 6.f * floorf(h6 * (1.f / 6.f));
-  h6 = h6 >= 6.f ? h6 - 6.f : h6;
-  h6 = fmaxf(h6, 0.f);
-  const float s = __saturatef((mx > 0.f ? __fdividef(d, mx) : 0.f) + ds);
+// hexcone RGB->HSV, shift (h mod 360, s/v clamped), HSV->RGB, round half up
+// (O9, reading R29).  Branch-free (no lane divergence):
+//  * bytes -> floats as 2^23 + byte (one LOP each); max/min/differences are
+//    exact in that biased form;
+//  * hue in sixths, dominant channel with ties r > g > b:
+//      h6 = num / d + off + dh6w,  dh6w = (dh / 60) mod 6 in [0, 6)
+//    (per image), so h6 in [-1, 11); d = 0 gives num = 0, off = 0;
+//    reciprocals are clamped to 2 so 0 * rcp(0) = 0 (d, mx are integers);
+//  * channel n (5, 3, 1 for R, G, B): k = h6 + n in [0, 16) and
+//      c = v - v s sat(2 - min(|k-2|, |k-8|, |k-14|)),
+//    the periodic form of SPEC.md:419's sector table sat(min(k', 4-k')),
+//    k' = k mod 6, so no explicit wrap of the hue is needed;
+//  * out = floor(255 c + 0.5) from the mantissa of a round-down add.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void hsv_shift_px(float dh6w, float ds, float dv, uint32_t& r, uint32_t& g,
+                                             uint32_t& b) {
+  const float M = 8388608.f;  // 2^23
+  const float Rb = __uint_as_float(r | 0x4B000000u), Gb = __uint_as_float(g | 0x4B000000u),
+              Bb = __uint_as_float(b | 0x4B000000u);
+  const float mxb = fmaxf(Rb, fmaxf(Gb, Bb));
+  const float mnb = fminf(Rb, fminf(Gb, Bb));
+  const float d = mxb - mnb;
+  const float mx = mxb - M;
+  const bool isr = mxb == Rb;
+  const bool isg = !isr && mxb == Gb;
+  const float pa = isr ? Gb : (isg ? Bb : Rb);
+  const float pb = isr ? Bb : (isg ? Rb : Gb);
+  const float off = isr ? dh6w : (isg ? dh6w + 2.f : dh6w + 4.f);
+  const float h6 = fmaf(pa - pb, fminf(rcp_approx(d), 2.f), off);
+  const float s = __saturatef(fmaf(d, fminf(rcp_approx(mx), 2.f), ds));
   const float v = __saturatef(fmaf(mx, 1.f / 255.f, dv));
   const float vs = v * s;
-  float k = h6 + 5.f;
-  k = k >= 6.f ? k - 6.f : k;
-  const float tr = __saturatef(fminf(k, 4.f - k));
-  k = h6 + 3.f;
-  k = k >= 6.f ? k - 6.f : k;
-  const float tg = __saturatef(fminf(k, 4.f - k));
-  k = h6 + 1.f;
-  k = k >= 6.f ? k - 6.f : k;
-  const float tb = __saturatef(fminf(k, 4.f - k));
-  r = (uint32_t)fmaf(255.f, fmaf(-vs, tr, v), 0.5f);
-  g = (uint32_t)fmaf(255.f, fmaf(-vs, tg, v), 0.5f);
-  b = (uint32_t)fmaf(255.f, fmaf(-vs, tb, v), 0.5f);
+  auto chan = [&](float n) {  // k = h6 + n; offsets folded: k - 2, k - 8, k - 14
+    const float m = fminf(fabsf(h6 + (n - 2.f)), fminf(fabsf(h6 + (n - 8.f)), fabsf(h6 + (n - 14.f))));
+    const float t = __saturatef(2.f - m);
+    const float y = fmaf(255.f, fmaf(-vs, t, v), 0.5f);
+    return __float_as_uint(__fadd_rd(y, M)) & 0xffu;
+  };
+  r = chan(5.f);
+  g = chan(3.f);
+  b = chan(1.f);
 }
 
 // exact BT.601 luma (299R + 587G + 114B + 500) / 1000

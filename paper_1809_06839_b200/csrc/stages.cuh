@@ -65,7 +65,9 @@ __device__ __forceinline__ void load_stages(const StepArgs& a, int img, uint32_t
       x.on[s] = fired_of(a.tab, img, a.stages[s].slot) ? 1 : 0;
       if (t == ST_HSV) {
         const double* q = prm_of(a.tab, img, a.stages[s].slot);
-        x.dh[s] = (float)(q[0] / 60.0);  // hue shift in sixths of a turn
+        double w = q[0] / 60.0;          // hue shift in sixths of a turn, wrapped to [0, 6)
+        w -= 6.0 * floor(w / 6.0);
+        x.dh[s] = (float)w;
         x.ds[s] = (float)q[1];
         x.dv[s] = (float)q[2];
       }
