@@ -10,4 +10,4 @@ for c in 3 4 5; do timeout 600 python bench.py --config $c > gpurun_out/bench_cf
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 0"
 $CMD > gpurun_out/plain_bench.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo launches=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo launches=$?
