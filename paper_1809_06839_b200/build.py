@@ -18,7 +18,8 @@ LIB = os.path.join(PKG, "libalb_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+         "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")] + \
+    os.environ.get("ALB_NVCC_FLAGS", "").split()  # e.g. -DALB_PROF (phase timing printouts)
 
 
 def _deps():

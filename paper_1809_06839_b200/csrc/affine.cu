@@ -33,6 +33,7 @@
 // Footprints larger than the staging capacity fall back to per-tap loads
 // (generic variant).
 #include <algorithm>
+#include <cstdio>
 
 #include "stages.cuh"
 
@@ -490,9 +491,9 @@ __global__ void __launch_bounds__(kAfThreads, kMask ? 2 : 3) k_affine(StepArgs a
 // ===================================================== pipelined fast path
 // Bilinear, no mask, u8 output, scale >= 0.9 (the single-op Rotate / SSR
 // path and any fused post crop / flip).  The footprint rows of tile t+1 are
-// fetched by the TMA engine (cp.async.bulk, one 16-byte aligned row range
-// per footprint row, completion on an mbarrier) into a RAW byte buffer while
-// the CTA computes tile t, so no warp waits on global loads.  Warps 0-10
+// fetched asynchronously (16-byte cp.async of each row's aligned range,
+// completion on an mbarrier) into a RAW byte buffer while the CTA computes
+// tile t, so no warp waits on global loads.  Warps 0-10
 // compute, warp 11 is the producer.  Per tile t:
 //   P: compute warps: wait raw(t); raw RGB -> RGBx stage (aligned 16-pixel
 //      runs, 3 LDS.128 + 16 byte permutes); border columns; anchor table
@@ -500,7 +501,7 @@ __global__ void __launch_bounds__(kAfThreads, kMask ? 2 : 3) k_affine(StepArgs a
 //      producer: geometry of tile t+1 (per-image state precomputed by
 //      k_affine_setup).                                        -- barrier
 //   C: compute warps: tile t, two rows x two columns per lane in flight.
-//      producer: TMA row copies of tile t+1 into the (now free) raw buffer.
+//      producer: async row copies of tile t+1 into the (now free) raw buffer.
 //                                                              -- barrier
 constexpr int kPThreads = 384;
 constexpr int kPWarps = kPThreads / 32;
@@ -615,8 +616,14 @@ __device__ __forceinline__ void pipe_geom(const StepArgs& a, int u, TileCtx* c, 
   __syncwarp();
 }
 
-// Producer warp, phase C: TMA row copies of c's footprint, row r ->
-// raw + r * kRawPitch, completion counted on `bar`.
+// Producer warp, phase C: asynchronous copies of c's footprint rows, row r ->
+// raw + r * kRawPitch (the 16-byte aligned hull of the row's columns).  Lane =
+// row; each lane issues 16-byte cp.async (LDGSTS) copies of its rows, then one
+// cp.async.mbarrier.arrive.noinc, so the mbarrier (32 expected arrivals)
+// completes when every copy of the tile has landed.  Measured alternatives
+// (ALB_PROF phase timing): one cp.async.bulk per row serialises the 32 lanes'
+// issue (bulk copies take uniform operands) and costs 1.5x the cycles; 8 lanes
+// per row (coalesced) or copies spread over all warps are slower still.
 __device__ __forceinline__ void pipe_issue(const StepArgs& a, const TileCtx* c, uint8_t* raw, uint32_t bar,
                                            int lane) {
   const TileGeom t = c->t;
@@ -624,7 +631,6 @@ __device__ __forceinline__ void pipe_issue(const StepArgs& a, const TileCtx* c, 
   const uint8_t* simg = a.src + sd.offset;
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
   const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
-  uint32_t bytes = 0;
   if (X1 > X0) {
     for (int r = lane; r < t.fh; r += 32) {
       bool row_in;
@@ -633,20 +639,13 @@ __device__ __forceinline__ void pipe_issue(const StepArgs& a, const TileCtx* c, 
       const uintptr_t g0 = (uintptr_t)(simg + (size_t)ry * sd.pitch + 3 * X0);
       const uintptr_t g1 = (uintptr_t)(simg + (size_t)ry * sd.pitch + 3 * X1);
       const uintptr_t ga = g0 & ~(uintptr_t)15, gb = (g1 + 15) & ~(uintptr_t)15;
-      const uint32_t nb = (uint32_t)(gb - ga);
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-              smem_u32(raw + r * kRawPitch)),
-          "l"(ga), "r"(nb), "r"(bar)
-          : "memory");
-      bytes += nb;
+      const uint32_t d0 = smem_u32(raw + r * kRawPitch);
+      for (uintptr_t g = ga; g < gb; g += 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + (uint32_t)(g - ga)), "l"(g)
+                     : "memory");
     }
   }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-  if (lane == 0)
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-  __syncwarp();
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 
 template <int kOne>
@@ -668,8 +667,8 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
   int u0, u1;
   unit_range(a.n_units, u0, u1);
   if (u0 >= u1) return;
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+  if (threadIdx.x == 0) {  // one arrival per producer lane per phase (pipe_issue)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;\n" ::"r"(bar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -679,6 +678,10 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
   }
   __syncthreads();
   int lut_img = -1;
+#ifdef ALB_PROF
+  long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tq = clock64();
+#endif
   for (int u = u0; u < u1; ++u) {
     const int it_t = u - u0;
     const TileCtx& c = ctx[it_t % 3];
@@ -725,7 +728,13 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
         const int rx = border_idx(t.fx0 + cc, Ws, reflect, col_in);
         stage[r * t.S + cc] = (row_in && col_in) ? fetch_rgb(simg + (size_t)ry * sd.pitch, rx) : a.fill;
       }
+#ifdef ALB_PROF
+      { const long long t1 = clock64(); pr[0] += t1 - tq; tq = t1; }
+#endif
       mbar_wait(bar, (uint32_t)(it_t & 1));
+#ifdef ALB_PROF
+      { const long long t1 = clock64(); pr[1] += t1 - tq; tq = t1; }
+#endif
       // raw RGB rows -> RGBx stage; thread -> (row = it % fh, run = it / fh)
       const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
       const int na = t.fh * t.nrun;
@@ -765,7 +774,13 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
         }
       }
     }
+#ifdef ALB_PROF
+    { const long long t1 = clock64(); pr[2] += t1 - tq; tq = t1; }
+#endif
     __syncthreads();
+#ifdef ALB_PROF
+    { const long long t1 = clock64(); pr[3] += t1 - tq; tq = t1; }
+#endif
     // ---------------- phase C
     if (producer) {
       if (u + 1 < u1) pipe_issue(a, &ctx[(it_t + 1) % 3], raw, bar, lane);
@@ -822,8 +837,20 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
         }
       }
     }
+#ifdef ALB_PROF
+    { const long long t1 = clock64(); pr[4] += t1 - tq; tq = t1; }
+#endif
     __syncthreads();
+#ifdef ALB_PROF
+    { const long long t1 = clock64(); pr[5] += t1 - tq; tq = t1; }
+#endif
   }
+#ifdef ALB_PROF
+  if ((blockIdx.x == 0 || blockIdx.x == 101) && lane == 0 && (warp == 0 || warp == 5 || producer))
+    printf("blk %d warp %d tiles %d: P-pre %lld mbar %lld P-post %lld barP %lld C %lld barC %lld (cycles/tile)\n",
+           blockIdx.x, warp, u1 - u0, pr[0] / (u1 - u0), pr[1] / (u1 - u0), pr[2] / (u1 - u0),
+           pr[3] / (u1 - u0), pr[4] / (u1 - u0), pr[5] / (u1 - u0));
+#endif
   if (!producer) {
     const TileCtx& p = ctx[(u1 - 1 - u0) % 3];
     copy_rows_out<kObFull, kCThreads>(p.drow0, p.dpitch, obuf, kObPitch, p.th, 3 * p.tw);
