@@ -519,11 +519,15 @@ struct AnEnt {
   int pad;
 };
 
+
 struct TileCtx {
   ImgState is;
   TileGeom t;
   uint8_t* drow0;
   int img, tx0, ty0, tw, th, cy0, ncy, dpitch;
+  // per footprint row r: staged columns [sx0[r], sx1[r]) (relative to fx0) --
+  // the rotated tile covers only this part of the bounding box's row
+  int16_t sx0[kRawRows], sx1[kRawRows];
 };
 
 static_assert(sizeof(ImgState) <= kGeoBytes, "ImgState must fit the per-image scratch");
@@ -555,15 +559,36 @@ __global__ void k_affine_setup(StepArgs a) {
   *reinterpret_cast<ImgState*>(reinterpret_cast<uint8_t*>(a.geo) + (size_t)img * kGeoBytes) = s;
 }
 
-// Producer warp, phase P: geometry of unit u into c.
-__device__ __forceinline__ void pipe_geom(const StepArgs& a, int u, TileCtx* c, const TileCtx* prev, int lane) {
-  const int2 unit = __ldg(a.units + u);
+// Global inputs of the producer's geometry for one unit (lane k holds word k
+// of the image's ImgState).  (Loading them one tile ahead measured slower.)
+struct GeomPre {
+  int2 unit;
+  uint32_t gw;
+  int ws;
+  alb_image_desc dd;
+};
+
+__device__ __forceinline__ GeomPre pipe_prefetch(const StepArgs& a, int u, int lane) {
+  constexpr int kW = (int)sizeof(ImgState) / 4;
+  GeomPre p;
+  p.unit = __ldg(a.units + u);
+  const int img = p.unit.x;
+  const uint32_t* g = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.geo) +
+                                                        (size_t)img * kGeoBytes);
+  p.gw = lane < kW ? __ldcg(g + lane) : 0u;
+  p.ws = a.sdesc[img].width;
+  p.dd = a.ddesc[img];
+  return p;
+}
+
+// Producer warp, phase P: geometry of the prefetched unit into c.
+__device__ __forceinline__ void pipe_geom(const StepArgs& a, const GeomPre& pre, TileCtx* c, const TileCtx* prev,
+                                          int lane) {
+  const int2 unit = pre.unit;
   const int img = unit.x;
   if (prev == nullptr || prev->img != img) {
     constexpr int kW = (int)sizeof(ImgState) / 4;
-    const uint32_t* g = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.geo) +
-                                                          (size_t)img * kGeoBytes);
-    if (lane < kW) reinterpret_cast<uint32_t*>(&c->is)[lane] = __ldcg(g + lane);
+    if (lane < kW) reinterpret_cast<uint32_t*>(&c->is)[lane] = pre.gw;
   } else if (lane == 0) {
     c->is = prev->is;
   }
@@ -588,8 +613,15 @@ __device__ __forceinline__ void pipe_geom(const StepArgs& a, int u, TileCtx* c, 
     ly = fmin(ly, __shfl_xor_sync(0xffffffffu, ly, o));
     hy = fmax(hy, __shfl_xor_sync(0xffffffffu, hy, o));
   }
+  // corners (xw0|xw1, yw0|yw1) of the tile in source space, lanes 0..3
+  double vx[4], vy[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    vx[k] = __shfl_sync(0xffffffffu, sx, k);
+    vy[k] = __shfl_sync(0xffffffffu, sy, k);
+  }
   if (lane == 0) {
-    const int Ws = a.sdesc[img].width;
+    const int Ws = pre.ws;
     TileGeom t;
     t.fx0 = (int)floor(lx) - 1;
     t.fy0 = (int)floor(ly) - 1;
@@ -609,9 +641,54 @@ __device__ __forceinline__ void pipe_geom(const StepArgs& a, int u, TileCtx* c, 
     c->img = img; c->tx0 = tx0; c->ty0 = ty0; c->tw = tw; c->th = th;
     c->cy0 = min(ywa, ywb) >> 4;
     c->ncy = (max(ywa, ywb) >> 4) - c->cy0 + 1;
-    const alb_image_desc dd = a.ddesc[img];
+    const alb_image_desc dd = pre.dd;
     c->drow0 = a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3;
     c->dpitch = dd.pitch;
+  }
+  __syncwarp();
+  // per-row spans: footprint row r (source row Y = fy0 + r) is tapped by the
+  // output pixels whose source y lies in [Y - 1, Y + 1); their source x range
+  // is the tile parallelogram cut by that strip (+ the right tap, 1 px margin).
+  // fp32 with per-edge reciprocal slopes (margins cover the rounding).
+  {
+    const int fx0 = c->t.fx0, fy0 = c->t.fy0, fw = c->t.fw, fh = c->t.fh;
+    const int ord[5] = {0, 1, 3, 2, 0};  // parallelogram vertex order
+    float ex[4], ey[4], edx[4], eiy[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      ex[e] = (float)(vx[ord[e]] - fx0);
+      ey[e] = (float)(vy[ord[e]] - fy0);
+      edx[e] = (float)(vx[ord[e + 1]] - vx[ord[e]]);
+      const float dy = (float)(vy[ord[e + 1]] - vy[ord[e]]);
+      eiy[e] = dy != 0.f ? 1.f / dy : 0.f;
+    }
+    for (int r = lane; r < fh; r += 32) {
+      const float ya = (float)r - 1.01f, yb = (float)r + 1.01f;
+      float xmn = 1e30f, xmx = -1e30f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (ey[e] >= ya && ey[e] <= yb) { xmn = fminf(xmn, ex[e]); xmx = fmaxf(xmx, ex[e]); }
+        if (eiy[e] != 0.f) {
+#pragma unroll
+          for (int bnd = 0; bnd < 2; ++bnd) {
+            const float tt = ((bnd ? yb : ya) - ey[e]) * eiy[e];
+            if (tt >= -1e-4f && tt <= 1.0001f) {
+              const float xx = fmaf(tt, edx[e], ex[e]);
+              xmn = fminf(xmn, xx);
+              xmx = fmaxf(xmx, xx);
+            }
+          }
+        }
+      }
+      int s0 = 0, s1 = 0;
+      if (xmx >= xmn) {
+        s0 = max((int)floorf(xmn) - 1, 0);
+        s1 = min((int)floorf(xmx) + 3, fw);
+        if (s1 < s0) s1 = s0;
+      }
+      c->sx0[r] = (int16_t)s0;
+      c->sx1[r] = (int16_t)s1;
+    }
   }
   __syncwarp();
 }
@@ -630,9 +707,10 @@ __device__ __forceinline__ void pipe_issue(const StepArgs& a, const TileCtx* c, 
   const alb_image_desc sd = a.sdesc[c->img];
   const uint8_t* simg = a.src + sd.offset;
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
-  const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
-  if (X1 > X0) {
+  {
     for (int r = lane; r < t.fh; r += 32) {
+      const int X0 = t.fx0 + max((int)c->sx0[r], t.ci0), X1 = t.fx0 + min((int)c->sx1[r], t.ci1);
+      if (X1 <= X0) continue;
       bool row_in;
       const int ry = border_idx(t.fy0 + r, sd.height, reflect, row_in);
       if (!row_in) continue;
@@ -673,7 +751,7 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
   }
   __syncthreads();
   if (producer) {
-    pipe_geom(a, u0, &ctx[0], nullptr, lane);
+    pipe_geom(a, pipe_prefetch(a, u0, lane), &ctx[0], nullptr, lane);
     pipe_issue(a, &ctx[0], raw, bar, lane);
   }
   __syncthreads();
@@ -693,7 +771,7 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
     }
     // ---------------- phase P
     if (producer) {
-      if (u + 1 < u1) pipe_geom(a, u + 1, &ctx[(it_t + 1) % 3], &c, lane);
+      if (u + 1 < u1) pipe_geom(a, pipe_prefetch(a, u + 1, lane), &ctx[(it_t + 1) % 3], &c, lane);
     } else {
       const int tid = threadIdx.x;
       if (it_t > 0) {  // copy-out of the previous tile
@@ -723,6 +801,7 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
       for (int it = tid; it < t.fh * t.P; it += kCThreads) {
         const int j = fdiv(it, t.m_fh), r = it - j * t.fh;
         const int cc = j < t.ci0 ? j : t.ci1 + (j - t.ci0);
+        if (cc < c.sx0[r] || cc >= c.sx1[r]) continue;
         bool row_in, col_in;
         const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
         const int rx = border_idx(t.fx0 + cc, Ws, reflect, col_in);
@@ -736,10 +815,11 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
       { const long long t1 = clock64(); pr[1] += t1 - tq; tq = t1; }
 #endif
       // raw RGB rows -> RGBx stage; thread -> (row = it % fh, run = it / fh)
-      const int X0 = t.fx0 + t.ci0, X1 = t.fx0 + t.ci1;
       const int na = t.fh * t.nrun;
       for (int it = tid; it < na; it += kCThreads) {
         const int k = fdiv(it, t.m_fh), r = it - k * t.fh;
+        const int X0 = t.fx0 + max((int)c.sx0[r], t.ci0), X1 = t.fx0 + min((int)c.sx1[r], t.ci1);
+        if (X1 <= X0) continue;
         bool row_in;
         const int ry = border_idx(t.fy0 + r, Hs, reflect, row_in);
         uint32_t* drow = stage + r * t.S - t.fx0;
