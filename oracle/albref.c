@@ -248,6 +248,14 @@ static int validate_ops(const albref_op* ops, int32_t n_ops) {
         if (o->out_w < 1 || o->out_h < 1 || o->min_side < 1 || o->max_side < o->min_side)
           return ALBREF_E_RANGE;
         break;
+      case ALBREF_ROT90:
+      case ALBREF_D4: { /* integer element range inside the group */
+        const double top = o->kind == ALBREF_ROT90 ? 3.0 : 7.0;
+        if (!(o->lo[0] >= 0.0 && o->hi[0] <= top) || floor(o->lo[0]) != o->lo[0] ||
+            floor(o->hi[0]) != o->hi[0])
+          return ALBREF_E_RANGE;
+        break;
+      }
       case ALBREF_NORMALIZE:
         if (k != n_ops - 1 || o->p != 1.0) return ALBREF_E_RANGE;
         for (int c = 0; c < 3; ++c)
@@ -277,6 +285,19 @@ static int step_shape(const albref_op* o, int32_t h, int32_t w, int32_t* oh, int
       int32_t mside = h < w ? h : w;
       if (o->min_side > mside) return ALBREF_E_INVALID_ARG;
       *oh = o->out_h; *ow = o->out_w; return ALBREF_OK;
+    }
+    case ALBREF_ROT90:
+    case ALBREF_D4: {
+      /* an odd number of quarter turns transposes the shape: the output shape
+       * must not depend on the draw, so a non-square image needs every
+       * outcome (including "gate not fired") to have the same parity */
+      int can_odd = 0, can_even = o->p < 1.0;
+      for (int32_t e = (int32_t)o->lo[0]; e <= (int32_t)o->hi[0]; ++e) {
+        if ((e & 1) != 0) can_odd = 1; else can_even = 1;
+      }
+      if (can_odd && can_even && h != w) return ALBREF_E_UNSUPPORTED;
+      if (can_odd) { *oh = w; *ow = h; } else { *oh = h; *ow = w; }
+      return ALBREF_OK;
     }
     default:
       *oh = h; *ow = w; return ALBREF_OK;
@@ -332,6 +353,11 @@ static void draw_params(const albref_op* o, uint64_t seed, uint64_t idx, int32_t
       prm[0] = (double)o->crop_x;
       prm[1] = (double)o->crop_y;
       break;
+    case ALBREF_ROT90: /* quarter turns, uniform over the integer range */
+    case ALBREF_D4:    /* group element, uniform over the integer range */
+      prm[0] = o->lo[0] + (double)uniform_int(albref_draw(seed, idx, slot, 1),
+                                              (int32_t)(o->hi[0] - o->lo[0]) + 1);
+      break;
     case ALBREF_RANDOM_SIZED_CROP: { /* side, x0, y0 (R6) */
       int32_t mside = h < w ? h : w;
       int32_t hi = o->max_side < mside ? o->max_side : mside;
@@ -360,6 +386,11 @@ int albref_sample_params(const albref_op* ops, int32_t n_ops, uint64_t seed,
     rc = step_shape(&ops[k], h, w, &nh, &nw);
     if (rc) return rc;
     draw_params(&ops[k], seed, image_index, k, h, w, &params[k * ALBREF_MAX_PARAMS]);
+    if (ops[k].kind == ALBREF_ROT90 || ops[k].kind == ALBREF_D4) {
+      /* the shape follows the drawn element (only square images may differ) */
+      nh = h; nw = w;
+      if (fired[k] && ((int32_t)params[k * ALBREF_MAX_PARAMS] & 1)) { nh = w; nw = h; }
+    }
     if (fired[k]) { h = nh; w = nw; }
   }
   return ALBREF_OK;
@@ -673,6 +704,46 @@ static void op_normalize(const state_t* s, const albref_op* o, float* out) {
       }
 }
 
+/* -------------------------------------------------- D4 / rot90 */
+
+/* One counter-clockwise (as displayed) quarter turn:
+ * out has height W, width H and out[y][x] = in[x][W-1-y].  Boxes in
+ * pixel-edge coordinates: a point (X, Y) goes to (Y, W - X), i.e. the
+ * normalized (x, y) -> (y, 1 - x) of SPEC.md:196, then corners re-sorted. */
+static void op_rot90_once(state_t* s) {
+  const int32_t H = s->h, W = s->w, ho = W, wo = H;
+  uint8_t* px = xalloc((size_t)ho * wo * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)ho * wo) : NULL;
+  for (int32_t y = 0; y < ho; ++y)
+    for (int32_t x = 0; x < wo; ++x) {
+      /* in[x][W-1-y]: row x, column W-1-y */
+      for (int c = 0; c < s->c; ++c)
+        px[((size_t)y * wo + x) * s->c + c] = s->px[((size_t)x * W + (W - 1 - y)) * s->c + c];
+      if (mk) mk[(size_t)y * wo + x] = s->mask[(size_t)x * W + (W - 1 - y)];
+    }
+  for (int32_t b = 0; b < s->nbox; ++b) {
+    const double X0 = s->box[4 * b + 0], Y0 = s->box[4 * b + 1];
+    const double X1 = s->box[4 * b + 2], Y1 = s->box[4 * b + 3];
+    s->box[4 * b + 0] = Y0;
+    s->box[4 * b + 2] = Y1;
+    s->box[4 * b + 1] = (double)W - X1;
+    s->box[4 * b + 3] = (double)W - X0;
+  }
+  replace_px(s, px, mk, ho, wo);
+}
+
+/* rot90 by k quarter turns = k single turns */
+static void op_rot90(state_t* s, int32_t k) {
+  for (int32_t i = 0; i < (k & 3); ++i) op_rot90_once(s);
+}
+
+/* D4 element e: e in {r^0..r^3, h o r^0..h o r^3}, r = rot90(1),
+ * h = hflip; h o r^k applies r^k first, then h. */
+static void op_d4(state_t* s, int32_t e) {
+  op_rot90(s, e & 3);
+  if (e >= 4) op_hflip(s);
+}
+
 /* ---------------------------------------------------------- O14 apply */
 
 int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
@@ -751,6 +822,8 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
       case ALBREF_GRAYSCALE: op_grayscale(&s); break;
       case ALBREF_EQUALIZE: op_equalize(&s); break;
       case ALBREF_NORMALIZE: op_normalize(&s, o, nchw_out); break;
+      case ALBREF_ROT90: op_rot90(&s, (int32_t)q[0]); break;
+      case ALBREF_D4: op_d4(&s, (int32_t)q[0]); break;
       default: break;
     }
   }

@@ -37,7 +37,9 @@ enum {
   ALBREF_BRIGHTNESS_CONTRAST = 10, ALBREF_GAMMA = 11, ALBREF_SHIFT_RGB = 12,
   ALBREF_SHIFT_HSV = 13, ALBREF_GRAYSCALE = 14, ALBREF_EQUALIZE = 15,
   ALBREF_NORMALIZE = 16, ALBREF_CROP = 17,
-  ALBREF_NUM_KINDS = 18
+  ALBREF_ROT90 = 18,  /* SPEC.md:193-201; k quarter turns, k in [lo[0], hi[0]] */
+  ALBREF_D4 = 19,     /* SPEC.md:202-210; element e in [lo[0], hi[0]] of 0..7 */
+  ALBREF_NUM_KINDS = 20
 };
 enum { ALBREF_INTERP_NEAREST = 0, ALBREF_INTERP_BILINEAR = 1 };
 enum { ALBREF_BORDER_CONSTANT = 0, ALBREF_BORDER_REFLECT_101 = 1 };

@@ -662,3 +662,95 @@ def test_validation_errors():
             run(ops, img)
     with pytest.raises(A.OracleError):
         A.apply([{"kind": "Grayscale"}], 0, 0, img[:, :, :1])
+
+
+# --------------------------------------------------- D4 / rot90
+
+def _r90(k):
+    return [{"kind": "Rotate90", "lo": [k], "hi": [k]}]
+
+
+def _d4(e):
+    return [{"kind": "D4", "lo": [e], "hi": [e]}]
+
+
+def test_rot90_spec_examples_and_numpy():
+    """1x2 [a, b], k=1 -> 2x1 [b; a]; k=0 identity; the pixel
+    map out[y][x] = in[x][W-1-y] is numpy's counter-clockwise np.rot90."""
+    ab = np.array([[[1, 1, 1], [2, 2, 2]]], np.uint8)
+    r = run(_r90(1), ab)["image"]
+    assert r.shape == (2, 1, 3) and (r[:, 0, 0] == [2, 1]).all()
+    img = rand_img(5, 8)
+    m = RNG.integers(0, 7, size=(5, 8), dtype=np.uint8)
+    for k in range(4):
+        out = run(_r90(k), img, mask=m)
+        assert (out["image"] == np.rot90(img, k)).all(), k
+        assert (out["mask"] == np.rot90(m, k)).all(), k
+    four = run(_r90(1) * 4, img)["image"]  # group law r^4 = e (SPEC.md:198)
+    assert (four == img).all()
+
+
+def test_rot90_boxes_spec_example_and_half_turn():
+    """SPEC.md:199: box (0.0, 0.0, 0.5, 0.25), k=1 -> envelope (0.0, 0.5, 0.25, 1.0);
+    k=2 on boxes equals hflip o vflip."""
+    img = rand_img(12, 12)
+    r = run(_r90(1), img, boxes=np.array([[0.0, 0.0, 0.5, 0.25]], np.float32))
+    assert np.allclose(r["boxes"][0], [0.0, 0.5, 0.25, 1.0], atol=1e-7)
+    rng = np.random.default_rng(21)
+    xs = np.sort(rng.uniform(0, 1, size=(20, 2)), axis=1)
+    ys = np.sort(rng.uniform(0, 1, size=(20, 2)), axis=1)
+    bx = np.stack([xs[:, 0], ys[:, 0], xs[:, 1], ys[:, 1]], 1).astype(np.float32)
+    img2 = rand_img(9, 14)
+    a = run(_r90(2), img2, boxes=bx)["boxes"]
+    b = run([{"kind": "HorizontalFlip"}, {"kind": "VerticalFlip"}], img2, boxes=bx)["boxes"]
+    assert np.allclose(a, b, atol=1e-6)
+    # k=1 boxes by the corner map (x, y) -> (y, 1 - x) (SPEC.md:196), non-square
+    c = run(_r90(1), img2, boxes=bx)["boxes"]
+    want = np.stack([bx[:, 1], 1 - bx[:, 2], bx[:, 3], 1 - bx[:, 0]], 1)
+    assert np.allclose(c, want, atol=1e-6)
+
+
+def test_d4_elements_and_cayley_closure():
+    """element 0 identity, element 4 = hflip, element e =
+    h^(e>=4) o r^(e&3) (= np.fliplr(np.rot90(x, e&3))), and the 8 x 8 Cayley
+    table is closed on a random 8x8 image (brute force)."""
+    ab = np.array([[[1, 1, 1], [2, 2, 2]]], np.uint8)
+    assert (run(_d4(4), ab)["image"] == ab[:, ::-1]).all()
+    img = rand_img(8, 8)
+    outs = []
+    for e in range(8):
+        o = run(_d4(e), img)["image"]
+        ref = np.rot90(img, e & 3)
+        if e >= 4:
+            ref = ref[:, ::-1]
+        assert (o == ref).all(), e
+        outs.append(o)
+    assert (outs[0] == img).all()
+    for i in range(8):
+        for j in range(8):
+            comp = run(_d4(i) + _d4(j), img)["image"]
+            assert any((comp == outs[k]).all() for k in range(8)), (i, j)
+    assert len({o.tobytes() for o in outs}) == 8  # the 8 elements are distinct
+
+
+def test_rot90_shape_rule_and_draws():
+    """Reading R25: a random element range whose parity can change on a
+    non-square image is rejected; odd-only ranges transpose the shape; on a
+    square image any range is fine; draws are uniform over the range."""
+    assert A.output_shape([{"kind": "Rotate90", "lo": [3], "hi": [3]}], 5, 8) == (8, 5)
+    assert A.output_shape([{"kind": "D4", "lo": [5], "hi": [5]}], 5, 8) == (8, 5)
+    assert A.output_shape([{"kind": "Rotate90", "lo": [2], "hi": [2]}], 5, 8) == (5, 8)
+    with pytest.raises(A.OracleError):  # {1, 2, 3} mixes parities on a non-square image
+        A.output_shape([{"kind": "Rotate90", "lo": [1], "hi": [3]}], 5, 8)
+    assert A.output_shape([{"kind": "Rotate90", "lo": [0], "hi": [3]}], 6, 6) == (6, 6)
+    with pytest.raises(A.OracleError):
+        A.output_shape([{"kind": "Rotate90", "lo": [0], "hi": [3]}], 5, 8)
+    with pytest.raises(A.OracleError):  # p < 1 on a non-square image with an odd element
+        A.output_shape([{"kind": "D4", "p": 0.5, "lo": [1], "hi": [1]}], 5, 8)
+    with pytest.raises(A.OracleError):
+        A.output_shape([{"kind": "D4", "lo": [0], "hi": [8]}], 6, 6)
+    counts = np.zeros(8, int)
+    for idx in range(4000):
+        prm, fired = A.sample_params([{"kind": "D4", "lo": [0], "hi": [7]}], 3, idx, 6, 6)
+        counts[int(prm[0][0])] += 1
+    assert counts.min() > 400 and counts.max() < 600
