@@ -77,7 +77,13 @@ typedef enum {
   ALB_EQUALIZE = 15,             /* BASELINE cfg2; O11/R15                       */
   ALB_NORMALIZE = 16,            /* BASELINE cfg4; O12/R16 -> fp32 NCHW, last op */
   ALB_CROP = 17,                 /* PAPER.md:37 "cropping"; O3 fixed window      */
-  ALB_NUM_KINDS = 18
+  ALB_ROT90 = 18,                /* PAPER.md:87; SPEC.md:193-201 k quarter turns
+                                    (counter-clockwise as displayed), k uniform in
+                                    the integer range [lo[0], hi[0]] within 0..3   */
+  ALB_D4 = 19,                   /* PAPER.md:87 "dihedral group"
+                                    element e uniform in [lo[0], hi[0]] within 0..7:
+                                    e < 4 -> rot90(e), else hflip(rot90(e - 4))   */
+  ALB_NUM_KINDS = 20
 } alb_kind;
 
 typedef enum { ALB_INTERP_NEAREST = 0, ALB_INTERP_BILINEAR = 1 } alb_interp;
@@ -86,7 +92,10 @@ typedef enum { ALB_BORDER_CONSTANT = 0, ALB_BORDER_REFLECT_101 = 1 } alb_border;
 /* One transform (SPEC.md:470-474 TransformSpec).  Continuous parameter j is
  * drawn as lo[j] + (hi[j]-lo[j])*u_j (O1); lo == hi fixes it.
  * Shape-changing kinds (RandomCrop, Crop, PadToSize, Resize, RandomSizedCrop)
- * require p == 1 (reading R17) so batch output shapes are static. */
+ * require p == 1 (reading R17) so batch output shapes are static.  Rot90 / D4
+ * transpose the shape for odd elements: on a non-square image every outcome
+ * (including an unfired gate) must have the same parity, else the plan fails
+ * with ALB_E_UNSUPPORTED (reading R25). */
 typedef struct {
   int32_t kind;
   double p;

@@ -63,7 +63,7 @@ struct alb_layout {
 
 namespace {
 
-enum StepKind { SK_ROW = 0, SK_POINT = 1, SK_RESAMPLE = 2, SK_AFFINE = 3, SK_EQ = 4 };
+enum StepKind { SK_ROW = 0, SK_POINT = 1, SK_RESAMPLE = 2, SK_AFFINE = 3, SK_EQ = 4, SK_D4 = 5 };
 enum BufId { B_IN = 0, B_OUT = 1, B_WS0 = 2, B_WS1 = 3, B_NONE = 4 };
 
 struct PlanStep {
@@ -160,6 +160,13 @@ static alb_status validate_ops(const alb_op* ops, int n_ops) {
         if (o.out_w < 1 || o.out_h < 1 || o.min_side < 1 || o.max_side < o.min_side)
           return fail(ALB_E_RANGE, at + "bad RandomSizedCrop sides");
         break;
+      case ALB_ROT90: case ALB_D4: {
+        const double top = o.kind == ALB_ROT90 ? 3.0 : 7.0;
+        if (!(o.lo[0] >= 0.0 && o.hi[0] <= top) || std::floor(o.lo[0]) != o.lo[0] ||
+            std::floor(o.hi[0]) != o.hi[0])
+          return fail(ALB_E_RANGE, at + "element range must be integers within the group");
+        break;
+      }
       case ALB_NORMALIZE:
         if (k != n_ops - 1 || o.p != 1.0) return fail(ALB_E_RANGE, at + "Normalize must be last, p = 1");
         for (int c = 0; c < 3; ++c)
@@ -194,6 +201,15 @@ static alb_status track_dims(const std::vector<alb_op>& ops, int h, int w,
       case ALB_RANDOM_SIZED_CROP:
         if (o.min_side > std::min(h, w)) return fail(ALB_E_INVALID_ARG, "RandomSizedCrop min side > image");
         h = o.out_h; w = o.out_w; break;
+      case ALB_ROT90: case ALB_D4: {
+        // the shape must not depend on the draw (reading R25)
+        bool can_odd = false, can_even = o.p < 1.0;
+        for (int e = (int)o.lo[0]; e <= (int)o.hi[0]; ++e) (e & 1 ? can_odd : can_even) = true;
+        if (can_odd && can_even && h != w)
+          return fail(ALB_E_UNSUPPORTED, "Rot90/D4 whose parity varies on a non-square image");
+        if (can_odd) std::swap(h, w);
+        break;
+      }
       default: break;
     }
   }
@@ -390,6 +406,13 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       geo_open = point_open = false;
       continue;
     }
+    if (kind == ALB_ROT90 || kind == ALB_D4) {  // signed permutation, own step
+      PlanStep st; st.kind = SK_D4; st.slot0 = k; st.slot1 = k + 1;
+      steps.push_back(st);
+      ++k;
+      geo_open = point_open = false;
+      continue;
+    }
     if (kind == ALB_RESIZE || kind == ALB_RANDOM_SIZED_CROP || kind == ALB_ROTATE ||
         kind == ALB_SHIFT_SCALE_ROTATE) {
       PlanStep st;
@@ -457,7 +480,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   }
   // rgb-only ops need 3 channels: images are always 3-channel here.
   const bool has_geo = std::any_of(steps.begin(), steps.end(), [](const PlanStep& s) {
-    return s.kind == SK_ROW || s.kind == SK_RESAMPLE || s.kind == SK_AFFINE;
+    return s.kind == SK_ROW || s.kind == SK_RESAMPLE || s.kind == SK_AFFINE || s.kind == SK_D4;
   });
   // masks ride on geometric steps; without one, an identity mask copy
   if (mask_in && !has_geo) {
@@ -554,6 +577,15 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
             for (int y = 0; y < sl->h[i].height; ++y) st.units.push_back(make_int2(i, y));
           }
         }
+        break;
+      }
+      case SK_D4: {  // 64 x 64 output tiles, unit.y = (row << 16) | col (images and masks)
+        for (int i = 0; i < P->n; ++i) {
+          const int H = dims[i][st.slot1].first, W = dims[i][st.slot1].second;
+          for (int ty = 0; ty < (H + 63) / 64; ++ty)
+            for (int tx = 0; tx < (W + 63) / 64; ++tx) st.units.push_back(make_int2(i, (ty << 16) | tx));
+        }
+        if (st.has_mask) st.munits = st.units;
         break;
       }
       case SK_AFFINE: {
@@ -664,7 +696,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   // launches per apply
   int L = 1;  // prep
   for (auto& st : steps) {
-    if (st.kind == SK_ROW) L += (st.has_image ? 1 : 0) + (st.has_mask ? 1 : 0);
+    if (st.kind == SK_ROW || st.kind == SK_D4) L += (st.has_image ? 1 : 0) + (st.has_mask ? 1 : 0);
     else if (st.kind == SK_EQ) L += 2;
     else L += 1;
   }
@@ -828,6 +860,18 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
       }
       case SK_RESAMPLE: launch_resample(a, stream); break;
       case SK_AFFINE: launch_affine(a, stream); break;
+      case SK_D4:
+        if (st.has_image) {
+          a.channels = 3;
+          launch_d4(a, stream);
+        }
+        if (st.has_mask) {
+          a.channels = 1;
+          a.units = P->d_units + st.munits_off;
+          a.n_units = (int)st.munits.size();
+          launch_d4(a, stream);
+        }
+        break;
       case SK_EQ: {
         EqArgs e{};
         e.src = a.src;

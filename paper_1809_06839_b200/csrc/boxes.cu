@@ -66,6 +66,20 @@ __device__ void box_through_op(const alb_op& o, const double* q, int hin, int wi
       X0 = lx; X1 = hx; Y0 = ly; Y1 = hy;
       break;
     }
+    case ALB_ROT90: case ALB_D4: {  // (x, y) -> (y, 1 - x) per quarter turn
+      const int e = (int)q[0];
+      double w = win;
+      for (int t = 0; t < (e & 3); ++t) {  // pixel-edge frame: (X, Y) -> (Y, w - X)
+        const double nx0 = Y0, nx1 = Y1, ny0 = __dsub_rn(w, X1), ny1 = __dsub_rn(w, X0);
+        w = (t & 1) ? (double)win : (double)hin;  // width of the frame after this turn
+        X0 = nx0; X1 = nx1; Y0 = ny0; Y1 = ny1;
+      }
+      if (e >= 4) {  // then hflip in the rotated frame
+        const double a = __dsub_rn(w, X1), b = __dsub_rn(w, X0);
+        X0 = a; X1 = b;
+      }
+      break;
+    }
     default: break;
   }
 }

@@ -150,6 +150,7 @@ void launch_point(const StepArgs& a, cudaStream_t s);
 void launch_rowgather(const StepArgs& a, cudaStream_t s);
 void launch_resample(const StepArgs& a, cudaStream_t s);
 void launch_affine(const StepArgs& a, cudaStream_t s);
+void launch_d4(const StepArgs& a, cudaStream_t s);
 void launch_eq_hist(const EqArgs& a, cudaStream_t s);
 void launch_eq_lut(const EqArgs& a, cudaStream_t s);
 void launch_boxes(const BoxArgs& a, cudaStream_t s);

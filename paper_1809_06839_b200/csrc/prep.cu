@@ -72,6 +72,10 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
         case ALB_PAD_TO_SIZE: case ALB_RESIZE:
           nh = o.out_h; nw = o.out_w;
           break;
+        case ALB_ROT90: case ALB_D4:  // element, uniform over the integer range
+          q[0] = o.lo[0] + (double)uint_draw(draw_u(a.seed, gi, k, 1), (int)(o.hi[0] - o.lo[0]) + 1);
+          if ((int)q[0] & 1) { nh = w; nw = h; }
+          break;
         default: break;
       }
       s_fired[k] = fired ? 1 : 0;

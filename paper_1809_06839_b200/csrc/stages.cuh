@@ -370,6 +370,39 @@ __device__ __forceinline__ void copy_partial(uint8_t* d, const uint8_t* s, int l
   }
 }
 
+// CTA copy of `rows` buffered rows to global.  Row r's n bytes sit in the
+// buffer at [r*pitch + phase, +n) where phase = (global row address) & 15, so
+// every 16-byte chunk is aligned on both sides.  Full chunks first (kFull =
+// max full chunks per row), then one item per partial head / tail chunk.
+template <int kFull, int NT>
+__device__ __forceinline__ void copy_rows_out(uint8_t* g0, int gpitch, const uint8_t* b0, int bpitch,
+                                              int rows, int n) {
+  for (int it = threadIdx.x; it < rows * kFull; it += NT) {
+    const int r = it / kFull, k = it - r * kFull;
+    uint8_t* grow = g0 + (size_t)r * gpitch;
+    const int o = (int)((uintptr_t)grow & 15);
+    const int c = ((o + 15) >> 4) + k;
+    if (16 * c + 16 <= o + n)
+      __stcs(reinterpret_cast<uint4*>(grow - o + 16 * c),
+             *reinterpret_cast<const uint4*>(b0 + r * bpitch + 16 * c));
+  }
+  for (int it = threadIdx.x; it < 2 * rows; it += NT) {
+    const bool head = it < rows;
+    const int r = head ? it : it - rows;
+    uint8_t* grow = g0 + (size_t)r * gpitch;
+    const int o = (int)((uintptr_t)grow & 15);
+    const uint8_t* s = b0 + r * bpitch;
+    uint8_t* d = grow - o;
+    const int e = o + n;
+    if (head) {  // chunk 0 when the row does not start on a chunk boundary
+      if (o > 0) copy_partial(d, s, o, min(e, 16));
+    } else {     // last chunk when the row does not end on a chunk boundary
+      const int c = e >> 4, hi = e & 15;
+      if (hi > 0 && (c > 0 || o == 0)) copy_partial(d + 16 * c, s + 16 * c, 0, hi);
+    }
+  }
+}
+
 // Warp copy of one buffered row to global: the row's n bytes sit in `buf`
 // (16-byte aligned) at [phase, phase + n), phase = (global row address) & 15,
 // so every 16-byte chunk is aligned on both sides.

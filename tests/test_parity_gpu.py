@@ -279,3 +279,55 @@ def test_cfg5_fused_equals_unfused_gpu_chain():
         r2 = run_gpu(tail, r1["out_batch"], masks=r1["mask_batch"])
         assert np.array_equal(r2["images"][0], fused["images"][i]), i
         assert np.array_equal(r2["masks"][0], fused["masks"][i]), i
+
+
+# ------------------------------------------------------ D4 / rot90 (§8(f) row 1)
+
+D4_CASES = [
+    # (specs, sizes): every element fixed on a non-square ragged batch (parity fixed
+    # per op), and random elements on square images of several tile counts
+    ([{"kind": "D4", "lo": [e], "hi": [e]}], [(45, 130), (70, 17), (129, 64), (1, 1), (3, 200)])
+    for e in range(8)
+] + [
+    ([{"kind": "D4", "lo": [0], "hi": [7], "p": 0.7}], [(s, s) for s in (1, 5, 63, 64, 65, 130, 200)]),
+    ([{"kind": "Rotate90", "lo": [0], "hi": [3]}], [(s, s) for s in (2, 31, 97, 128, 150)]),
+    ([{"kind": "Rotate90", "lo": [3], "hi": [3]}, {"kind": "HorizontalFlip", "p": 0.5},
+      {"kind": "Brightness", "lo": [0.8], "hi": [1.2]}], [(40, 90), (91, 33), (64, 200)]),
+]
+
+
+@pytest.mark.parametrize("case", range(len(D4_CASES)))
+def test_d4_rot90_image_mask_boxes_bit_exact(case):
+    specs, sizes = D4_CASES[case]
+    n = len(sizes)
+    b = gen.gen_images(sizes, seed=0, first_image_index=40, device="cuda")
+    bx, lb, cnt, masks = gen.gen_boxes(sizes, seed=0, first_image_index=40)
+    masks = masks.to("cuda")
+    res = run_gpu(specs, b, seed=11, first=40, masks=masks, boxes=bx, labels=lb, count=cnt,
+                  max_boxes=bx.shape[1], min_visibility=0.0)
+    imgs = [b.image(i) for i in range(n)]
+    mk = [masks.image(i) for i in range(n)]
+    ref = run_oracle(specs, imgs, seed=11, first=40, masks=mk, boxes=bx, labels=lb, count=cnt)
+    cmp_exact(res["images"], [o["image"] for o in ref])
+    cmp_exact(res["masks"], [o["mask"] for o in ref])
+    for i in range(n):
+        k = res["count"][i]
+        assert k == len(ref[i]["labels"]), (i, k, len(ref[i]["labels"]))
+        assert np.array_equal(res["labels"][i, :k], ref[i]["labels"])
+        assert np.abs(res["boxes"][i, :k] - ref[i]["boxes"]).max(initial=0) <= 1e-6
+
+
+def test_d4_params_and_shape_rule():
+    from oracle import albref as A
+    from paper_1809_06839_b200 import Pipeline
+    from paper_1809_06839_b200._lib import AlbError
+    specs = [{"kind": "D4", "lo": [0], "hi": [7], "p": 0.5}]
+    sizes = [(33, 33)] * 200
+    p, f = Pipeline(specs).sample_params(77, 3, sizes)
+    for i, (h, w) in enumerate(sizes):
+        rp, rf = A.sample_params(specs, 77, 3 + i, h, w)
+        assert np.array_equal(rf, f[i]) and np.array_equal(rp, p[i]), i
+    pipe = Pipeline([{"kind": "Rotate90", "lo": [1], "hi": [1]}])
+    assert pipe.output_shape(20, 30) == (30, 20)
+    with pytest.raises(AlbError):
+        Pipeline([{"kind": "Rotate90", "lo": [0], "hi": [1]}]).output_shape(20, 30)

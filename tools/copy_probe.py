@@ -32,8 +32,11 @@ def timeit(fn, reps=20):
 t = timeit(lambda: out.copy_(b.buf))
 print("torch copy_ corpus: %.3f ms  %.1f GB/s (alg %.1f GB/s)" % (t, 2 * b.buf.numel() / t / 1e6, 2 * nbytes / t / 1e6))
 inl = Layout(b.desc, 3)
+EXTRA = {"Rot90k1": [{"kind": "Rotate90", "lo": [1], "hi": [1]}],
+         "D4e5": [{"kind": "D4", "lo": [5], "hi": [5]}],
+         "D4e2": [{"kind": "D4", "lo": [2], "hi": [2]}]}
 for name in sys.argv[1:] or ["Brightness", "HorizontalFlip", "Grayscale"]:
-    specs = C.CFG2_MENU[name]
+    specs = EXTRA.get(name) or C.CFG2_MENU[name]
     p = Pipeline(specs)
     ob = gen.empty_batch([p.output_shape(h, w) for h, w in sizes], 3, "cuda")
     plan = Plan(p, inl, Layout(ob.desc, 3))
