@@ -566,8 +566,11 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
             flat = flat && st.dst_l->h[i].pitch == st.dst_l->h[i].width * 3 && st.dst_l->h[i].offset % 16 == 0;
         }
         st.flat = flat;
-        // histogram units are 4x larger: fewer per-unit zero / merge passes
-        const int chunk = st.kind == SK_EQ ? 4 * kChunk : kChunk;
+        // histogram units are 96 KB (fewer per-unit zero / merge passes);
+        // pointwise steps take a whole image per unit: one CTA per image stages
+        // the image's lane-replicated LUTs once and the hardware balances the
+        // CTAs (measured faster than persistent CTAs over 24 KB chunks)
+        const int chunk = st.kind == SK_EQ ? 4 * kChunk : (st.kind == SK_POINT ? (1 << 30) : kChunk);
         st.unit_size = chunk;
         for (int i = 0; i < P->n; ++i) {
           if (flat) {

@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
 template <bool kNL1>
 static void launch_lut(const StepArgs& a, size_t smem, cudaStream_t s) {
   smem += 8192;  // slack to align the LUT base to 8 KB
-  const int grid = persistent_grid((const void*)k_point_lut<kNL1>, kThreads, smem, a.n_units);
+  persistent_grid((const void*)k_point_lut<kNL1>, kThreads, smem, a.n_units);  // smem attribute
+  const int grid = a.n_units;  // one CTA per unit (whole images in flat mode)
   k_point_lut<kNL1><<<grid, kThreads, smem, s>>>(a);
 }
 
