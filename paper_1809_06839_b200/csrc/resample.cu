@@ -547,8 +547,8 @@ size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normali
 
 template <int kOne, bool kNorm, int kCols>
 static void launch_sep_v(const StepArgs& a, size_t smem, cudaStream_t s) {
-  const int grid = persistent_grid((const void*)k_resample_sep<kOne, kNorm, kCols>, 256 / kCols, smem, a.n_units);
-  k_resample_sep<kOne, kNorm, kCols><<<grid, 256 / kCols, smem, s>>>(a);
+  persistent_grid((const void*)k_resample_sep<kOne, kNorm, kCols>, 256 / kCols, smem, a.n_units);  // smem attribute
+  k_resample_sep<kOne, kNorm, kCols><<<a.n_units, 256 / kCols, smem, s>>>(a);  // one CTA per unit
 }
 
 template <int kOne>
