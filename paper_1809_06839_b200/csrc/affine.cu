@@ -169,17 +169,12 @@ __global__ void __launch_bounds__(kAfThreads, kMask ? 2 : 3) k_affine(StepArgs a
     __syncthreads();  // previous tile fully consumed
     if (img != cur_img) {
       load_stages(a, img, sm, x, kAfThreads);
-      if (threadIdx.x == 0) {
-        const AfCoef cf = af_coef(a, img);
-        ImgState s;
-        for (int k = 0; k < 6; ++k) s.A[k] = cf.A[k];
-        s.Af[0] = (float)cf.A[0]; s.Af[1] = (float)cf.A[1];
-        s.Af[2] = (float)cf.A[3]; s.Af[3] = (float)cf.A[4];
-        s.Wo = a.normalize ? a.out_w : a.ddesc[img].width;
-        s.Ho = a.normalize ? a.out_h : a.ddesc[img].height;
-        s.m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, s.Wo, s.Ho);
-        s.tiles_x = (s.Wo + kTileW - 1) / kTileW;
-        *is = s;
+      {  // per-image state precomputed by k_affine_setup (one word per thread)
+        constexpr int kW = (int)sizeof(ImgState) / 4;
+        if (threadIdx.x < kW)
+          reinterpret_cast<uint32_t*>(is)[threadIdx.x] = __ldcg(
+              reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.geo) + (size_t)img * kGeoBytes) +
+              threadIdx.x);
       }
       cur_img = img;
       __syncthreads();
@@ -518,8 +513,8 @@ __global__ void k_affine_setup(StepArgs a) {
   for (int k = 0; k < 6; ++k) s.A[k] = cf.A[k];
   s.Af[0] = (float)cf.A[0]; s.Af[1] = (float)cf.A[1];
   s.Af[2] = (float)cf.A[3]; s.Af[3] = (float)cf.A[4];
-  s.Wo = a.ddesc[img].width;
-  s.Ho = a.ddesc[img].height;
+  s.Wo = a.normalize ? a.out_w : a.ddesc[img].width;
+  s.Ho = a.normalize ? a.out_h : a.ddesc[img].height;
   s.m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, s.Wo, s.Ho);
   s.tiles_x = (s.Wo + kTileW - 1) / kTileW;
   s.pad = 0;
@@ -911,8 +906,8 @@ static size_t affine_smem(const StepArgs& a) {
 
 template <int kOne, bool kMask, int kMode>
 static void launch_affine_v(const StepArgs& a, size_t smem, cudaStream_t s) {
-  const int grid = persistent_grid((const void*)k_affine<kOne, kMask, kMode>, kAfThreads, smem, a.n_units);
-  k_affine<kOne, kMask, kMode><<<grid, kAfThreads, smem, s>>>(a);
+  persistent_grid((const void*)k_affine<kOne, kMask, kMode>, kAfThreads, smem, a.n_units);  // smem attribute
+  k_affine<kOne, kMask, kMode><<<a.n_units, kAfThreads, smem, s>>>(a);  // one CTA per tile
 }
 
 template <int kOne>
@@ -928,15 +923,18 @@ static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
   } else if (mask) {
     launch_affine_v<kOne, true, 0>(a, smem, s);
   } else {  // pipelined TMA-staged path
-    k_affine_setup<<<(a.n_img + 127) / 128, 128, 0, s>>>(a);
     const size_t psmem = (size_t)count_lut_stages(a) * kLutWords * 4 + kPSmem;
-    const int grid = persistent_grid((const void*)k_affine_pipe<kOne>, kPThreads, psmem, a.n_units);
+    // ~16 tiles per CTA: long enough to pipeline, short enough that the
+    // hardware re-balances CTAs across SMs (measured: 16 > 8, 32 > persistent)
+    const int grid = std::max(persistent_grid((const void*)k_affine_pipe<kOne>, kPThreads, psmem, a.n_units),
+                              (a.n_units + 15) / 16);
     k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(a);
   }
 }
 
 void launch_affine(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
+  k_affine_setup<<<(a.n_img + 127) / 128, 128, 0, s>>>(a);  // per-image state for both kernels
   const size_t smem = affine_smem(a);
   const int mode = stage_mode(a);
   ALB_DISPATCH_STAGES(mode, launch_affine_t, a, smem, s)
