@@ -158,6 +158,60 @@ __device__ __forceinline__ void hsv_shift_px(float dh6w, float ds, float dv, uin
   b = chan(1.f);
 }
 
+// Two pixels at once on the paired fp32 pipe (FADD2 / FFMA2 / FMUL2 where
+// both pixels run the same operation; min / max / select / reciprocal per
+// pixel).  Every per-pixel value equals hsv_shift_px's bit for bit (a paired
+// op rounds each lane exactly like its scalar op), so the fused resample /
+// affine paths (scalar) and the pointwise kernel (paired) agree.
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, uint32_t (&r)[2], uint32_t (&g)[2],
+                                              uint32_t (&b)[2]) {
+  const float M = 8388608.f;
+  float2 Rb, Gb, Bb;
+  Rb.x = __uint_as_float(r[0] | 0x4B000000u); Rb.y = __uint_as_float(r[1] | 0x4B000000u);
+  Gb.x = __uint_as_float(g[0] | 0x4B000000u); Gb.y = __uint_as_float(g[1] | 0x4B000000u);
+  Bb.x = __uint_as_float(b[0] | 0x4B000000u); Bb.y = __uint_as_float(b[1] | 0x4B000000u);
+  float2 mxb, mnb, pa, pb, off;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float R = i ? Rb.y : Rb.x, G = i ? Gb.y : Gb.x, B = i ? Bb.y : Bb.x;
+    const float hi = fmaxf(R, fmaxf(G, B)), lo = fminf(R, fminf(G, B));
+    const bool isr = hi == R;
+    const bool isg = !isr && hi == G;
+    const float A_ = isr ? G : (isg ? B : R), B_ = isr ? B : (isg ? R : G);
+    const float o = isr ? dh6w : (isg ? dh6w + 2.f : dh6w + 4.f);
+    if (i) { mxb.y = hi; mnb.y = lo; pa.y = A_; pb.y = B_; off.y = o; }
+    else { mxb.x = hi; mnb.x = lo; pa.x = A_; pb.x = B_; off.x = o; }
+  }
+  const float2 d = f2add(mxb, make_float2(-mnb.x, -mnb.y));
+  const float2 mx = f2add(mxb, make_float2(-M, -M));
+  const float2 rd = make_float2(fminf(rcp_approx(d.x), 2.f), fminf(rcp_approx(d.y), 2.f));
+  const float2 rm = make_float2(fminf(rcp_approx(mx.x), 2.f), fminf(rcp_approx(mx.y), 2.f));
+  const float2 h6 = f2fma(f2add(pa, make_float2(-pb.x, -pb.y)), rd, off);
+  float2 sv = f2fma(d, rm, make_float2(ds, ds));
+  sv = make_float2(__saturatef(sv.x), __saturatef(sv.y));
+  float2 vv = f2fma(mx, make_float2(1.f / 255.f, 1.f / 255.f), make_float2(dv, dv));
+  vv = make_float2(__saturatef(vv.x), __saturatef(vv.y));
+  const float2 vs = __fmul2_rn(vv, sv);
+  const float2 nvs = make_float2(-vs.x, -vs.y);
+  auto chan = [&](float n, uint32_t (&out)[2]) {
+    const float2 k2 = f2add(h6, make_float2(n - 2.f, n - 2.f));
+    const float2 k8 = f2add(h6, make_float2(n - 8.f, n - 8.f));
+    const float2 k14 = f2add(h6, make_float2(n - 14.f, n - 14.f));
+    const float2 t = make_float2(__saturatef(2.f - fminf(fabsf(k2.x), fminf(fabsf(k8.x), fabsf(k14.x)))),
+                                 __saturatef(2.f - fminf(fabsf(k2.y), fminf(fabsf(k8.y), fabsf(k14.y)))));
+    const float2 y = f2fma(make_float2(255.f, 255.f), f2fma(nvs, t, vv), make_float2(0.5f, 0.5f));
+    out[0] = __float_as_uint(__fadd_rd(y.x, M)) & 0xffu;
+    out[1] = __float_as_uint(__fadd_rd(y.y, M)) & 0xffu;
+  };
+  uint32_t ro[2], go[2], bo[2];
+  chan(5.f, ro);
+  chan(3.f, go);
+  chan(1.f, bo);
+  r[0] = ro[0]; r[1] = ro[1]; g[0] = go[0]; g[1] = go[1]; b[0] = bo[0]; b[1] = bo[1];
+}
+
 // exact BT.601 luma (299R + 587G + 114B + 500) / 1000
 __device__ __forceinline__ uint32_t gray_px(uint32_t r, uint32_t g, uint32_t b) {
   return (299u * r + 587u * g + 114u * b + 500u) / 1000u;

@@ -228,6 +228,27 @@ __global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
 #pragma unroll
         for (int q = 0; q < 12; ++q) o[q] = 0;
         const size_t p0 = s.pidx0 + (s.bA + 48 * gi) / 3;
+        if constexpr (kOne == ST_HSV && !kNorm) {  // pixel pairs on the paired fp32 pipe
+          if (x.on[0]) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              const uint32_t p0 = rgbx_of(w[k], i), p1 = rgbx_of(w[k], i + 1);
+              uint32_t r[2] = {p0 & 0xff, p1 & 0xff}, g[2] = {(p0 >> 8) & 0xff, (p1 >> 8) & 0xff},
+                       b[2] = {p0 >> 16, p1 >> 16};
+              hsv_shift_px2(x.dh[0], x.ds[0], x.dv[0], r, g, b);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int ii = i + h;
+                o[(3 * ii) >> 2] |= r[h] << (((3 * ii) & 3) * 8);
+                o[(3 * ii + 1) >> 2] |= g[h] << (((3 * ii + 1) & 3) * 8);
+                o[(3 * ii + 2) >> 2] |= b[h] << (((3 * ii + 2) & 3) * 8);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 12; ++q) o[q] = w[k][q];
+          }
+        } else
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const uint32_t px = rgbx_of(w[k], i);

@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
           else hrow(rw.y1, h1);
           hr1 = rw.y1;
         }
+        uint32_t rq[kCols], gq[kCols], bq[kCols];
 #pragma unroll
         for (int q = 0; q < kCols; ++q) {
           const float2 V = __ffma2_rn(make_float2(rw.fy, rw.fy),
@@ -509,11 +510,16 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
                                       make_float2(h0[q].x, h0[q].y));
           const float vb = fmaf(rw.fy, h1[q].z - h0[q].z, h0[q].z);
           const float2 R2 = fadd2_rm(V, make_float2(8388608.f, 8388608.f));
-          uint32_t r = __float_as_uint(R2.x), gg = __float_as_uint(R2.y), b = __float_as_uint(__fadd_rd(vb, 8388608.f));
+          rq[q] = __float_as_uint(R2.x); gq[q] = __float_as_uint(R2.y); bq[q] = __float_as_uint(__fadd_rd(vb, 8388608.f));
           if constexpr (kOne != kStagesNone || kNorm) {
-            r &= 0xffu; gg &= 0xffu; b &= 0xffu;
+            rq[q] &= 0xffu; gq[q] &= 0xffu; bq[q] &= 0xffu;
           }
-          apply_stages_t<kOne>(x, sm, lane, r, gg, b);
+        }
+        if constexpr (kCols == 2) apply_stages2_t<kOne>(x, sm, lane, rq, gq, bq);
+        else apply_stages_t<kOne>(x, sm, lane, rq[0], gq[0], bq[0]);
+#pragma unroll
+        for (int q = 0; q < kCols; ++q) {
+          const uint32_t r = rq[q], gg = gq[q], b = bq[q];
           if (cb + 32 * q < cw) {
             if constexpr (kNorm) {
               const size_t plane = (size_t)Ho * Wo;
@@ -553,9 +559,10 @@ static void launch_sep_v(const StepArgs& a, size_t smem, cudaStream_t s) {
 
 template <int kOne>
 static void launch_sep_t(const StepArgs& a, size_t smem, cudaStream_t s) {
+  // two columns per lane (shared row control, paired-pipe stage chains),
+  // except for Normalize outputs where one column per lane measured faster
   if (a.normalize) launch_sep_v<kOne, true, 1>(a, smem, s);
-  else if (kOne == kStagesNone) launch_sep_v<kOne, false, 2>(a, smem, s);
-  else launch_sep_v<kOne, false, 1>(a, smem, s);
+  else launch_sep_v<kOne, false, 2>(a, smem, s);
 }
 
 static size_t resample_smem(const StepArgs& a) {

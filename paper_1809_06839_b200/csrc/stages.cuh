@@ -121,6 +121,43 @@ __device__ __forceinline__ void apply_stages_t(const StageCtx& x, const uint32_t
   }
 }
 
+// Two pixels through the stage program (kOne as apply_stages_t): HSV runs on
+// the paired fp32 pipe (hsv_shift_px2, bit-identical per pixel), LUT / gray
+// stages per pixel.
+template <int kOne>
+__device__ __forceinline__ void apply_stages2_t(const StageCtx& x, const uint32_t* sm, int lane,
+                                                uint32_t (&r)[2], uint32_t (&g)[2], uint32_t (&b)[2]) {
+  if constexpr (kOne == kStagesNone) {
+    return;
+  } else if constexpr (kOne == ST_HSV) {
+    if (x.on[0]) hsv_shift_px2(x.dh[0], x.ds[0], x.dv[0], r, g, b);
+  } else if constexpr (kOne == kStagesGeneric) {
+#pragma unroll
+    for (int s = 0; s < kMaxStages; ++s) {
+      const int t = x.type[s];
+      if (t == ST_LUT || t == ST_EQ) {
+        const uint32_t* L = sm + x.smb[s];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          r[h] = lut_look(L, 0, r[h], lane);
+          g[h] = lut_look(L, 2048, g[h], lane);
+          b[h] = lut_look(L, 4096, b[h], lane);
+        }
+      } else if (t == ST_HSV) {
+        if (x.on[s]) hsv_shift_px2(x.dh[s], x.ds[s], x.dv[s], r, g, b);
+      } else if (t == ST_GRAY) {
+        if (x.on[s]) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) r[h] = g[h] = b[h] = gray_px(r[h], g[h], b[h]);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) apply_stages_t<kOne>(x, sm, lane, r[h], g[h], b[h]);
+  }
+}
+
 inline int stage_mode(const StepArgs& a) {
   if (a.n_stages == 0) return kStagesNone;
   if (a.n_stages == 1) return a.stages[0].type;
