@@ -95,7 +95,7 @@ typedef enum { ALB_BORDER_CONSTANT = 0, ALB_BORDER_REFLECT_101 = 1 } alb_border;
  * require p == 1 (reading R17) so batch output shapes are static.  Rot90 / D4
  * transpose the shape for odd elements: on a non-square image every outcome
  * (including an unfired gate) must have the same parity, else the plan fails
- * with ALB_E_UNSUPPORTED (reading R25). */
+ * with ALB_E_UNSUPPORTED (reading R30). */
 typedef struct {
   int32_t kind;
   double p;

@@ -202,7 +202,7 @@ static alb_status track_dims(const std::vector<alb_op>& ops, int h, int w,
         if (o.min_side > std::min(h, w)) return fail(ALB_E_INVALID_ARG, "RandomSizedCrop min side > image");
         h = o.out_h; w = o.out_w; break;
       case ALB_ROT90: case ALB_D4: {
-        // the shape must not depend on the draw (reading R25)
+        // the shape must not depend on the draw (reading R30)
         bool can_odd = false, can_even = o.p < 1.0;
         for (int e = (int)o.lo[0]; e <= (int)o.hi[0]; ++e) (e & 1 ? can_odd : can_even) = true;
         if (can_odd && can_even && h != w)

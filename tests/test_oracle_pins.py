@@ -734,7 +734,7 @@ def test_d4_elements_and_cayley_closure():
 
 
 def test_rot90_shape_rule_and_draws():
-    """Reading R25: a random element range whose parity can change on a
+    """Reading R30: a random element range whose parity can change on a
     non-square image is rejected; odd-only ranges transpose the shape; on a
     square image any range is fine; draws are uniform over the range."""
     assert A.output_shape([{"kind": "Rotate90", "lo": [3], "hi": [3]}], 5, 8) == (8, 5)
