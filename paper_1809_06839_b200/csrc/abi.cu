@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -252,7 +253,7 @@ static void row_units(PlanStep& st, const alb_layout* dst, int channels, std::ve
   int wmax = 1;
   for (auto& d : dst->h) wmax = std::max(wmax, d.width);
   const int nbmax = 2 + wmax / 16;
-  usize = std::max(1, 1024 / nbmax);
+  usize = std::max(1, 2048 / nbmax);  // ~8 blocks of 16 px per thread (measured: 2048 > 1024, 4096)
   (void)channels;
   (void)st;
   for (int i = 0; i < dst->n; ++i)
