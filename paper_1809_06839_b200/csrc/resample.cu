@@ -262,7 +262,8 @@ struct SepRow {
   float fy;
   int ob;      // byte offset of the row in the output row buffers (incl. 16-byte phase)
   int yo;      // output row
-  int pad[3];
+  int s0, s1;  // ring slots of y0, y1
+  int pad;
 };
 struct SepState {
   RsGeom g;
@@ -340,7 +341,9 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
         const alb_image_desc dd = a.ddesc[img];
         e.ob = (i % G) * kSepObp + (int)((uintptr_t)(a.dst + dd.offset + (size_t)yo * dd.pitch + (size_t)xs0 * 3) & 15);
       }
-      e.pad[0] = e.pad[1] = e.pad[2] = 0;
+      e.s0 = slot(e.y0);
+      e.s1 = slot(e.y1);
+      e.pad = 0;
       rowt[i] = e;
     }
     // this lane's two columns (fp64, definition order O5) and the strip's window columns
@@ -418,8 +421,8 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
 #pragma unroll
     for (int q = 0; q < kCols; ++q) h0[q] = h1[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     int hr0 = -1, hr1 = -1;
-    auto hrow = [&](int r, float4 (&h)[kCols]) {  // horizontal lerps of staged window row r
-      const uint32_t* srow = src + slot(r) * SW;
+    auto hrow = [&](int sl, float4 (&h)[kCols]) {  // horizontal lerps of the staged row in slot sl
+      const uint32_t* srow = src + sl * SW;
 #pragma unroll
       for (int q = 0; q < kCols; ++q) {
         const uint32_t t0 = srow[o0[q]], t1 = srow[o1[q]];
@@ -492,14 +495,14 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
             for (int q = 0; q < kCols; ++q) h0[q] = h1[q];
             hr0 = hr1;
           }
-          else { hrow(rw.y0, h0); hr0 = rw.y0; }
+          else { hrow(rw.s0, h0); hr0 = rw.y0; }
         }
         if (rw.y1 != hr1) {
           if (rw.y1 == hr0) {
 #pragma unroll
             for (int q = 0; q < kCols; ++q) h1[q] = h0[q];
           }
-          else hrow(rw.y1, h1);
+          else hrow(rw.s1, h1);
           hr1 = rw.y1;
         }
         uint32_t rq[kCols], gq[kCols], bq[kCols];
