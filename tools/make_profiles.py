@@ -108,16 +108,17 @@ def main():
                     op, d['name'].split('(')[0][:40], t, rd, wr, (rd + wr) / t if t else 0.0, d.get(M[4], 0.0), d.get(M[5], 0.0),
                     int(d.get(M[6], 0)), inst, inst * 32.0 / px.get(op, same), d.get(M[8], 0.0), d.get(M[9], 0.0)))
             traffic[op] = round((tot_r + tot_w) * 1e6)
-    with open(os.path.join(out_dir, '%s_ncu_summary.md' % tag), 'w') as f:
-        f.write('\n'.join(lines) + '\n\n"inst / out px" = lane instructions (warp instructions x 32) per output '
-                'pixel.\n')
-    tj = os.path.join(out_dir, 'ncu_traffic.json')
-    old = json.load(open(tj)) if os.path.exists(tj) else {}
-    old['cfg2'] = traffic
-    old['note'] = ('dram__bytes_read.sum + dram__bytes_write.sum per launch of each transform\'s kernels '
-                   '(ncu --set full, %s)' % tag)
-    with open(tj, 'w') as f:
-        json.dump(old, f, indent=1)
+    if fulls:
+        with open(os.path.join(out_dir, '%s_ncu_summary.md' % tag), 'w') as f:
+            f.write('\n'.join(lines) + '\n\n"inst / out px" = lane instructions (warp instructions x 32) per output '
+                    'pixel.\n')
+        tj = os.path.join(out_dir, 'ncu_traffic.json')
+        old = json.load(open(tj)) if os.path.exists(tj) else {}
+        old['cfg2'] = traffic
+        old['note'] = ('dram__bytes_read.sum + dram__bytes_write.sum per launch of each transform\'s kernels '
+                       '(ncu --set full, %s)' % tag)
+        with open(tj, 'w') as f:
+            json.dump(old, f, indent=1)
     if launches:
         t = defaultdict(float)
         c = defaultdict(int)
