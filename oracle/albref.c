@@ -256,6 +256,10 @@ static int validate_ops(const albref_op* ops, int32_t n_ops) {
           return ALBREF_E_RANGE;
         break;
       }
+      case ALBREF_GRID_DISTORTION: /* step factors 1 + U(lo, hi) must stay > 0 */
+        if (o->num_steps < 1 || o->num_steps > ALBREF_GRID_MAX_STEPS) return ALBREF_E_RANGE;
+        if (!(o->lo[0] > -1.0 && o->hi[0] < 1.0)) return ALBREF_E_RANGE;
+        break;
       case ALBREF_NORMALIZE:
         if (k != n_ops - 1 || o->p != 1.0) return ALBREF_E_RANGE;
         for (int c = 0; c < 3; ++c)
@@ -744,6 +748,89 @@ static void op_d4(state_t* s, int32_t e) {
   if (e >= 4) op_hflip(s);
 }
 
+/* ------------------------------------------- GridDistortion */
+
+/* Reading R31.  Destination knots d_i = i (L-1)/n, i = 0..n; the
+ * cells get lengths proportional to the step factors f_0..f_{n-1} rescaled to
+ * the span L-1 ("rescaled to preserve total span"):
+ *   c_0 = 0, c_{i+1} = c_i + f_i, S = c_n,  s_i = (L-1) c_i / S.
+ * The map is kept as a displacement field ("converts to
+ * DisplacementField"): e_i = s_i - d_i at the knots (e_0 = e_n = 0), linear in
+ * between, so for destination x with u = x n / (L-1), i = min(floor(u), n-1),
+ * t = u - i:
+ *   src(x) = x + (e_i + t (e_{i+1} - e_i)),  clamped to [0, L-1].
+ * f_n is drawn (SPEC.md:330 draws n+1 factors per axis) but no cell uses it. */
+int albref_grid_axis(int32_t L, int32_t n, const double* f, double* src) {
+  if (n < 1 || n > ALBREF_GRID_MAX_STEPS || L < 1) return ALBREF_E_RANGE;
+  for (int32_t i = 0; i < n; ++i)
+    if (!(f[i] > 0.0)) return ALBREF_E_RANGE;
+  if (L == 1) { src[0] = 0.0; return ALBREF_OK; }
+  double c[ALBREF_GRID_MAX_STEPS + 1], e[ALBREF_GRID_MAX_STEPS + 1];
+  c[0] = 0.0;
+  for (int32_t i = 0; i < n; ++i) c[i + 1] = c[i] + f[i];
+  const double S = c[n], span = (double)(L - 1);
+  e[0] = 0.0;
+  e[n] = 0.0;
+  for (int32_t i = 1; i < n; ++i) e[i] = span * c[i] / S - span * (double)i / (double)n;
+  for (int32_t x = 0; x < L; ++x) {
+    const double u = (double)x * (double)n / span;
+    int32_t i = (int32_t)floor(u);
+    if (i > n - 1) i = n - 1;
+    const double t = u - (double)i;
+    double v = (double)x + (e[i] + t * (e[i + 1] - e[i]));
+    if (v < 0.0) v = 0.0;
+    if (v > span) v = span;
+    src[x] = v;
+  }
+  return ALBREF_OK;
+}
+
+/* Remap with the separable maps (mx, my): bilinear taps (x0, min(x0+1, W-1)),
+ * as O5 (the maps stay inside the image, so no border rule is reached);
+ * nearest = round_half_up; masks nearest. */
+static void op_grid(state_t* s, const albref_op* o, uint64_t seed, uint64_t idx, int32_t slot) {
+  const int32_t n = o->num_steps;
+  double fx[ALBREF_GRID_MAX_STEPS + 1], fy[ALBREF_GRID_MAX_STEPS + 1];
+  for (int32_t i = 0; i <= n; ++i) { /* x factors j = 1..n+1, then y factors */
+    fx[i] = 1.0 + uniform_range(o->lo[0], o->hi[0], albref_draw(seed, idx, slot, 1 + i));
+    fy[i] = 1.0 + uniform_range(o->lo[0], o->hi[0], albref_draw(seed, idx, slot, n + 2 + i));
+  }
+  double* mx = (double*)malloc(sizeof(double) * s->w);
+  double* my = (double*)malloc(sizeof(double) * s->h);
+  albref_grid_axis(s->w, n, fx, mx);
+  albref_grid_axis(s->h, n, fy, my);
+  uint8_t* px = xalloc((size_t)s->h * s->w * s->c);
+  uint8_t* mk = s->mask ? xalloc((size_t)s->h * s->w) : NULL;
+  for (int32_t y = 0; y < s->h; ++y) {
+    const double ys = my[y];
+    for (int32_t x = 0; x < s->w; ++x) {
+      const double xs = mx[x];
+      uint8_t* out = &px[((size_t)y * s->w + x) * s->c];
+      const int32_t xn = (int32_t)floor(xs + 0.5), yn = (int32_t)floor(ys + 0.5);
+      if (o->interp == ALBREF_INTERP_NEAREST) {
+        for (int c = 0; c < s->c; ++c) out[c] = s->px[((size_t)yn * s->w + xn) * s->c + c];
+      } else {
+        const double fx0 = floor(xs), fy0 = floor(ys);
+        const int32_t x0 = (int32_t)fx0, y0 = (int32_t)fy0;
+        const int32_t x1 = x0 + 1 < s->w ? x0 + 1 : s->w - 1;
+        const int32_t y1 = y0 + 1 < s->h ? y0 + 1 : s->h - 1;
+        const double ax = xs - fx0, ay = ys - fy0;
+        for (int c = 0; c < s->c; ++c) {
+          double p00 = s->px[((size_t)y0 * s->w + x0) * s->c + c];
+          double p10 = s->px[((size_t)y0 * s->w + x1) * s->c + c];
+          double p01 = s->px[((size_t)y1 * s->w + x0) * s->c + c];
+          double p11 = s->px[((size_t)y1 * s->w + x1) * s->c + c];
+          out[c] = albref_clip_round(bilerp(p00, p10, p01, p11, ax, ay));
+        }
+      }
+      if (mk) mk[(size_t)y * s->w + x] = s->mask[(size_t)yn * s->w + xn];
+    }
+  }
+  free(mx);
+  free(my);
+  replace_px(s, px, mk, s->h, s->w);
+}
+
 /* ---------------------------------------------------------- O14 apply */
 
 int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
@@ -762,6 +849,8 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
     return ALBREF_E_INVALID_ARG;
   for (int32_t k = 0; k < n_ops; ++k) {
     int32_t kd = ops[k].kind;
+    if (kd == ALBREF_GRID_DISTORTION && n_boxes > 0)
+      return ALBREF_E_UNSUPPORTED; /* boxes under free-form warps */
     if (channels != 3 && (kd == ALBREF_SHIFT_RGB || kd == ALBREF_SHIFT_HSV ||
                           kd == ALBREF_GRAYSCALE || kd == ALBREF_NORMALIZE))
       return ALBREF_E_UNSUPPORTED; /* SPEC.md:411, 429, 438 */
@@ -824,6 +913,7 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
       case ALBREF_NORMALIZE: op_normalize(&s, o, nchw_out); break;
       case ALBREF_ROT90: op_rot90(&s, (int32_t)q[0]); break;
       case ALBREF_D4: op_d4(&s, (int32_t)q[0]); break;
+      case ALBREF_GRID_DISTORTION: op_grid(&s, o, seed, image_index, k); break;
       default: break;
     }
   }

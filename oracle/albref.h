@@ -39,7 +39,8 @@ enum {
   ALBREF_NORMALIZE = 16, ALBREF_CROP = 17,
   ALBREF_ROT90 = 18,  /* SPEC.md:193-201; k quarter turns, k in [lo[0], hi[0]] */
   ALBREF_D4 = 19,     /* SPEC.md:202-210; element e in [lo[0], hi[0]] of 0..7 */
-  ALBREF_NUM_KINDS = 20
+  ALBREF_GRID_DISTORTION = 20, /* SPEC.md:325-332; Fig. 4: factors 1 + U(lo[0], hi[0]) */
+  ALBREF_NUM_KINDS = 21
 };
 enum { ALBREF_INTERP_NEAREST = 0, ALBREF_INTERP_BILINEAR = 1 };
 enum { ALBREF_BORDER_CONSTANT = 0, ALBREF_BORDER_REFLECT_101 = 1 };
@@ -60,7 +61,11 @@ typedef struct {
   int32_t interp, border;   /* ALBREF_INTERP_*, ALBREF_BORDER_*             */
   uint8_t fill[3], mask_fill;
   double mean[3], std[3];   /* Normalize                                    */
+  int32_t num_steps;        /* GridDistortion cells per axis, [1, 32]       */
+  int32_t reserved;
 } albref_op;
+
+#define ALBREF_GRID_MAX_STEPS 32
 
 #define ALBREF_MAX_PARAMS 8
 
@@ -75,6 +80,11 @@ double albref_draw(uint64_t seed, uint64_t image_index, int32_t slot, int32_t j)
 uint8_t albref_clip_round(double v);
 /* reflect-101 index (periodic extension R7). */
 int32_t albref_reflect101(int32_t i, int32_t n);
+
+/* GridDistortion axis map (reading R31): source coordinate src[x] of every
+ * destination index x in [0, L) for step factors f[0..n] (f[n] is drawn but
+ * unused).  Returns ALBREF_E_RANGE for n outside [1, 32] or a factor <= 0. */
+int albref_grid_axis(int32_t L, int32_t n, const double* f, double* src);
 
 /* hexcone colour model, double precision. */
 void albref_rgb_to_hsv(double r, double g, double b, double* h, double* s, double* v);

@@ -27,7 +27,7 @@ KINDS = {
     "RandomCrop": 4, "PadToSize": 5, "Resize": 6, "RandomSizedCrop": 7,
     "Brightness": 8, "Contrast": 9, "BrightnessContrast": 10, "Gamma": 11,
     "ShiftRGB": 12, "ShiftHSV": 13, "Grayscale": 14, "Equalize": 15,
-    "Normalize": 16, "Crop": 17, "Rotate90": 18, "D4": 19,
+    "Normalize": 16, "Crop": 17, "Rotate90": 18, "D4": 19, "GridDistortion": 20,
 }
 INTERP = {"nearest": 0, "bilinear": 1}
 BORDER = {"constant": 0, "reflect_101": 1}
@@ -46,6 +46,7 @@ class AlbrefOp(ctypes.Structure):
         ("interp", ctypes.c_int32), ("border", ctypes.c_int32),
         ("fill", ctypes.c_uint8 * 3), ("mask_fill", ctypes.c_uint8),
         ("mean", ctypes.c_double * 3), ("std", ctypes.c_double * 3),
+        ("num_steps", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 
@@ -84,6 +85,7 @@ def lib():
         L.albref_hsv_to_rgb.argtypes = [ctypes.c_double] * 3 + [D] * 3
         L.albref_build_lut.argtypes = [ctypes.c_int32, D, ctypes.c_void_p]
         L.albref_equalize_lut.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        L.albref_grid_axis.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
         L.albref_output_shape.argtypes = [P(AlbrefOp), ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, P(ctypes.c_int32), P(ctypes.c_int32)]
         L.albref_sample_params.argtypes = [P(AlbrefOp), ctypes.c_int32, ctypes.c_uint64,
@@ -131,6 +133,7 @@ def make_ops(specs):
         for c in range(3):
             o.fill[c] = int(f[c])
         o.mask_fill = int(s.get("mask_fill", 0))
+        o.num_steps = int(s.get("num_steps", 0))
         m = s.get("mean", (0.0, 0.0, 0.0))
         d = s.get("std", (1.0, 1.0, 1.0))
         for c in range(3):
@@ -193,6 +196,15 @@ def equalize_lut(hist):
     lut = np.zeros(256, np.uint8)
     _check(lib().albref_equalize_lut(h.ctypes.data, lut.ctypes.data))
     return lut
+
+
+def grid_axis(L, n, factors):
+    """GridDistortion source coordinate of every destination index along an
+    axis of length L for step factors f[0..n] (reading R31)."""
+    f = np.ascontiguousarray(factors, np.float64)
+    out = np.zeros(max(1, L), np.float64)
+    _check(lib().albref_grid_axis(L, n, f.ctypes.data, out.ctypes.data))
+    return out[:L]
 
 
 def output_shape(specs, h, w):

@@ -5,7 +5,7 @@ memory and the current stream.  Op specs are dicts:
     {"kind": "Rotate", "p": 1.0, "lo": [-90], "hi": [90],
      "interp": "bilinear", "border": "reflect_101"}
 
-with optional size=(w, h), side=(min, max), origin=(x, y), fill, mask_fill,
+with optional size=(w, h), side=(min, max), origin=(x, y), fill, mask_fill, num_steps,
 mean, std (see include/alb_b200.h for the meaning of every field).
 """
 from __future__ import annotations
@@ -40,6 +40,7 @@ def make_ops(specs):
         for c in range(3):
             o.fill[c] = int(f[c])
         o.mask_fill = int(s.get("mask_fill", 0))
+        o.num_steps = int(s.get("num_steps", 0))
         m = s.get("mean", (0.0, 0.0, 0.0))
         d = s.get("std", (1.0, 1.0, 1.0))
         for c in range(3):

@@ -754,3 +754,111 @@ def test_rot90_shape_rule_and_draws():
         prm, fired = A.sample_params([{"kind": "D4", "lo": [0], "hi": [7]}], 3, idx, 6, 6)
         counts[int(prm[0][0])] += 1
     assert counts.min() > 400 and counts.max() < 600
+
+
+# ------------------------------------------------------------ GridDistortion
+
+def _grid(lo, hi, n, interp="bilinear", p=1.0):
+    return [{"kind": "GridDistortion", "p": p, "lo": [lo], "hi": [hi], "num_steps": n, "interp": interp}]
+
+
+def test_grid_axis_hand_example():
+    """Reading R31 traced by hand: L = 11, n = 2, f = (1.5, 0.5): knots d = (0, 5, 10),
+    S = 2, s = (0, 7.5, 10), so slope 1.5 on [0, 5] and 0.5 on [5, 10].  f[n] is unused."""
+    want = [0, 1.5, 3, 4.5, 6, 7.5, 8, 8.5, 9, 9.5, 10]
+    for last in (1.0, 0.3, 1.9):
+        assert A.grid_axis(11, 2, [1.5, 0.5, last]).tolist() == want
+    assert A.grid_axis(1, 3, [1.2, 0.7, 1.1, 1.0]).tolist() == [0.0]
+    with pytest.raises(A.OracleError):
+        A.grid_axis(10, 0, [1.0])
+    with pytest.raises(A.OracleError):
+        A.grid_axis(10, 2, [1.0, 0.0, 1.0])
+
+
+def test_grid_axis_monotone_span_and_knots():
+    """over 1000 random draws the axis map is strictly
+    monotone, keeps the span (src[0] = 0, src[L-1] = L-1 exactly), passes
+    through the rescaled knots s_i = (L-1) c_i / S (exact rational arithmetic)
+    and is linear inside each cell with slope n f_i / S."""
+    rng = np.random.default_rng(31)
+    for _ in range(1000):
+        L = int(rng.integers(1, 400))
+        n = int(rng.integers(1, 33))
+        d = float(rng.uniform(0.0, 0.95))
+        f = 1.0 + rng.uniform(-d, d, n + 1)
+        src = A.grid_axis(L, n, f)
+        assert src[0] == 0.0 and src[-1] == L - 1
+        if L == 1:
+            continue
+        assert (np.diff(src) > 0).all()
+        S = sum(Fraction(float(v)) for v in f[:n])
+        c = Fraction(0)
+        for i in range(n + 1):
+            if (i * (L - 1)) % n == 0:  # knot on an integer destination index
+                x = i * (L - 1) // n
+                assert abs(src[x] - float((L - 1) * c / S)) < 1e-9, (L, n, i)
+            if i < n:
+                c += Fraction(float(f[i]))
+        cell = np.minimum((np.arange(L) * n) // (L - 1), n - 1)
+        for x in range(L - 1):
+            if (x + 1) * n <= (cell[x] + 1) * (L - 1):  # x + 1 still inside (or closing) x's cell
+                assert abs((src[x + 1] - src[x]) - n * f[cell[x]] / float(S)) < 1e-9
+
+
+def test_grid_identity_at_zero_limit():
+    """distort_limit = 0 is the identity, bit-exact, for both
+    interpolations, image and mask, any n (also n > L - 1) and degenerate sizes."""
+    rng = np.random.default_rng(7)
+    for (h, w) in [(1, 1), (1, 17), (23, 1), (19, 31), (64, 48)]:
+        img = rand_img(h, w, rng=rng)
+        m = rng.integers(0, 5, (h, w), dtype=np.uint8)
+        for n in (1, 5, 32):
+            for interp in ("bilinear", "nearest"):
+                r = run(_grid(0.0, 0.0, n, interp), img, mask=m, seed=3, idx=9)
+                assert (r["image"] == img).all() and (r["mask"] == m).all()
+
+
+def _grid_maps(lo, hi, n, h, w, seed, idx, slot=0):
+    """factor draws as SPEC.md:330 orders them: x steps j = 1..n+1, then y steps"""
+    fx = [1.0 + lo + (hi - lo) * A.draw(seed, idx, slot, 1 + i) for i in range(n + 1)]
+    fy = [1.0 + lo + (hi - lo) * A.draw(seed, idx, slot, n + 2 + i) for i in range(n + 1)]
+    return A.grid_axis(w, n, fx), A.grid_axis(h, n, fy)
+
+
+def test_grid_remap_of_linear_ramp():
+    """Bilinear interpolation reproduces an affine image g(x, y) exactly, so the
+    bilinear output is round_half_up(g(mx[x], my[y])) and the nearest output is
+    g(round(mx), round(my)): pins the draw order (x factors before y), the axis
+    orientation and the taps.  Masks follow the nearest taps."""
+    h, w = 90, 100
+    yy, xx = np.mgrid[0:h, 0:w]
+    img = np.stack([xx + yy, 2 * xx, 255 - yy], -1).astype(np.uint8)
+    mask = ((3 * xx + 7 * yy) % 11).astype(np.uint8)
+    for (lo, hi, n, seed) in [(-0.3, 0.3, 5, 11), (-0.6, 0.2, 3, 12), (-0.1, 0.5, 8, 13)]:
+        mx, my = _grid_maps(lo, hi, n, h, w, seed, 4)
+        assert np.abs(mx - np.arange(w)).max() > 0.5  # a visible distortion
+        X, Y = np.meshgrid(mx, my)
+        g = np.stack([X + Y, 2 * X, 255 - Y], -1)
+        r = run(_grid(lo, hi, n), img, mask=mask, seed=seed, idx=4)
+        frac = g - np.floor(g)
+        ok = np.abs(frac - 0.5) > 1e-9
+        assert (r["image"][ok] == np.floor(g + 0.5)[ok]).all()
+        xn, yn = np.floor(mx + 0.5).astype(int), np.floor(my + 0.5).astype(int)
+        rn = run(_grid(lo, hi, n, "nearest"), img, mask=mask, seed=seed, idx=4)
+        assert (rn["image"] == img[yn][:, xn]).all()
+        assert (r["mask"] == mask[yn][:, xn]).all() and (rn["mask"] == mask[yn][:, xn]).all()
+
+
+def test_grid_validation_and_boxes_rejected():
+    """SPEC.md:313 factors stay > 0 (|d| < 1), num_steps >= 1 (cap 32, R31);
+    SPEC.md:318/346: boxes under a free-form warp are an unsupported target."""
+    img = rand_img(10, 12)
+    for bad in (_grid(-1.0, 0.2, 4), _grid(0.0, 1.0, 4), _grid(0.0, 0.1, 0), _grid(0.0, 0.1, 33)):
+        with pytest.raises(A.OracleError) as e:
+            run(bad, img)
+        assert e.value.code == -3
+    with pytest.raises(A.OracleError) as e:
+        run(_grid(-0.2, 0.2, 4), img, boxes=np.array([[0.1, 0.1, 0.5, 0.5]], np.float32))
+    assert e.value.code == -5
+    r = run(_grid(-0.2, 0.2, 4, p=0.0), img)  # gate off: identity
+    assert (r["image"] == img).all()
