@@ -83,7 +83,13 @@ typedef enum {
   ALB_D4 = 19,                   /* PAPER.md:87 "dihedral group"
                                     element e uniform in [lo[0], hi[0]] within 0..7:
                                     e < 4 -> rot90(e), else hflip(rot90(e - 4))   */
-  ALB_NUM_KINDS = 20
+  ALB_GRID_DISTORTION = 20,      /* PAPER.md Fig. 4 "grid distortion"; SPEC.md:325-332;
+                                    reading R31: num_steps cells per axis, cell
+                                    lengths proportional to factors 1 + U(lo[0], hi[0])
+                                    (-1 < lo <= hi < 1), span preserved; bilinear or
+                                    nearest remap (border unused: maps stay inside);
+                                    masks nearest; boxes rejected (ALB_E_UNSUPPORTED) */
+  ALB_NUM_KINDS = 21
 } alb_kind;
 
 typedef enum { ALB_INTERP_NEAREST = 0, ALB_INTERP_BILINEAR = 1 } alb_interp;
@@ -106,7 +112,11 @@ typedef struct {
   int32_t interp, border;        /* alb_interp, alb_border                       */
   uint8_t fill[3], mask_fill;    /* constant-border / pad fill                   */
   double mean[3], std[3];        /* Normalize                                    */
+  int32_t num_steps;             /* GridDistortion cells per axis, 1..ALB_GRID_MAX_STEPS */
+  int32_t reserved;              /* unused                                       */
 } alb_op;
+
+#define ALB_GRID_MAX_STEPS 32
 
 /* Geometry of image i of a ragged batch (bytes). */
 typedef struct {

@@ -114,7 +114,9 @@ struct alb_plan {
   bool has_eq = false;
   // workspace layout
   size_t off_params = 0, off_fired = 0, off_dims = 0, off_luts = 0, off_norm = 0,
-         off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, off_geo = 0, ws_bytes = 0;
+         off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, off_geo = 0, off_grid = 0,
+         ws_bytes = 0;
+  int n_grid = 0;  // GridDistortion slots (per-image knot tables in the workspace)
   int2* d_units = nullptr;
   int n_launches = 0;
   ~alb_plan() {
@@ -168,6 +170,11 @@ static alb_status validate_ops(const alb_op* ops, int n_ops) {
           return fail(ALB_E_RANGE, at + "element range must be integers within the group");
         break;
       }
+      case ALB_GRID_DISTORTION:  // every step factor 1 + U(lo, hi) stays > 0
+        if (o.num_steps < 1 || o.num_steps > ALB_GRID_MAX_STEPS)
+          return fail(ALB_E_RANGE, at + "num_steps outside [1, 32]");
+        if (!(o.lo[0] > -1.0 && o.hi[0] < 1.0)) return fail(ALB_E_RANGE, at + "distort limit outside (-1, 1)");
+        break;
       case ALB_NORMALIZE:
         if (k != n_ops - 1 || o.p != 1.0) return fail(ALB_E_RANGE, at + "Normalize must be last, p = 1");
         for (int c = 0; c < 3; ++c)
@@ -178,6 +185,10 @@ static alb_status validate_ops(const alb_op* ops, int n_ops) {
   }
   return ALB_OK;
 }
+
+// GridDistortion: largest source/destination slope of an axis map, n f_i / S
+// <= (1 + hi) / (1 + lo) (reading R31), with a margin for rounding
+static double grid_stretch(const alb_op& o) { return (1.0 + o.hi[0]) / (1.0 + o.lo[0]) * (1.0 + 1e-9); }
 
 // dims each slot sees for an h x w input; error if a window does not fit
 static alb_status track_dims(const std::vector<alb_op>& ops, int h, int w,
@@ -319,6 +330,9 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   if (in->channels != 3) return fail(ALB_E_UNSUPPORTED, "images must have 3 channels");
   if ((mask_in == nullptr) != (mask_out == nullptr)) return fail(ALB_E_INVALID_ARG, "mask_in/mask_out must both be set");
   if (max_boxes < 0) return fail(ALB_E_INVALID_ARG, "max_boxes < 0");
+  for (const alb_op& o : p->ops)
+    if (o.kind == ALB_GRID_DISTORTION && max_boxes > 0)
+      return fail(ALB_E_UNSUPPORTED, "boxes under GridDistortion (free-form warp)");
   std::unique_ptr<alb_plan> P(new alb_plan);
   P->ops = p->ops;
   P->n = in->n;
@@ -415,7 +429,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       continue;
     }
     if (kind == ALB_RESIZE || kind == ALB_RANDOM_SIZED_CROP || kind == ALB_ROTATE ||
-        kind == ALB_SHIFT_SCALE_ROTATE) {
+        kind == ALB_SHIFT_SCALE_ROTATE || kind == ALB_GRID_DISTORTION) {
       PlanStep st;
       st.kind = (kind == ALB_ROTATE || kind == ALB_SHIFT_SCALE_ROTATE) ? SK_AFFINE : SK_RESAMPLE;
       st.slot0 = k; st.slot1 = k + 1;
@@ -610,14 +624,15 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
           // new window rows (ratio = largest window/output row ratio); strips of
           // 256 output columns need <= 256 * ww / nw + 3 window columns
           int max_ww = 0;
-          double ratio = 0.0;
+          double ratio = 0.0, cratio = 0.0;
           for (int i = 0; i < P->n; ++i) {
             int wh = dims[i][st.slot0].first, ww = dims[i][st.slot0].second;
             if (o.kind == ALB_RANDOM_SIZED_CROP) wh = ww = std::min(o.max_side, std::min(wh, ww));
             max_ww = std::max(max_ww, ww);
-            ratio = std::max(ratio, (double)wh / o.out_h);
+            if (o.kind != ALB_GRID_DISTORTION) ratio = std::max(ratio, (double)wh / o.out_h);
           }
-          const double cratio = (double)max_ww / o.out_w;
+          if (o.kind == ALB_GRID_DISTORTION) ratio = cratio = grid_stretch(o);
+          else cratio = (double)max_ww / o.out_w;
           const int sw = (std::min(max_ww, (int)std::ceil(256.0 * cratio) + 3)) | 1;
           int nl = 0;
           for (auto& sg : st.stages) nl += (sg.type == ST_LUT || sg.type == ST_EQ);
@@ -650,7 +665,8 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
           int wh = dims[i][st.slot0].first, ww = dims[i][st.slot0].second;
           if (o.kind == ALB_RANDOM_SIZED_CROP) wh = ww = std::min(o.max_side, std::min(wh, ww));
           const double rows = (double)kStageWords / ww - 2.0;  // staged window rows that fit
-          R = std::min(R, std::max(1, (int)(rows * o.out_h / wh)));
+          const double rr = o.kind == ALB_GRID_DISTORTION ? grid_stretch(o) : (double)wh / o.out_h;
+          R = std::min(R, std::max(1, (int)(rows / rr)));
         }
         R = std::max(1, std::min(R, 32));
         st.unit_rows = R;
@@ -692,6 +708,8 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   P->off_eqh = take(P->has_eq ? nn * 768 * sizeof(uint32_t) : 0);
   P->off_eql = take(P->has_eq ? nn * 768 : 0);
   P->off_geo = take(nn * kGeoBytes);  // per-image affine state (affine steps)
+  for (const alb_op& o : P->ops) P->n_grid += o.kind == ALB_GRID_DISTORTION;
+  P->off_grid = take(nn * P->n_grid * kGridStride * sizeof(double));  // knot displacements (R31)
   P->off_buf[0] = take(max_inter + 64);
   P->off_buf[1] = take(max_inter + 64);
   P->off_mbuf[0] = take(max_minter + 64);
@@ -762,6 +780,8 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
   tab.eq_luts = ws + P->off_eql;
   tab.n_ops = n_ops;
   tab.n_luts = P->n_luts;
+  tab.grid = (const double*)(ws + P->off_grid);
+  tab.n_grid = P->n_grid;
 
   PrepArgs pa{};
   pa.ops = P->d_ops;
@@ -778,6 +798,8 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
   for (int s = 0; s < P->n_luts; ++s) { pa.lut_k0[s] = P->lut_k0[s]; pa.lut_k1[s] = P->lut_k1[s]; }
   pa.norm_lut = (float*)(ws + P->off_norm);
   pa.norm_slot = P->norm_slot;
+  pa.grid = (double*)(ws + P->off_grid);
+  pa.n_grid = P->n_grid;
   launch_prep(pa, stream);
 
   auto img_buf = [&](int id) -> uint8_t* {

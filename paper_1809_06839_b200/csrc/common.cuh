@@ -101,7 +101,13 @@ struct Tables {
   const uint8_t* eq_luts; // [n][768] (Equalize, R15)
   int32_t n_ops;
   int32_t n_luts;
+  const double* grid;     // [n][n_grid][kGridStride] GridDistortion knot displacements
+  int32_t n_grid;
 };
+
+// GridDistortion knot tables: e^x[0..n] at +0, e^y[0..n] at +kGridAxis (reading R31)
+constexpr int kGridAxis = ALB_GRID_MAX_STEPS + 1;
+constexpr int kGridStride = 2 * kGridAxis;
 
 __device__ __forceinline__ const double* prm_of(const Tables& t, int img, int slot) {
   return t.params + ((size_t)img * t.n_ops + slot) * kMaxParams;

@@ -23,6 +23,8 @@ struct PrepArgs {
   int32_t lut_k0[kMaxLuts], lut_k1[kMaxLuts];
   float* norm_lut;
   int32_t norm_slot;
+  double* grid;       // [n][n_grid][kGridStride] (reading R31)
+  int32_t n_grid;
 };
 
 // One geometric / pointwise kernel launch.
@@ -139,6 +141,29 @@ __device__ __forceinline__ int dim_h(const Tables& t, int img, int k) {
 }
 __device__ __forceinline__ int dim_w(const Tables& t, int img, int k) {
   return t.dims[((size_t)img * (t.n_ops + 1) + k) * 2 + 1];
+}
+
+// knot displacements of GridDistortion slot `slot` for image img (ordinal = GridDistortion
+// slots before it)
+__device__ __forceinline__ const double* grid_of(const Tables& t, const alb_op* ops, int img, int slot) {
+  int g = 0;
+  for (int k = 0; k < slot; ++k) g += ops[k].kind == ALB_GRID_DISTORTION;
+  return t.grid + ((size_t)img * t.n_grid + g) * kGridStride;
+}
+
+// GridDistortion source coordinate of destination index x on an axis of length
+// L (reading R31, operation order as DESIGN.md states it)
+__device__ __forceinline__ double grid_coord(int x, int L, int n, const double* e) {
+  if (L == 1) return 0.0;
+  const double span = (double)(L - 1);
+  const double u = __ddiv_rn(__dmul_rn((double)x, (double)n), span);
+  int i = (int)floor(u);
+  if (i > n - 1) i = n - 1;
+  const double t = __dsub_rn(u, (double)i);
+  double v = __dadd_rn((double)x, __dadd_rn(e[i], __dmul_rn(t, __dsub_rn(e[i + 1], e[i]))));
+  if (v < 0.0) v = 0.0;
+  if (v > span) v = span;
+  return v;
 }
 
 // grid of a persistent kernel: min(n_units, SMs x occupancy), cached (launch.cu)

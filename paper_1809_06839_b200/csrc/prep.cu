@@ -21,6 +21,23 @@ __device__ int lut_entry(int kind, const double* q, int c, int x) {
   }
 }
 
+// GridDistortion knot displacements of one axis (reading R31, in the
+// order DESIGN.md states): factors f_i = 1 + U(lo, hi) from draws j0 + i,
+// c_{i+1} = c_i + f_i, e_i = (L-1) c_i / S - (L-1) i / n, e_0 = e_n = 0.
+__device__ void grid_knots(const alb_op& o, uint64_t seed, uint32_t gi, int k, int j0, int L,
+                           double* e) {
+  const int n = o.num_steps;
+  double c[ALB_GRID_MAX_STEPS + 1];
+  c[0] = 0.0;
+  for (int i = 0; i < n; ++i)
+    c[i + 1] = __dadd_rn(c[i], __dadd_rn(1.0, urange(o.lo[0], o.hi[0], draw_u(seed, gi, k, j0 + i))));
+  const double S = c[n], span = (double)(L - 1);
+  e[0] = 0.0;
+  e[n] = 0.0;
+  for (int i = 1; i < n; ++i)
+    e[i] = __dsub_rn(__ddiv_rn(__dmul_rn(span, c[i]), S), __ddiv_rn(__dmul_rn(span, (double)i), (double)n));
+}
+
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   const int i = blockIdx.x;
   __shared__ double s_prm[kMaxOps][kMaxParams];
@@ -28,6 +45,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   if (threadIdx.x == 0) {
     const uint32_t gi = a.first_image + (uint32_t)i;
     int h = a.in_desc[i].height, w = a.in_desc[i].width;
+    int g_ord = 0;
     for (int k = 0; k < a.n_ops; ++k) {
       const alb_op& o = a.ops[k];
       double* q = s_prm[k];
@@ -72,6 +90,12 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
         case ALB_PAD_TO_SIZE: case ALB_RESIZE:
           nh = o.out_h; nw = o.out_w;
           break;
+        case ALB_GRID_DISTORTION: {  // x factors: draws 1..n+1, y factors: n+2..2n+2
+          double* e = a.grid + ((size_t)i * a.n_grid + g_ord++) * kGridStride;
+          grid_knots(o, a.seed, gi, k, 1, w, e);
+          grid_knots(o, a.seed, gi, k, o.num_steps + 2, h, e + kGridAxis);
+          break;
+        }
         case ALB_ROT90: case ALB_D4:  // element, uniform over the integer range
           q[0] = o.lo[0] + (double)uint_draw(draw_u(a.seed, gi, k, 1), (int)(o.hi[0] - o.lo[0]) + 1);
           if ((int)q[0] & 1) { nh = w; nw = h; }

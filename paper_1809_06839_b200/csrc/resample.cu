@@ -8,6 +8,10 @@
 // order, so the coordinates equal the oracle's bit for bit; the blend runs in
 // fp32.  Masks: nearest, round_half_up(x_s).
 //
+// GridDistortion (reading R31) runs through the same kernels: its source
+// coordinates are separable monotone axis maps inside the image, so only the
+// coordinate function changes (g_cx / g_cy, knot tables built by K0).
+//
 // Work unit = (image, band of `unit_rows` output rows); persistent grid over
 // contiguous unit ranges; the column table is rebuilt only when the image
 // changes.  Per band, the window rows it needs are staged in shared memory as
@@ -29,6 +33,8 @@ constexpr int kRsChunk = 512;  // output columns per row-buffer flush
 struct RsGeom {
   int wx0, wy0, ww, wh;  // source window
   int nw, nh;            // resize output dims
+  const double* ge;      // GridDistortion knot displacements (x at +0, y at +kGridAxis), else null
+  int gn;                // GridDistortion cells per axis
 };
 
 __device__ __forceinline__ RsGeom rs_geom(const StepArgs& a, int img) {
@@ -36,7 +42,17 @@ __device__ __forceinline__ RsGeom rs_geom(const StepArgs& a, int img) {
   RsGeom g;
   g.nw = o.out_w;
   g.nh = o.out_h;
-  if (o.kind == ALB_RANDOM_SIZED_CROP) {
+  g.ge = nullptr;
+  g.gn = 0;
+  if (o.kind == ALB_GRID_DISTORTION) {  // same-size remap through the axis maps (R31)
+    g.wx0 = g.wy0 = 0;
+    g.nw = g.ww = dim_w(a.tab, img, a.slot0);
+    g.nh = g.wh = dim_h(a.tab, img, a.slot0);
+    if (fired_of(a.tab, img, a.slot0)) {  // else the same-size resize map: x_s == x_d exactly
+      g.ge = grid_of(a.tab, a.ops, img, a.slot0);
+      g.gn = o.num_steps;
+    }
+  } else if (o.kind == ALB_RANDOM_SIZED_CROP) {
     const double* q = prm_of(a.tab, img, a.slot0);
     g.ww = g.wh = (int)q[0];
     g.wx0 = (int)q[1];
@@ -55,6 +71,15 @@ __device__ __forceinline__ double rs_coord(int d, int n_src, int n_dst) {
   if (s < 0.0) s = 0.0;
   if (s > (double)(n_src - 1)) s = (double)(n_src - 1);
   return s;
+}
+
+// window source column / row of output index d: the resize map, or the
+// GridDistortion axis maps
+__device__ __forceinline__ double g_cx(const RsGeom& g, int d) {
+  return g.ge ? grid_coord(d, g.ww, g.gn, g.ge) : rs_coord(d, g.ww, g.nw);
+}
+__device__ __forceinline__ double g_cy(const RsGeom& g, int d) {
+  return g.ge ? grid_coord(d, g.wh, g.gn, g.ge + kGridAxis) : rs_coord(d, g.wh, g.nh);
 }
 
 struct ColEnt {
@@ -104,7 +129,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
       const int Ho = a.normalize ? a.out_h : a.ddesc[img].height;
       const Map1 m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, Wo, Ho);
       for (int xo = threadIdx.x; xo < Wo; xo += kRsThreads) {
-        const double s = rs_coord(m.ax * xo + m.bx, g.ww, g.nw);
+        const double s = g_cx(g, m.ax * xo + m.bx);
         const double f = floor(s);
         ColEnt e;
         e.x0 = (uint16_t)(int)f;
@@ -123,7 +148,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_resample(StepArgs a) {
     const int Wo = st->Wo, Ho = st->Ho;
     const int y0 = unit.y * R, y1 = min(Ho, y0 + R);
     if (threadIdx.x < y1 - y0) {
-      const double s = rs_coord(m.ay * (y0 + threadIdx.x) + m.by, g.wh, g.nh);
+      const double s = g_cy(g, m.ay * (y0 + threadIdx.x) + m.by);
       const double f = floor(s);
       row_y0[threadIdx.x] = (int)f;
       row_fy[threadIdx.x] = (float)__dsub_rn(s, f);
@@ -329,7 +354,7 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
     const int y0 = band * R, nr = min(R, Ho - y0);
     for (int i = tid; i < nr; i += kSepThreads) {  // i-th row in increasing source order
       const int yo = m.ay > 0 ? y0 + i : y0 + nr - 1 - i;
-      const double sy = rs_coord(m.ay * yo + m.by, g.wh, g.nh);
+      const double sy = g_cy(g, m.ay * yo + m.by);
       const double f = floor(sy);
       SepRow e;
       e.y0 = (int)f;
@@ -349,13 +374,13 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
     // this lane's two columns (fp64, definition order O5) and the strip's window columns
     const int cb = warp * 32 * kCols + lane;
     const int xe0 = m.ax * xs0 + m.bx, xe1 = m.ax * (xs0 + cw - 1) + m.bx;
-    const int sxa = (int)floor(rs_coord(min(xe0, xe1), g.ww, g.nw));
-    const int sxb = min((int)floor(rs_coord(max(xe0, xe1), g.ww, g.nw)) + 1, g.ww - 1) + 1;
+    const int sxa = (int)floor(g_cx(g, min(xe0, xe1)));
+    const int sxb = min((int)floor(g_cx(g, max(xe0, xe1))) + 1, g.ww - 1) + 1;
     int o0[kCols], o1[kCols];
     float fx[kCols];
 #pragma unroll
     for (int q = 0; q < kCols; ++q) {
-      const double sx = rs_coord(m.ax * (xs0 + min(cb + 32 * q, cw - 1)) + m.bx, g.ww, g.nw);
+      const double sx = g_cx(g, m.ax * (xs0 + min(cb + 32 * q, cw - 1)) + m.bx);
       const double f = floor(sx);
       o0[q] = (int)f - sxa;
       o1[q] = min((int)f + 1, g.ww - 1) - sxa;
