@@ -260,6 +260,11 @@ static int validate_ops(const albref_op* ops, int32_t n_ops) {
         if (o->num_steps < 1 || o->num_steps > ALBREF_GRID_MAX_STEPS) return ALBREF_E_RANGE;
         if (!(o->lo[0] > -1.0 && o->hi[0] < 1.0)) return ALBREF_E_RANGE;
         break;
+      case ALBREF_ELASTIC: /* fixed alpha >= 0, sigma in (0, 16] (R32) */
+        if (o->lo[0] != o->hi[0] || o->lo[1] != o->hi[1]) return ALBREF_E_RANGE;
+        if (!(o->lo[0] >= 0.0) || !(o->lo[1] > 0.0 && o->lo[1] <= ALBREF_ELASTIC_MAX_SIGMA))
+          return ALBREF_E_RANGE;
+        break;
       case ALBREF_NORMALIZE:
         if (k != n_ops - 1 || o->p != 1.0) return ALBREF_E_RANGE;
         for (int c = 0; c < 3; ++c)
@@ -831,6 +836,82 @@ static void op_grid(state_t* s, const albref_op* o, uint64_t seed, uint64_t idx,
   replace_px(s, px, mk, s->h, s->w);
 }
 
+/* ------------------------------------------ ElasticTransform */
+
+/* Reading R32: g_k = exp(-k^2 / (2 sigma^2)), k = -r..r, r = ceil(3 sigma),
+ * divided by their sum (accumulated in ascending k) -- SPEC.md:337. */
+int albref_gauss_kernel(double sigma, double* w) {
+  if (!(sigma > 0.0 && sigma <= ALBREF_ELASTIC_MAX_SIGMA)) return ALBREF_E_RANGE;
+  const int32_t r = (int32_t)ceil(3.0 * sigma);
+  double sum = 0.0;
+  for (int32_t k = -r; k <= r; ++k) {
+    w[k + r] = exp(-(double)(k * k) / (2.0 * sigma * sigma));
+    sum += w[k + r];
+  }
+  for (int32_t k = 0; k <= 2 * r; ++k) w[k] /= sum;
+  return r;
+}
+
+/* raw planes u, v ~ U(-1, 1) per pixel, row-major, the u plane
+ * fully first (draw j = 1 + p for u, 1 + h w + p for v, p = y w + x); each
+ * convolved with the kernel along x, then along y (reflect-101 edges),
+ * accumulated in ascending k with fused multiply-adds (acc = fma(w, x, acc));
+ * then scaled by alpha. */
+int albref_elastic_field(int32_t h, int32_t w, double alpha, double sigma, uint64_t seed,
+                         uint64_t image_index, int32_t slot, double* dx, double* dy) {
+  double g[2 * 48 + 1];
+  const int32_t r = albref_gauss_kernel(sigma, g);
+  if (r < 0) return r;
+  if (h < 1 || w < 1) return ALBREF_E_SHAPE;
+  const size_t n = (size_t)h * w;
+  double* raw = (double*)malloc(sizeof(double) * n);
+  double* bx = (double*)malloc(sizeof(double) * n);
+  for (int plane = 0; plane < 2; ++plane) {
+    double* d = plane == 0 ? dx : dy;
+    for (size_t p = 0; p < n; ++p)
+      raw[p] = uniform_range(-1.0, 1.0,
+                             albref_draw(seed, image_index, slot, (int32_t)(1 + plane * n + p)));
+    for (int32_t y = 0; y < h; ++y)
+      for (int32_t x = 0; x < w; ++x) {
+        double acc = 0.0;
+        for (int32_t k = -r; k <= r; ++k)
+          acc = fma(g[k + r], raw[(size_t)y * w + albref_reflect101(x + k, w)], acc);
+        bx[(size_t)y * w + x] = acc;
+      }
+    for (int32_t y = 0; y < h; ++y)
+      for (int32_t x = 0; x < w; ++x) {
+        double acc = 0.0;
+        for (int32_t k = -r; k <= r; ++k)
+          acc = fma(g[k + r], bx[(size_t)albref_reflect101(y + k, h) * w + x], acc);
+        d[(size_t)y * w + x] = alpha * acc;
+      }
+  }
+  free(raw);
+  free(bx);
+  return ALBREF_OK;
+}
+
+/* Remap at source (x + dx, y + dy) with the op's interpolation
+ * and border, exactly as the affine ops sample (O7); masks nearest. */
+static void op_elastic(state_t* s, const albref_op* o, uint64_t seed, uint64_t idx, int32_t slot) {
+  const size_t n = (size_t)s->h * s->w;
+  double* dx = (double*)malloc(sizeof(double) * n);
+  double* dy = (double*)malloc(sizeof(double) * n);
+  albref_elastic_field(s->h, s->w, o->lo[0], o->lo[1], seed, idx, slot, dx, dy);
+  uint8_t* px = xalloc(n * s->c);
+  uint8_t* mk = s->mask ? xalloc(n) : NULL;
+  for (int32_t y = 0; y < s->h; ++y)
+    for (int32_t x = 0; x < s->w; ++x) {
+      const size_t p = (size_t)y * s->w + x;
+      const double xs = (double)x + dx[p], ys = (double)y + dy[p];
+      sample_affine(s, xs, ys, o->interp, o->border, o->fill, &px[p * s->c]);
+      if (mk) mk[p] = sample_mask_nearest(s, xs, ys, o->border, o->mask_fill);
+    }
+  free(dx);
+  free(dy);
+  replace_px(s, px, mk, s->h, s->w);
+}
+
 /* ---------------------------------------------------------- O14 apply */
 
 int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
@@ -849,7 +930,7 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
     return ALBREF_E_INVALID_ARG;
   for (int32_t k = 0; k < n_ops; ++k) {
     int32_t kd = ops[k].kind;
-    if (kd == ALBREF_GRID_DISTORTION && n_boxes > 0)
+    if ((kd == ALBREF_GRID_DISTORTION || kd == ALBREF_ELASTIC) && n_boxes > 0)
       return ALBREF_E_UNSUPPORTED; /* boxes under free-form warps */
     if (channels != 3 && (kd == ALBREF_SHIFT_RGB || kd == ALBREF_SHIFT_HSV ||
                           kd == ALBREF_GRAYSCALE || kd == ALBREF_NORMALIZE))
@@ -914,6 +995,7 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
       case ALBREF_ROT90: op_rot90(&s, (int32_t)q[0]); break;
       case ALBREF_D4: op_d4(&s, (int32_t)q[0]); break;
       case ALBREF_GRID_DISTORTION: op_grid(&s, o, seed, image_index, k); break;
+      case ALBREF_ELASTIC: op_elastic(&s, o, seed, image_index, k); break;
       default: break;
     }
   }

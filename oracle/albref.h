@@ -40,7 +40,8 @@ enum {
   ALBREF_ROT90 = 18,  /* SPEC.md:193-201; k quarter turns, k in [lo[0], hi[0]] */
   ALBREF_D4 = 19,     /* SPEC.md:202-210; element e in [lo[0], hi[0]] of 0..7 */
   ALBREF_GRID_DISTORTION = 20, /* SPEC.md:325-332; Fig. 4: factors 1 + U(lo[0], hi[0]) */
-  ALBREF_NUM_KINDS = 21
+  ALBREF_ELASTIC = 21,         /* SPEC.md:333-338; alpha = lo[0], sigma = lo[1] */
+  ALBREF_NUM_KINDS = 22
 };
 enum { ALBREF_INTERP_NEAREST = 0, ALBREF_INTERP_BILINEAR = 1 };
 enum { ALBREF_BORDER_CONSTANT = 0, ALBREF_BORDER_REFLECT_101 = 1 };
@@ -66,6 +67,7 @@ typedef struct {
 } albref_op;
 
 #define ALBREF_GRID_MAX_STEPS 32
+#define ALBREF_ELASTIC_MAX_SIGMA 16.0 /* radius ceil(3 sigma) <= 48 (reading R32) */
 
 #define ALBREF_MAX_PARAMS 8
 
@@ -85,6 +87,16 @@ int32_t albref_reflect101(int32_t i, int32_t n);
  * destination index x in [0, L) for step factors f[0..n] (f[n] is drawn but
  * unused).  Returns ALBREF_E_RANGE for n outside [1, 32] or a factor <= 0. */
 int albref_grid_axis(int32_t L, int32_t n, const double* f, double* src);
+
+/* ElasticTransform (reading R32).  Normalised truncated Gaussian of std sigma:
+ * w[0..2r], r = ceil(3 sigma); returns r (w must hold 2*48+1 entries), or
+ * ALBREF_E_RANGE for sigma outside (0, 16]. */
+int albref_gauss_kernel(double sigma, double* w);
+/* Displacement planes dx, dy [h][w] of slot `slot` of image `image_index`:
+ * raw u, v ~ U(-1, 1) (draws 1 + y w + x, then 1 + h w + y w + x), blurred
+ * x then y with w[] and reflect-101, times alpha. */
+int albref_elastic_field(int32_t h, int32_t w, double alpha, double sigma, uint64_t seed,
+                         uint64_t image_index, int32_t slot, double* dx, double* dy);
 
 /* hexcone colour model, double precision. */
 void albref_rgb_to_hsv(double r, double g, double b, double* h, double* s, double* v);

@@ -27,7 +27,7 @@ KINDS = {
     "RandomCrop": 4, "PadToSize": 5, "Resize": 6, "RandomSizedCrop": 7,
     "Brightness": 8, "Contrast": 9, "BrightnessContrast": 10, "Gamma": 11,
     "ShiftRGB": 12, "ShiftHSV": 13, "Grayscale": 14, "Equalize": 15,
-    "Normalize": 16, "Crop": 17, "Rotate90": 18, "D4": 19, "GridDistortion": 20,
+    "Normalize": 16, "Crop": 17, "Rotate90": 18, "D4": 19, "GridDistortion": 20, "ElasticTransform": 21,
 }
 INTERP = {"nearest": 0, "bilinear": 1}
 BORDER = {"constant": 0, "reflect_101": 1}
@@ -86,6 +86,10 @@ def lib():
         L.albref_build_lut.argtypes = [ctypes.c_int32, D, ctypes.c_void_p]
         L.albref_equalize_lut.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         L.albref_grid_axis.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+        L.albref_gauss_kernel.argtypes = [ctypes.c_double, ctypes.c_void_p]
+        L.albref_elastic_field.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
+                                           ctypes.c_void_p, ctypes.c_void_p]
         L.albref_output_shape.argtypes = [P(AlbrefOp), ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, P(ctypes.c_int32), P(ctypes.c_int32)]
         L.albref_sample_params.argtypes = [P(AlbrefOp), ctypes.c_int32, ctypes.c_uint64,
@@ -205,6 +209,23 @@ def grid_axis(L, n, factors):
     out = np.zeros(max(1, L), np.float64)
     _check(lib().albref_grid_axis(L, n, f.ctypes.data, out.ctypes.data))
     return out[:L]
+
+
+def gauss_kernel(sigma):
+    """ElasticTransform smoothing weights w[0..2r] (reading R32)."""
+    w = np.zeros(97, np.float64)
+    r = lib().albref_gauss_kernel(sigma, w.ctypes.data)
+    _check(min(r, 0))
+    return w[:2 * r + 1]
+
+
+def elastic_field(h, w, alpha, sigma, seed, image_index, slot=0):
+    """ElasticTransform displacement planes (dx, dy), each (h, w) float64."""
+    dx = np.zeros((h, w), np.float64)
+    dy = np.zeros((h, w), np.float64)
+    _check(lib().albref_elastic_field(h, w, alpha, sigma, seed, image_index, slot,
+                                      dx.ctypes.data, dy.ctypes.data))
+    return dx, dy
 
 
 def output_shape(specs, h, w):

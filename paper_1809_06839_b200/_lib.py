@@ -18,7 +18,7 @@ KINDS = {
     "RandomCrop": 4, "PadToSize": 5, "Resize": 6, "RandomSizedCrop": 7,
     "Brightness": 8, "Contrast": 9, "BrightnessContrast": 10, "Gamma": 11,
     "ShiftRGB": 12, "ShiftHSV": 13, "Grayscale": 14, "Equalize": 15,
-    "Normalize": 16, "Crop": 17, "Rotate90": 18, "D4": 19, "GridDistortion": 20,
+    "Normalize": 16, "Crop": 17, "Rotate90": 18, "D4": 19, "GridDistortion": 20, "ElasticTransform": 21,
 }
 INTERP = {"nearest": 0, "bilinear": 1}
 BORDER = {"constant": 0, "reflect_101": 1}

@@ -862,3 +862,117 @@ def test_grid_validation_and_boxes_rejected():
     assert e.value.code == -5
     r = run(_grid(-0.2, 0.2, 4, p=0.0), img)  # gate off: identity
     assert (r["image"] == img).all()
+
+
+# ---------------------------------------------------------- ElasticTransform
+
+def _elastic(alpha, sigma, interp="bilinear", border="reflect_101", p=1.0):
+    return [{"kind": "ElasticTransform", "p": p, "lo": [alpha, sigma], "hi": [alpha, sigma],
+             "interp": interp, "border": border}]
+
+
+def test_elastic_gauss_kernel():
+    """SPEC.md:337 / invariant SPEC.md:341: symmetric, nonnegative, sums to 1
+    (1e-12), radius ceil(3 sigma), weights proportional to math.exp(-k^2/2s^2)."""
+    import math
+    for sigma in (0.1, 0.5, 1.0, 1.7, 3.0, 4.0, 7.3, 16.0):
+        w = A.gauss_kernel(sigma)
+        r = math.ceil(3 * sigma)
+        assert len(w) == 2 * r + 1
+        assert (w >= 0).all() and abs(w.sum() - 1.0) < 1e-12
+        assert np.array_equal(w, w[::-1])
+        for k in range(-r, r + 1):
+            assert abs(w[k + r] / w[r] - math.exp(-k * k / (2 * sigma * sigma))) < 1e-14
+    for bad in (0.0, -1.0, 16.5):
+        with pytest.raises(A.OracleError):
+            A.gauss_kernel(bad)
+
+
+def _reflect_idx(i, n):
+    """reflect-101 by literal mirror steps (independent of the oracle's modular form)"""
+    if n == 1:
+        return 0
+    while i < 0 or i >= n:
+        i = -i if i < 0 else 2 * (n - 1) - i
+    return i
+
+
+def test_elastic_field_direct_2d_convolution():
+    """separable blur == direct 2-D convolution (1e-9) on small
+    fields, incl. kernels wider than the image (repeated reflection); the raw
+    planes come from the draws in SPEC.md:337's order (u plane, then v plane,
+    row-major) -- a transposed or swapped plane fails."""
+    import math
+    for (h, w, sigma, alpha) in [(9, 9, 1.0, 3.0), (9, 9, 2.5, 1.0), (5, 12, 1.3, 7.0), (1, 6, 0.7, 2.0),
+                                 (4, 1, 2.0, 5.0)]:
+        seed, idx, slot = 5, 17, 2
+        raw = [np.array([[-1.0 + 2.0 * A.draw(seed, idx, slot, 1 + pl * h * w + y * w + x)
+                          for x in range(w)] for y in range(h)]) for pl in (0, 1)]
+        r = math.ceil(3 * sigma)
+        g = np.array([math.exp(-k * k / (2 * sigma * sigma)) for k in range(-r, r + 1)])
+        g /= g.sum()
+        dx, dy = A.elastic_field(h, w, alpha, sigma, seed, idx, slot)
+        for plane, d in zip(raw, (dx, dy)):
+            ref = np.zeros((h, w))
+            for y in range(h):
+                for x in range(w):
+                    ref[y, x] = alpha * sum(g[a + r] * g[b + r] * plane[_reflect_idx(y + a, h), _reflect_idx(x + b, w)]
+                                            for a in range(-r, r + 1) for b in range(-r, r + 1))
+            assert np.abs(d - ref).max() < 1e-9, (h, w, sigma)
+
+
+def test_elastic_bound_and_identity():
+    """SPEC.md:338: |displacement| <= alpha (convexity); SPEC.md:336: alpha = 0
+    is the identity bit-exact (nearest and bilinear, image and mask)."""
+    rng = np.random.default_rng(32)
+    for _ in range(40):
+        h, w = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+        alpha, sigma = float(rng.uniform(0, 50)), float(rng.uniform(0.05, 6))
+        dx, dy = A.elastic_field(h, w, alpha, sigma, int(rng.integers(0, 1 << 40)), int(rng.integers(0, 1000)))
+        assert np.abs(dx).max() <= alpha and np.abs(dy).max() <= alpha
+    img = rand_img(23, 37, rng=rng)
+    m = rng.integers(0, 4, (23, 37), dtype=np.uint8)
+    for interp in ("bilinear", "nearest"):
+        for border in ("constant", "reflect_101"):
+            r = run(_elastic(0.0, 4.0, interp, border), img, mask=m, seed=9)
+            assert (r["image"] == img).all() and (r["mask"] == m).all()
+
+
+def test_elastic_remap_of_linear_ramp():
+    """source = (x + dx, y + dy): on an affine ramp the bilinear
+    output equals round(g(x + dx, y + dy)) wherever the sample is inside the
+    image, the nearest output and the mask equal the ramp at the rounded
+    source; outside, constant border gives the fill (all four taps out)."""
+    h, w = 60, 80
+    yy, xx = np.mgrid[0:h, 0:w]
+    img = np.stack([xx + yy, 3 * xx, 200 - yy], -1).astype(np.uint8)
+    mask = ((5 * xx + 3 * yy) % 7).astype(np.uint8)
+    alpha, sigma = 40.0, 2.0
+    dx, dy = A.elastic_field(h, w, alpha, sigma, 3, 6)
+    xs, ys = xx + dx, yy + dy
+    g = np.stack([xs + ys, 3 * xs, 200 - ys], -1)
+    inside = (xs >= 0) & (xs <= w - 1) & (ys >= 0) & (ys <= h - 1)
+    r = run(_elastic(alpha, sigma, border="constant"), img, mask=mask, seed=3, idx=6)
+    ok = inside[..., None] & (np.abs(g - np.floor(g) - 0.5) > 1e-9)
+    assert inside.mean() > 0.8 and (~inside).sum() > 0
+    assert (r["image"][ok] == np.floor(g + 0.5)[ok]).all()
+    out = (xs < -1) | (xs > w) | (ys < -1) | (ys > h)
+    assert (r["image"][out] == 0).all()
+    xn, yn = np.floor(xs + 0.5).astype(int), np.floor(ys + 0.5).astype(int)
+    inn = (xn >= 0) & (xn < w) & (yn >= 0) & (yn < h)
+    rn = run(_elastic(alpha, sigma, "nearest", "constant"), img, mask=mask, seed=3, idx=6)
+    assert (rn["image"][inn] == img[yn[inn], xn[inn]]).all()
+    assert (r["mask"][inn] == mask[yn[inn], xn[inn]]).all() and (r["mask"][~inn] == 0).all()
+
+
+def test_elastic_validation_and_boxes_rejected():
+    img = rand_img(10, 12)
+    bad = [_elastic(-1.0, 2.0), _elastic(1.0, 0.0), _elastic(1.0, 17.0),
+           [{"kind": "ElasticTransform", "lo": [1.0, 2.0], "hi": [2.0, 2.0]}]]
+    for b in bad:
+        with pytest.raises(A.OracleError) as e:
+            run(b, img)
+        assert e.value.code == -3
+    with pytest.raises(A.OracleError) as e:
+        run(_elastic(5.0, 2.0), img, boxes=np.array([[0.1, 0.1, 0.5, 0.5]], np.float32))
+    assert e.value.code == -5
