@@ -89,7 +89,14 @@ typedef enum {
                                     (-1 < lo <= hi < 1), span preserved; bilinear or
                                     nearest remap (border unused: maps stay inside);
                                     masks nearest; boxes rejected (ALB_E_UNSUPPORTED) */
-  ALB_NUM_KINDS = 21
+  ALB_ELASTIC = 21,              /* PAPER.md:85 "elastic transform"; SPEC.md:333-338;
+                                    reading R32: alpha = lo[0] (>= 0), sigma = lo[1]
+                                    (0 < sigma <= 16), both fixed (lo == hi); raw
+                                    U(-1,1) planes from Philox, fp64 Gaussian blur
+                                    (radius ceil(3 sigma), reflect-101), remap at
+                                    (x + dx, y + dy) with interp / border / fill;
+                                    masks nearest; boxes rejected                  */
+  ALB_NUM_KINDS = 22
 } alb_kind;
 
 typedef enum { ALB_INTERP_NEAREST = 0, ALB_INTERP_BILINEAR = 1 } alb_interp;

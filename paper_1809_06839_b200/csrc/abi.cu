@@ -64,7 +64,7 @@ struct alb_layout {
 
 namespace {
 
-enum StepKind { SK_ROW = 0, SK_POINT = 1, SK_RESAMPLE = 2, SK_AFFINE = 3, SK_EQ = 4, SK_D4 = 5 };
+enum StepKind { SK_ROW = 0, SK_POINT = 1, SK_RESAMPLE = 2, SK_AFFINE = 3, SK_EQ = 4, SK_D4 = 5, SK_ELASTIC = 6 };
 enum BufId { B_IN = 0, B_OUT = 1, B_WS0 = 2, B_WS1 = 3, B_NONE = 4 };
 
 struct PlanStep {
@@ -88,6 +88,8 @@ struct PlanStep {
   int eq_slot = -1;
   float min_scale = 1.0f;
   int rs_ring = 0, rs_sw = 0, rs_hw = 0;  // separable resample parameters (0 = old kernel)
+  int g_r = 0, g_off = 0;                  // ElasticTransform radius, weights offset in d_gauss
+  double alpha = 0.0;
 };
 
 constexpr int kChunk = 48 * 512;         // pointwise / histogram bytes per unit
@@ -117,10 +119,13 @@ struct alb_plan {
          off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, off_geo = 0, off_grid = 0,
          ws_bytes = 0;
   int n_grid = 0;  // GridDistortion slots (per-image knot tables in the workspace)
+  std::vector<double> gauss;  // ElasticTransform weights of every elastic step (host copy)
+  double* d_gauss = nullptr;
   int2* d_units = nullptr;
   int n_launches = 0;
   ~alb_plan() {
     if (d_ops) cudaFree(d_ops);
+    if (d_gauss) cudaFree(d_gauss);
     if (d_units) cudaFree(d_units);
   }
 };
@@ -170,6 +175,11 @@ static alb_status validate_ops(const alb_op* ops, int n_ops) {
           return fail(ALB_E_RANGE, at + "element range must be integers within the group");
         break;
       }
+      case ALB_ELASTIC:  // fixed alpha >= 0, sigma in (0, 16] (reading R32)
+        if (o.lo[0] != o.hi[0] || o.lo[1] != o.hi[1]) return fail(ALB_E_RANGE, at + "alpha / sigma must be fixed");
+        if (!(o.lo[0] >= 0.0)) return fail(ALB_E_RANGE, at + "alpha < 0");
+        if (!(o.lo[1] > 0.0 && o.lo[1] <= 16.0)) return fail(ALB_E_RANGE, at + "sigma outside (0, 16]");
+        break;
       case ALB_GRID_DISTORTION:  // every step factor 1 + U(lo, hi) stays > 0
         if (o.num_steps < 1 || o.num_steps > ALB_GRID_MAX_STEPS)
           return fail(ALB_E_RANGE, at + "num_steps outside [1, 32]");
@@ -331,8 +341,8 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   if ((mask_in == nullptr) != (mask_out == nullptr)) return fail(ALB_E_INVALID_ARG, "mask_in/mask_out must both be set");
   if (max_boxes < 0) return fail(ALB_E_INVALID_ARG, "max_boxes < 0");
   for (const alb_op& o : p->ops)
-    if (o.kind == ALB_GRID_DISTORTION && max_boxes > 0)
-      return fail(ALB_E_UNSUPPORTED, "boxes under GridDistortion (free-form warp)");
+    if ((o.kind == ALB_GRID_DISTORTION || o.kind == ALB_ELASTIC) && max_boxes > 0)
+      return fail(ALB_E_UNSUPPORTED, "boxes under a free-form warp (GridDistortion / ElasticTransform)");
   std::unique_ptr<alb_plan> P(new alb_plan);
   P->ops = p->ops;
   P->n = in->n;
@@ -421,6 +431,29 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       geo_open = point_open = false;
       continue;
     }
+    if (kind == ALB_ELASTIC) {  // field + remap, own step (post ops start a new step)
+      PlanStep st; st.kind = SK_ELASTIC; st.slot0 = k; st.slot1 = k + 1;
+      st.interp = o.interp; st.border = o.border;
+      st.fill = o.fill[0] | (o.fill[1] << 8) | (o.fill[2] << 16);
+      st.mask_fill = o.mask_fill;
+      // normalised truncated Gaussian, ascending-k sum (reading R32)
+      const double sigma = o.lo[1];
+      const int r = (int)std::ceil(3.0 * sigma);
+      st.g_r = r;
+      st.g_off = (int)P->gauss.size();
+      st.alpha = o.lo[0];
+      std::vector<double> g(2 * r + 1);
+      double sum = 0.0;
+      for (int q = -r; q <= r; ++q) {
+        g[q + r] = std::exp(-(double)(q * q) / (2.0 * sigma * sigma));
+        sum += g[q + r];
+      }
+      for (double& v : g) P->gauss.push_back(v / sum);
+      steps.push_back(st);
+      ++k;
+      geo_open = point_open = false;
+      continue;
+    }
     if (kind == ALB_ROT90 || kind == ALB_D4) {  // signed permutation, own step
       PlanStep st; st.kind = SK_D4; st.slot0 = k; st.slot1 = k + 1;
       steps.push_back(st);
@@ -495,7 +528,8 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   }
   // rgb-only ops need 3 channels: images are always 3-channel here.
   const bool has_geo = std::any_of(steps.begin(), steps.end(), [](const PlanStep& s) {
-    return s.kind == SK_ROW || s.kind == SK_RESAMPLE || s.kind == SK_AFFINE || s.kind == SK_D4;
+    return s.kind == SK_ROW || s.kind == SK_RESAMPLE || s.kind == SK_AFFINE || s.kind == SK_D4 ||
+           s.kind == SK_ELASTIC;
   });
   // masks ride on geometric steps; without one, an identity mask copy
   if (mask_in && !has_geo) {
@@ -606,6 +640,14 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
         if (st.has_mask) st.munits = st.units;
         break;
       }
+      case SK_ELASTIC:
+        for (int i = 0; i < P->n; ++i) {  // 32x32 output tiles, unit.y = (row << 16) | col
+          const int H = dims[i][st.slot0].first, W = dims[i][st.slot0].second;
+          if ((long long)H * W >= (1ll << 30)) return fail(ALB_E_UNSUPPORTED, "ElasticTransform image >= 2^30 pixels");
+          for (int ty = 0; ty < (H + 31) / 32; ++ty)
+            for (int tx = 0; tx < (W + 31) / 32; ++tx) st.units.push_back(make_int2(i, (ty << 16) | tx));
+        }
+        break;
       case SK_AFFINE: {
         // 55 KB: a 64x64 tile at scale >= 0.9 needs <= (99 + 5 + 31) x (99 + 5) = 14040 words
         st.unit_size = 14080;
@@ -694,6 +736,10 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   if (n_ops > 0) {
     CUDA_TRY(cudaMalloc(&P->d_ops, sizeof(alb_op) * n_ops));
     CUDA_TRY(cudaMemcpy(P->d_ops, P->ops.data(), sizeof(alb_op) * n_ops, cudaMemcpyHostToDevice));
+  }
+  if (!P->gauss.empty()) {
+    CUDA_TRY(cudaMalloc(&P->d_gauss, sizeof(double) * P->gauss.size()));
+    CUDA_TRY(cudaMemcpy(P->d_gauss, P->gauss.data(), sizeof(double) * P->gauss.size(), cudaMemcpyHostToDevice));
   }
   // ------------------------------------------------------------ workspace
   size_t off = 0;
@@ -856,6 +902,11 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
     a.rs_ring = st.rs_ring;
     a.rs_sw = st.rs_sw;
     a.rs_hw = st.rs_hw;
+    a.seed = seed;
+    a.first_image = (uint32_t)first_image_index;
+    a.gauss = P->d_gauss ? P->d_gauss + st.g_off : nullptr;
+    a.g_r = st.g_r;
+    a.alpha = st.alpha;
     switch (st.kind) {
       case SK_ROW:
         if (st.has_image) {
@@ -886,6 +937,7 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
       }
       case SK_RESAMPLE: launch_resample(a, stream); break;
       case SK_AFFINE: launch_affine(a, stream); break;
+      case SK_ELASTIC: launch_elastic(a, stream); break;
       case SK_D4:
         if (st.has_image) {
           a.channels = 3;

@@ -85,21 +85,6 @@ __device__ __forceinline__ AfCoef af_coef(const StepArgs& a, int img) {
   return c;
 }
 
-__device__ __forceinline__ uint32_t fetch_rgb(const uint8_t* row, int x) {
-  const uint8_t* p = row + 3 * x;
-  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
-}
-
-// border index: one reflection without modulo (the common case), else general
-__device__ __forceinline__ int border_idx(int i, int n, bool reflect, bool& in) {
-  if (i >= 0 && i < n) { in = true; return i; }
-  if (!reflect) { in = false; return 0; }
-  in = true;
-  int k = i < 0 ? -i : i;
-  if (k >= n) k = 2 * n - 2 - k;
-  return (k >= 0 && k < n) ? k : reflect101(i, n);
-}
-
 // Per-column cell anchor: fp64 source coordinate of the cell origin, split
 // into integer part (ix, iy) and fp32 fraction, plus the column's fp32 offset.
 struct Anchor {

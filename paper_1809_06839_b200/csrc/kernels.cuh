@@ -61,7 +61,16 @@ struct StepArgs {
   int32_t n_img;  // images in the batch
   int32_t rs_ring, rs_sw, rs_hw;  // separable resample: ring rows (0 = old kernel), staged row
                                    // stride (words), output rows per group
+  uint64_t seed;                   // Philox key of this apply (ElasticTransform raw planes)
+  uint32_t first_image;            // global index of image 0
+  const double* gauss;             // ElasticTransform: normalised weights w[0..2 g_r] (R32)
+  int32_t g_r;                     // ElasticTransform kernel radius ceil(3 sigma)
+  double alpha;                    // ElasticTransform displacement scale
 };
+
+constexpr int kElMaxR = 48;  // ElasticTransform radius cap (sigma <= 16, reading R32)
+// shared memory of the ElasticTransform kernel for radius r (elastic.cu)
+size_t elastic_smem(int r);
 
 // shared memory of the separable resample kernel (resample.cu)
 size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize);
@@ -176,6 +185,7 @@ void launch_rowgather(const StepArgs& a, cudaStream_t s);
 void launch_resample(const StepArgs& a, cudaStream_t s);
 void launch_affine(const StepArgs& a, cudaStream_t s);
 void launch_d4(const StepArgs& a, cudaStream_t s);
+void launch_elastic(const StepArgs& a, cudaStream_t s);
 void launch_eq_hist(const EqArgs& a, cudaStream_t s);
 void launch_eq_lut(const EqArgs& a, cudaStream_t s);
 void launch_boxes(const BoxArgs& a, cudaStream_t s);

@@ -487,6 +487,21 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
 // Contiguous range of units for CTA b of G (persistent kernels): consecutive
 // units belong mostly to the same image, so per-image state is reloaded only
 // when the image changes.
+__device__ __forceinline__ uint32_t fetch_rgb(const uint8_t* row, int x) {
+  const uint8_t* p = row + 3 * x;
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
+}
+
+// border index: one reflection without modulo (the common case), else general
+__device__ __forceinline__ int border_idx(int i, int n, bool reflect, bool& in) {
+  if (i >= 0 && i < n) { in = true; return i; }
+  if (!reflect) { in = false; return 0; }
+  in = true;
+  int k = i < 0 ? -i : i;
+  if (k >= n) k = 2 * n - 2 - k;
+  return (k >= 0 && k < n) ? k : reflect101(i, n);
+}
+
 __device__ __forceinline__ void unit_range(int n_units, int& u0, int& u1) {
   const long long G = gridDim.x, b = blockIdx.x;
   u0 = (int)(b * n_units / G);

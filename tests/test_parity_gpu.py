@@ -419,3 +419,74 @@ def test_grid_distortion_rejects_boxes_and_bad_params():
     for bad in (_grid(-1.0, 0.3, 5), _grid(-0.3, 0.3, 0), _grid(-0.3, 0.3, 33)):
         with pytest.raises(AlbError):
             Pipeline([bad])
+
+
+# ---------------------------------------------- ElasticTransform (reading R32)
+
+def _elastic(alpha, sigma, interp="bilinear", border="reflect_101", p=1.0, fill=(0, 0, 0)):
+    return {"kind": "ElasticTransform", "p": p, "lo": [alpha, sigma], "hi": [alpha, sigma],
+            "interp": interp, "border": border, "fill": fill, "mask_fill": 3}
+
+
+EL_SIZES = [(45, 130), (70, 17), (129, 100), (1, 1), (3, 70), (2, 1), (1, 33), (64, 64), (33, 95)]
+EL_CASES = [
+    [_elastic(34.0, 4.0)],
+    [_elastic(34.0, 4.0, "nearest")],
+    [_elastic(120.0, 6.0, border="constant", fill=(10, 200, 77))],
+    [_elastic(8.0, 0.6, "nearest", "constant", p=0.6)],
+    [_elastic(400.0, 16.0)],
+    [{"kind": "HorizontalFlip", "p": 0.5}, _elastic(20.0, 3.0), {"kind": "Brightness", "lo": [0.8], "hi": [1.2]},
+     _elastic(10.0, 2.0, "nearest", "constant")],
+]
+
+
+def _coords_exact_kinds(specs):
+    return all(s.get("interp") == "nearest" for s in specs if s["kind"] == "ElasticTransform")
+
+
+@pytest.mark.parametrize("with_mask", [False, True])
+@pytest.mark.parametrize("case", range(len(EL_CASES)))
+def test_elastic_image_mask(case, with_mask):
+    """GPU ElasticTransform vs the oracle: the fp64 field is computed in the
+    oracle's order from the same weights, so nearest images and masks are
+    bit-exact; bilinear images <= 1 LSB / >= 99.9% exact (fp32 blend)."""
+    specs = EL_CASES[case]
+    n = len(EL_SIZES)
+    b = gen.gen_images(EL_SIZES, seed=6, first_image_index=3, device="cuda")
+    masks = gen.gen_boxes(EL_SIZES, seed=6, first_image_index=3)[3].to("cuda") if with_mask else None
+    res = run_gpu(specs, b, seed=13, first=3, masks=masks)
+    imgs = [b.image(i) for i in range(n)]
+    mk = [masks.image(i) for i in range(n)] if with_mask else None
+    ref = run_oracle(specs, imgs, seed=13, first=3, masks=mk)
+    if _coords_exact_kinds(specs):
+        cmp_exact(res["images"], [o["image"] for o in ref])
+    else:
+        cmp_interp(res["images"], [o["image"] for o in ref])
+    if with_mask:
+        cmp_exact(res["masks"], [o["mask"] for o in ref])
+
+
+def test_elastic_identity_large_and_errors():
+    """alpha = 0 is the identity bit for bit; a 1000x1400 image
+    (many tiles) against the oracle; boxes and bad parameters rejected."""
+    from paper_1809_06839_b200 import Layout, Pipeline, Plan
+    from paper_1809_06839_b200._lib import AlbError
+    sizes = [(50, 70), (1, 1), (33, 2)]
+    b = gen.gen_images(sizes, seed=2, first_image_index=0, device="cuda")
+    for interp in ("bilinear", "nearest"):
+        res = run_gpu([_elastic(0.0, 5.0, interp)], b, seed=1)
+        cmp_exact(res["images"], [b.image(i) for i in range(len(sizes))])
+    sizes = [(1000, 1400)]
+    b = gen.gen_images(sizes, seed=4, first_image_index=50, device="cuda")
+    specs = [_elastic(34.0, 4.0)]
+    res = run_gpu(specs, b, seed=2, first=50)
+    cmp_interp(res["images"], [run_oracle(specs, [b.image(0)], seed=2, first=50)[0]["image"]])
+    out = out_batch([(20, 30)])
+    b = gen.gen_images([(20, 30)], seed=0, first_image_index=0, device="cuda")
+    with pytest.raises(AlbError) as e:
+        Plan(Pipeline([_elastic(5.0, 2.0)]), Layout(b.desc, 3), Layout(out.desc, 3), None, None, 2, 0.0)
+    assert e.value.code == -5
+    for bad in (_elastic(-1.0, 2.0), _elastic(1.0, 0.0), _elastic(1.0, 17.0),
+                {"kind": "ElasticTransform", "lo": [1.0, 2.0], "hi": [3.0, 2.0]}):
+        with pytest.raises(AlbError):
+            Pipeline([bad])
