@@ -85,3 +85,12 @@ CONFIGS = {
     4: dict(n=1024, size=(375, 500)),    # H=375, W=500 (R23)
     5: dict(n=512, size=(1024, 1024)),
 }
+
+
+# next-row transforms measured by tools/copy_probe.py / profile_ops.py on the cfg2 corpus
+EXTRA_OPS = {"Rot90k1": [{"kind": "Rotate90", "lo": [1], "hi": [1]}],
+             "D4e5": [{"kind": "D4", "lo": [5], "hi": [5]}],
+             "D4e2": [{"kind": "D4", "lo": [2], "hi": [2]}],
+             "Grid5": [{"kind": "GridDistortion", "lo": [-0.3], "hi": [0.3], "num_steps": 5}],
+             "Elastic": [{"kind": "ElasticTransform", "lo": [34.0, 4.0], "hi": [34.0, 4.0], "border": "reflect_101"}],
+             "Grid5n": [{"kind": "GridDistortion", "lo": [-0.3], "hi": [0.3], "num_steps": 5, "interp": "nearest"}]}

@@ -32,12 +32,7 @@ def timeit(fn, reps=20):
 t = timeit(lambda: out.copy_(b.buf))
 print("torch copy_ corpus: %.3f ms  %.1f GB/s (alg %.1f GB/s)" % (t, 2 * b.buf.numel() / t / 1e6, 2 * nbytes / t / 1e6))
 inl = Layout(b.desc, 3)
-EXTRA = {"Rot90k1": [{"kind": "Rotate90", "lo": [1], "hi": [1]}],
-         "D4e5": [{"kind": "D4", "lo": [5], "hi": [5]}],
-         "D4e2": [{"kind": "D4", "lo": [2], "hi": [2]}],
-         "Grid5": [{"kind": "GridDistortion", "lo": [-0.3], "hi": [0.3], "num_steps": 5}],
-         "Elastic": [{"kind": "ElasticTransform", "lo": [34.0, 4.0], "hi": [34.0, 4.0], "border": "reflect_101"}],
-         "Grid5n": [{"kind": "GridDistortion", "lo": [-0.3], "hi": [0.3], "num_steps": 5, "interp": "nearest"}]}
+EXTRA = C.EXTRA_OPS
 for name in sys.argv[1:] or ["Brightness", "HorizontalFlip", "Grayscale"]:
     specs = EXTRA.get(name) or C.CFG2_MENU[name]
     p = Pipeline(specs)

@@ -20,7 +20,7 @@ sizes = gen.cfg2_sizes(a.n)
 b = gen.gen_images(sizes, seed=0, device="cuda")
 inl = Layout(b.desc, 3)
 for name in a.ops.split(","):
-    specs = C.CFG2_MENU[name]
+    specs = C.EXTRA_OPS.get(name) or C.CFG2_MENU[name]
     p = Pipeline(specs)
     osz = [p.output_shape(h, w) for h, w in sizes]
     ob = gen.empty_batch(osz, 3, "cuda")
