@@ -641,11 +641,11 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
         break;
       }
       case SK_ELASTIC:
-        for (int i = 0; i < P->n; ++i) {  // strips x bands of 128 rows, unit.y = (band << 16) | strip
+        for (int i = 0; i < P->n; ++i) {  // strips x bands of kElBand rows, unit.y = (band << 16) | strip
           const int H = dims[i][st.slot0].first, W = dims[i][st.slot0].second;
           if ((long long)H * W >= (1ll << 30)) return fail(ALB_E_UNSUPPORTED, "ElasticTransform image >= 2^30 pixels");
           const int sw = elastic_strip(st.g_r);
-          for (int ty = 0; ty < (H + 127) / 128; ++ty)
+          for (int ty = 0; ty < (H + kElBand - 1) / kElBand; ++ty)
             for (int tx = 0; tx < (W + sw - 1) / sw; ++tx) st.units.push_back(make_int2(i, (ty << 16) | tx));
         }
         break;

@@ -32,7 +32,6 @@ namespace alb {
 constexpr int kElThreads = 256;
 constexpr int kElWarps = 8;
 constexpr int kElChunk = 32;  // rows per produce / consume step (= lanes)
-constexpr int kElBand = 128;  // output rows per unit
 
 // tap steps of a U-output register block: outputs i < U, taps k <= 2r, m = i + k,
 // rounded up to a multiple of U
@@ -50,7 +49,7 @@ struct ElLayout {
     ring_off = raw_off + kElChunk * rw;
   }
   __host__ __device__ size_t bytes(int U) const {
-    return ((size_t)ring_off + (size_t)2 * ring_rows * 8 * U) * 8;
+    return ((size_t)ring_off + (size_t)2 * ring_rows * (8 * U + 1)) * 8;
   }
 };
 
@@ -78,13 +77,14 @@ __device__ __forceinline__ int refl(int i, int n) {
 template <int U>
 __global__ void __launch_bounds__(kElThreads) k_elastic(StepArgs a) {
   constexpr int TW = 8 * U;
+  constexpr int RS = TW + 1;  // ring row stride: x-pass stores (lane = row) hit distinct banks
   extern __shared__ double esm[];
   const int r = a.g_r;
   const ElLayout L(r, U);
   const int M = el_msteps(r, U);      // tap steps per output block
   double* wz = esm;                   // wz[t] = w_{t - (U-1)}, zero outside [0, 2r]
   double* raw = esm + L.raw_off;      // [32][rw]
-  double* ring = esm + L.ring_off;    // [2][ring_rows][TW]
+  double* ring = esm + L.ring_off;    // [2][ring_rows][RS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int2 unit = a.units[blockIdx.x];
   const int img = unit.x;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kElThreads) k_elastic(StepArgs a) {
   }
   const int RW = TW + 2 * r;  // raw columns a halo row needs
   const int RR = L.ring_rows;
-  for (int i = tid; i < 2 * RR * TW; i += kElThreads) ring[i] = 0.0;  // rows past the data meet zero weights
+  for (int i = tid; i < 2 * RR * RS; i += kElThreads) ring[i] = 0.0;  // rows past the data meet zero weights
   for (int i = tid; i < kElChunk * (L.rw - RW); i += kElThreads) {  // finite padding columns
     const int row = i / (L.rw - RW);
     raw[row * L.rw + RW + (i - row * (L.rw - RW))] = 0.0;
@@ -171,27 +171,28 @@ __global__ void __launch_bounds__(kElThreads) k_elastic(StepArgs a) {
   auto produce = [&](int Y0, int n, int slot0) {
     for (int plane = 0; plane < 2; ++plane) {
       const int j0 = 1 + plane * plane_j;
-      // raw values: work item = (row, pair of columns sharing one Philox block)
+      // raw values: warp = row, lane = pair of columns sharing one Philox block
       const int npair = (RW + 2) >> 1;
-      for (int it = tid; it < n * npair; it += kElThreads) {
-        const int row = it / npair, p = it - row * npair;
+      for (int row = warp; row < n; row += kElWarps) {
         const int jr = j0 + refl(Y0 + row, H) * W;
         const int J0 = jr + (x0 - r);  // j of raw column 0 if unreflected
-        const int q0 = 2 * p - (J0 & 1);
-        const int xa = x0 - r + q0;
         double* dst = raw + row * L.rw;
-        if (xa >= 0 && xa + 1 < W) {  // both unreflected: one block
-          const uint4 o = philox10(make_uint4(gi, (uint32_t)a.slot0, (uint32_t)((J0 + q0) >> 1), 0u), key);
-          if (q0 >= 0) dst[q0] = raw_of(o.x, o.y);
-          if (q0 + 1 < RW) dst[q0 + 1] = raw_of(o.z, o.w);
-        } else {
+        for (int p = lane; p < npair; p += 32) {
+          const int q0 = 2 * p - (J0 & 1);
+          const int xa = x0 - r + q0;
+          if (xa >= 0 && xa + 1 < W) {  // both unreflected: one block
+            const uint4 o = philox10(make_uint4(gi, (uint32_t)a.slot0, (uint32_t)((J0 + q0) >> 1), 0u), key);
+            if (q0 >= 0) dst[q0] = raw_of(o.x, o.y);
+            if (q0 + 1 < RW) dst[q0 + 1] = raw_of(o.z, o.w);
+          } else {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int q = q0 + e;
-            if (q < 0 || q >= RW) continue;
-            const int j = jr + refl(x0 - r + q, W);
-            const uint4 o = philox10(make_uint4(gi, (uint32_t)a.slot0, (uint32_t)(j >> 1), 0u), key);
-            dst[q] = (j & 1) ? raw_of(o.z, o.w) : raw_of(o.x, o.y);
+            for (int e = 0; e < 2; ++e) {
+              const int q = q0 + e;
+              if (q < 0 || q >= RW) continue;
+              const int j = jr + refl(x0 - r + q, W);
+              const uint4 o = philox10(make_uint4(gi, (uint32_t)a.slot0, (uint32_t)(j >> 1), 0u), key);
+              dst[q] = (j & 1) ? raw_of(o.z, o.w) : raw_of(o.x, o.y);
+            }
           }
         }
       }
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kElThreads) k_elastic(StepArgs a) {
         }
         int sl = slot0 + lane;
         if (sl >= RR) sl -= RR;
-        double* d = ring + ((size_t)plane * RR + sl) * TW + U * warp;
+        double* d = ring + ((size_t)plane * RR + sl) * RS + U * warp;
 #pragma unroll
         for (int i = 0; i < U; ++i) d[i] = acc[i];
       }
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kElThreads) k_elastic(StepArgs a) {
       double dv[2][U];
 #pragma unroll
       for (int plane = 0; plane < 2; ++plane) {
-        const double* rp = ring + (size_t)plane * RR * TW + col;
+        const double* rp = ring + (size_t)plane * RR * RS + col;
         double acc[U], wv[U];
 #pragma unroll
         for (int i = 0; i < U; ++i) acc[i] = 0.0;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kElThreads) k_elastic(StepArgs a) {
 #pragma unroll
           for (int s = 0; s < U; ++s) {
             wv[(s + U - 1) % U] = wz[mb + s + U - 1];
-            const double v = rp[s_row * TW];
+            const double v = rp[s_row * RS];
             if (++s_row == RR) s_row = 0;
 #pragma unroll
             for (int i = 0; i < U; ++i) acc[i] = __fma_rn(wv[(s + U - 1 - i) % U], v, acc[i]);

@@ -71,8 +71,9 @@ struct StepArgs {
 constexpr int kElMaxR = 48;  // ElasticTransform radius cap (sigma <= 16, reading R32)
 // shared memory of the ElasticTransform kernel for radius r (elastic.cu)
 size_t elastic_smem(int r);
-// output columns per ElasticTransform unit for radius r (elastic.cu); bands are 128 rows
+// output columns per ElasticTransform unit for radius r (elastic.cu)
 int elastic_strip(int r);
+constexpr int kElBand = 256;  // output rows per ElasticTransform unit
 
 // shared memory of the separable resample kernel (resample.cu)
 size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize);
