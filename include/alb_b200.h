@@ -204,6 +204,33 @@ alb_status alb_sample_params(const alb_pipeline* p, uint64_t seed, uint64_t firs
                              uint8_t* fired_out);
 
 /* Thread-local message for the last non-OK status of this thread. */
+/* Pipeline configs: UTF-8 JSON
+ *   {"seed": <optional u64>, "transforms": [{"name": "<kind>", "p": <number>,
+ *                                            "params": {...}}, ...]}
+ * with the kind names of alb_kind's comments (HorizontalFlip, ..., ElasticTransform)
+ * and per-kind params (range params take a number = fixed value or [lo, hi]):
+ *   Rotate {angle, interpolation?, border?, fill?, mask_fill?}
+ *   ShiftScaleRotate {shift_x, shift_y, scale, angle, interpolation?, border?, fill?, mask_fill?}
+ *   RandomCrop {width, height}   Crop {x, y, width, height}   PadToSize {width, height, fill?, mask_fill?}
+ *   Resize {width, height, interpolation?}   RandomSizedCrop {min_side, max_side, width, height, interpolation?}
+ *   Brightness {beta}  Contrast {c}  BrightnessContrast {beta, c}  Gamma {g}
+ *   ShiftRGB {dr, dg, db}  ShiftHSV {dh, ds, dv}  Normalize {mean[3], std[3]}
+ *   Rotate90 {k}  D4 {element}  GridDistortion {num_steps, distort_limit (d = [-d, d]), interpolation?}
+ *   ElasticTransform {alpha, sigma (numbers), interpolation?, border?, fill?, mask_fill?}
+ *   HorizontalFlip, VerticalFlip, Grayscale, Equalize: {}
+ * interpolation "nearest" | "bilinear" (default), border "constant" (default) |
+ * "reflect_101", fill [r, g, b] (default 0), mask_fill (default 0).  "p" is
+ * mandatory.  from_json: text NUL-terminated; *out as alb_pipeline_create;
+ * seed / has_seed (may be NULL) receive the optional seed.  Errors:
+ * ALB_E_INVALID_ARG (syntax, type, unknown field, missing required param --
+ * alb_last_error names it), ALB_E_UNKNOWN_OP (message lists the valid names),
+ * ALB_E_RANGE / ALB_E_UNSUPPORTED as alb_pipeline_create.
+ * to_json: every param of each kind written explicitly, numbers round-trip
+ * exact; *len = bytes excluding the NUL; buf may be NULL to query the size,
+ * else cap must be >= *len + 1 (ALB_E_INVALID_ARG).  seed NULL = no seed field. */
+alb_status alb_pipeline_from_json(const char* text, alb_pipeline** out, uint64_t* seed, int32_t* has_seed);
+alb_status alb_pipeline_to_json(const alb_pipeline* p, const uint64_t* seed, char* buf, size_t cap, size_t* len);
+
 const char* alb_last_error(void);
 int32_t alb_version(void);
 

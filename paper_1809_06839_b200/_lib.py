@@ -58,7 +58,8 @@ class AlbError(RuntimeError):
 EXPORTS = ["alb_pipeline_create", "alb_pipeline_destroy", "alb_output_shape",
            "alb_layout_create", "alb_layout_destroy", "alb_plan_create", "alb_plan_destroy",
            "alb_plan_workspace_size", "alb_plan_num_launches", "alb_apply", "alb_apply_host",
-           "alb_sample_params", "alb_last_error", "alb_version"]
+           "alb_sample_params", "alb_last_error", "alb_version", "alb_pipeline_from_json",
+           "alb_pipeline_to_json"]
 
 _lib = None
 
@@ -96,9 +97,12 @@ def lib():
     L.alb_last_error.restype = ctypes.c_char_p
     L.alb_last_error.argtypes = []
     L.alb_version.restype = ctypes.c_int32
+    L.alb_pipeline_from_json.argtypes = [ctypes.c_char_p, P(vp), P(ctypes.c_uint64), P(ctypes.c_int32)]
+    L.alb_pipeline_to_json.argtypes = [vp, P(ctypes.c_uint64), ctypes.c_char_p, ctypes.c_size_t,
+                                       P(ctypes.c_size_t)]
     for name in ["alb_pipeline_create", "alb_output_shape", "alb_layout_create",
                  "alb_plan_create", "alb_plan_workspace_size", "alb_apply", "alb_apply_host",
-                 "alb_sample_params"]:
+                 "alb_sample_params", "alb_pipeline_from_json", "alb_pipeline_to_json"]:
         getattr(L, name).restype = ctypes.c_int32
     _lib = L
     return L

@@ -11,6 +11,7 @@ mean, std (see include/alb_b200.h for the meaning of every field).
 from __future__ import annotations
 
 import ctypes
+import json
 
 import numpy as np
 import torch
@@ -59,6 +60,29 @@ class Pipeline:
         check(lib().alb_pipeline_create(ops, n, ctypes.byref(h)))
         self.handle = h
         self.n_ops = n
+
+    @classmethod
+    def from_json(cls, text):
+        """alb_pipeline_from_json: (Pipeline, seed or None) from a config document."""
+        h = ctypes.c_void_p()
+        seed = ctypes.c_uint64()
+        has = ctypes.c_int32()
+        check(lib().alb_pipeline_from_json(text.encode("utf-8"), ctypes.byref(h), ctypes.byref(seed),
+                                           ctypes.byref(has)))
+        self = cls.__new__(cls)
+        self.specs = None
+        self.handle = h
+        self.n_ops = len(json.loads(self.to_json())["transforms"])
+        return self, (seed.value if has.value else None)
+
+    def to_json(self, seed=None):
+        """alb_pipeline_to_json: the config document (str)."""
+        s = None if seed is None else ctypes.byref(ctypes.c_uint64(seed))
+        size = ctypes.c_size_t()
+        check(lib().alb_pipeline_to_json(self.handle, s, None, 0, ctypes.byref(size)))
+        buf = ctypes.create_string_buffer(size.value + 1)
+        check(lib().alb_pipeline_to_json(self.handle, s, buf, size.value + 1, ctypes.byref(size)))
+        return buf.value.decode("utf-8")
 
     def __del__(self):
         if getattr(self, "handle", None) and _lib._lib is not None:

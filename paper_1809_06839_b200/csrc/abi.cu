@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "config.h"
 #include "kernels.cuh"
 #include "stages.cuh"
 
@@ -282,6 +283,11 @@ static void row_units(PlanStep& st, const alb_layout* dst, int channels, std::ve
 }
 
 // ----------------------------------------------------------------- the ABI
+
+namespace alb {
+alb_status set_error(alb_status s, const std::string& msg) { return fail(s, msg); }
+const std::vector<alb_op>& pipeline_ops(const alb_pipeline* p) { return p->ops; }
+}  // namespace alb
 
 extern "C" {
 
