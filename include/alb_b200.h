@@ -231,6 +231,28 @@ alb_status alb_sample_params(const alb_pipeline* p, uint64_t seed, uint64_t firs
 alb_status alb_pipeline_from_json(const char* text, alb_pipeline** out, uint64_t* seed, int32_t* has_seed);
 alb_status alb_pipeline_to_json(const alb_pipeline* p, const uint64_t* seed, char* buf, size_t cap, size_t* len);
 
+/* GPU input front-end ("GPUs idle
+ * while the CPU prepares batches"): JPEG bitstreams in HOST memory decoded by
+ * nvJPEG (a library, loaded with dlopen on first use) into a ragged RGB u8
+ * layout on the device -- the input of alb_apply.
+ * alb_decoder_create: prefer_hardware != 0 asks for nvJPEG's hardware backend
+ *   (the GPU's JPEG engines), falling back to its CUDA backend.  Errors:
+ *   ALB_E_UNSUPPORTED (nvJPEG missing), ALB_E_CUDA.  One decoder per stream /
+ *   thread at a time.
+ * alb_decoder_backend: 1 = hardware engines, 2 = GPU-assisted Huffman, 0 = default backend.
+ * alb_jpeg_info: dims of a bitstream (host parse) for building the layout.
+ * alb_decode_jpeg: data[i] / lengths[i] host bitstreams (caller-owned, valid
+ *   until the stream reaches this point), out a 3-channel layout whose image i
+ *   has the bitstream's dims (ALB_E_SHAPE otherwise), dev_out its device base.
+ *   Asynchronous on `stream`; ALB_E_UNSUPPORTED for bitstreams nvJPEG rejects. */
+typedef struct alb_decoder alb_decoder;
+alb_status alb_decoder_create(int32_t prefer_hardware, alb_decoder** out);
+void alb_decoder_destroy(alb_decoder* d);
+int32_t alb_decoder_backend(const alb_decoder* d);
+alb_status alb_jpeg_info(alb_decoder* d, const uint8_t* data, size_t length, int32_t* height, int32_t* width);
+alb_status alb_decode_jpeg(alb_decoder* d, const uint8_t* const* data, const size_t* lengths, int32_t n,
+                           const alb_layout* out, uint8_t* dev_out, void* stream);
+
 const char* alb_last_error(void);
 int32_t alb_version(void);
 

@@ -59,7 +59,8 @@ EXPORTS = ["alb_pipeline_create", "alb_pipeline_destroy", "alb_output_shape",
            "alb_layout_create", "alb_layout_destroy", "alb_plan_create", "alb_plan_destroy",
            "alb_plan_workspace_size", "alb_plan_num_launches", "alb_apply", "alb_apply_host",
            "alb_sample_params", "alb_last_error", "alb_version", "alb_pipeline_from_json",
-           "alb_pipeline_to_json"]
+           "alb_pipeline_to_json", "alb_decoder_create", "alb_decoder_destroy", "alb_decoder_backend",
+           "alb_jpeg_info", "alb_decode_jpeg"]
 
 _lib = None
 
@@ -100,7 +101,14 @@ def lib():
     L.alb_pipeline_from_json.argtypes = [ctypes.c_char_p, P(vp), P(ctypes.c_uint64), P(ctypes.c_int32)]
     L.alb_pipeline_to_json.argtypes = [vp, P(ctypes.c_uint64), ctypes.c_char_p, ctypes.c_size_t,
                                        P(ctypes.c_size_t)]
-    for name in ["alb_pipeline_create", "alb_output_shape", "alb_layout_create",
+    L.alb_decoder_create.argtypes = [ctypes.c_int32, P(vp)]
+    L.alb_decoder_destroy.argtypes = [vp]
+    L.alb_decoder_backend.argtypes = [vp]
+    L.alb_decoder_backend.restype = ctypes.c_int32
+    L.alb_jpeg_info.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t, P(ctypes.c_int32), P(ctypes.c_int32)]
+    L.alb_decode_jpeg.argtypes = [vp, P(ctypes.c_char_p), P(ctypes.c_size_t), ctypes.c_int32, vp, vp, vp]
+    for name in ["alb_decoder_create", "alb_jpeg_info", "alb_decode_jpeg",
+                 "alb_pipeline_create", "alb_output_shape", "alb_layout_create",
                  "alb_plan_create", "alb_plan_workspace_size", "alb_apply", "alb_apply_host",
                  "alb_sample_params", "alb_pipeline_from_json", "alb_pipeline_to_json"]:
         getattr(L, name).restype = ctypes.c_int32

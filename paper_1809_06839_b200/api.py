@@ -191,3 +191,42 @@ class Plan:
                                    dev_in.data_ptr(), host_out.data_ptr(),
                                    host_out.numel() * host_out.element_size(), dev_out.data_ptr(),
                                    wp, wn, stream.cuda_stream))
+
+
+class Decoder:
+    """alb_decoder: nvJPEG batch decode of host JPEG bitstreams into a ragged
+    RGB u8 device layout (the input of Plan.apply)."""
+
+    def __init__(self, prefer_hardware=True):
+        h = ctypes.c_void_p()
+        check(lib().alb_decoder_create(1 if prefer_hardware else 0, ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib._lib is not None:
+            _lib._lib.alb_decoder_destroy(self.handle)
+            self.handle = None
+
+    @property
+    def backend(self):
+        """1 = hardware JPEG engines, 2 = GPU-assisted Huffman, 0 = default backend"""
+        return lib().alb_decoder_backend(self.handle)
+
+    @property
+    def hardware(self):
+        return self.backend == 1
+
+    def info(self, data):
+        """(height, width) of one bitstream (bytes)."""
+        h, w = ctypes.c_int32(), ctypes.c_int32()
+        check(lib().alb_jpeg_info(self.handle, data, len(data), ctypes.byref(h), ctypes.byref(w)))
+        return h.value, w.value
+
+    def decode(self, streams, layout, dev_out):
+        """Decode the list of bitstreams into dev_out (uint8 CUDA tensor) laid out
+        by `layout` (a 3-channel Layout), on the current stream."""
+        n = len(streams)
+        arr = (ctypes.c_char_p * max(1, n))(*streams)
+        lens = (ctypes.c_size_t * max(1, n))(*[len(s) for s in streams])
+        stream = torch.cuda.current_stream(dev_out.device)
+        check(lib().alb_decode_jpeg(self.handle, arr, lens, n, layout.handle, _ptr(dev_out), stream.cuda_stream))

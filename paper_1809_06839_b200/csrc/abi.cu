@@ -287,6 +287,8 @@ static void row_units(PlanStep& st, const alb_layout* dst, int channels, std::ve
 namespace alb {
 alb_status set_error(alb_status s, const std::string& msg) { return fail(s, msg); }
 const std::vector<alb_op>& pipeline_ops(const alb_pipeline* p) { return p->ops; }
+const std::vector<alb_image_desc>& layout_desc(const alb_layout* l) { return l->h; }
+int layout_channels(const alb_layout* l) { return l->channels; }
 }  // namespace alb
 
 extern "C" {

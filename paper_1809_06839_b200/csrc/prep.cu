@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
           nh = o.out_h; nw = o.out_w;
           break;
         case ALB_GRID_DISTORTION: {  // x factors: draws 1..n+1, y factors: n+2..2n+2
+          if (!a.grid) break;  // alb_sample_params: gates and params only
           double* e = a.grid + ((size_t)i * a.n_grid + g_ord++) * kGridStride;
           grid_knots(o, a.seed, gi, k, 1, w, e);
           grid_knots(o, a.seed, gi, k, o.num_steps + 2, h, e + kGridAxis);
