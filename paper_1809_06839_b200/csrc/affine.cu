@@ -725,6 +725,9 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
         const TileCtx& p = ctx[(it_t + 2) % 3];
         copy_rows_out<kObFull, kCThreads>(p.drow0, p.dpitch, obuf, kObPitch, p.th, 3 * p.tw);
       }
+#ifdef ALB_PROF
+      { const long long t1 = clock64(); pr[6] += t1 - tq; tq = t1; }
+#endif
       {  // anchor table: (cell row q, column) -> fp32 offsets + tap base
         const double* A = c.is.A;
         const float A0f = c.is.Af[0], A3f = c.is.Af[2];
@@ -741,6 +744,9 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
           an[e] = en;
         }
       }
+#ifdef ALB_PROF
+      { const long long t1 = clock64(); pr[7] += t1 - tq; tq = t1; }
+#endif
       const alb_image_desc sd = a.sdesc[img];
       const int Ws = sd.width, Hs = sd.height;
       const uint8_t* simg = a.src + sd.offset;
@@ -874,8 +880,8 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
   }
 #ifdef ALB_PROF
   if ((blockIdx.x == 0 || blockIdx.x == 101) && lane == 0 && (warp == 0 || warp == 5 || producer))
-    printf("blk %d warp %d tiles %d: P-pre %lld mbar %lld P-post %lld barP %lld C %lld barC %lld (cycles/tile)\n",
-           blockIdx.x, warp, u1 - u0, pr[0] / (u1 - u0), pr[1] / (u1 - u0), pr[2] / (u1 - u0),
+    printf("blk %d warp %d tiles %d: copyout %lld anchor %lld border %lld mbar %lld P-post %lld barP %lld C %lld barC %lld (cycles/tile)\n",
+           blockIdx.x, warp, u1 - u0, pr[6] / (u1 - u0), pr[7] / (u1 - u0), pr[0] / (u1 - u0), pr[1] / (u1 - u0), pr[2] / (u1 - u0),
            pr[3] / (u1 - u0), pr[4] / (u1 - u0), pr[5] / (u1 - u0));
 #endif
   if (!producer) {
