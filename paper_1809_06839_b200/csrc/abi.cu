@@ -82,6 +82,7 @@ struct PlanStep {
   const alb_layout* mdst_l = nullptr;
   std::vector<int2> units, munits;
   size_t units_off = 0, munits_off = 0;  // into the plan's device unit table
+  std::vector<int> ustart, mstart;       // first unit (mask unit) of image i, size n + 1
   int unit_size = 0, munit_size = 0, unit_rows = 0;
   bool flat = false;
   uint32_t fill = 0, mask_fill = 0;
@@ -124,10 +125,16 @@ struct alb_plan {
   double* d_gauss = nullptr;
   int2* d_units = nullptr;
   int n_launches = 0;
+  // alb_apply_host pipeline: copy streams and per-chunk events (created on first use)
+  mutable cudaStream_t s_in = nullptr, s_out = nullptr;
+  mutable std::vector<cudaEvent_t> ev;
   ~alb_plan() {
     if (d_ops) cudaFree(d_ops);
     if (d_gauss) cudaFree(d_gauss);
     if (d_units) cudaFree(d_units);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
   }
 };
 
@@ -283,6 +290,193 @@ static void row_units(PlanStep& st, const alb_layout* dst, int channels, std::ve
 }
 
 // ----------------------------------------------------------------- the ABI
+
+// Launch the plan's kernels for images [i0, i1) (alb_apply: the whole batch;
+// alb_apply_host: chunks, so copies and kernels of different chunks overlap).
+// Every kernel either iterates per-image (K0, affine setup, equalize LUT) over
+// the range or takes the range's contiguous slice of its step's unit table.
+static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_image_index,
+                               const uint8_t* img_in, uint8_t* img_out, float* out_nchw,
+                               const uint8_t* mask_in, uint8_t* mask_out, const float* boxes_in,
+                               const int32_t* labels_in, const int32_t* count_in, float* boxes_out,
+                               int32_t* labels_out, int32_t* count_out, uint8_t* ws, int i0, int i1,
+                               cudaStream_t stream) {
+  const int n_ops = (int)P->ops.size();
+
+  Tables tab{};
+  tab.params = (const double*)(ws + P->off_params);
+  tab.fired = ws + P->off_fired;
+  tab.dims = (const int32_t*)(ws + P->off_dims);
+  tab.luts = ws + P->off_luts;
+  tab.norm_lut = (const float*)(ws + P->off_norm);
+  tab.eq_luts = ws + P->off_eql;
+  tab.n_ops = n_ops;
+  tab.n_luts = P->n_luts;
+  tab.grid = (const double*)(ws + P->off_grid);
+  tab.n_grid = P->n_grid;
+
+  PrepArgs pa{};
+  pa.ops = P->d_ops;
+  pa.n_ops = n_ops;
+  pa.n = i1 - i0;
+  pa.img0 = i0;
+  pa.seed = seed;
+  pa.first_image = (uint32_t)first_image_index;
+  pa.in_desc = P->in->d;
+  pa.params = (double*)(ws + P->off_params);
+  pa.fired = ws + P->off_fired;
+  pa.dims = (int32_t*)(ws + P->off_dims);
+  pa.luts = ws + P->off_luts;
+  pa.n_luts = P->n_luts;
+  for (int s = 0; s < P->n_luts; ++s) { pa.lut_k0[s] = P->lut_k0[s]; pa.lut_k1[s] = P->lut_k1[s]; }
+  pa.norm_lut = (float*)(ws + P->off_norm);
+  pa.norm_slot = P->norm_slot;
+  pa.grid = (double*)(ws + P->off_grid);
+  pa.n_grid = P->n_grid;
+  launch_prep(pa, stream);
+
+  auto img_buf = [&](int id) -> uint8_t* {
+    switch (id) {
+      case B_IN: return const_cast<uint8_t*>(img_in);
+      case B_OUT: return img_out;
+      case B_WS0: return ws + P->off_buf[0];
+      case B_WS1: return ws + P->off_buf[1];
+      default: return nullptr;
+    }
+  };
+  auto mask_buf = [&](int id) -> uint8_t* {
+    switch (id) {
+      case B_IN: return const_cast<uint8_t*>(mask_in);
+      case B_OUT: return mask_out;
+      case B_WS0: return ws + P->off_mbuf[0];
+      case B_WS1: return ws + P->off_mbuf[1];
+      default: return nullptr;
+    }
+  };
+
+  for (const PlanStep& st : P->steps) {
+    StepArgs a{};
+    a.src = img_buf(st.src);
+    a.sdesc = st.src_l ? st.src_l->d : nullptr;
+    a.dst = img_buf(st.dst);
+    a.ddesc = st.dst_l ? st.dst_l->d : nullptr;
+    a.nchw = st.normalize ? out_nchw : nullptr;
+    a.out_h = P->out_h;
+    a.out_w = P->out_w;
+    a.msrc = st.has_mask ? mask_buf(st.msrc) : nullptr;
+    a.msdesc = st.has_mask ? st.msrc_l->d : nullptr;
+    a.mdst = st.has_mask ? mask_buf(st.mdst) : nullptr;
+    a.mddesc = st.has_mask ? st.mdst_l->d : nullptr;
+    a.units = P->d_units + st.units_off + st.ustart[i0];
+    a.n_units = st.ustart[i1] - st.ustart[i0];
+    a.unit_size = st.unit_size;
+    a.unit_rows = st.unit_rows;
+    a.slot0 = st.slot0;
+    a.slot1 = st.slot1;
+    a.n_stages = (int)st.stages.size();
+    for (int s = 0; s < a.n_stages; ++s) a.stages[s] = st.stages[s];
+    a.normalize = st.normalize ? 1 : 0;
+    a.flat = st.flat ? 1 : 0;
+    a.fill = st.fill;
+    a.mask_fill = st.mask_fill;
+    a.interp = st.interp;
+    a.border = st.border;
+    a.min_scale = st.min_scale;
+    a.tab = tab;
+    a.ops = P->d_ops;
+    a.geo = ws + P->off_geo;
+    a.img0 = i0;
+    a.n_img = i1;
+    a.rs_ring = st.rs_ring;
+    a.rs_sw = st.rs_sw;
+    a.rs_hw = st.rs_hw;
+    a.seed = seed;
+    a.first_image = (uint32_t)first_image_index;
+    a.gauss = P->d_gauss ? P->d_gauss + st.g_off : nullptr;
+    a.g_r = st.g_r;
+    a.alpha = st.alpha;
+    switch (st.kind) {
+      case SK_ROW:
+        if (st.has_image) {
+          a.channels = 3;
+          launch_rowgather(a, stream);
+        }
+        if (st.has_mask) {
+          a.channels = 1;
+          a.units = P->d_units + st.munits_off + st.mstart[i0];
+          a.n_units = st.mstart[i1] - st.mstart[i0];
+          a.unit_size = st.munit_size;
+          launch_rowgather(a, stream);
+        }
+        break;
+      case SK_POINT: {
+        // 16-byte co-alignment of source and destination segments
+        bool vec = true;
+        if (a.dst) {
+          for (int i = 0; i < P->n && vec; ++i) {
+            const uintptr_t s = (uintptr_t)a.src + st.src_l->h[i].offset;
+            const uintptr_t d = (uintptr_t)a.dst + st.dst_l->h[i].offset;
+            vec = ((s ^ d) & 15) == 0 && (st.flat || ((st.src_l->h[i].pitch - st.dst_l->h[i].pitch) % 16) == 0);
+          }
+        }
+        a.vec_ok = vec ? 1 : 0;
+        launch_point(a, stream);
+        break;
+      }
+      case SK_RESAMPLE: launch_resample(a, stream); break;
+      case SK_AFFINE: launch_affine(a, stream); break;
+      case SK_ELASTIC: launch_elastic(a, stream); break;
+      case SK_D4:
+        if (st.has_image) {
+          a.channels = 3;
+          launch_d4(a, stream);
+        }
+        if (st.has_mask) {
+          a.channels = 1;
+          a.units = P->d_units + st.munits_off + st.mstart[i0];
+          a.n_units = st.mstart[i1] - st.mstart[i0];
+          launch_d4(a, stream);
+        }
+        break;
+      case SK_EQ: {
+        EqArgs e{};
+        e.src = a.src;
+        e.sdesc = a.sdesc;
+        e.hist = (uint32_t*)(ws + P->off_eqh);
+        e.lut = ws + P->off_eql;
+        e.units = a.units;
+        e.n_units = a.n_units;
+        e.unit_size = st.flat ? st.unit_size : 0;
+        e.n = i1 - i0;
+        e.img0 = i0;
+        e.slot = st.eq_slot;
+        e.tab = tab;
+        CUDA_TRY(cudaMemsetAsync(e.hist + (size_t)i0 * 768, 0, (size_t)(i1 - i0) * 768 * sizeof(uint32_t), stream));
+        launch_eq_hist(e, stream);
+        launch_eq_lut(e, stream);
+        break;
+      }
+    }
+  }
+  if (P->max_boxes > 0) {  // (boxes only on full-range launches)
+    BoxArgs b{};
+    b.boxes_in = boxes_in;
+    b.labels_in = labels_in;
+    b.count_in = count_in;
+    b.boxes_out = boxes_out;
+    b.labels_out = labels_out;
+    b.count_out = count_out;
+    b.max_boxes = P->max_boxes;
+    b.min_visibility = P->min_vis;
+    b.n = P->n;
+    b.tab = tab;
+    b.ops = P->d_ops;
+    launch_boxes(b, stream);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ALB_E_CUDA, std::string("launch failed: ") + cudaGetErrorString(e));
+  return ALB_OK;
+}
 
 namespace alb {
 alb_status set_error(alb_status s, const std::string& msg) { return fail(s, msg); }
@@ -730,6 +924,18 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
     }
     total_units += st.units.size() + st.munits.size();
   }
+  // units are generated image by image: image i owns [ustart[i], ustart[i+1])
+  for (auto& st : steps) {
+    for (int pass = 0; pass < 2; ++pass) {
+      const std::vector<int2>& u = pass ? st.munits : st.units;
+      std::vector<int>& start = pass ? st.mstart : st.ustart;
+      start.assign(P->n + 1, (int)u.size());
+      for (int k = (int)u.size() - 1; k >= 0; --k) start[u[k].x] = k;
+      for (int i = P->n - 1; i >= 0; --i) start[i] = std::min(start[i], start[i + 1]);
+      for (size_t k = 1; k < u.size(); ++k)
+        if (u[k].x < u[k - 1].x) return fail(ALB_E_CUDA, "internal: units not image-major");
+    }
+  }
   if (total_units) {
     std::vector<int2> all;
     all.reserve(total_units);
@@ -822,180 +1028,9 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
     return fail(ALB_E_INVALID_ARG, "img_in and out_nchw overlap");
   if (P->min && overlap(mask_in, P->min->span, mask_out, P->mout->span))
     return fail(ALB_E_INVALID_ARG, "mask_in and mask_out overlap");
-  cudaStream_t stream = (cudaStream_t)stream_;
-  uint8_t* ws = (uint8_t*)workspace;
-  const int n_ops = (int)P->ops.size();
-
-  Tables tab{};
-  tab.params = (const double*)(ws + P->off_params);
-  tab.fired = ws + P->off_fired;
-  tab.dims = (const int32_t*)(ws + P->off_dims);
-  tab.luts = ws + P->off_luts;
-  tab.norm_lut = (const float*)(ws + P->off_norm);
-  tab.eq_luts = ws + P->off_eql;
-  tab.n_ops = n_ops;
-  tab.n_luts = P->n_luts;
-  tab.grid = (const double*)(ws + P->off_grid);
-  tab.n_grid = P->n_grid;
-
-  PrepArgs pa{};
-  pa.ops = P->d_ops;
-  pa.n_ops = n_ops;
-  pa.n = P->n;
-  pa.seed = seed;
-  pa.first_image = (uint32_t)first_image_index;
-  pa.in_desc = P->in->d;
-  pa.params = (double*)(ws + P->off_params);
-  pa.fired = ws + P->off_fired;
-  pa.dims = (int32_t*)(ws + P->off_dims);
-  pa.luts = ws + P->off_luts;
-  pa.n_luts = P->n_luts;
-  for (int s = 0; s < P->n_luts; ++s) { pa.lut_k0[s] = P->lut_k0[s]; pa.lut_k1[s] = P->lut_k1[s]; }
-  pa.norm_lut = (float*)(ws + P->off_norm);
-  pa.norm_slot = P->norm_slot;
-  pa.grid = (double*)(ws + P->off_grid);
-  pa.n_grid = P->n_grid;
-  launch_prep(pa, stream);
-
-  auto img_buf = [&](int id) -> uint8_t* {
-    switch (id) {
-      case B_IN: return const_cast<uint8_t*>(img_in);
-      case B_OUT: return img_out;
-      case B_WS0: return ws + P->off_buf[0];
-      case B_WS1: return ws + P->off_buf[1];
-      default: return nullptr;
-    }
-  };
-  auto mask_buf = [&](int id) -> uint8_t* {
-    switch (id) {
-      case B_IN: return const_cast<uint8_t*>(mask_in);
-      case B_OUT: return mask_out;
-      case B_WS0: return ws + P->off_mbuf[0];
-      case B_WS1: return ws + P->off_mbuf[1];
-      default: return nullptr;
-    }
-  };
-
-  for (const PlanStep& st : P->steps) {
-    StepArgs a{};
-    a.src = img_buf(st.src);
-    a.sdesc = st.src_l ? st.src_l->d : nullptr;
-    a.dst = img_buf(st.dst);
-    a.ddesc = st.dst_l ? st.dst_l->d : nullptr;
-    a.nchw = st.normalize ? out_nchw : nullptr;
-    a.out_h = P->out_h;
-    a.out_w = P->out_w;
-    a.msrc = st.has_mask ? mask_buf(st.msrc) : nullptr;
-    a.msdesc = st.has_mask ? st.msrc_l->d : nullptr;
-    a.mdst = st.has_mask ? mask_buf(st.mdst) : nullptr;
-    a.mddesc = st.has_mask ? st.mdst_l->d : nullptr;
-    a.units = P->d_units + st.units_off;
-    a.n_units = (int)st.units.size();
-    a.unit_size = st.unit_size;
-    a.unit_rows = st.unit_rows;
-    a.slot0 = st.slot0;
-    a.slot1 = st.slot1;
-    a.n_stages = (int)st.stages.size();
-    for (int s = 0; s < a.n_stages; ++s) a.stages[s] = st.stages[s];
-    a.normalize = st.normalize ? 1 : 0;
-    a.flat = st.flat ? 1 : 0;
-    a.fill = st.fill;
-    a.mask_fill = st.mask_fill;
-    a.interp = st.interp;
-    a.border = st.border;
-    a.min_scale = st.min_scale;
-    a.tab = tab;
-    a.ops = P->d_ops;
-    a.geo = ws + P->off_geo;
-    a.n_img = P->n;
-    a.rs_ring = st.rs_ring;
-    a.rs_sw = st.rs_sw;
-    a.rs_hw = st.rs_hw;
-    a.seed = seed;
-    a.first_image = (uint32_t)first_image_index;
-    a.gauss = P->d_gauss ? P->d_gauss + st.g_off : nullptr;
-    a.g_r = st.g_r;
-    a.alpha = st.alpha;
-    switch (st.kind) {
-      case SK_ROW:
-        if (st.has_image) {
-          a.channels = 3;
-          launch_rowgather(a, stream);
-        }
-        if (st.has_mask) {
-          a.channels = 1;
-          a.units = P->d_units + st.munits_off;
-          a.n_units = (int)st.munits.size();
-          a.unit_size = st.munit_size;
-          launch_rowgather(a, stream);
-        }
-        break;
-      case SK_POINT: {
-        // 16-byte co-alignment of source and destination segments
-        bool vec = true;
-        if (a.dst) {
-          for (int i = 0; i < P->n && vec; ++i) {
-            const uintptr_t s = (uintptr_t)a.src + st.src_l->h[i].offset;
-            const uintptr_t d = (uintptr_t)a.dst + st.dst_l->h[i].offset;
-            vec = ((s ^ d) & 15) == 0 && (st.flat || ((st.src_l->h[i].pitch - st.dst_l->h[i].pitch) % 16) == 0);
-          }
-        }
-        a.vec_ok = vec ? 1 : 0;
-        launch_point(a, stream);
-        break;
-      }
-      case SK_RESAMPLE: launch_resample(a, stream); break;
-      case SK_AFFINE: launch_affine(a, stream); break;
-      case SK_ELASTIC: launch_elastic(a, stream); break;
-      case SK_D4:
-        if (st.has_image) {
-          a.channels = 3;
-          launch_d4(a, stream);
-        }
-        if (st.has_mask) {
-          a.channels = 1;
-          a.units = P->d_units + st.munits_off;
-          a.n_units = (int)st.munits.size();
-          launch_d4(a, stream);
-        }
-        break;
-      case SK_EQ: {
-        EqArgs e{};
-        e.src = a.src;
-        e.sdesc = a.sdesc;
-        e.hist = (uint32_t*)(ws + P->off_eqh);
-        e.lut = ws + P->off_eql;
-        e.units = a.units;
-        e.n_units = a.n_units;
-        e.unit_size = st.flat ? st.unit_size : 0;
-        e.n = P->n;
-        e.slot = st.eq_slot;
-        e.tab = tab;
-        CUDA_TRY(cudaMemsetAsync(e.hist, 0, (size_t)P->n * 768 * sizeof(uint32_t), stream));
-        launch_eq_hist(e, stream);
-        launch_eq_lut(e, stream);
-        break;
-      }
-    }
-  }
-  if (P->max_boxes > 0) {
-    BoxArgs b{};
-    b.boxes_in = boxes_in;
-    b.labels_in = labels_in;
-    b.count_in = count_in;
-    b.boxes_out = boxes_out;
-    b.labels_out = labels_out;
-    b.count_out = count_out;
-    b.max_boxes = P->max_boxes;
-    b.min_visibility = P->min_vis;
-    b.n = P->n;
-    b.tab = tab;
-    b.ops = P->d_ops;
-    launch_boxes(b, stream);
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(ALB_E_CUDA, std::string("launch failed: ") + cudaGetErrorString(e));
-  return ALB_OK;
+  return launch_range(P, seed, first_image_index, img_in, img_out, out_nchw, mask_in, mask_out, boxes_in,
+                      labels_in, count_in, boxes_out, labels_out, count_out, (uint8_t*)workspace, 0, P->n,
+                      (cudaStream_t)stream_);
 }
 
 alb_status alb_apply_host(const alb_plan* P, uint64_t seed, uint64_t first_image_index,
@@ -1006,15 +1041,75 @@ alb_status alb_apply_host(const alb_plan* P, uint64_t seed, uint64_t first_image
   if (P->min || P->max_boxes > 0) return fail(ALB_E_UNSUPPORTED, "alb_apply_host carries images only");
   if (in_bytes < P->in->span) return fail(ALB_E_INVALID_ARG, "in_bytes smaller than the input layout");
   const bool ends_norm = P->norm_slot >= 0;
-  const size_t need = ends_norm ? (size_t)P->n * 3 * P->out_h * P->out_w * 4 : P->out->span;
+  const size_t nchw_img = (size_t)3 * P->out_h * P->out_w * 4;
+  const size_t need = ends_norm ? (size_t)P->n * nchw_img : P->out->span;
   if (out_bytes < need) return fail(ALB_E_INVALID_ARG, "out_bytes smaller than the output");
   cudaStream_t stream = (cudaStream_t)stream_;
-  CUDA_TRY(cudaMemcpyAsync(dev_in, host_in, in_bytes, cudaMemcpyHostToDevice, stream));
-  alb_status s = alb_apply(P, seed, first_image_index, dev_in, ends_norm ? nullptr : (uint8_t*)dev_out,
-                           ends_norm ? (float*)dev_out : nullptr, nullptr, nullptr, nullptr, nullptr,
-                           nullptr, nullptr, nullptr, nullptr, workspace, workspace_bytes, stream_);
-  if (s) return s;
-  CUDA_TRY(cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, stream));
+  // chunk boundaries: images in layout order with increasing, disjoint byte
+  // ranges can be copied chunk by chunk, so that the H2D copy of chunk k+1,
+  // the kernels of chunk k and the D2H copy of chunk k-1 overlap (two copy
+  // engines + the SMs); otherwise one chunk (copy, kernels, copy)
+  auto ends_in = [&](int i) {
+    const alb_image_desc& d = P->in->h[i];
+    return (size_t)d.offset + (size_t)(d.height - 1) * d.pitch + (size_t)d.width * 3;
+  };
+  auto ends_out = [&](int i) {
+    if (ends_norm) return (size_t)(i + 1) * nchw_img;
+    const alb_image_desc& d = P->out->h[i];
+    return (size_t)d.offset + (size_t)(d.height - 1) * d.pitch + (size_t)d.width * 3;
+  };
+  auto start_out = [&](int i) { return ends_norm ? (size_t)i * nchw_img : (size_t)P->out->h[i].offset; };
+  bool mono = P->n >= 2;
+  for (int i = 1; i < P->n && mono; ++i)
+    mono = (size_t)P->in->h[i].offset >= ends_in(i - 1) && start_out(i) >= ends_out(i - 1);
+  const int K = mono ? std::min(P->n, 16) : 1;
+  if (K > 1 && !P->s_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
+  }
+  while ((int)P->ev.size() < 2 * K + 2) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    P->ev.push_back(e);
+  }
+  uint8_t* ws = (uint8_t*)workspace;
+  if (!ws || workspace_bytes < P->ws_bytes) return fail(ALB_E_WORKSPACE, "workspace too small");
+  if (((uintptr_t)ws & 255) != 0) return fail(ALB_E_WORKSPACE, "workspace must be 256-byte aligned");
+  if (first_image_index + (uint64_t)P->n > (1ull << 32)) return fail(ALB_E_INVALID_ARG, "image index >= 2^32");
+  uint8_t* dout = ends_norm ? nullptr : (uint8_t*)dev_out;
+  float* dnchw = ends_norm ? (float*)dev_out : nullptr;
+  if (K == 1) {
+    CUDA_TRY(cudaMemcpyAsync(dev_in, host_in, in_bytes, cudaMemcpyHostToDevice, stream));
+    alb_status s = launch_range(P, seed, first_image_index, dev_in, dout, dnchw, nullptr, nullptr, nullptr,
+                                nullptr, nullptr, nullptr, nullptr, nullptr, ws, 0, P->n, stream);
+    if (s) return s;
+    CUDA_TRY(cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, stream));
+    return ALB_OK;
+  }
+  cudaEvent_t ev_start = P->ev[2 * K], ev_done = P->ev[2 * K + 1];
+  CUDA_TRY(cudaEventRecord(ev_start, stream));  // everything earlier on the caller's stream first
+  CUDA_TRY(cudaStreamWaitEvent(P->s_in, ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(P->s_out, ev_start, 0));
+  size_t in_pos = 0, out_pos = 0;
+  for (int k = 0; k < K; ++k) {
+    const int i0 = (int)((long long)P->n * k / K), i1 = (int)((long long)P->n * (k + 1) / K);
+    const size_t in_end = k == K - 1 ? in_bytes : (size_t)P->in->h[i1].offset;
+    const size_t out_end = k == K - 1 ? out_bytes : start_out(i1);
+    CUDA_TRY(cudaMemcpyAsync(dev_in + in_pos, host_in + in_pos, in_end - in_pos, cudaMemcpyHostToDevice, P->s_in));
+    CUDA_TRY(cudaEventRecord(P->ev[2 * k], P->s_in));
+    CUDA_TRY(cudaStreamWaitEvent(stream, P->ev[2 * k], 0));
+    alb_status s = launch_range(P, seed, first_image_index, dev_in, dout, dnchw, nullptr, nullptr, nullptr,
+                                nullptr, nullptr, nullptr, nullptr, nullptr, ws, i0, i1, stream);
+    if (s) return s;
+    CUDA_TRY(cudaEventRecord(P->ev[2 * k + 1], stream));
+    CUDA_TRY(cudaStreamWaitEvent(P->s_out, P->ev[2 * k + 1], 0));
+    CUDA_TRY(cudaMemcpyAsync((uint8_t*)host_out + out_pos, (uint8_t*)dev_out + out_pos, out_end - out_pos,
+                             cudaMemcpyDeviceToHost, P->s_out));
+    in_pos = in_end;
+    out_pos = out_end;
+  }
+  CUDA_TRY(cudaEventRecord(ev_done, P->s_out));
+  CUDA_TRY(cudaStreamWaitEvent(stream, ev_done, 0));  // the caller's stream sees the whole result
   return ALB_OK;
 }
 

@@ -491,7 +491,7 @@ constexpr int kPSmem = kPOffStage + kPStageWords * 4;
 // Per-image state of the affine step (one thread per image), read by the
 // producer warp whenever a tile starts a new image.
 __global__ void k_affine_setup(StepArgs a) {
-  const int img = blockIdx.x * blockDim.x + threadIdx.x;
+  const int img = a.img0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (img >= a.n_img) return;
   const AfCoef cf = af_coef(a, img);
   ImgState s;
@@ -925,7 +925,7 @@ static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
 
 void launch_affine(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
-  k_affine_setup<<<(a.n_img + 127) / 128, 128, 0, s>>>(a);  // per-image state for both kernels
+  k_affine_setup<<<(a.n_img - a.img0 + 127) / 128, 128, 0, s>>>(a);  // per-image state for both kernels
   const size_t smem = affine_smem(a);
   const int mode = stage_mode(a);
   ALB_DISPATCH_STAGES(mode, launch_affine_t, a, smem, s)

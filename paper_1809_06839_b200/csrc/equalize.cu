@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kEqThreads) k_eq_hist(EqArgs a) {
 }
 
 __global__ void __launch_bounds__(256) k_eq_lut(EqArgs a) {
-  const int img = blockIdx.x;
+  const int img = a.img0 + blockIdx.x;
   const int v = threadIdx.x;
   __shared__ uint32_t sc[256];
   __shared__ uint32_t s_cmin;

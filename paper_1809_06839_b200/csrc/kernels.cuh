@@ -23,6 +23,7 @@ struct PrepArgs {
   int32_t lut_k0[kMaxLuts], lut_k1[kMaxLuts];
   float* norm_lut;
   int32_t norm_slot;
+  int32_t img0;       // first image of this launch (CTA i -> image img0 + i)
   double* grid;       // [n][n_grid][kGridStride] (reading R31)
   int32_t n_grid;
 };
@@ -58,7 +59,7 @@ struct StepArgs {
   Tables tab;
   const alb_op* ops;
   void* geo;  // workspace scratch: per-image affine state, kGeoBytes each
-  int32_t n_img;  // images in the batch
+  int32_t img0, n_img;  // image range [img0, n_img) of this launch (per-image kernels)
   int32_t rs_ring, rs_sw, rs_hw;  // separable resample: ring rows (0 = old kernel), staged row
                                    // stride (words), output rows per group
   uint64_t seed;                   // Philox key of this apply (ElasticTransform raw planes)
@@ -90,6 +91,7 @@ struct EqArgs {
   int32_t n_units;
   int32_t unit_size;
   int32_t n;
+  int32_t img0;       // k_eq_lut: CTA i -> image img0 + i
   int32_t slot;
   Tables tab;
 };

@@ -39,7 +39,7 @@ __device__ void grid_knots(const alb_op& o, uint64_t seed, uint32_t gi, int k, i
 }
 
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
-  const int i = blockIdx.x;
+  const int i = a.img0 + blockIdx.x;
   __shared__ double s_prm[kMaxOps][kMaxParams];
   __shared__ uint8_t s_fired[kMaxOps];
   if (threadIdx.x == 0) {
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
       a.luts[((size_t)i * a.n_luts + s) * 768 + c * 256 + v] = (uint8_t)x;
     }
   }
-  if (a.norm_slot >= 0 && i == 0) {
+  if (a.norm_slot >= 0 && blockIdx.x == 0) {  // per plan; every launch writes the same values
     const alb_op& o = a.ops[a.norm_slot];
     for (int c = 0; c < 3; ++c)
       a.norm_lut[c * 256 + v] =
