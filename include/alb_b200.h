@@ -188,9 +188,15 @@ alb_status alb_apply(const alb_plan* plan, uint64_t seed, uint64_t first_image_i
 
 /* End-to-end variant with HOST buffers (pinned for async copies): copies the
  * input batch host->device into dev_in, applies, copies the output
- * device->host, all enqueued on `stream` (no sync).  in_bytes / out_bytes are
- * the flat buffer sizes of the batch buffers (layout offsets index into them).
- * Masks and boxes are not carried by this entry point. */
+ * device->host (no sync).  in_bytes / out_bytes are the flat buffer sizes of
+ * the batch buffers (layout offsets index into them).  When the layouts'
+ * images lie in increasing, disjoint byte ranges the batch runs as up to 16
+ * image chunks: H2D copies on a plan-owned stream, the kernels of each chunk
+ * on `stream`, D2H copies on a second plan-owned stream, chained by events, so
+ * copies in both directions overlap the kernels; the work is ordered after
+ * everything earlier on `stream` and everything later on `stream` sees the
+ * host output complete.  One alb_apply_host per plan at a time.  Masks and
+ * boxes are not carried by this entry point (ALB_E_UNSUPPORTED). */
 alb_status alb_apply_host(const alb_plan* plan, uint64_t seed, uint64_t first_image_index,
                           const uint8_t* host_in, size_t in_bytes, uint8_t* dev_in,
                           void* host_out, size_t out_bytes, void* dev_out,
