@@ -397,6 +397,11 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.alpha = st.alpha;
     switch (st.kind) {
       case SK_ROW:
+        a.rg_wide = 0;
+        for (int k = st.slot0; k < st.slot1; ++k) {
+          const int kd = P->ops[k].kind;
+          a.rg_wide |= kd == ALB_PAD_TO_SIZE || kd == ALB_CROP || kd == ALB_RANDOM_CROP;
+        }
         if (st.has_image) {
           a.channels = 3;
           launch_rowgather(a, stream);

@@ -253,6 +253,23 @@ __device__ __forceinline__ void load_window(const uint8_t* __restrict__ p, const
   for (int i = 0; i < NW; ++i) w[i] = __funnelshift_r(t2[i], t2[i + 1], kb);
 }
 
+// 256-bit streaming global accesses (sm_100: LDG/STG.E.EF.ENL2.256), 32-byte aligned
+__device__ __forceinline__ void ld256_cs(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.cs.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_nc(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st256_cs(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+               "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* w, int j) {
   return (w[j >> 2] >> ((j & 3) * 8)) & 0xffu;
 }
