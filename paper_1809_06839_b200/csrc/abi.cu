@@ -460,7 +460,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
         e.lut = ws + P->off_eql;
         e.units = a.units;
         e.n_units = a.n_units;
-        e.unit_size = st.flat ? st.unit_size : 0;
+        e.unit_size = st.flat ? -1 : 0;  // -1: whole flat images (k_eq_hist_lane)
         e.n = i1 - i0;
         e.img0 = i0;
         e.slot = st.eq_slot;
@@ -839,7 +839,8 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
         // images; persistent CTAs over 24 KB chunks were slower still)
         bool lut_only = !st.normalize && !st.stages.empty();
         for (auto& sg : st.stages) lut_only = lut_only && (sg.type == ST_LUT || sg.type == ST_EQ);
-        const int chunk = st.kind == SK_EQ ? 4 * kChunk : (lut_only ? kLutChunk : kPxChunk);
+        // Equalize on flat images: one whole-image unit (lane-private histogram kernel)
+        const int chunk = st.kind == SK_EQ ? (flat ? (1 << 30) : 4 * kChunk) : (lut_only ? kLutChunk : kPxChunk);
         st.unit_size = chunk;
         for (int i = 0; i < P->n; ++i) {
           if (flat) {

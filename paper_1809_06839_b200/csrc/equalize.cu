@@ -106,8 +106,68 @@ __global__ void __launch_bounds__(256) k_eq_lut(EqArgs a) {
   }
 }
 
+// Whole-image variant (flat images, one CTA of 1024 threads per image): lane-
+// private histograms hl[bin][lane] (96 KB), so the 32 atomics of one warp
+// instruction always hit 32 different banks (the warp-private layout above
+// lets equal-bank bins collide: ~4 shared wavefronts per atomic).  The 32
+// lanes' counts are summed with a rotated read order (conflict-free) and
+// stored: the CTA owns the image's whole histogram.
+constexpr int kEqLThreads = 1024;
+constexpr size_t kEqLSmem = 768 * 32 * sizeof(uint32_t);
+
+__global__ void __launch_bounds__(kEqLThreads) k_eq_hist_lane(EqArgs a) {
+  extern __shared__ uint32_t hl[];  // [768][32]
+  const int img = a.units[blockIdx.x].x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < 768 * 32; i += kEqLThreads) hl[i] = 0;
+  __syncthreads();
+  const alb_image_desc sd = a.sdesc[img];
+  const uint8_t* src = a.src + sd.offset;
+  const int n = sd.height * sd.width * 3;
+  uint32_t* hw = hl + lane;
+  int bA = (int)((16 - ((uintptr_t)src & 15)) & 15);
+  if (bA > n) bA = n;
+  const int bE = bA + ((n - bA) / 16) * 16;
+  for (int b = tid; b < bA; b += kEqLThreads) atomicAdd(&hw[((b % 3) * 256 + src[b]) * 32], 1u);
+  for (int b = bE + tid; b < n; b += kEqLThreads) atomicAdd(&hw[((b % 3) * 256 + src[b]) * 32], 1u);
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + bA);
+  const int nv = (bE - bA) / 16;
+  for (int v0 = tid; v0 < nv; v0 += 2 * kEqLThreads) {
+    uint4 t[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (v0 + k * kEqLThreads < nv) t[k] = __ldcs(s4 + v0 + k * kEqLThreads);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int v = v0 + k * kEqLThreads;
+      if (v >= nv) break;
+      const uint32_t w[4] = {t[k].x, t[k].y, t[k].z, t[k].w};
+      const int ph = (bA + 16 * v) % 3;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        int c = ph + (j % 3);
+        c = c >= 3 ? c - 3 : c;
+        atomicAdd(&hw[(c * 256 + ((w[j >> 2] >> ((j & 3) * 8)) & 0xffu)) * 32], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < 768; i += kEqLThreads) {
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) sum += hl[i * 32 + ((l + i) & 31)];
+    a.hist[(size_t)img * 768 + i] = sum;
+  }
+}
+
 void launch_eq_hist(const EqArgs& a, cudaStream_t s) {
-  if (a.n_units > 0) k_eq_hist<<<a.n_units, kEqThreads, 0, s>>>(a);
+  if (a.n_units <= 0) return;
+  if (a.unit_size == -1) {  // flat images, one unit per image
+    persistent_grid((const void*)k_eq_hist_lane, kEqLThreads, kEqLSmem, a.n_units);  // smem attribute
+    k_eq_hist_lane<<<a.n_units, kEqLThreads, kEqLSmem, s>>>(a);
+  } else {
+    k_eq_hist<<<a.n_units, kEqThreads, 0, s>>>(a);
+  }
 }
 void launch_eq_lut(const EqArgs& a, cudaStream_t s) {
   if (a.n > 0) k_eq_lut<<<a.n, 256, 0, s>>>(a);
