@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
 // pixel-wise chain (HSV / gray / mixed / Normalize output); kNorm is
 // compile-time so the unused output path is not issued per pixel
 template <int kOne, bool kNorm>
-__global__ void __launch_bounds__(kThreads) k_point_px(StepArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_point_px(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31;
   StageCtx x;
