@@ -91,7 +91,7 @@ __device__ __forceinline__ void load_window32(const uint8_t* __restrict__ p, con
 // launches); the per-image integer map is composed once per image change.  Item = (row, 16-pixel block whose first
 // destination byte is 16-byte aligned and on a pixel boundary).
 template <int C, int NPX>
-__global__ void __launch_bounds__(kRgThreads) k_rowgather(StepArgs a, uint32_t fill) {
+__global__ void __launch_bounds__(kRgThreads, 6) k_rowgather(StepArgs a, uint32_t fill) {
   constexpr int NW = NPX * C / 4, AL = NPX == 32 ? 32 : 16;  // words per item, store alignment
   __shared__ Map1 smap;
   int u0, u1;
