@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -13,13 +14,15 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
+OBJ_ROOT = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libalb_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")] + \
     os.environ.get("ALB_NVCC_FLAGS", "").split()  # e.g. -DALB_PROF (phase timing printouts)
+# objects live in a directory per flag set, so changing ALB_NVCC_FLAGS rebuilds
+OBJ = os.path.join(OBJ_ROOT, hashlib.sha1(" ".join(ARCH + FLAGS).encode()).hexdigest()[:12])
 
 
 def _deps():
@@ -48,13 +51,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, log in res:
             if log:
                 sys.stderr.write(log)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+    stamp = os.path.join(OBJ_ROOT, "linked_from")  # which object set the library holds
+    same_set = os.path.exists(stamp) and open(stamp).read() == OBJ
+    if (force or not same_set or not os.path.exists(LIB)
+            or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)):
         tmp = LIB + ".tmp%d" % os.getpid()
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
         os.replace(tmp, LIB)
+        with open(stamp, "w") as f:
+            f.write(OBJ)
     return LIB
 
 
