@@ -96,9 +96,11 @@ __device__ __forceinline__ void apply_stages(const StageCtx& x, const uint32_t* 
   }
 }
 
-// Compile-time stage program: kOne = -2 no stages, -1 generic chain, or the
-// type of the single stage (its LUT, if any, sits at shared word 0).
-constexpr int kStagesNone = -2, kStagesGeneric = -1;
+// Compile-time stage program: kOne = -2 no stages, -1 generic chain, the
+// type of the single stage (its LUT, if any, sits at shared word 0), or one of
+// the two-stage programs HSV -> LUT (cfg4's ShiftHSV -> BrightnessContrast) and
+// LUT -> HSV (the single LUT sits at shared word 0 in both).
+constexpr int kStagesNone = -2, kStagesGeneric = -1, kStagesHsvLut = 10, kStagesLutHsv = 11;
 
 template <int kOne>
 __device__ __forceinline__ void apply_stages_t(const StageCtx& x, const uint32_t* sm, int lane,
@@ -116,6 +118,16 @@ __device__ __forceinline__ void apply_stages_t(const StageCtx& x, const uint32_t
       const uint32_t y = gray_px(r, g, b);
       r = g = b = y;
     }
+  } else if constexpr (kOne == kStagesHsvLut) {
+    if (x.on[0]) hsv_shift_px(x.dh[0], x.ds[0], x.dv[0], r, g, b);
+    r = lut_look(sm, 0, r, lane);
+    g = lut_look(sm, 2048, g, lane);
+    b = lut_look(sm, 4096, b, lane);
+  } else if constexpr (kOne == kStagesLutHsv) {
+    r = lut_look(sm, 0, r, lane);
+    g = lut_look(sm, 2048, g, lane);
+    b = lut_look(sm, 4096, b, lane);
+    if (x.on[1]) hsv_shift_px(x.dh[1], x.ds[1], x.dv[1], r, g, b);
   } else {
     apply_stages(x, sm, lane, r, g, b);
   }
@@ -131,6 +143,22 @@ __device__ __forceinline__ void apply_stages2_t(const StageCtx& x, const uint32_
     return;
   } else if constexpr (kOne == ST_HSV) {
     if (x.on[0]) hsv_shift_px2(x.dh[0], x.ds[0], x.dv[0], r, g, b);
+  } else if constexpr (kOne == kStagesHsvLut) {
+    if (x.on[0]) hsv_shift_px2(x.dh[0], x.ds[0], x.dv[0], r, g, b);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      r[h] = lut_look(sm, 0, r[h], lane);
+      g[h] = lut_look(sm, 2048, g[h], lane);
+      b[h] = lut_look(sm, 4096, b[h], lane);
+    }
+  } else if constexpr (kOne == kStagesLutHsv) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      r[h] = lut_look(sm, 0, r[h], lane);
+      g[h] = lut_look(sm, 2048, g[h], lane);
+      b[h] = lut_look(sm, 4096, b[h], lane);
+    }
+    if (x.on[1]) hsv_shift_px2(x.dh[1], x.ds[1], x.dv[1], r, g, b);
   } else if constexpr (kOne == kStagesGeneric) {
 #pragma unroll
     for (int s = 0; s < kMaxStages; ++s) {
@@ -161,6 +189,12 @@ __device__ __forceinline__ void apply_stages2_t(const StageCtx& x, const uint32_
 inline int stage_mode(const StepArgs& a) {
   if (a.n_stages == 0) return kStagesNone;
   if (a.n_stages == 1) return a.stages[0].type;
+  if (a.n_stages == 2) {
+    const int t0 = a.stages[0].type, t1 = a.stages[1].type;
+    const bool l0 = t0 == ST_LUT || t0 == ST_EQ, l1 = t1 == ST_LUT || t1 == ST_EQ;
+    if (t0 == ST_HSV && l1) return kStagesHsvLut;
+    if (l0 && t1 == ST_HSV) return kStagesLutHsv;
+  }
   return kStagesGeneric;
 }
 
@@ -172,6 +206,8 @@ inline int stage_mode(const StepArgs& a) {
     case ST_EQ: KERNEL<ST_EQ>(__VA_ARGS__); break;              \
     case ST_HSV: KERNEL<ST_HSV>(__VA_ARGS__); break;            \
     case ST_GRAY: KERNEL<ST_GRAY>(__VA_ARGS__); break;          \
+    case kStagesHsvLut: KERNEL<kStagesHsvLut>(__VA_ARGS__); break; \
+    case kStagesLutHsv: KERNEL<kStagesLutHsv>(__VA_ARGS__); break; \
     default: KERNEL<kStagesGeneric>(__VA_ARGS__); break;        \
   }
 
