@@ -998,9 +998,17 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   // launches per apply
   int L = 1;  // prep
   for (auto& st : steps) {
-    if (st.kind == SK_ROW || st.kind == SK_D4) L += (st.has_image ? 1 : 0) + (st.has_mask ? 1 : 0);
-    else if (st.kind == SK_EQ) L += 2;
-    else L += 1;
+    if (st.kind == SK_ROW || st.kind == SK_D4) {
+      L += (st.has_image ? 1 : 0) + (st.has_mask ? 1 : 0);
+    } else if (st.kind == SK_EQ) {
+      L += 2;
+    } else if (st.kind == SK_AFFINE) {  // setup + image kernel (+ label kernel beside the pipelined one)
+      const bool generic = st.interp == ALB_INTERP_NEAREST || st.normalize || st.min_scale < 0.9f ||
+                           st.unit_size < 14040;
+      L += 2 + (st.has_mask && !generic ? 1 : 0);
+    } else {
+      L += 1;
+    }
   }
   if (max_boxes > 0) L += 1;
   P->n_launches = L;

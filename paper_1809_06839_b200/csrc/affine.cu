@@ -890,6 +890,94 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
   }
 }
 
+// Nearest-label mask warp beside the pipelined image kernel (cfg3 / cfg5):
+// the same fp64 cell anchors and fp32 local offsets as the image kernels, so
+// a mask pixel takes the label at its image source coordinate rounded half up
+// -- exactly the decision the fused masked kernel makes.  One
+// CTA per 64 x 64 output tile; labels are read straight from global (1 byte
+// per pixel, L1/L2 resident neighbourhood).
+__global__ void __launch_bounds__(kAfThreads) k_affine_mask(StepArgs a) {
+  const int2 unit = a.units[blockIdx.x];
+  const int img = unit.x;
+  __shared__ ImgState sis;  // per-image state, one word per thread
+  {
+    constexpr int kW = (int)sizeof(ImgState) / 4;
+    if (threadIdx.x < kW)
+      reinterpret_cast<uint32_t*>(&sis)[threadIdx.x] = __ldcg(
+          reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.geo) + (size_t)img * kGeoBytes) +
+          threadIdx.x);
+    __syncthreads();
+  }
+  const ImgState& is = sis;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
+  const int tw = min(kTileW, is.Wo - tx0), th = min(kTileH, is.Ho - ty0);
+  const alb_image_desc msd = a.msdesc[img], mdd = a.mddesc[img];
+  const uint8_t* msrc = a.msrc + msd.offset;
+  uint8_t* mdst = a.mdst + mdd.offset + (size_t)ty0 * mdd.pitch + tx0;
+  const bool reflect = a.border == ALB_BORDER_REFLECT_101;
+  const float2 A14 = make_float2(is.Af[1], is.Af[3]);
+  const int ncol = tw > 32 ? 2 : 1;
+  int xw[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) xw[j] = is.m.ax * min(tx0 + lane + 32 * j, is.Wo - 1) + is.m.bx;
+  // warp w owns the contiguous rows [8w, 8w + 8): at most two cell rows of
+  // fp64 anchors; all 16 label addresses first, then 16 independent loads
+  constexpr int kR = kTileH / (kAfThreads / 32);
+  int cur_cy = -0x7fffffff;
+  float2 bxy[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  int aix[2] = {0, 0}, aiy[2] = {0, 0};
+  int src_off[kR][2];  // label offset in the source mask, or -1 for the fill
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    const int row = warp * kR + i;
+    src_off[i][0] = src_off[i][1] = -1;
+    if (row >= th) continue;
+    const int yw = is.m.ay * (ty0 + row) + is.m.by;
+    if ((yw >> 4) != cur_cy) {
+      cur_cy = yw >> 4;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (j < ncol) {
+          const Anchor an = cell_anchor(is.A, is.Af[0], is.Af[2], xw[j], cur_cy);
+          bxy[j] = make_float2(an.bx, an.by);
+          aix[j] = an.ix;
+          aiy[j] = an.iy;
+        }
+      }
+    }
+    const float dyl = (float)(yw & 15);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float2 l = __ffma2_rn(A14, make_float2(dyl, dyl), bxy[j]);
+      const float2 tq = fadd2_rm(l, make_float2(kMagic15, kMagic15));
+      const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
+      const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
+      const int nx = aix[j] + (int)(__float_as_uint(tq.x) - kMagic15Bits) + (fr.x >= 0.5f ? 1 : 0);
+      const int ny = aiy[j] + (int)(__float_as_uint(tq.y) - kMagic15Bits) + (fr.y >= 0.5f ? 1 : 0);
+      bool ri, ci;
+      const int yy = border_idx(ny, msd.height, reflect, ri);
+      const int xx = border_idx(nx, msd.width, reflect, ci);
+      src_off[i][j] = (ri && ci) ? yy * msd.pitch + xx : -1;
+    }
+  }
+  uint8_t v[kR][2];
+#pragma unroll
+  for (int i = 0; i < kR; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      v[i][j] = src_off[i][j] >= 0 ? __ldg(msrc + src_off[i][j]) : (uint8_t)a.mask_fill;
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    const int row = warp * kR + i;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = lane + 32 * j;
+      if (row < th && j < ncol && c < tw) mdst[(size_t)row * mdd.pitch + c] = v[i][j];
+    }
+  }
+}
+
 static size_t affine_smem(const StepArgs& a) {
   return (size_t)count_lut_stages(a) * kLutWords * 4 + kOffStage + (size_t)a.unit_size * 4 + 16 +
          (a.mdst ? (size_t)(kTileH * kMobPitch + kMStageBytes) : 0);
@@ -911,15 +999,17 @@ static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
   if (generic) {
     if (mask) launch_affine_v<kOne, true, 1>(a, smem, s);
     else launch_affine_v<kOne, false, 1>(a, smem, s);
-  } else if (mask) {
-    launch_affine_v<kOne, true, 0>(a, smem, s);
-  } else {  // pipelined TMA-staged path
+  } else {  // pipelined TMA-staged path; masks (cfg3 / cfg5) through the label kernel beside it
+    StepArgs ai = a;
+    ai.msrc = nullptr;
+    ai.mdst = nullptr;
     const size_t psmem = (size_t)count_lut_stages(a) * kLutWords * 4 + kPSmem;
     // ~16 tiles per CTA: long enough to pipeline, short enough that the
     // hardware re-balances CTAs across SMs (measured: 16 > 8, 32 > persistent)
     const int grid = std::max(persistent_grid((const void*)k_affine_pipe<kOne>, kPThreads, psmem, a.n_units),
                               (a.n_units + 15) / 16);
-    k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(a);
+    k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(ai);
+    if (mask) k_affine_mask<<<a.n_units, kAfThreads, 0, s>>>(a);
   }
 }
 
