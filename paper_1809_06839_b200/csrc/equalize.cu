@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kEqLThreads) k_eq_hist_lane(EqArgs a) {
   const uint8_t* src = a.src + sd.offset;
   const int n = sd.height * sd.width * 3;
   uint32_t* hw = hl + lane;
+  const uint32_t hl_base = (uint32_t)__cvta_generic_to_shared(hl) + 4u * (uint32_t)lane;
   int bA = (int)((16 - ((uintptr_t)src & 15)) & 15);
   if (bA > n) bA = n;
   const int bE = bA + ((n - bA) / 16) * 16;
@@ -143,11 +144,16 @@ __global__ void __launch_bounds__(kEqLThreads) k_eq_hist_lane(EqArgs a) {
       if (v >= nv) break;
       const uint32_t w[4] = {t[k].x, t[k].y, t[k].z, t[k].w};
       const int ph = (bA + 16 * v) % 3;
+      // shared byte address of (channel c, value x, lane) = base_c + 128 x:
+      // one byte extract (PRMT), one IMAD, one RED per byte
+      const uint32_t b0 = hl_base + (uint32_t)ph * 32768u;
+      const uint32_t b1 = hl_base + (uint32_t)(ph == 2 ? 0 : ph + 1) * 32768u;
+      const uint32_t b2 = hl_base + (uint32_t)(ph == 0 ? 2 : ph - 1) * 32768u;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        int c = ph + (j % 3);
-        c = c >= 3 ? c - 3 : c;
-        atomicAdd(&hw[(c * 256 + ((w[j >> 2] >> ((j & 3) * 8)) & 0xffu)) * 32], 1u);
+        const uint32_t cb = (j % 3 == 0) ? b0 : ((j % 3 == 1) ? b1 : b2);
+        const uint32_t x = __byte_perm(w[j >> 2], 0u, 0x4440u + (uint32_t)(j & 3));
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(x * 128u + cb) : "memory");
       }
     }
   }
