@@ -626,3 +626,39 @@ def test_hsv_round_value_shift_differs_only_at_ties():
         val = min(max(val - 0.1, 0.0), 1.0)
         t = A.hsv_to_rgb(h, sat, val)[c]
         assert abs(t - (np.floor(t) + 0.5)) < 1e-3, (y, x, c, t, g[y, x, c], r[y, x, c])
+
+
+def test_apply_host_unordered_layout_single_chunk():
+    """Images laid out in decreasing offset order (not chunkable): alb_apply_host
+    takes the single-copy path and still equals alb_apply."""
+    from paper_1809_06839_b200 import Layout, Pipeline, Plan
+    sizes = gen.cfg2_sizes(9)
+    b = gen.gen_images(sizes, seed=4, first_image_index=0, device="cuda")
+    desc = b.desc.copy()
+    order = np.argsort(-desc[:, 0])  # reverse the byte order of the images
+    desc2 = desc.copy()
+    pos = 0
+    buf2 = torch.zeros_like(b.buf)
+    for i in order:
+        off, h, w, pitch = [int(v) for v in desc[i]]
+        n = h * pitch
+        buf2[pos:pos + n] = b.buf[off:off + n]
+        desc2[i, 0] = pos
+        pos = (pos + n + 255) // 256 * 256
+    b2 = gen.Batch(buf2, desc2, 3)
+    pipe = Pipeline(C.CFG2_MENU["Rotate"])
+    out = out_batch([pipe.output_shape(h, w) for h, w in sizes])
+    plan = Plan(pipe, Layout(b2.desc, 3), Layout(out.desc, 3))
+    ws = plan.workspace()
+    plan.apply(3, 0, b2.buf, out.buf, workspace=ws)
+    torch.cuda.synchronize()
+    want = out.buf.cpu().numpy().copy()
+    host_in = b2.buf.cpu().pin_memory()
+    host_out = torch.zeros(out.buf.shape, dtype=torch.uint8).pin_memory()
+    plan.apply_host(3, 0, host_in, torch.empty_like(b2.buf), host_out, torch.zeros_like(out.buf), ws)
+    torch.cuda.synchronize()
+    for i in range(len(sizes)):
+        off, h, w, pitch = [int(v) for v in out.desc[i]]
+        g = host_out.numpy()[off:off + h * pitch].reshape(h, pitch)[:, :3 * w]
+        r = want[off:off + h * pitch].reshape(h, pitch)[:, :3 * w]
+        assert np.array_equal(g, r), i
