@@ -1060,6 +1060,10 @@ alb_status alb_apply(const alb_plan* P, uint64_t seed, uint64_t first_image_inde
                       (cudaStream_t)stream_);
 }
 
+#ifndef ALB_HOST_CHUNKS
+#define ALB_HOST_CHUNKS 16
+#endif
+
 alb_status alb_apply_host(const alb_plan* P, uint64_t seed, uint64_t first_image_index,
                           const uint8_t* host_in, size_t in_bytes, uint8_t* dev_in,
                           void* host_out, size_t out_bytes, void* dev_out, void* workspace,
@@ -1089,7 +1093,7 @@ alb_status alb_apply_host(const alb_plan* P, uint64_t seed, uint64_t first_image
   bool mono = P->n >= 2;
   for (int i = 1; i < P->n && mono; ++i)
     mono = (size_t)P->in->h[i].offset >= ends_in(i - 1) && start_out(i) >= ends_out(i - 1);
-  const int K = mono ? std::min(P->n, 16) : 1;
+  const int K = mono ? std::min(P->n, ALB_HOST_CHUNKS) : 1;
   if (K > 1 && !P->s_in) {
     CUDA_TRY(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
