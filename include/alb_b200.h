@@ -177,6 +177,10 @@ int32_t alb_plan_num_launches(const alb_plan* plan);
  * global index first_image_index + i (< 2^32).  Boxes: boxes_in [n][max_boxes][4],
  * labels_in [n][max_boxes] or NULL, count_in [n]; outputs likewise (kept
  * boxes compacted stably to the front, count_out = kept count).
+ * Asynchronous on `stream`: it enqueues kernels (and, for Equalize, a
+ * memset of its histogram workspace) and nothing else -- no host
+ * synchronisation, allocation or copy -- so it can be captured into a CUDA
+ * graph and replayed (seed and pointers are baked into the graph).
  * Errors: ALB_E_INVALID_ARG (null required pointer, in/out overlap),
  * ALB_E_WORKSPACE, ALB_E_CUDA (launch failure). */
 alb_status alb_apply(const alb_plan* plan, uint64_t seed, uint64_t first_image_index,

@@ -662,3 +662,36 @@ def test_apply_host_unordered_layout_single_chunk():
         g = host_out.numpy()[off:off + h * pitch].reshape(h, pitch)[:, :3 * w]
         r = want[off:off + h * pitch].reshape(h, pitch)[:, :3 * w]
         assert np.array_equal(g, r), i
+
+
+@pytest.mark.parametrize("name", ["cfg4", "Equalize", "Rotate"])
+def test_apply_captures_into_cuda_graph(name):
+    """alb_apply enqueues kernels (and the Equalize memset) only -- no host
+    synchronisation or allocation -- so a whole apply can be captured into a
+    CUDA graph and replayed; the replay equals the eager result."""
+    from paper_1809_06839_b200 import Layout, Pipeline, Plan
+    specs = C.CFG4_OPS if name == "cfg4" else C.CFG2_MENU[name]
+    sizes = [(375, 500)] * 12 if name == "cfg4" else gen.cfg2_sizes(12)
+    b = gen.gen_images(sizes, seed=5, first_image_index=0, device="cuda")
+    pipe = Pipeline(specs)
+    if name == "cfg4":
+        plan = Plan(pipe, Layout(b.desc, 3), None)
+        out = torch.zeros((len(sizes), 3, 224, 224), device="cuda")
+        kw = dict(img_out=None, out_nchw=out)
+    else:
+        ob = out_batch([pipe.output_shape(h, w) for h, w in sizes])
+        plan = Plan(pipe, Layout(b.desc, 3), Layout(ob.desc, 3))
+        out = ob.buf
+        kw = dict(img_out=out)
+    ws = plan.workspace()
+    plan.apply(9, 0, b.buf, workspace=ws, **kw)
+    torch.cuda.synchronize()
+    want = out.clone()
+    out.fill_(0 if name == "cfg4" else 0xAB)  # gap bytes between images keep the buffer's fill
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.apply(9, 0, b.buf, workspace=ws, stream=s, **kw)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
