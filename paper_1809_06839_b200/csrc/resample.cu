@@ -319,6 +319,11 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
   uint32_t* src = reinterpret_cast<uint32_t*>(mbar + 2);              // [K][SW] RGBx rows
   uint8_t* raw = reinterpret_cast<uint8_t*>(src + ((K * SW + 3) & ~3)) + 64;  // [K][RP] raw rows
   uint8_t* obuf = raw + K * RP + 64;                                  // [G][kSepObp] output rows
+  // kNorm: the 3 x 256 fp32 Normalize LUT in shared memory (in place of the row buffers)
+  float* nls = reinterpret_cast<float*>(obuf);
+  if constexpr (kNorm) {
+    for (int i = threadIdx.x; i < 768; i += kSepThreads) nls[i] = __ldg(a.tab.norm_lut + i);
+  }
   const uint32_t bar = smem_u32(mbar);
   const int R = a.unit_rows;
   const uint32_t mK = magic_of((uint32_t)K);
@@ -552,10 +557,9 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
             if constexpr (kNorm) {
               const size_t plane = (size_t)Ho * Wo;
               float* o = a.nchw + (size_t)img * 3 * plane + (size_t)rw.yo * Wo + xs0 + cb + 32 * q;
-              const float* nl = a.tab.norm_lut;
-              __stcs(o, __ldg(nl + r));
-              __stcs(o + plane, __ldg(nl + 256 + gg));
-              __stcs(o + 2 * plane, __ldg(nl + 512 + b));
+              __stcs(o, nls[r]);
+              __stcs(o + plane, nls[256 + gg]);
+              __stcs(o + 2 * plane, nls[512 + b]);
             } else {
               uint8_t* orow = olane + rw.ob + 96 * q;
               orow[0] = (uint8_t)r;
@@ -576,7 +580,7 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
 size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize) {
   return (size_t)n_lut_stages * kLutWords * 4 + 128 + kSepMaxBand * sizeof(SepRow) + 256 + 16 +
          (size_t)((ring * sw + 3) & ~3) * 4 + 64 + (size_t)ring * sep_raw_pitch(sw) + 64 +
-         (normalize ? 0 : (size_t)g * kSepObp);
+         (normalize ? (size_t)768 * 4 : (size_t)g * kSepObp);
 }
 
 template <int kOne, bool kNorm, int kCols>
