@@ -5,6 +5,7 @@
 from __future__ import annotations
 
 import concurrent.futures as cf
+import fcntl
 import glob
 import hashlib
 import os
@@ -42,7 +43,17 @@ def _compile(src, force):
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    # several processes (e.g. torchrun ranks) may call build() at once: serialise
     os.makedirs(OBJ, exist_ok=True)
+    with open(os.path.join(OBJ_ROOT, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            return _build_locked(force, verbose)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _build_locked(force: bool, verbose: bool) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max(1, min(len(srcs), os.cpu_count() or 4))) as ex:
         res = list(ex.map(lambda s: _compile(s, force), srcs))
