@@ -128,7 +128,8 @@ __device__ __forceinline__ bool fired_of(const Tables& t, int img, int slot) {
 //  * channel n (5, 3, 1 for R, G, B): k = h6 + n in [0, 16) and
 //      c = v - v s sat(2 - min(|k-2|, |k-8|, |k-14|)),
 //    the periodic form of SPEC.md:419's sector table sat(min(k', 4-k')),
-//    k' = k mod 6, so no explicit wrap of the hue is needed;
+//    k' = k mod 6; h6 is moved down one period when >= 5 (exactly), which
+//    leaves k < 10 so the |k-14| term is never the minimum and is dropped;
 //  * out = floor(255 c + 0.5) from the mantissa of a round-down add.
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -149,12 +150,15 @@ __device__ __forceinline__ void hsv_shift_px(float dh6w, float ds, float dv, uin
   const float pa = isr ? Gb : (isg ? Bb : Rb);
   const float pb = isr ? Bb : (isg ? Rb : Gb);
   const float off = isr ? dh6w : (isg ? dh6w + 2.f : dh6w + 4.f);
-  const float h6 = fmaf(pa - pb, fminf(rcp_approx(d), 2.f), off);
+  const float h6r = fmaf(pa - pb, fminf(rcp_approx(d), 2.f), off);  // in [-1, 11)
+  // one period down when h6 >= 5 (exact: Sterbenz), so k = h6 + n < 10 and the
+  // |k - 14| term can never be the minimum: fl(h6 - 6 + c) == fl(h6 + (c - 6))
+  const float h6 = h6r >= 5.f ? h6r - 6.f : h6r;
   const float s = __saturatef(fmaf(d, fminf(rcp_approx(mx), 2.f), ds));
   const float v = __saturatef(fmaf(mx, 1.f / 255.f, dv));
   const float vs = v * s;
-  auto chan = [&](float n) {  // k = h6 + n; offsets folded: k - 2, k - 8, k - 14
-    const float m = fminf(fabsf(h6 + (n - 2.f)), fminf(fabsf(h6 + (n - 8.f)), fabsf(h6 + (n - 14.f))));
+  auto chan = [&](float n) {  // k = h6 + n; offsets folded: k - 2, k - 8
+    const float m = fminf(fabsf(h6 + (n - 2.f)), fabsf(h6 + (n - 8.f)));
     const float t = __saturatef(2.f - m);
     const float y = fmaf(255.f, fmaf(-vs, t, v), 0.5f);
     return __float_as_uint(__fadd_rd(y, M)) & 0xffu;
@@ -194,7 +198,8 @@ __device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, ui
   const float2 mx = f2add(mxb, make_float2(-M, -M));
   const float2 rd = make_float2(fminf(rcp_approx(d.x), 2.f), fminf(rcp_approx(d.y), 2.f));
   const float2 rm = make_float2(fminf(rcp_approx(mx.x), 2.f), fminf(rcp_approx(mx.y), 2.f));
-  const float2 h6 = f2fma(f2add(pa, make_float2(-pb.x, -pb.y)), rd, off);
+  const float2 h6r = f2fma(f2add(pa, make_float2(-pb.x, -pb.y)), rd, off);
+  const float2 h6 = make_float2(h6r.x >= 5.f ? h6r.x - 6.f : h6r.x, h6r.y >= 5.f ? h6r.y - 6.f : h6r.y);
   float2 sv = f2fma(d, rm, make_float2(ds, ds));
   sv = make_float2(__saturatef(sv.x), __saturatef(sv.y));
   float2 vv = f2fma(mx, make_float2(1.f / 255.f, 1.f / 255.f), make_float2(dv, dv));
@@ -204,9 +209,8 @@ __device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, ui
   auto chan = [&](float n, uint32_t (&out)[2]) {
     const float2 k2 = f2add(h6, make_float2(n - 2.f, n - 2.f));
     const float2 k8 = f2add(h6, make_float2(n - 8.f, n - 8.f));
-    const float2 k14 = f2add(h6, make_float2(n - 14.f, n - 14.f));
-    const float2 t = make_float2(__saturatef(2.f - fminf(fabsf(k2.x), fminf(fabsf(k8.x), fabsf(k14.x)))),
-                                 __saturatef(2.f - fminf(fabsf(k2.y), fminf(fabsf(k8.y), fabsf(k14.y)))));
+    const float2 t = make_float2(__saturatef(2.f - fminf(fabsf(k2.x), fabsf(k8.x))),
+                                 __saturatef(2.f - fminf(fabsf(k2.y), fabsf(k8.y))));
     const float2 y = f2fma(make_float2(255.f, 255.f), f2fma(nvs, t, vv), make_float2(0.5f, 0.5f));
     out[0] = __float_as_uint(__fadd_rd(y.x, M)) & 0xffu;
     out[1] = __float_as_uint(__fadd_rd(y.y, M)) & 0xffu;
