@@ -20,9 +20,10 @@
  *  - Images are HWC uint8, RGB, row-major, x = column, y = row, origin top
  *    left.  A batch is ragged: image i lives at
  *    base + desc[i].offset with desc[i].pitch >= width*channels bytes per row.
- *    Every 16-byte-aligned block that contains a byte of an image must be
- *    readable (allocate batches with >= 16 bytes of slack at both ends; torch
- *    caching-allocator blocks satisfy this).
+ *    Every 32-byte-aligned block that contains a byte of an image must be
+ *    readable (the kernels read whole aligned 16- / 32-byte blocks; allocate
+ *    batches with >= 32 bytes of slack at both ends or on 32-byte aligned
+ *    sizes; torch caching-allocator blocks satisfy this).
  *  - Boxes are normalized xyxy float32, [n][max_boxes][4],
  *    with a per-image count; labels int32 [n][max_boxes] (optional).
  *  - Randomness: parameters of (image i, op slot k) are a pure function of
