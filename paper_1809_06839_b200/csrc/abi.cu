@@ -343,6 +343,21 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
   pa.grid = (double*)(ws + P->off_grid);
   pa.n_grid = P->n_grid;
   launch_prep(pa, stream);
+  if (P->max_boxes > 0) {  // (boxes only on full-range launches; side stream, beside the pixel steps)
+    BoxArgs b{};
+    b.boxes_in = boxes_in;
+    b.labels_in = labels_in;
+    b.count_in = count_in;
+    b.boxes_out = boxes_out;
+    b.labels_out = labels_out;
+    b.count_out = count_out;
+    b.max_boxes = P->max_boxes;
+    b.min_visibility = P->min_vis;
+    b.n = P->n;
+    b.tab = tab;
+    b.ops = P->d_ops;
+    launch_boxes(b, side_fork(stream));
+  }
 
   auto img_buf = [&](int id) -> uint8_t* {
     switch (id) {
@@ -404,6 +419,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.gauss = P->d_gauss ? P->d_gauss + st.g_off : nullptr;
     a.g_r = st.g_r;
     a.alpha = st.alpha;
+    cudaStream_t ms;
     switch (st.kind) {
       case SK_ROW:
         a.rg_wide = 0;
@@ -411,6 +427,8 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
           const int kd = P->ops[k].kind;
           a.rg_wide |= kd == ALB_PAD_TO_SIZE || kd == ALB_CROP || kd == ALB_RANDOM_CROP;
         }
+        // labels on the side stream (forked before the pixels launch), beside the pixels
+        ms = st.has_mask && st.has_image ? side_fork(stream) : stream;
         if (st.has_image) {
           a.channels = 3;
           launch_rowgather(a, stream);
@@ -420,7 +438,8 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
           a.units = P->d_units + st.munits_off + st.mstart[i0];
           a.n_units = st.mstart[i1] - st.mstart[i0];
           a.unit_size = st.munit_size;
-          launch_rowgather(a, stream);
+          launch_rowgather(a, ms);
+          if (ms != stream) side_join(stream);
         }
         break;
       case SK_POINT: {
@@ -441,6 +460,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
       case SK_AFFINE: launch_affine(a, stream); break;
       case SK_ELASTIC: launch_elastic(a, stream); break;
       case SK_D4:
+        ms = st.has_mask && st.has_image ? side_fork(stream) : stream;
         if (st.has_image) {
           a.channels = 3;
           launch_d4(a, stream);
@@ -449,7 +469,8 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
           a.channels = 1;
           a.units = P->d_units + st.munits_off + st.mstart[i0];
           a.n_units = st.mstart[i1] - st.mstart[i0];
-          launch_d4(a, stream);
+          launch_d4(a, ms);
+          if (ms != stream) side_join(stream);
         }
         break;
       case SK_EQ: {
@@ -472,21 +493,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
       }
     }
   }
-  if (P->max_boxes > 0) {  // (boxes only on full-range launches)
-    BoxArgs b{};
-    b.boxes_in = boxes_in;
-    b.labels_in = labels_in;
-    b.count_in = count_in;
-    b.boxes_out = boxes_out;
-    b.labels_out = labels_out;
-    b.count_out = count_out;
-    b.max_boxes = P->max_boxes;
-    b.min_visibility = P->min_vis;
-    b.n = P->n;
-    b.tab = tab;
-    b.ops = P->d_ops;
-    launch_boxes(b, stream);
-  }
+  if (P->max_boxes > 0) side_join(stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ALB_E_CUDA, std::string("launch failed: ") + cudaGetErrorString(e));
   return ALB_OK;

@@ -989,25 +989,6 @@ static void launch_affine_v(const StepArgs& a, size_t smem, cudaStream_t s) {
   k_affine<kOne, kMask, kMode><<<a.n_units, kAfThreads, smem, s>>>(a);  // one CTA per tile
 }
 
-// one non-blocking side stream + fork/join events per (device, host thread);
-// created on first use and kept for the process lifetime
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-static SideStream& side_stream() {
-  thread_local SideStream t[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  SideStream& r = t[dev & 63];
-  if (!r.s) {
-    cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
-  }
-  return r;
-}
-
 template <int kOne>
 static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
   // fast variant always stages: a 64x64 tile's footprint (+halo) at scale
@@ -1028,14 +1009,10 @@ static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
     const int grid = std::max(persistent_grid((const void*)k_affine_pipe<kOne>, kPThreads, psmem, a.n_units),
                               (a.n_units + 15) / 16);
     if (mask) {  // label kernel on a side stream, overlapping the image kernel (fork / join by events)
-      SideStream& ss = side_stream();
-      cudaEventRecord(ss.fork, s);
-      cudaStreamWaitEvent(ss.s, ss.fork, 0);
-      k_affine_mask<<<a.n_units, kAfThreads, 0, ss.s>>>(a);
-      cudaEventRecord(ss.join, ss.s);
+      k_affine_mask<<<a.n_units, kAfThreads, 0, side_fork(s)>>>(a);
     }
     k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(ai);
-    if (mask) cudaStreamWaitEvent(s, side_stream().join, 0);
+    if (mask) side_join(s);
   }
 }
 

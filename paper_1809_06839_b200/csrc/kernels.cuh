@@ -183,6 +183,12 @@ __device__ __forceinline__ double grid_coord(int x, int L, int n, const double* 
 
 // grid of a persistent kernel: min(n_units, SMs x occupancy), cached (launch.cu)
 int persistent_grid(const void* fn, int threads, size_t smem, int n_units);
+// fork / join of this (device, host thread)'s side stream: side_fork(s)
+// returns a stream ordered after everything enqueued on s so far; side_join(s)
+// orders s after everything enqueued on the side stream.  Work that touches
+// disjoint buffers (labels vs pixels, boxes) overlaps through it.
+cudaStream_t side_fork(cudaStream_t s);
+void side_join(cudaStream_t s);
 
 // kernel entry points (launch helpers live next to each kernel)
 void launch_prep(const PrepArgs& a, cudaStream_t s);

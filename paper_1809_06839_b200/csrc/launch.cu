@@ -53,4 +53,37 @@ int persistent_grid(const void* fn, int threads, size_t smem, int n_units) {
   return std::min(n_units, g_sms * occ);
 }
 
+namespace {
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+// created on first use, kept for the process lifetime
+SideStream& side_stream() {
+  thread_local SideStream t[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& r = t[dev & 63];
+  if (!r.s) {
+    cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+  }
+  return r;
+}
+}  // namespace
+
+cudaStream_t side_fork(cudaStream_t s) {
+  SideStream& r = side_stream();
+  cudaEventRecord(r.fork, s);
+  cudaStreamWaitEvent(r.s, r.fork, 0);
+  return r.s;
+}
+
+void side_join(cudaStream_t s) {
+  SideStream& r = side_stream();
+  cudaEventRecord(r.join, r.s);
+  cudaStreamWaitEvent(s, r.join, 0);
+}
+
 }  // namespace alb
