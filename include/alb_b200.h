@@ -181,7 +181,11 @@ int32_t alb_plan_num_launches(const alb_plan* plan);
  * Asynchronous on `stream`: it enqueues kernels (and, for Equalize, a
  * memset of its histogram workspace) and nothing else -- no host
  * synchronisation, allocation or copy -- so it can be captured into a CUDA
- * graph and replayed (seed and pointers are baked into the graph).
+ * graph and replayed (seed and pointers are baked into the graph).  Label
+ * (mask) and box work may run on a library-owned side stream (one per
+ * device and host thread), forked from `stream` by an event after the
+ * work already enqueued there and joined back into `stream` before the call
+ * returns, so `stream` ordering holds as if everything ran on it.
  * Errors: ALB_E_INVALID_ARG (null required pointer, in/out overlap),
  * ALB_E_WORKSPACE, ALB_E_CUDA (launch failure). */
 alb_status alb_apply(const alb_plan* plan, uint64_t seed, uint64_t first_image_index,
