@@ -422,10 +422,11 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     cudaStream_t ms;
     switch (st.kind) {
       case SK_ROW:
-        a.rg_wide = 0;
+        a.rg_wide = st.slot1 > st.slot0 ? 2 : 0;
         for (int k = st.slot0; k < st.slot1; ++k) {
           const int kd = P->ops[k].kind;
-          a.rg_wide |= kd == ALB_PAD_TO_SIZE || kd == ALB_CROP || kd == ALB_RANDOM_CROP;
+          if (kd == ALB_PAD_TO_SIZE || kd == ALB_CROP || kd == ALB_RANDOM_CROP) a.rg_wide = 1;
+          else if (kd != ALB_HFLIP && kd != ALB_VFLIP && a.rg_wide == 2) a.rg_wide = 0;
         }
         // labels on the side stream (forked before the pixels launch), beside the pixels
         ms = st.has_mask && st.has_image ? side_fork(stream) : stream;

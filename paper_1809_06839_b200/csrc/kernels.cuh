@@ -52,7 +52,8 @@ struct StepArgs {
   int32_t flat;       // pointwise: 1 = whole image is one segment
   int32_t vec_ok;     // src/dst 16-byte co-aligned per segment
   int32_t channels;   // rowgather: 3 (image) or 1 (mask)
-  int32_t rg_wide;    // rowgather: the step holds a crop / pad (32-pixel, 256-bit items)
+  int32_t rg_wide;    // rowgather: 1 = the step holds a crop / pad (32-pixel, 256-bit items);
+                      // 2 = flips only (warp-per-row kernel, no fill)
   uint32_t fill;      // constant fill, packed RGB (pad / constant border)
   uint32_t mask_fill;
   int32_t interp, border;  // resampling op settings

@@ -5,7 +5,8 @@
 // Each thread produces one 16-pixel block of an output row whose first byte is
 // 16-byte aligned AND on a pixel boundary (16*C bytes = 1 or 3 uint4 stores),
 // or, for window steps, one 32-pixel block on a 32-byte boundary (3 256-bit
-// stores, source from 256-bit loads).
+// stores, source from 256-bit loads).  Flip-only steps use k_rowflip (one
+// warp per row, see there).
 // The 16 source pixels are fetched with aligned 16-byte loads and realigned in
 // registers (funnel shifts); HFlip reverses pixel order with byte permutes.
 #include "stages.cuh"
@@ -190,6 +191,70 @@ __global__ void __launch_bounds__(kRgThreads, 6) k_rowgather(StepArgs a, uint32_
   }
 }
 
+// Flips only (any chain of HFlip / VFlip: the map's valid rectangle is the
+// whole output, no fill).  One warp per output row: the row's 16-pixel blocks
+// whose first byte is 16-byte aligned go one per lane (three aligned 16-byte
+// loads + one more when the source run is misaligned, funnel-shift realign,
+// compile-time byte-permute reversal, C aligned 16-byte streaming stores); the
+// row's unaligned head and tail bytes (< 16 pixels each) are copied one byte
+// per lane by the whole warp, so no lane runs a divergent byte loop.
+template <int C>
+__global__ void __launch_bounds__(kRgThreads) k_rowflip(StepArgs a) {
+  constexpr int NW = 4 * C, NV = C + 1;  // words per block, 16-byte loads per block
+  __shared__ Map1 smap;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int2 unit = a.units[blockIdx.x];
+  const int img = unit.x;
+  const alb_image_desc sd = C == 3 ? a.sdesc[img] : a.msdesc[img];
+  const alb_image_desc dd = C == 3 ? a.ddesc[img] : a.mddesc[img];
+  const int Wo = dd.width, Ho = dd.height;
+  if (threadIdx.x == 0) smap = compose_exact(a.ops, a.tab, img, a.slot0, a.slot1, Wo, Ho);
+  __syncthreads();
+  const Map1 m = smap;
+  const uint8_t* sbase = (C == 3 ? a.src : a.msrc) + sd.offset;
+  uint8_t* dbase = (C == 3 ? a.dst : a.mdst) + dd.offset;
+  const int y0 = unit.y * a.unit_size, y1 = min(Ho, y0 + a.unit_size);
+  for (int y = y0 + warp; y < y1; y += kRgThreads / 32) {
+    uint8_t* drow = dbase + (size_t)y * dd.pitch;
+    const uint8_t* srow = sbase + (size_t)(m.ay * y + m.by) * sd.pitch;
+    const int o = (int)((uintptr_t)drow & 15);
+    const int pa = min(Wo, C == 3 ? (11 * (16 - o)) & 15 : (16 - o) & 15);  // first aligned pixel
+    const int nfull = (Wo - pa) >> 4;
+    for (int k = lane; k < nfull; k += 32) {
+      const int xb = pa + 16 * k;
+      const int sx_lo = m.ax > 0 ? xb + m.bx : m.bx - (xb + 15);
+      const uintptr_t p = (uintptr_t)(srow + (ptrdiff_t)sx_lo * C);
+      const uint4* q = reinterpret_cast<const uint4*>(p & ~(uintptr_t)15);
+      const int sh = (int)(p & 15);
+      uint32_t r[4 * NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (v < NV - 1 || sh != 0) x = __ldg(q + v);  // the last vector only when the run is misaligned
+        r[4 * v] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
+      }
+      const int qw = sh >> 2, kb = (sh & 3) * 8;
+      uint32_t t1[4 * NV - 1], t2[NW + 1], w[NW];
+#pragma unroll
+      for (int i = 0; i < 4 * NV - 1; ++i) t1[i] = (qw & 1) ? r[i + 1] : r[i];
+#pragma unroll
+      for (int i = 0; i < NW + 1; ++i) t2[i] = (qw & 2) ? t1[i + 2] : t1[i];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) w[i] = __funnelshift_r(t2[i], t2[i + 1], kb);
+      if (m.ax < 0) reverse_px<C, 16>(w);
+      uint4* d4 = reinterpret_cast<uint4*>(drow + (ptrdiff_t)xb * C);
+#pragma unroll
+      for (int v = 0; v < C; ++v) __stcs(d4 + v, make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]));
+    }
+    const int nh = pa * C, xt = pa + 16 * nfull, nb = nh + (Wo - xt) * C;
+    for (int t = lane; t < nb; t += 32) {
+      const int b = t < nh ? t : xt * C + (t - nh);
+      const int x = C == 3 ? b / 3 : b;
+      drow[b] = srow[(m.ax * x + m.bx) * C + (b - x * C)];
+    }
+  }
+}
+
 void launch_rowgather(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
   // one CTA per unit (unit_range gives each CTA exactly its own unit)
@@ -197,7 +262,10 @@ void launch_rowgather(const StepArgs& a, cudaStream_t s) {
   // loads per store; measured: pad 0.455 -> 0.404 ms); 16-pixel items with
   // 16-byte loads where every output byte is read from a shifted source (flips:
   // 40 vs 64 registers, measured 0.43 vs 0.55 ms)
-  if (a.channels == 3 && a.rg_wide)
+  if (a.rg_wide == 2) {
+    if (a.channels == 3) k_rowflip<3><<<a.n_units, kRgThreads, 0, s>>>(a);
+    else k_rowflip<1><<<a.n_units, kRgThreads, 0, s>>>(a);
+  } else if (a.channels == 3 && a.rg_wide)
     k_rowgather<3, 32><<<a.n_units, kRgThreads, 0, s>>>(a, a.fill);
   else if (a.channels == 3)
     k_rowgather<3, 16><<<a.n_units, kRgThreads, 0, s>>>(a, a.fill);

@@ -180,6 +180,26 @@ def test_empty_batch_and_errors():
 
 # ------------------------------------------------------------------- cfg3
 
+@pytest.mark.parametrize("specs", [
+    [{"kind": "HorizontalFlip", "p": 0.5}, {"kind": "VerticalFlip", "p": 0.5}],
+    [{"kind": "VerticalFlip"}],
+    [{"kind": "HorizontalFlip"}, {"kind": "HorizontalFlip", "p": 0.5}]])
+def test_flip_steps_with_masks(specs):
+    """Flip-only steps (warp-per-row kernel): images and masks bit-exact on
+    tiny, narrow and ragged sizes (heads / tails shorter than one 16-pixel
+    block, rows with no full block)."""
+    sizes = TINY + gen.cfg2_sizes(12, first_image_index=70) + [(9, 15), (4, 31), (6, 47)]
+    b = gen.gen_images(sizes, seed=1, first_image_index=70, device="cuda")
+    _, _, _, masks = gen.gen_boxes(sizes, seed=1, first_image_index=70)
+    masks = masks.to("cuda")
+    res = run_gpu(specs, b, seed=8, first=70, masks=masks)
+    imgs = [b.image(i) for i in range(len(sizes))]
+    mk = [masks.image(i) for i in range(len(sizes))]
+    ref = run_oracle(specs, imgs, seed=8, first=70, masks=mk)
+    cmp_exact(res["images"], [o["image"] for o in ref])
+    cmp_exact(res["masks"], [o["mask"] for o in ref])
+
+
 @pytest.mark.parametrize("name", list(C.CFG3_OPS))
 def test_cfg3_with_masks(name):
     specs = C.CFG3_OPS[name]
