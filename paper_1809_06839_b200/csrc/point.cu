@@ -95,6 +95,13 @@ __device__ __forceinline__ void scalar_edges(const StepArgs& a, const Seg& s, co
 //   word  = LDS(addr)
 // then four looked-up words pack into the output word with PRMT selectors
 // built from (w & 0x03030303) for all four bytes at once.
+// x >> (32 - k) computed by the multiplier: hi32(x * 2^k)
+__device__ __forceinline__ uint32_t mulhi_pow2(uint32_t x, int k) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << k));
+  return r;
+}
+
 template <bool kNL1>
 __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
   extern __shared__ uint32_t sm_raw[];
@@ -146,15 +153,18 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
               for (int j = 0; j < 4; ++j) {
                 const int jj = q * 4 + j;
                 const uint32_t cb = (jj % 3 == 0) ? c0 : ((jj % 3 == 1) ? c1 : c2);
-                const uint32_t t = j == 0 ? (w[q] << 5) : (w[q] >> (8 * j - 5));
+                // right shifts as IMAD.HI (FMA pipe; this loop is ALU-pipe bound)
+                const uint32_t t = j == 0 ? (w[q] << 5) : mulhi_pow2(w[q], 37 - 8 * j);
                 const uint32_t addr = (t & 0x1F80u) | cb;
                 asm("ld.shared.u32 %0, [%1];" : "=r"(r[j]) : "r"(addr));
               }
               // byte (v & 3) of each looked-up word: selector nibbles from w & 0x03030303
+              // (PRMT reads only the low 16 selector bits, and the result's
+              // upper two bytes are dropped by the final permute)
               const uint32_t xs = w[q] & 0x03030303u;
-              const uint32_t y = xs | (xs >> 4);  // byte k: (v_k & 3) | (v_{k+1} & 3) << 4
-              const uint32_t lo = __byte_perm(r[0], r[1], (y & 0xffu) + 0x40u);
-              const uint32_t hi = __byte_perm(r[2], r[3], ((y >> 16) & 0xffu) + 0x40u);
+              const uint32_t y = xs | (xs >> 4) | 0x00400040u;  // byte k: (v_k & 3) | (4 + (v_{k+1} & 3)) << 4
+              const uint32_t lo = __byte_perm(r[0], r[1], y);
+              const uint32_t hi = __byte_perm(r[2], r[3], y >> 16);
               w[q] = __byte_perm(lo, hi, 0x5410u);
             }
           } else {
