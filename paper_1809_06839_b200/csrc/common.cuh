@@ -175,13 +175,12 @@ __device__ __forceinline__ void hsv_shift_px(float dh6w, float ds, float dv, uin
 // affine paths (scalar) and the pointwise kernel (paired) agree.
 __device__ __forceinline__ float2 f2add(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, uint32_t (&r)[2], uint32_t (&g)[2],
-                                              uint32_t (&b)[2]) {
+// Core on biased floats (2^23 + byte) in, biased bit patterns out (byte in
+// bits 0-7, 0x4B0000 above): callers that unpack / pack with byte permutes
+// skip the per-channel masks and ORs.
+__device__ __forceinline__ void hsv_shift_px2b(float dh6w, float ds, float dv, float2 Rb, float2 Gb, float2 Bb,
+                                               uint32_t (&ro)[2], uint32_t (&go)[2], uint32_t (&bo)[2]) {
   const float M = 8388608.f;
-  float2 Rb, Gb, Bb;
-  Rb.x = __uint_as_float(r[0] | 0x4B000000u); Rb.y = __uint_as_float(r[1] | 0x4B000000u);
-  Gb.x = __uint_as_float(g[0] | 0x4B000000u); Gb.y = __uint_as_float(g[1] | 0x4B000000u);
-  Bb.x = __uint_as_float(b[0] | 0x4B000000u); Bb.y = __uint_as_float(b[1] | 0x4B000000u);
   float2 mxb, mnb, pa, pb, off;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -212,14 +211,23 @@ __device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, ui
     const float2 t = make_float2(__saturatef(2.f - fminf(fabsf(k2.x), fabsf(k8.x))),
                                  __saturatef(2.f - fminf(fabsf(k2.y), fabsf(k8.y))));
     const float2 y = f2fma(make_float2(255.f, 255.f), f2fma(nvs, t, vv), make_float2(0.5f, 0.5f));
-    out[0] = __float_as_uint(__fadd_rd(y.x, M)) & 0xffu;
-    out[1] = __float_as_uint(__fadd_rd(y.y, M)) & 0xffu;
+    out[0] = __float_as_uint(__fadd_rd(y.x, M));
+    out[1] = __float_as_uint(__fadd_rd(y.y, M));
   };
-  uint32_t ro[2], go[2], bo[2];
   chan(5.f, ro);
   chan(3.f, go);
   chan(1.f, bo);
-  r[0] = ro[0]; r[1] = ro[1]; g[0] = go[0]; g[1] = go[1]; b[0] = bo[0]; b[1] = bo[1];
+}
+__device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, uint32_t (&r)[2], uint32_t (&g)[2],
+                                              uint32_t (&b)[2]) {
+  float2 Rb, Gb, Bb;
+  Rb.x = __uint_as_float(r[0] | 0x4B000000u); Rb.y = __uint_as_float(r[1] | 0x4B000000u);
+  Gb.x = __uint_as_float(g[0] | 0x4B000000u); Gb.y = __uint_as_float(g[1] | 0x4B000000u);
+  Bb.x = __uint_as_float(b[0] | 0x4B000000u); Bb.y = __uint_as_float(b[1] | 0x4B000000u);
+  uint32_t ro[2], go[2], bo[2];
+  hsv_shift_px2b(dh6w, ds, dv, Rb, Gb, Bb, ro, go, bo);
+  r[0] = ro[0] & 0xffu; r[1] = ro[1] & 0xffu; g[0] = go[0] & 0xffu; g[1] = go[1] & 0xffu;
+  b[0] = bo[0] & 0xffu; b[1] = bo[1] & 0xffu;
 }
 
 // exact BT.601 luma (299R + 587G + 114B + 500) / 1000

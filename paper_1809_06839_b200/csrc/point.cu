@@ -240,18 +240,32 @@ __global__ void __launch_bounds__(kThreads, 4) k_point_px(StepArgs a) {
         const size_t p0 = s.pidx0 + (s.bA + 48 * gi) / 3;
         if constexpr (kOne == ST_HSV && !kNorm) {  // pixel pairs on the paired fp32 pipe
           if (x.on[0]) {
+            // 4 pixels (12 bytes = 3 words) at a time: each channel byte
+            // becomes a biased float with one byte permute, and the 12
+            // biased results pack into 3 words with 3 byte permutes each
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-              const uint32_t p0 = rgbx_of(w[k], i), p1 = rgbx_of(w[k], i + 1);
-              uint32_t r[2] = {p0 & 0xff, p1 & 0xff}, g[2] = {(p0 >> 8) & 0xff, (p1 >> 8) & 0xff},
-                       b[2] = {p0 >> 16, p1 >> 16};
-              hsv_shift_px2(x.dh[0], x.ds[0], x.dv[0], r, g, b);
+            for (int i = 0; i < 16; i += 4) {
+              uint32_t res[12];
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int ii = i + h;
-                o[(3 * ii) >> 2] |= r[h] << (((3 * ii) & 3) * 8);
-                o[(3 * ii + 1) >> 2] |= g[h] << (((3 * ii + 1) & 3) * 8);
-                o[(3 * ii + 2) >> 2] |= b[h] << (((3 * ii + 2) & 3) * 8);
+              for (int pp = 0; pp < 4; pp += 2) {
+                float2 Rb, Gb, Bb;
+                auto bf = [&](int j) {  // byte j of the group -> 2^23 + byte
+                  return __uint_as_float(__byte_perm(w[k][j >> 2], 0x4B000000u, 0x7540u | (uint32_t)(j & 3)));
+                };
+                const int j0 = 3 * (i + pp), j1 = j0 + 3;
+                Rb = make_float2(bf(j0), bf(j1));
+                Gb = make_float2(bf(j0 + 1), bf(j1 + 1));
+                Bb = make_float2(bf(j0 + 2), bf(j1 + 2));
+                uint32_t ro[2], go[2], bo[2];
+                hsv_shift_px2b(x.dh[0], x.ds[0], x.dv[0], Rb, Gb, Bb, ro, go, bo);
+                res[3 * pp] = ro[0]; res[3 * pp + 1] = go[0]; res[3 * pp + 2] = bo[0];
+                res[3 * pp + 3] = ro[1]; res[3 * pp + 4] = go[1]; res[3 * pp + 5] = bo[1];
+              }
+#pragma unroll
+              for (int m = 0; m < 3; ++m) {
+                const uint32_t lo = __byte_perm(res[4 * m], res[4 * m + 1], 0x0040u);
+                const uint32_t hi = __byte_perm(res[4 * m + 2], res[4 * m + 3], 0x0040u);
+                o[(3 * i) / 4 + m] = __byte_perm(lo, hi, 0x5410u);
               }
             }
           } else {
