@@ -57,8 +57,13 @@ namespace {
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  ~SideStream() {  // at host-thread exit (errors during process teardown are ignored)
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (s) cudaStreamDestroy(s);
+  }
 };
-// created on first use, kept for the process lifetime
+// created on first use per (host thread, device), destroyed at thread exit
 SideStream& side_stream() {
   thread_local SideStream t[64];
   int dev = 0;
