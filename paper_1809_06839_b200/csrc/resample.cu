@@ -451,11 +451,20 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
 #pragma unroll
     for (int q = 0; q < kCols; ++q) h0[q] = h1[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     int hr0 = -1, hr1 = -1;
+    uint32_t a0[kCols], a1[kCols];
+#pragma unroll
+    for (int q = 0; q < kCols; ++q) {
+      a0[q] = smem_u32(src) + 4u * (uint32_t)o0[q];
+      a1[q] = smem_u32(src) + 4u * (uint32_t)o1[q];
+    }
     auto hrow = [&](int sl, float4 (&h)[kCols]) {  // horizontal lerps of the staged row in slot sl
-      const uint32_t* srow = src + sl * SW;
+      // shared-window byte addresses: per-column bases + one row offset
+      const uint32_t roff = (uint32_t)(sl * SW) * 4u;
 #pragma unroll
       for (int q = 0; q < kCols; ++q) {
-        const uint32_t t0 = srow[o0[q]], t1 = srow[o1[q]];
+        uint32_t t0, t1;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t0) : "r"(a0[q] + roff));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t1) : "r"(a1[q] + roff));
         constexpr uint32_t kM = 0x4B000000u;
         auto cv = [](uint32_t t, uint32_t ch) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | ch)); };
         const float2 P0 = make_float2(cv(t0, 0), cv(t0, 1)), P1 = make_float2(cv(t1, 0), cv(t1, 1));
