@@ -739,7 +739,8 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
           AnEnt en;
           en.bx = ae.bx;
           en.by = ae.by;
-          en.c0 = (uint32_t)((ae.iy - t.fy0) * t.S + (ae.ix - t.fx0)) - kMagic15Bits * (uint32_t)(t.S + 1);
+          // byte offset (the consumer forms 4 * index directly)
+          en.c0 = 4u * ((uint32_t)((ae.iy - t.fy0) * t.S + (ae.ix - t.fx0)) - kMagic15Bits * (uint32_t)(t.S + 1));
           en.pad = 0;
           an[e] = en;
         }
@@ -819,6 +820,7 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
       if (u + 1 < u1) pipe_issue(a, &ctx[(it_t + 1) % 3], raw, bar, lane);
     } else {
       const float2 A14 = make_float2(c.is.Af[1], c.is.Af[3]);
+      const uint32_t S4 = 4u * (uint32_t)t.S;  // stage row pitch in bytes
       const Map1 m = c.is.m;
       const int th = c.th, ncol = c.tw > 32 ? 2 : 1;
       const uint8_t* drow0 = c.drow0;
@@ -849,9 +851,9 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
             const float2 tq = fadd2_rm(l, make_float2(kMagic15, kMagic15));
             const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
             const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
-            const uint32_t idx = __float_as_uint(tq.y) * (uint32_t)t.S + __float_as_uint(tq.x) + e.c0;
-            const uint32_t* p0 = stage + idx;
-            const uint32_t* p1 = p0 + t.S;
+            const uint32_t off = __float_as_uint(tq.y) * S4 + (__float_as_uint(tq.x) * 4u + e.c0);  // 4 * index
+            const uint32_t* p0 = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(stage) + off);
+            const uint32_t* p1 = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(stage) + (off + S4));
             bilerp3(p0[0], p0[1], p1[0], p1[1], fr, rr[h], gg[h], bb[h]);
           }
 #pragma unroll
