@@ -9,9 +9,13 @@ per second, summed over ranks (weak scaling: each rank owns its own 2000
 images, global indices rank*2000 + i; no collective on the data path).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 2|3|4|5]
+                    [--config 0|2|3|4|5]
 
-Under torchrun every rank runs its shard; rank 0 prints ONE JSON line.
+The default run (--config 0) measures the cfg2 menu as the headline line and
+the composed configs (cfg3 warps with masks, cfg4 fused Compose -> fp32 NCHW,
+cfg5 co-transform with masks and boxes) into its "composed" object, each
+with its own images/s, roofline and end-to-end number.  Under torchrun every
+rank runs its shard; rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -69,14 +73,16 @@ def workload(cfg, rank):
     raise SystemExit("unknown config %d" % cfg)
 
 
-def alg_bytes(label, specs, sizes, prm=None):
+def alg_bytes(label, specs, sizes, prm=None, masks=False, boxes=False):
     """Algorithmic bytes (read + write) of one apply over the batch (DESIGN.md
     measurement section).  prm: device-drawn params (RSC side)."""
     tot = 0
-    last = specs[-1]["kind"]
+    cpp = 4 if masks else 3  # bytes per pixel moved: RGB (+ the uint8 label)
     for i, (h, w) in enumerate(sizes):
-        inb = h * w * 3
+        inb = h * w * cpp
         kind = specs[0]["kind"]
+        if boxes:
+            tot += 2 * 16 * C.CFG5_MAX_BOXES + 2 * 4 * C.CFG5_MAX_BOXES + 8  # xyxy + labels + count, in and out
         if label == "cfg4_compose":
             side = int(prm[i, 0, 0])
             tot += side * side * 3 + 3 * 224 * 224 * 4
@@ -86,17 +92,16 @@ def alg_bytes(label, specs, sizes, prm=None):
             tot += foot * 4 + 512 * 512 * 4
         elif kind == "RandomCrop":
             ow, oh = specs[0]["size"]
-            tot += 2 * ow * oh * 3
+            tot += 2 * ow * oh * cpp
         elif kind in ("PadToSize", "Resize"):
             ow, oh = specs[0]["size"]
-            tot += inb + ow * oh * 3
+            tot += inb + ow * oh * cpp
         elif kind == "RandomSizedCrop":
             side = int(prm[i, 0, 0])
             ow, oh = specs[0]["size"]
-            tot += side * side * 3 + ow * oh * 3
+            tot += side * side * cpp + ow * oh * cpp
         else:
             tot += 2 * inb
-    del last
     return tot
 
 
@@ -162,13 +167,284 @@ def oracle_menu_rate(menu, sizes, n_img, seed, threads, first=0, batch=None):
 
 # -------------------------------------------------------------------- main
 
+ALL_CONFIGS = (2, 3, 4, 5)
+
+
+def config_dict(cfg, name, sizes, world):
+    """The `config` object of a line (identical in both arms for one config)."""
+    n = len(sizes)
+    _, total = gen.layout(sizes, 3)
+    return {"workload": name, "images_per_gpu": n, "global_batch": n * world,
+            "parallelism": "dp%d (independent shards, no collective)" % world,
+            "l2": "inputs larger than L2 (%.0f MB of images per GPU), seed advances per step"
+                  % (total / 1e6)}
+
+
+def unit_of(cfg, menu):
+    if cfg == 2:
+        return "images/s (each image through all %d transforms of the menu)" % len(menu)
+    return "images/s (each image through the %s)" % (
+        "composed pipeline" if len(menu) == 1 else "%d transforms of the config" % len(menu))
+
+
+class Workload:
+    """Inputs (resident in HBM), plans, outputs and workspaces of one config."""
+
+    def __init__(self, cfg, rank, dev):
+        from paper_1809_06839_b200 import Layout, Pipeline, Plan
+        self.cfg = cfg
+        self.name, self.menu, self.sizes, self.extra = workload(cfg, rank)
+        self.n = n = len(self.sizes)
+        self.first = rank * n
+        self.dev = dev
+        self.batch = gen.gen_images(self.sizes, seed=0, first_image_index=self.first, device=dev)
+        self.masks = self.boxes = None
+        if self.extra.get("masks"):
+            bx, lb, cnt, masks = gen.gen_boxes(self.sizes, seed=0, first_image_index=self.first,
+                                               with_mask=True)
+            self.masks = masks.to(dev)
+            if self.extra.get("boxes"):
+                self.boxes = [torch.from_numpy(bx).to(dev), torch.from_numpy(lb).to(dev),
+                              torch.from_numpy(cnt).to(dev)]
+        in_l = Layout(self.batch.desc, 3)
+        m_l = Layout(self.masks.desc, 1) if self.masks is not None else None
+        self.plans = {}
+        for label, specs in self.menu.items():
+            pipe = Pipeline(specs)
+            osz = [pipe.output_shape(h, w) for h, w in self.sizes]
+            ends_norm = specs[-1]["kind"] == "Normalize"
+            ob = None if ends_norm else gen.empty_batch(osz, 3, dev)
+            nchw = (torch.empty((n, 3) + tuple(osz[0]), dtype=torch.float32, device=dev)
+                    if ends_norm else None)
+            ol = None if ob is None else Layout(ob.desc, 3)
+            mo = mol = None
+            if self.masks is not None:
+                mo = gen.empty_batch(osz, 1, dev)
+                mol = Layout(mo.desc, 1)
+            bo = None
+            if self.boxes is not None:
+                bo = [torch.empty_like(t) for t in self.boxes]
+            mb = C.CFG5_MAX_BOXES if self.boxes is not None else 0
+            plan = Plan(pipe, in_l, ol, m_l, mol, mb,
+                        C.CFG5_MIN_VISIBILITY if self.boxes is not None else 0.0)
+            self.plans[label] = dict(pipe=pipe, plan=plan, out=ob, nchw=nchw, mo=mo, bo=bo, ol=ol,
+                                     mol=mol, ws=plan.workspace(dev), specs=specs)
+        self.layouts = (in_l, m_l)
+
+    def apply(self, label, seed, stream, img_in=None, mask_in=None, boxes_in=None):
+        P = self.plans[label]
+        bi = boxes_in or self.boxes or [None] * 3
+        bo = P["bo"] or [None] * 3
+        masks_in = mask_in if mask_in is not None else (None if self.masks is None else self.masks.buf)
+        P["plan"].apply(seed, self.first, self.batch.buf if img_in is None else img_in,
+                        None if P["out"] is None else P["out"].buf, P["nchw"], masks_in,
+                        None if P["mo"] is None else P["mo"].buf, bi[0], bi[1], bi[2],
+                        bo[0], bo[1], bo[2], workspace=P["ws"], stream=stream)
+
+    def alg_bytes(self, seeds):
+        hw = np.array(self.sizes, np.int32)
+        per = {label: 0 for label in self.menu}
+        for s in seeds:
+            for label, specs in self.menu.items():
+                prm = None
+                if specs[0]["kind"] in ("RandomSizedCrop", "ShiftScaleRotate"):
+                    prm, _ = self.plans[label]["pipe"].sample_params(s, self.first, hw)
+                per[label] += alg_bytes(label, specs, self.sizes, prm,
+                                        masks=self.masks is not None,
+                                        boxes=self.boxes is not None)
+        return per
+
+    def launches(self):
+        return sum(P["plan"].num_launches for P in self.plans.values())
+
+
+def timed_steps(W, seeds, stream, dist, dev):
+    """Time len(seeds) steps (every transform of the menu once per step) between
+    a barrier + synchronize on both sides; per-apply CUDA events on the launch
+    stream.  Returns (max-over-ranks elapsed s, {label: [s per apply]})."""
+    labels = list(W.menu)
+    ev = {label: [] for label in labels}
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in seeds:
+        for label in labels:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            W.apply(label, s, stream)
+            e1.record(stream)
+            ev[label].append((e0, e1))
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t = torch.tensor([t0.elapsed_time(t1) / 1e3], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), {l: [a.elapsed_time(b) / 1e3 for a, b in ev[l]] for l in labels}
+
+
+def e2e_run(W, args, stream, dist, dev, world):
+    """The same metric end to end through the public API with HOST buffers:
+    every step copies its inputs from pinned host memory and its results back,
+    inside the timed region.  Unmasked plans use alb_apply_host (chunked,
+    copies overlapping the kernels); masked / boxed plans copy images, masks and
+    boxes in with torch and call alb_apply."""
+    labels = list(W.menu)
+    host_in = W.batch.buf.cpu().pin_memory()
+    dev_in = torch.empty_like(W.batch.buf)
+    hm = dm = hb = db = None
+    if W.masks is not None:
+        hm = W.masks.buf.cpu().pin_memory()
+        dm = torch.empty_like(W.masks.buf)
+    if W.boxes is not None:
+        hb = [t.cpu().pin_memory() for t in W.boxes]
+        db = [torch.empty_like(t) for t in W.boxes]
+    hosts = {}
+    for label in labels:
+        P = W.plans[label]
+        outs = [P["out"].buf if P["out"] is not None else P["nchw"]]
+        if P["mo"] is not None:
+            outs.append(P["mo"].buf)
+        if P["bo"] is not None:
+            outs += P["bo"]
+        hosts[label] = [(torch.empty(o.shape, dtype=o.dtype).pin_memory(), o) for o in outs]
+
+    def step(seed):
+        for label in labels:
+            P = W.plans[label]
+            if hm is None and hb is None:
+                (ho, do), = hosts[label]
+                P["plan"].apply_host(seed, W.first, host_in, dev_in, ho, do, P["ws"], stream)
+                continue
+            with torch.cuda.stream(stream):
+                dev_in.copy_(host_in, non_blocking=True)
+                if hm is not None:
+                    dm.copy_(hm, non_blocking=True)
+                if hb is not None:
+                    for d, h in zip(db, hb):
+                        d.copy_(h, non_blocking=True)
+                W.apply(label, seed, stream, img_in=dev_in, mask_in=dm, boxes_in=db)
+                for ho, do in hosts[label]:
+                    ho.copy_(do, non_blocking=True)
+
+    step(args.seed)  # warm
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(args.e2e_steps):
+        step(args.seed + s)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
+    if dist:
+        dist.barrier()
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    in_bytes = host_in.numel() + (hm.numel() if hm is not None else 0) + \
+        (sum(t.numel() * t.element_size() for t in hb) if hb is not None else 0)
+    h2d = len(labels) * in_bytes
+    d2h = sum(h.numel() * h.element_size() for v in hosts.values() for h, _ in v)
+    return {"value": round(world * W.n * args.e2e_steps / float(te.item()), 2),
+            "unit": unit_of(W.cfg, W.menu),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "path": "alb_apply_host (pinned host in -> HBM -> kernels -> pinned host out, 16 "
+                    "image chunks, copies overlap kernels)" if hm is None and hb is None else
+                    "pinned host images/masks/boxes -> HBM (torch copies), alb_apply, "
+                    "results -> pinned host, on one stream"}
+
+
+def measure(cfg, args, dev, rank, world, dist, peak, peak_src, local):
+    """One config: warm up, time K steps, per-transform numbers, roofline, e2e."""
+    W = Workload(cfg, rank, dev)
+    stream = torch.cuda.current_stream(dev)
+    labels = list(W.menu)
+    for s in range(args.warmup):
+        for label in labels:
+            W.apply(label, args.seed + 1000 + s, stream)
+    torch.cuda.synchronize()
+    seeds = [args.seed + s for s in range(args.steps)]
+    bytes_per = W.alg_bytes(seeds)
+
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.5)
+    elapsed, op_times = timed_steps(W, seeds, stream, dist, dev)
+    clocks.stop()
+    per = {}
+    for label in labels:
+        ts = op_times[label]
+        tot = sum(ts)
+        gbs = bytes_per[label] / tot / 1e9
+        per[label] = {"images_per_s": round(world * W.n * len(ts) / tot, 1),
+                      "ms_per_apply": round(tot / len(ts) * 1e3, 4),
+                      "ms_median": round(statistics.median(ts) * 1e3, 4),
+                      "alg_GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
+    dom = max(labels, key=lambda l: sum(op_times[l]))
+    dom_gbs = bytes_per[dom] / sum(op_times[dom]) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("cfg%d" % cfg, {}).get(dom)
+    e2e = e2e_run(W, args, stream, dist, dev, world) if args.e2e_steps > 0 else None
+    res = {
+        "value": round(world * W.n * args.steps / elapsed, 2),
+        "unit": unit_of(cfg, W.menu),
+        "ms_per_step": round(elapsed / args.steps * 1e3, 4),
+        "config": config_dict(cfg, W.name, W.sizes, world),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(dom_gbs / peak, 4),
+                     "traffic": traffic, "peak_source": peak_src,
+                     "note": "achieved = algorithmic bytes of the dominant transform / its "
+                             "apply duration (CUDA events on the launch stream around the "
+                             "whole alb_apply, K0 parameter launch included)"},
+        "per_transform": per,
+        "e2e": e2e,
+        "gpu_launches": args.steps * W.launches(),
+        "clocks": clocks.summary(),
+    }
+    return W, res
+
+
+def cpu_baseline(W, args):
+    """The oracle as it stands, on the host cores: all 2000 cfg2 images through
+    the menu on every core, plus a single-threaded 32-image subset."""
+    threads = os.cpu_count() or 1
+    n_img = min(W.n, 2000 if W.cfg == 2 else 16)
+    host = gen.Batch(W.batch.buf.cpu(), W.batch.desc, 3)
+    rate, dt = oracle_menu_rate(W.menu, W.sizes, n_img, args.seed, threads, W.first, host)
+    n1 = min(n_img, 32 if W.cfg == 2 else 2)
+    rate1, dt1 = oracle_menu_rate(W.menu, W.sizes, n1, args.seed, 1, W.first, host)
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": round(rate, 3), "unit": unit_of(W.cfg, W.menu), "cores": threads,
+            "kind": "oracle", "cpu_model": model,
+            "single_thread": {"value": round(rate1, 3), "images": n1, "seconds": round(dt1, 2)},
+            "sample": "first %d images of the same workload, every transform of the menu, "
+                      "oracle/libalbref.so (plain C fp64) on %d host threads, %.1f s" % (
+                          n_img, threads, dt)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=0,
+                    help="0 (default): cfg2 menu as the headline + cfg3/4/5 composed configs")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
@@ -192,205 +468,52 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_1809_06839_b200 import Layout, Pipeline, Plan, build
+    from paper_1809_06839_b200 import build
     build.build()
 
-    name, menu, sizes, extra = workload(args.config, rank)
-    n = len(sizes)
-    first = rank * n
-    batch = gen.gen_images(sizes, seed=0, first_image_index=first, device=dev)
-    masks = boxes = None
-    if extra.get("masks"):
-        bx, lb, cnt, masks = gen.gen_boxes(sizes, seed=0, first_image_index=first,
-                                           with_mask=True)
-        masks = masks.to(dev)
-        if extra.get("boxes"):
-            boxes = [torch.from_numpy(bx).to(dev), torch.from_numpy(lb).to(dev),
-                     torch.from_numpy(cnt).to(dev)]
-    in_l = Layout(batch.desc, 3)
-    m_l = Layout(masks.desc, 1) if masks is not None else None
-
-    plans = {}
-    for label, specs in menu.items():
-        pipe = Pipeline(specs)
-        osz = [pipe.output_shape(h, w) for h, w in sizes]
-        ends_norm = specs[-1]["kind"] == "Normalize"
-        ob = None if ends_norm else gen.empty_batch(osz, 3, dev)
-        nchw = (torch.empty((n, 3) + tuple(osz[0]), dtype=torch.float32, device=dev)
-                if ends_norm else None)
-        ol = None if ob is None else Layout(ob.desc, 3)
-        mo = mol = None
-        if masks is not None:
-            mo = gen.empty_batch(osz, 1, dev)
-            mol = Layout(mo.desc, 1)
-        bo = None
-        if boxes is not None:
-            bo = [torch.empty_like(boxes[0]), torch.empty_like(boxes[1]), torch.empty_like(boxes[2])]
-        plan = Plan(pipe, in_l, ol, m_l, mol, C.CFG5_MAX_BOXES if boxes is not None else 0,
-                    C.CFG5_MIN_VISIBILITY if boxes is not None else 0.0)
-        plans[label] = dict(pipe=pipe, plan=plan, out=ob, nchw=nchw, mo=mo, bo=bo, ol=ol, mol=mol,
-                            ws=plan.workspace(dev), specs=specs)
-
-    stream = torch.cuda.current_stream(dev)
-
-    def apply_one(label, seed):
-        P = plans[label]
-        bi = boxes if boxes is not None else [None] * 3
-        bo = P["bo"] if P["bo"] is not None else [None] * 3
-        P["plan"].apply(seed, first, batch.buf, None if P["out"] is None else P["out"].buf,
-                        P["nchw"], None if masks is None else masks.buf,
-                        None if P["mo"] is None else P["mo"].buf, bi[0], bi[1], bi[2],
-                        bo[0], bo[1], bo[2], workspace=P["ws"], stream=stream)
-
-    labels = list(menu)
-    for s in range(args.warmup):
-        for label in labels:
-            apply_one(label, args.seed + 1000 + s)
-    torch.cuda.synchronize()
-
-    # algorithmic bytes per step for each op (params drawn by the device sampler)
-    hw = np.array(sizes, np.int32)
-    seeds = [args.seed + s for s in range(args.steps)]
-    bytes_per = {label: 0 for label in labels}
-    for s in seeds:
-        for label in labels:
-            prm = None
-            if menu[label][0]["kind"] in ("RandomSizedCrop", "ShiftScaleRotate"):
-                prm, _ = plans[label]["pipe"].sample_params(s, first, hw)
-            bytes_per[label] += alg_bytes(label, menu[label], sizes, prm)
-
-    clocks = Clocks(local)
-    clocks.start()
-    time.sleep(0.5)
-    ev = {label: [] for label in labels}
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for s in seeds:
-        for label in labels:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            apply_one(label, s)
-            e1.record(stream)
-            ev[label].append((e0, e1))
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    clocks.stop()
-    elapsed = t_start.elapsed_time(t_end) / 1e3
-    op_time = {label: sum(a.elapsed_time(b) for a, b in ev[label]) / 1e3 for label in labels}
-    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_max = float(t.item())
-
-    launches = args.steps * sum(P["plan"].num_launches for P in plans.values())
-    per = {}
-    for label in labels:
-        gbs = bytes_per[label] / op_time[label] / 1e9
-        per[label] = {"images_per_s": round(world * n * args.steps / op_time[label], 1),
-                      "ms_per_apply": round(op_time[label] / args.steps * 1e3, 4),
-                      "alg_GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
-    dom = max(labels, key=lambda l: op_time[l])
-    dom_gbs = bytes_per[dom] / op_time[dom] / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("cfg%d" % args.config, {}).get(dom)
-
-    # ---------------------------------------------------------------- e2e
-    e2e = None
-    if args.e2e_steps > 0 and "cfg2" in name:
-        host_in = batch.buf.cpu().pin_memory()
-        dev_in = torch.empty_like(batch.buf)
-        hosts = {}
-        for label in labels:
-            P = plans[label]
-            dout = P["out"].buf if P["out"] is not None else P["nchw"]
-            hosts[label] = (torch.empty(dout.shape, dtype=dout.dtype).pin_memory(),
-                            torch.empty_like(dout))
-        for label in labels:  # warm
-            plans[label]["plan"].apply_host(args.seed, first, host_in, dev_in, hosts[label][0],
-                                            hosts[label][1], plans[label]["ws"], stream)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for s in range(args.e2e_steps):
-            for label in labels:
-                plans[label]["plan"].apply_host(args.seed + s, first, host_in, dev_in,
-                                                hosts[label][0], hosts[label][1],
-                                                plans[label]["ws"], stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
-        if dist:
-            dist.barrier()
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h2d = len(labels) * host_in.numel()
-        d2h = sum(h[0].numel() * h[0].element_size() for h in hosts.values())
-        e2e = {"value": round(world * n * args.e2e_steps / float(te.item()), 2),
-               "unit": "images/s (full 16-transform menu, pinned host in -> HBM -> host out)",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
-
-    # ------------------------------------------------------- cpu baseline
+    cfgs = ALL_CONFIGS if args.config == 0 else (args.config,)
+    head = None
+    composed = {}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        n_img = 2000 if args.config == 2 else 16  # ~10 s of host work on the GPU box
-        host = gen.Batch(batch.buf.cpu(), batch.desc, 3)
-        rate, dt = oracle_menu_rate(menu, sizes, n_img, args.seed, threads, first, host)
-        cpu = {"value": round(rate, 3), "unit": "images/s (whole menu)", "cores": threads,
-               "kind": "oracle",
-               "sample": "first %d images of the same workload, every transform of the menu, "
-                         "oracle/libalbref.so (plain C fp64) on %d host threads, %.1f s" % (
-                             n_img, threads, dt)}
+    for cfg in cfgs:
+        W, res = measure(cfg, args, dev, rank, world, dist, peak, peak_src, local)
+        if head is None:
+            head = res
+            if rank == 0 and world == 1 and not args.no_cpu:
+                cpu = cpu_baseline(W, args)
+        else:
+            composed["cfg%d" % cfg] = res
+        del W
+        torch.cuda.empty_cache()
 
     if rank == 0:
-        out = {
-            "metric": METRIC,
-            "value": round(world * n * args.steps / elapsed_max, 2),
-            "unit": "images/s (each image through all %d transforms of the menu)" % len(labels)
-            if "cfg2" in name else "images/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(elapsed_max / args.steps * 1e3, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u8", "data": "synthetic (seeded gradient+noise, synth/gen.py)",
-            "config": {"workload": name, "images_per_gpu": n, "global_batch": n * world,
-                       "parallelism": "dp%d (independent shards, no collective)" % world,
-                       "l2": "inputs larger than L2 (%.0f MB corpus per GPU), seed advances per step"
-                             % (batch.buf.numel() / 1e6)},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1),
-                         "peak": peak, "unit": "GB/s", "frac": round(dom_gbs / peak, 4),
-                         "traffic": traffic, "peak_source": peak_src,
-                         "note": "achieved = algorithmic bytes of the dominant transform / its "
-                                 "apply duration (CUDA events on the launch stream; includes the "
-                                 "K0 param/LUT launch)"},
-            "per_transform": per,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clocks.summary(),
-        }
+        out = {"metric": METRIC, "value": head["value"], "unit": head["unit"],
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "u8",
+               "data": "synthetic (seeded gradient+noise, synth/gen.py)",
+               "config": head["config"], "roofline": head["roofline"],
+               "per_transform": head["per_transform"], "cpu_baseline": cpu, "e2e": head["e2e"],
+               "gpu_launches": head["gpu_launches"] + sum(c["gpu_launches"] for c in composed.values()),
+               "clocks": head["clocks"]}
+        if composed:
+            out["composed"] = composed
         print(json.dumps(out))
     if dist:
         dist.destroy_process_group()
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the oracle as it stands, on the host cores, bounded."""
+    """--impl reference: the oracle as it stands, on the host cores, bounded.
+    Same config object, metric and unit as our arm's headline line (cfg2 by
+    default), so the driver's ratios compare like with like; each step is a
+    bounded sample of that workload (stated in cpu_baseline.sample)."""
     if rank != 0:
         return
-    name, menu, sizes, _ = workload(args.config, 0)
+    cfg = 2 if args.config == 0 else args.config
+    name, menu, sizes, _ = workload(cfg, 0)
     threads = os.cpu_count() or 1
-    n_img = 256 if args.config == 2 else 4
+    n_img = 256 if cfg == 2 else 4
     for s in range(args.warmup):
         oracle_menu_rate(menu, sizes, 2, args.seed + s, threads)
     t = 0.0
@@ -398,16 +521,17 @@ def run_reference(args, world, rank):
         _, dt = oracle_menu_rate(menu, sizes, n_img, args.seed + s, threads)
         t += dt
     val = n_img * args.steps / t
-    unit = "images/s (each image through all %d transforms of the menu)" % len(menu)
+    unit = unit_of(cfg, menu)
     out = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": unit,
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(t / args.steps * 1e3, 2), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": name, "images_per_step": n_img},
+           "config": config_dict(cfg, name, sizes, world),
            "cpu_baseline": {"value": round(val, 3), "unit": unit, "cores": threads,
                             "kind": "oracle",
                             "sample": "each step = first %d images of the workload through the "
-                                      "whole menu, plain C oracle" % n_img},
+                                      "whole menu, plain C oracle on %d host threads"
+                                      % (n_img, threads)},
            "e2e": {"value": round(val, 3), "unit": unit, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))

@@ -15,8 +15,11 @@
  * Conventions
  *  - Pixel / mask / box buffers passed to alb_apply are DEVICE pointers owned
  *    by the caller.  The library owns only its opaque handles (pipeline,
- *    layout, plan) and the small device tables a plan uploads at creation.
- *    No allocation happens inside alb_apply.
+ *    layout, plan), the small device tables a plan uploads at creation and a
+ *    side stream per (device, host thread) for label / box work, which
+ *    alb_plan_create creates for its thread.  alb_apply allocates no memory;
+ *    it creates the side stream only when called with a masked / boxed plan
+ *    from a thread other than the one that created the plan.
  *  - Images are HWC uint8, RGB, row-major, x = column, y = row, origin top
  *    left.  A batch is ragged: image i lives at
  *    base + desc[i].offset with desc[i].pitch >= width*channels bytes per row.
@@ -84,13 +87,13 @@ typedef enum {
   ALB_D4 = 19,                   /* PAPER.md:87 "dihedral group"
                                     element e uniform in [lo[0], hi[0]] within 0..7:
                                     e < 4 -> rot90(e), else hflip(rot90(e - 4))   */
-  ALB_GRID_DISTORTION = 20,      /* PAPER.md Fig. 4 "grid distortion"; SPEC.md:325-332;
+  ALB_GRID_DISTORTION = 20,      /* PAPER.md Fig. 4 "grid distortion"; SPEC.md:329-337;
                                     reading R31: num_steps cells per axis, cell
                                     lengths proportional to factors 1 + U(lo[0], hi[0])
                                     (-1 < lo <= hi < 1), span preserved; bilinear or
                                     nearest remap (border unused: maps stay inside);
                                     masks nearest; boxes rejected (ALB_E_UNSUPPORTED) */
-  ALB_ELASTIC = 21,              /* PAPER.md:85 "elastic transform"; SPEC.md:333-338;
+  ALB_ELASTIC = 21,              /* PAPER.md:102 "elastic transform"; SPEC.md:338-346;
                                     reading R32: alpha = lo[0] (>= 0), sigma = lo[1]
                                     (0 < sigma <= 16), both fixed (lo == hi); raw
                                     U(-1,1) planes from Philox, fp64 Gaussian blur
@@ -160,7 +163,14 @@ alb_status alb_layout_create(const alb_image_desc* desc, int32_t n, int32_t chan
 void alb_layout_destroy(alb_layout* l);
 
 /* Bind a pipeline to batch layouts and build the launch plan (kernel
- * selection / fusion, work tables).  `out` is NULL iff the pipeline ends in
+ * selection / fusion, work tables).  This is SURVEY.md §8(b)'s alb_batch +
+ * alb_workspace_size split in two: the geometry of a batch (alb_layout) and
+ * the fusion decisions depend only on the op list and the image sizes, so
+ * they are computed and uploaded once here instead of on every apply; the
+ * per-step inputs (seed, image index, buffers) stay in alb_apply.  The
+ * transforms are applied in list order with every
+ * op's u8 rounding kept, masks nearest
+ * and boxes clipped once at the end (readings R18, R19).  `out` is NULL iff the pipeline ends in
  * Normalize (the output is then fp32 NCHW [n][3][oh][ow], all images must map
  * to one output size).  mask_in/mask_out both NULL or both set (1-channel,
  * same dims as the images).  max_boxes > 0 enables box co-transform with the
@@ -174,8 +184,16 @@ alb_status alb_plan_workspace_size(const alb_plan* plan, size_t* bytes);
 /* Number of kernel launches one alb_apply of this plan enqueues. */
 int32_t alb_plan_num_launches(const alb_plan* plan);
 
-/* Apply the plan to one batch (device pointers).  Image i of the batch uses
- * global index first_image_index + i (< 2^32).  Boxes: boxes_in [n][max_boxes][4],
+/* Apply the plan to one batch (device pointers): SPEC.md:482-490 apply(p,
+ * bundle, seed) for a whole batch -- "apply transform T with parameters p to
+ * image/mask/bboxes" (BASELINE.json north_star; Fig. 2).  The
+ * seed is an argument here rather than a pipeline field (SURVEY.md §8(b)
+ * puts it in alb_pipeline_create): the pipeline and plan stay immutable while
+ * a training loop advances the seed per step (SPEC.md:485 seed_override).
+ * Image i of the batch uses global index first_image_index + i (< 2^32);
+ * its gate and parameters are draws (seed, first_image_index + i, slot) of
+ * Philox4x32-10, so the output does not depend on how a
+ * batch is split across calls or GPUs (SPEC.md:502 determinism).  Boxes: boxes_in [n][max_boxes][4],
  * labels_in [n][max_boxes] or NULL, count_in [n]; outputs likewise (kept
  * boxes compacted stably to the front, count_out = kept count).
  * Asynchronous on `stream`: it enqueues kernels (and, for Equalize, a
@@ -185,7 +203,8 @@ int32_t alb_plan_num_launches(const alb_plan* plan);
  * (mask) and box work may run on a library-owned side stream (one per
  * device and host thread), forked from `stream` by an event after the
  * work already enqueued there and joined back into `stream` before the call
- * returns, so `stream` ordering holds as if everything ran on it.
+ * returns, so `stream` ordering holds as if everything ran on it; if that
+ * stream could not be created, the label / box work runs on `stream`.
  * Errors: ALB_E_INVALID_ARG (null required pointer, in/out overlap),
  * ALB_E_WORKSPACE, ALB_E_CUDA (launch failure). */
 alb_status alb_apply(const alb_plan* plan, uint64_t seed, uint64_t first_image_index,
@@ -212,8 +231,16 @@ alb_status alb_apply_host(const alb_plan* plan, uint64_t seed, uint64_t first_im
                           void* workspace, size_t workspace_bytes, void* stream);
 
 /* Parameters the device sampler draws (bit-identical to what alb_apply uses):
- * params_out HOST [n][n_ops][ALB_MAX_PARAMS], fired_out HOST [n][n_ops];
- * in_hw HOST [n][2] (height, width) of each input image.  Synchronous. */
+ * SPEC.md:485 "draw gate = uniform_f64() (always drawn, even when p=1) ...
+ * then draw that transform's parameters in its documented order", with the
+ * counter-based layout of SURVEY.md §8(c) O1.  params_out HOST
+ * [n][n_ops][ALB_MAX_PARAMS], fired_out HOST [n][n_ops]; in_hw HOST [n][2]
+ * (height, width) of each input image -- RandomCrop / RandomSizedCrop draw
+ * their windows from the size each slot sees, which is why
+ * this call takes sizes and a seed beyond §8(b)'s signature.  Runs the same
+ * device sampler as alb_apply, then copies back; synchronous.  Errors:
+ * ALB_E_INVALID_ARG (null pointers, n < 0, a window larger than the image),
+ * ALB_E_SHAPE (dims < 1), ALB_E_CUDA. */
 alb_status alb_sample_params(const alb_pipeline* p, uint64_t seed, uint64_t first_image_index,
                              const int32_t* in_hw, int32_t n, double* params_out,
                              uint8_t* fired_out);

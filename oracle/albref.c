@@ -414,6 +414,13 @@ typedef struct {
   double* box;      /* [n][4] pixel-edge coordinates, unclipped (R18/R19) */
   int32_t* label;
   int32_t nbox;
+  /* Nearest-tie candidate sets (tolerance table "Mask nearest", R20), kept
+   * only when the caller asks for them (albref_apply_cand): per pixel up to
+   * ALBREF_MAX_CAND values that a correct implementation may produce.  They
+   * never feed back into px / mask: the oracle's own result is unchanged. */
+  int track;
+  uint8_t *cpx, *cnpx;   /* [h][w][K][c], [h][w] (0 = any value) */
+  uint8_t *cmk, *cnmk;   /* [h][w][K],    [h][w] */
 } state_t;
 
 static uint8_t* xalloc(size_t n) {
@@ -482,6 +489,152 @@ static void replace_px(state_t* s, uint8_t* px, uint8_t* mask, int32_t h, int32_
   s->h = h; s->w = w;
 }
 
+/* ----------------------------------------- nearest-tie candidate sets (R20)
+ *
+ * SURVEY.md §8(c) tolerance table, "Mask nearest": a nearest sample whose
+ * source coordinate lies within ALBREF_TIE_BAND px of a .5 rounding tie may
+ * legitimately take either neighbour (fp32 vs fp64 coordinates).  Each pixel
+ * of the image and of the mask carries the set of values reachable that way;
+ * exact geometric ops move the sets with the pixels, pointwise ops map every
+ * member, a bilinear sample resets the set to its own result. */
+
+typedef struct {
+  uint8_t *v, *n;  /* [npix][K][c], [npix] */
+  int32_t c;
+} cset_t;
+
+static cset_t cset_new(size_t npix, int32_t c) {
+  cset_t t;
+  t.v = xalloc(npix * ALBREF_MAX_CAND * (size_t)c);
+  t.n = xalloc(npix);
+  t.c = c;
+  return t;
+}
+
+static void cset_one(cset_t t, size_t i, const uint8_t* val) {
+  t.n[i] = 1;
+  memcpy(&t.v[i * ALBREF_MAX_CAND * t.c], val, (size_t)t.c);
+}
+
+/* union of the source set (sv, sn) into element i (sn == 0: any value) */
+static void cset_add(cset_t t, size_t i, const uint8_t* sv, uint8_t sn) {
+  if (t.n[i] == 0) return;
+  if (sn == 0) { t.n[i] = 0; return; }
+  for (int32_t a = 0; a < sn; ++a) {
+    const uint8_t* v = &sv[(size_t)a * t.c];
+    int32_t have = 0;
+    for (int32_t b = 0; b < t.n[i] && !have; ++b)
+      have = memcmp(&t.v[(i * ALBREF_MAX_CAND + b) * t.c], v, (size_t)t.c) == 0;
+    if (have) continue;
+    if (t.n[i] == ALBREF_MAX_CAND) { t.n[i] = 0; return; }
+    memcpy(&t.v[(i * ALBREF_MAX_CAND + t.n[i]) * t.c], v, (size_t)t.c);
+    t.n[i]++;
+  }
+}
+
+static void cset_copy(cset_t t, size_t i, const uint8_t* cv, const uint8_t* cn, size_t j) {
+  t.n[i] = 1;  /* seed with the first member, then union the rest */
+  if (cn[j] == 0) { t.n[i] = 0; return; }
+  memcpy(&t.v[i * ALBREF_MAX_CAND * t.c], &cv[j * ALBREF_MAX_CAND * t.c], (size_t)t.c);
+  cset_add(t, i, &cv[j * ALBREF_MAX_CAND * t.c], cn[j]);
+}
+
+static void cand_init(state_t* s) {
+  const size_t n = (size_t)s->h * s->w;
+  cset_t a = cset_new(n, s->c);
+  for (size_t i = 0; i < n; ++i) cset_one(a, i, &s->px[i * s->c]);
+  s->cpx = a.v; s->cnpx = a.n;
+  s->cmk = s->cnmk = NULL;
+  if (s->mask) {
+    cset_t m = cset_new(n, 1);
+    for (size_t i = 0; i < n; ++i) cset_one(m, i, &s->mask[i]);
+    s->cmk = m.v; s->cnmk = m.n;
+  }
+}
+
+static void cand_replace(state_t* s, cset_t a, cset_t m) {
+  free(s->cpx); free(s->cnpx);
+  s->cpx = a.v; s->cnpx = a.n;
+  if (s->cmk) { free(s->cmk); free(s->cnmk); s->cmk = m.v; s->cnmk = m.n; }
+  else { free(m.v); free(m.n); }
+}
+
+/* Exact geometric op: output pixel i takes the sets of input pixel map[i], or
+ * the constant fill (map[i] < 0).  Called before replace_px (s = input). */
+static void cand_gather(state_t* s, size_t nout, const int64_t* map, const uint8_t* fill,
+                        uint8_t mask_fill) {
+  cset_t a = cset_new(nout, s->c), m = cset_new(s->cmk ? nout : 1, 1);
+  for (size_t i = 0; i < nout; ++i) {
+    if (map[i] >= 0) {
+      cset_copy(a, i, s->cpx, s->cnpx, (size_t)map[i]);
+      if (s->cmk) cset_copy(m, i, s->cmk, s->cnmk, (size_t)map[i]);
+    } else {
+      cset_one(a, i, fill);
+      if (s->cmk) cset_one(m, i, &mask_fill);
+    }
+  }
+  cand_replace(s, a, m);
+}
+
+/* The integer taps a nearest sample at coordinate v may take: round_half_up(v),
+ * plus the other neighbour when v is within ALBREF_TIE_BAND of k + 0.5. */
+static int32_t tie_taps(double v, int32_t* t) {
+  const double f = floor(v);
+  if (fabs(v - f - 0.5) < ALBREF_TIE_BAND) { t[0] = (int32_t)f; t[1] = (int32_t)f + 1; return 2; }
+  t[0] = (int32_t)floor(v + 0.5);
+  return 1;
+}
+
+/* Candidate sets of a nearest sample at (xs, ys) into output pixel i.
+ * clamp_w > 0: taps clamp to the window [0, clamp_w) x [0, clamp_h) offset by
+ * (wx0, wy0) (resize, grid); otherwise the border rule applies per tap
+ * (affine, elastic) with fill / mask_fill for constant borders. */
+static void cand_nearest(const state_t* s, cset_t* a, cset_t* m, size_t i, double xs, double ys,
+                         int32_t clamp_w, int32_t clamp_h, int32_t wx0, int32_t wy0,
+                         int32_t border, const uint8_t* fill, uint8_t mask_fill) {
+  int32_t tx[2], ty[2];
+  const int32_t nx = tie_taps(xs, tx), ny = tie_taps(ys, ty);
+  if (a) a->n[i] = 1;
+  if (m) m->n[i] = 1;
+  int first = 1;
+  for (int32_t u = 0; u < ny; ++u)
+    for (int32_t q = 0; q < nx; ++q) {
+      int32_t xi = 0, yi = 0, in;
+      if (clamp_w > 0) {
+        xi = tx[q] < 0 ? 0 : tx[q] > clamp_w - 1 ? clamp_w - 1 : tx[q];
+        yi = ty[u] < 0 ? 0 : ty[u] > clamp_h - 1 ? clamp_h - 1 : ty[u];
+        xi += wx0; yi += wy0; in = 1;
+      } else {
+        in = border_index(border, tx[q], ty[u], s->w, s->h, &xi, &yi);
+      }
+      const size_t j = (size_t)yi * s->w + xi;
+      if (a) {
+        const uint8_t* sv = in ? &s->cpx[j * ALBREF_MAX_CAND * s->c] : fill;
+        const uint8_t sn = in ? s->cnpx[j] : 1;
+        if (first) { if (sn == 0) a->n[i] = 0; else memcpy(&a->v[i * ALBREF_MAX_CAND * s->c], sv, (size_t)s->c); }
+        cset_add(*a, i, sv, sn);
+      }
+      if (m) {
+        const uint8_t* sv = in ? &s->cmk[j * ALBREF_MAX_CAND] : &mask_fill;
+        const uint8_t sn = in ? s->cnmk[j] : 1;
+        if (first) { if (sn == 0) m->n[i] = 0; else m->v[i * ALBREF_MAX_CAND] = *sv; }
+        cset_add(*m, i, sv, sn);
+      }
+      first = 0;
+    }
+}
+
+/* Candidate sets of an affine-convention sample (affine ops, elastic): the
+ * image takes the nearest-tie sets when interpolating nearest, else its own
+ * bilinear result; the mask is always nearest. */
+static void cand_sample(const state_t* s, cset_t* ca, cset_t* cm, size_t i, double xs, double ys,
+                        const albref_op* o, const uint8_t* out) {
+  const int nearest = o->interp == ALBREF_INTERP_NEAREST;
+  cand_nearest(s, nearest ? ca : NULL, s->mask ? cm : NULL, i, xs, ys, 0, 0, 0, 0, o->border,
+               o->fill, o->mask_fill);
+  if (!nearest) cset_one(*ca, i, out);
+}
+
 /* ---------------------------------------------------- O2 flips, O3/O4 window */
 
 /* HFlip: out[y][x] = in[y][W-1-x]; boxes x' = W - x */
@@ -498,6 +651,13 @@ static void op_hflip(state_t* s) {
     double x0 = s->box[4 * b + 0], x1 = s->box[4 * b + 2];
     s->box[4 * b + 0] = (double)s->w - x1;
     s->box[4 * b + 2] = (double)s->w - x0;
+  }
+  if (s->track) {
+    int64_t* map = (int64_t*)malloc(sizeof(int64_t) * ((size_t)s->h * s->w + 1));
+    for (int32_t y = 0; y < s->h; ++y)
+      for (int32_t x = 0; x < s->w; ++x) map[(size_t)y * s->w + x] = (int64_t)y * s->w + (s->w - 1 - x);
+    cand_gather(s, (size_t)s->h * s->w, map, NULL, 0);
+    free(map);
   }
   replace_px(s, px, mk, s->h, s->w);
 }
@@ -517,6 +677,13 @@ static void op_vflip(state_t* s) {
     s->box[4 * b + 1] = (double)s->h - y1;
     s->box[4 * b + 3] = (double)s->h - y0;
   }
+  if (s->track) {
+    int64_t* map = (int64_t*)malloc(sizeof(int64_t) * ((size_t)s->h * s->w + 1));
+    for (int32_t y = 0; y < s->h; ++y)
+      for (int32_t x = 0; x < s->w; ++x) map[(size_t)y * s->w + x] = (int64_t)(s->h - 1 - y) * s->w + x;
+    cand_gather(s, (size_t)s->h * s->w, map, NULL, 0);
+    free(map);
+  }
   replace_px(s, px, mk, s->h, s->w);
 }
 
@@ -534,6 +701,13 @@ static void op_crop(state_t* s, int32_t x0, int32_t y0, int32_t cw, int32_t ch) 
   for (int32_t b = 0; b < s->nbox; ++b) {
     s->box[4 * b + 0] -= x0; s->box[4 * b + 2] -= x0;
     s->box[4 * b + 1] -= y0; s->box[4 * b + 3] -= y0;
+  }
+  if (s->track) {
+    int64_t* map = (int64_t*)malloc(sizeof(int64_t) * ((size_t)ch * cw + 1));
+    for (int32_t y = 0; y < ch; ++y)
+      for (int32_t x = 0; x < cw; ++x) map[(size_t)y * cw + x] = (int64_t)(y0 + y) * s->w + (x0 + x);
+    cand_gather(s, (size_t)ch * cw, map, NULL, 0);
+    free(map);
   }
   replace_px(s, px, mk, ch, cw);
 }
@@ -558,6 +732,17 @@ static void op_pad(state_t* s, const albref_op* o) {
     s->box[4 * b + 0] += left; s->box[4 * b + 2] += left;
     s->box[4 * b + 1] += top; s->box[4 * b + 3] += top;
   }
+  if (s->track) {
+    int64_t* map = (int64_t*)malloc(sizeof(int64_t) * ((size_t)th * tw + 1));
+    for (int32_t y = 0; y < th; ++y)
+      for (int32_t x = 0; x < tw; ++x) {
+        int32_t sx = x - left, sy = y - top;
+        map[(size_t)y * tw + x] = (sx >= 0 && sx < s->w && sy >= 0 && sy < s->h)
+                                      ? (int64_t)sy * s->w + sx : -1;
+      }
+    cand_gather(s, (size_t)th * tw, map, o->fill, o->mask_fill);
+    free(map);
+  }
   replace_px(s, px, mk, th, tw);
 }
 
@@ -571,6 +756,8 @@ static void op_resize_window(state_t* s, int32_t wx0, int32_t wy0, int32_t ww, i
                              int32_t nw, int32_t nh, int32_t interp) {
   uint8_t* px = xalloc((size_t)nh * nw * s->c);
   uint8_t* mk = s->mask ? xalloc((size_t)nh * nw) : NULL;
+  cset_t ca = {0}, cm = {0};
+  if (s->track) { ca = cset_new((size_t)nh * nw, s->c); cm = cset_new(s->mask ? (size_t)nh * nw : 1, 1); }
   for (int32_t y = 0; y < nh; ++y) {
     double ys = ((double)y + 0.5) * (double)wh / (double)nh - 0.5;
     if (ys < 0.0) ys = 0.0;
@@ -599,8 +786,16 @@ static void op_resize_window(state_t* s, int32_t wx0, int32_t wy0, int32_t ww, i
         }
       }
       if (mk) mk[(size_t)y * nw + x] = s->mask[(size_t)(wy0 + yn) * s->w + (wx0 + xn)];
+      if (s->track) {
+        const size_t i = (size_t)y * nw + x;
+        const int nearest = interp == ALBREF_INTERP_NEAREST;
+        cand_nearest(s, nearest ? &ca : NULL, s->mask ? &cm : NULL, i, xs, ys, ww, wh, wx0, wy0,
+                     0, NULL, 0);
+        if (!nearest) cset_one(ca, i, o);
+      }
     }
   }
+  if (s->track) cand_replace(s, ca, cm);
   for (int32_t b = 0; b < s->nbox; ++b) {
     s->box[4 * b + 0] = (s->box[4 * b + 0] - wx0) * (double)nw / (double)ww;
     s->box[4 * b + 2] = (s->box[4 * b + 2] - wx0) * (double)nw / (double)ww;
@@ -628,6 +823,8 @@ static void op_affine(state_t* s, const albref_op* o, double dx, double dy, doub
   double tx = dx * (double)s->w, ty = dy * (double)s->h;
   uint8_t* px = xalloc((size_t)s->h * s->w * s->c);
   uint8_t* mk = s->mask ? xalloc((size_t)s->h * s->w) : NULL;
+  cset_t ca = {0}, cm = {0};
+  if (s->track) { ca = cset_new((size_t)s->h * s->w, s->c); cm = cset_new(s->mask ? (size_t)s->h * s->w : 1, 1); }
   for (int32_t y = 0; y < s->h; ++y)
     for (int32_t x = 0; x < s->w; ++x) {
       double ux = (double)x - cx - tx, uy = (double)y - cy - ty;
@@ -635,7 +832,9 @@ static void op_affine(state_t* s, const albref_op* o, double dx, double dy, doub
       double ys = cy + (sn * ux + cs * uy) / scale;
       sample_affine(s, xs, ys, o->interp, o->border, o->fill, &px[((size_t)y * s->w + x) * s->c]);
       if (mk) mk[(size_t)y * s->w + x] = sample_mask_nearest(s, xs, ys, o->border, o->mask_fill);
+      if (s->track) cand_sample(s, &ca, &cm, (size_t)y * s->w + x, xs, ys, o, &px[((size_t)y * s->w + x) * s->c]);
     }
+  if (s->track) cand_replace(s, ca, cm);
   for (int32_t b = 0; b < s->nbox; ++b) {
     double lo_x = 0, lo_y = 0, hi_x = 0, hi_y = 0;
     for (int k = 0; k < 4; ++k) {
@@ -658,16 +857,37 @@ static void op_affine(state_t* s, const albref_op* o, double dx, double dy, doub
 
 /* ------------------------------------------------------ O8-O12 colour ops */
 
+/* Map every member of every image candidate set through a per-pixel op. */
+static void cand_map(state_t* s, void (*f)(uint8_t* px, int32_t c, const void* arg), const void* arg) {
+  if (!s->track) return;
+  for (size_t i = 0; i < (size_t)s->h * s->w; ++i) {
+    uint8_t tmp[ALBREF_MAX_CAND * 3];
+    const int32_t n = s->cnpx[i];
+    if (n == 0) continue;
+    memcpy(tmp, &s->cpx[i * ALBREF_MAX_CAND * s->c], (size_t)n * s->c);
+    for (int32_t a = 0; a < n; ++a) f(&tmp[a * s->c], s->c, arg);
+    cset_t t = {s->cpx, s->cnpx, s->c};
+    cset_one(t, i, tmp);
+    cset_add(t, i, tmp, (uint8_t)n);
+  }
+}
+
+static void lut3_px(uint8_t* p, int32_t nc, const void* lut) {
+  for (int c = 0; c < nc; ++c) p[c] = ((const uint8_t*)lut)[c * 256 + p[c]];
+}
+
 static void apply_lut3(state_t* s, const uint8_t* lut) {
   for (size_t i = 0; i < (size_t)s->h * s->w; ++i)
     for (int c = 0; c < s->c; ++c) s->px[i * s->c + c] = lut[c * 256 + s->px[i * s->c + c]];
+  cand_map(s, lut3_px, lut);
 }
 
 /* ShiftHSV per pixel: to HSV, h = (h+dh) mod 360,
  * s, v clamped to [0,1], back to RGB with clip_round. */
-static void op_shift_hsv(state_t* s, double dh, double ds, double dv) {
-  for (size_t i = 0; i < (size_t)s->h * s->w; ++i) {
-    uint8_t* p = &s->px[i * 3];
+static void shift_hsv_px(uint8_t* p, int32_t nc, const void* arg) {
+  const double dh = ((const double*)arg)[0], ds = ((const double*)arg)[1], dv = ((const double*)arg)[2];
+  (void)nc;
+  {
     double h, sat, val, r, g, b;
     albref_rgb_to_hsv((double)p[0], (double)p[1], (double)p[2], &h, &sat, &val);
     h = fmod_pos(h + dh, 360.0);
@@ -680,27 +900,38 @@ static void op_shift_hsv(state_t* s, double dh, double ds, double dv) {
   }
 }
 
+static void op_shift_hsv(state_t* s, double dh, double ds, double dv) {
+  const double d[3] = {dh, ds, dv};
+  for (size_t i = 0; i < (size_t)s->h * s->w; ++i) shift_hsv_px(&s->px[i * 3], 3, d);
+  cand_map(s, shift_hsv_px, d);
+}
+
 /* Grayscale: y = round_half_up(0.299R + 0.587G + 0.114B) in exact integers,
  * floor((299R + 587G + 114B + 500) / 1000), to all 3 channels (
  * PAPER.md:133; R14). */
+static void grayscale_px(uint8_t* p, int32_t nc, const void* arg) {
+  (void)nc; (void)arg;
+  int32_t y = (299 * (int32_t)p[0] + 587 * (int32_t)p[1] + 114 * (int32_t)p[2] + 500) / 1000;
+  p[0] = p[1] = p[2] = (uint8_t)y;
+}
+
 static void op_grayscale(state_t* s) {
-  for (size_t i = 0; i < (size_t)s->h * s->w; ++i) {
-    uint8_t* p = &s->px[i * 3];
-    int32_t y = (299 * (int32_t)p[0] + 587 * (int32_t)p[1] + 114 * (int32_t)p[2] + 500) / 1000;
-    p[0] = p[1] = p[2] = (uint8_t)y;
-  }
+  for (size_t i = 0; i < (size_t)s->h * s->w; ++i) grayscale_px(&s->px[i * 3], 3, NULL);
+  cand_map(s, grayscale_px, NULL);
 }
 
 /* Equalize per channel (R15). */
 static void op_equalize(state_t* s) {
+  uint8_t all[768];
   for (int c = 0; c < s->c; ++c) {
     int64_t hist[256];
-    uint8_t lut[256];
+    uint8_t* lut = &all[c * 256];
     memset(hist, 0, sizeof(hist));
     for (size_t i = 0; i < (size_t)s->h * s->w; ++i) hist[s->px[i * s->c + c]]++;
     albref_equalize_lut(hist, lut);
     for (size_t i = 0; i < (size_t)s->h * s->w; ++i) s->px[i * s->c + c] = lut[s->px[i * s->c + c]];
   }
+  cand_map(s, lut3_px, all);
 }
 
 /* Normalize to fp32 NCHW: (float)((v/255 - mean_c)/std_c) (R16). */
@@ -738,6 +969,13 @@ static void op_rot90_once(state_t* s) {
     s->box[4 * b + 1] = (double)W - X1;
     s->box[4 * b + 3] = (double)W - X0;
   }
+  if (s->track) {
+    int64_t* map = (int64_t*)malloc(sizeof(int64_t) * ((size_t)ho * wo + 1));
+    for (int32_t y = 0; y < ho; ++y)
+      for (int32_t x = 0; x < wo; ++x) map[(size_t)y * wo + x] = (int64_t)x * W + (W - 1 - y);
+    cand_gather(s, (size_t)ho * wo, map, NULL, 0);
+    free(map);
+  }
   replace_px(s, px, mk, ho, wo);
 }
 
@@ -753,18 +991,18 @@ static void op_d4(state_t* s, int32_t e) {
   if (e >= 4) op_hflip(s);
 }
 
-/* ------------------------------------------- GridDistortion (SPEC.md:325-332) */
+/* ------------------------------------------- GridDistortion (SPEC.md:329-337) */
 
 /* Reading R31.  Destination knots d_i = i (L-1)/n, i = 0..n; the
  * cells get lengths proportional to the step factors f_0..f_{n-1} rescaled to
- * the span L-1 (SPEC.md:330 "rescaled to preserve total span"):
+ * the span L-1 (SPEC.md:332 "rescaled to preserve total span"):
  *   c_0 = 0, c_{i+1} = c_i + f_i, S = c_n,  s_i = (L-1) c_i / S.
- * The map is kept as a displacement field (SPEC.md:330 "converts to
+ * The map is kept as a displacement field (SPEC.md:332 "converts to
  * DisplacementField"): e_i = s_i - d_i at the knots (e_0 = e_n = 0), linear in
  * between, so for destination x with u = x n / (L-1), i = min(floor(u), n-1),
  * t = u - i:
  *   src(x) = x + (e_i + t (e_{i+1} - e_i)),  clamped to [0, L-1].
- * f_n is drawn (SPEC.md:330 draws n+1 factors per axis) but no cell uses it. */
+ * f_n is drawn (SPEC.md:332 draws n+1 factors per axis) but no cell uses it. */
 int albref_grid_axis(int32_t L, int32_t n, const double* f, double* src) {
   if (n < 1 || n > ALBREF_GRID_MAX_STEPS || L < 1) return ALBREF_E_RANGE;
   for (int32_t i = 0; i < n; ++i)
@@ -796,7 +1034,7 @@ int albref_grid_axis(int32_t L, int32_t n, const double* f, double* src) {
 static void op_grid(state_t* s, const albref_op* o, uint64_t seed, uint64_t idx, int32_t slot) {
   const int32_t n = o->num_steps;
   double fx[ALBREF_GRID_MAX_STEPS + 1], fy[ALBREF_GRID_MAX_STEPS + 1];
-  for (int32_t i = 0; i <= n; ++i) { /* x factors j = 1..n+1, then y factors (SPEC.md:330) */
+  for (int32_t i = 0; i <= n; ++i) { /* x factors j = 1..n+1, then y factors (SPEC.md:332) */
     fx[i] = 1.0 + uniform_range(o->lo[0], o->hi[0], albref_draw(seed, idx, slot, 1 + i));
     fy[i] = 1.0 + uniform_range(o->lo[0], o->hi[0], albref_draw(seed, idx, slot, n + 2 + i));
   }
@@ -806,6 +1044,8 @@ static void op_grid(state_t* s, const albref_op* o, uint64_t seed, uint64_t idx,
   albref_grid_axis(s->h, n, fy, my);
   uint8_t* px = xalloc((size_t)s->h * s->w * s->c);
   uint8_t* mk = s->mask ? xalloc((size_t)s->h * s->w) : NULL;
+  cset_t ca = {0}, cm = {0};
+  if (s->track) { ca = cset_new((size_t)s->h * s->w, s->c); cm = cset_new(s->mask ? (size_t)s->h * s->w : 1, 1); }
   for (int32_t y = 0; y < s->h; ++y) {
     const double ys = my[y];
     for (int32_t x = 0; x < s->w; ++x) {
@@ -829,17 +1069,25 @@ static void op_grid(state_t* s, const albref_op* o, uint64_t seed, uint64_t idx,
         }
       }
       if (mk) mk[(size_t)y * s->w + x] = s->mask[(size_t)yn * s->w + xn];
+      if (s->track) {
+        const size_t i = (size_t)y * s->w + x;
+        const int nearest = o->interp == ALBREF_INTERP_NEAREST;
+        cand_nearest(s, nearest ? &ca : NULL, s->mask ? &cm : NULL, i, xs, ys, s->w, s->h, 0, 0,
+                     0, NULL, 0);
+        if (!nearest) cset_one(ca, i, out);
+      }
     }
   }
+  if (s->track) cand_replace(s, ca, cm);
   free(mx);
   free(my);
   replace_px(s, px, mk, s->h, s->w);
 }
 
-/* ------------------------------------------ ElasticTransform (SPEC.md:333-338) */
+/* ------------------------------------------ ElasticTransform (SPEC.md:338-346) */
 
 /* Reading R32: g_k = exp(-k^2 / (2 sigma^2)), k = -r..r, r = ceil(3 sigma),
- * divided by their sum (accumulated in ascending k) -- SPEC.md:337. */
+ * divided by their sum (accumulated in ascending k) -- SPEC.md:341. */
 int albref_gauss_kernel(double sigma, double* w) {
   if (!(sigma > 0.0 && sigma <= ALBREF_ELASTIC_MAX_SIGMA)) return ALBREF_E_RANGE;
   const int32_t r = (int32_t)ceil(3.0 * sigma);
@@ -852,11 +1100,11 @@ int albref_gauss_kernel(double sigma, double* w) {
   return r;
 }
 
-/* SPEC.md:335-337: raw planes u, v ~ U(-1, 1) per pixel, row-major, the u plane
+/* SPEC.md:341: raw planes u, v ~ U(-1, 1) per pixel, row-major, the u plane
  * fully first (draw j = 1 + p for u, 1 + h w + p for v, p = y w + x); each
  * convolved with the kernel along x, then along y (reflect-101 edges),
- * accumulated in ascending k with fused multiply-adds (acc = fma(w, x, acc));
- * then scaled by alpha. */
+ * accumulated in ascending k as acc = acc + w * x (IEEE double, no
+ * contraction: SURVEY.md §8(c) arithmetic rules); then scaled by alpha. */
 int albref_elastic_field(int32_t h, int32_t w, double alpha, double sigma, uint64_t seed,
                          uint64_t image_index, int32_t slot, double* dx, double* dy) {
   double g[2 * 48 + 1];
@@ -875,14 +1123,14 @@ int albref_elastic_field(int32_t h, int32_t w, double alpha, double sigma, uint6
       for (int32_t x = 0; x < w; ++x) {
         double acc = 0.0;
         for (int32_t k = -r; k <= r; ++k)
-          acc = fma(g[k + r], raw[(size_t)y * w + albref_reflect101(x + k, w)], acc);
+          acc = acc + g[k + r] * raw[(size_t)y * w + albref_reflect101(x + k, w)];
         bx[(size_t)y * w + x] = acc;
       }
     for (int32_t y = 0; y < h; ++y)
       for (int32_t x = 0; x < w; ++x) {
         double acc = 0.0;
         for (int32_t k = -r; k <= r; ++k)
-          acc = fma(g[k + r], bx[(size_t)albref_reflect101(y + k, h) * w + x], acc);
+          acc = acc + g[k + r] * bx[(size_t)albref_reflect101(y + k, h) * w + x];
         d[(size_t)y * w + x] = alpha * acc;
       }
   }
@@ -900,13 +1148,17 @@ static void op_elastic(state_t* s, const albref_op* o, uint64_t seed, uint64_t i
   albref_elastic_field(s->h, s->w, o->lo[0], o->lo[1], seed, idx, slot, dx, dy);
   uint8_t* px = xalloc(n * s->c);
   uint8_t* mk = s->mask ? xalloc(n) : NULL;
+  cset_t ca = {0}, cm = {0};
+  if (s->track) { ca = cset_new(n, s->c); cm = cset_new(s->mask ? n : 1, 1); }
   for (int32_t y = 0; y < s->h; ++y)
     for (int32_t x = 0; x < s->w; ++x) {
       const size_t p = (size_t)y * s->w + x;
       const double xs = (double)x + dx[p], ys = (double)y + dy[p];
       sample_affine(s, xs, ys, o->interp, o->border, o->fill, &px[p * s->c]);
       if (mk) mk[p] = sample_mask_nearest(s, xs, ys, o->border, o->mask_fill);
+      if (s->track) cand_sample(s, &ca, &cm, p, xs, ys, o, &px[p * s->c]);
     }
+  if (s->track) cand_replace(s, ca, cm);
   free(dx);
   free(dy);
   replace_px(s, px, mk, s->h, s->w);
@@ -914,13 +1166,15 @@ static void op_elastic(state_t* s, const albref_op* o, uint64_t seed, uint64_t i
 
 /* ---------------------------------------------------------- O14 apply */
 
-int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
-                 const uint8_t* img, int32_t h, int32_t w, int32_t channels,
-                 const uint8_t* mask,
-                 const float* boxes, const int32_t* labels, int32_t n_boxes,
-                 float min_visibility,
-                 uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
-                 float* boxes_out, int32_t* labels_out, int32_t* n_boxes_out) {
+static int apply_impl(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
+                      const uint8_t* img, int32_t h, int32_t w, int32_t channels,
+                      const uint8_t* mask,
+                      const float* boxes, const int32_t* labels, int32_t n_boxes,
+                      float min_visibility,
+                      uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
+                      float* boxes_out, int32_t* labels_out, int32_t* n_boxes_out,
+                      uint8_t* cand_img, uint8_t* cand_img_n, uint8_t* cand_mask,
+                      uint8_t* cand_mask_n) {
   int rc = validate_ops(ops, n_ops);
   if (rc) return rc;
   if (h < 1 || w < 1) return ALBREF_E_SHAPE;
@@ -951,6 +1205,9 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
   memcpy(s.px, img, (size_t)h * w * channels);
   s.mask = NULL;
   if (mask) { s.mask = xalloc((size_t)h * w); memcpy(s.mask, mask, (size_t)h * w); }
+  s.track = cand_img != NULL && cand_img_n != NULL;
+  s.cpx = s.cnpx = s.cmk = s.cnmk = NULL;
+  if (s.track) cand_init(&s);
   s.nbox = n_boxes;
   s.box = (double*)malloc(sizeof(double) * 4 * (n_boxes ? n_boxes : 1));
   s.label = (int32_t*)malloc(sizeof(int32_t) * (n_boxes ? n_boxes : 1));
@@ -1002,6 +1259,15 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
 
   if (!ends_norm) memcpy(img_out, s.px, (size_t)s.h * s.w * s.c);
   if (mask && mask_out) memcpy(mask_out, s.mask, (size_t)s.h * s.w);
+  if (s.track) {
+    const size_t np = (size_t)s.h * s.w;
+    memcpy(cand_img, s.cpx, np * ALBREF_MAX_CAND * s.c);
+    memcpy(cand_img_n, s.cnpx, np);
+    if (mask && cand_mask && cand_mask_n) {
+      memcpy(cand_mask, s.cmk, np * ALBREF_MAX_CAND);
+      memcpy(cand_mask_n, s.cnmk, np);
+    }
+  }
 
   /* boxes: clip the final unclipped envelope to the image, keep iff non-empty
    * and clipped area >= min_visibility * unclipped area (R19), stable. */
@@ -1028,5 +1294,30 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
   }
 
   free(s.px); free(s.mask); free(s.box); free(s.label); free(prm); free(fired);
+  free(s.cpx); free(s.cnpx); free(s.cmk); free(s.cnmk);
   return ALBREF_OK;
+}
+
+int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
+                 const uint8_t* img, int32_t h, int32_t w, int32_t channels,
+                 const uint8_t* mask,
+                 const float* boxes, const int32_t* labels, int32_t n_boxes,
+                 float min_visibility,
+                 uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
+                 float* boxes_out, int32_t* labels_out, int32_t* n_boxes_out) {
+  return apply_impl(ops, n_ops, seed, image_index, img, h, w, channels, mask, boxes, labels,
+                    n_boxes, min_visibility, img_out, nchw_out, mask_out, boxes_out, labels_out,
+                    n_boxes_out, NULL, NULL, NULL, NULL);
+}
+
+int albref_apply_cand(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
+                      const uint8_t* img, int32_t h, int32_t w, int32_t channels,
+                      const uint8_t* mask, uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
+                      uint8_t* cand_img, uint8_t* cand_img_n, uint8_t* cand_mask,
+                      uint8_t* cand_mask_n) {
+  if (!cand_img || !cand_img_n || (mask && (!cand_mask || !cand_mask_n)))
+    return ALBREF_E_INVALID_ARG;
+  return apply_impl(ops, n_ops, seed, image_index, img, h, w, channels, mask, NULL, NULL, 0, 0.0f,
+                    img_out, nchw_out, mask_out, NULL, NULL, NULL, cand_img, cand_img_n,
+                    cand_mask, cand_mask_n);
 }

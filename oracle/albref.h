@@ -39,8 +39,8 @@ enum {
   ALBREF_NORMALIZE = 16, ALBREF_CROP = 17,
   ALBREF_ROT90 = 18,  /* SPEC.md:193-201; k quarter turns, k in [lo[0], hi[0]] */
   ALBREF_D4 = 19,     /* SPEC.md:202-210; element e in [lo[0], hi[0]] of 0..7 */
-  ALBREF_GRID_DISTORTION = 20, /* SPEC.md:325-332; Fig. 4: factors 1 + U(lo[0], hi[0]) */
-  ALBREF_ELASTIC = 21,         /* SPEC.md:333-338; alpha = lo[0], sigma = lo[1] */
+  ALBREF_GRID_DISTORTION = 20, /* SPEC.md:329-337; Fig. 4: factors 1 + U(lo[0], hi[0]) */
+  ALBREF_ELASTIC = 21,         /* SPEC.md:338-346; alpha = lo[0], sigma = lo[1] */
   ALBREF_NUM_KINDS = 22
 };
 enum { ALBREF_INTERP_NEAREST = 0, ALBREF_INTERP_BILINEAR = 1 };
@@ -94,7 +94,7 @@ int albref_grid_axis(int32_t L, int32_t n, const double* f, double* src);
 int albref_gauss_kernel(double sigma, double* w);
 /* Displacement planes dx, dy [h][w] of slot `slot` of image `image_index`:
  * raw u, v ~ U(-1, 1) (draws 1 + y w + x, then 1 + h w + y w + x), blurred
- * x then y with w[] and reflect-101, times alpha. */
+ * x then y with w[] and reflect-101 (acc = acc + w x, ascending k), times alpha. */
 int albref_elastic_field(int32_t h, int32_t w, double alpha, double sigma, uint64_t seed,
                          uint64_t image_index, int32_t slot, double* dx, double* dy);
 
@@ -132,6 +132,24 @@ int albref_apply(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t im
                  float min_visibility,
                  uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
                  float* boxes_out, int32_t* labels_out, int32_t* n_boxes_out);
+
+/* Nearest-tie candidate sets (SURVEY.md §8(c) tolerance table "Mask nearest",
+ * reading R20): the same computation as albref_apply (no boxes; its image /
+ * mask / nchw outputs are identical), plus for every output pixel the set of
+ * values an implementation may produce when a nearest sample's source
+ * coordinate is within ALBREF_TIE_BAND px of a .5 rounding tie (either
+ * neighbour accepted).  Sets follow the pixels through exact geometric ops
+ * and through pointwise ops; a bilinear sample resets the image set to its
+ * own value.  cand_img [oh][ow][ALBREF_MAX_CAND][channels], cand_img_n
+ * [oh][ow] (member count; 0 = more than ALBREF_MAX_CAND members: any value),
+ * cand_mask [oh][ow][ALBREF_MAX_CAND] / cand_mask_n [oh][ow] (mask given). */
+#define ALBREF_MAX_CAND 8
+#define ALBREF_TIE_BAND 1e-4
+int albref_apply_cand(const albref_op* ops, int32_t n_ops, uint64_t seed, uint64_t image_index,
+                      const uint8_t* img, int32_t h, int32_t w, int32_t channels,
+                      const uint8_t* mask, uint8_t* img_out, float* nchw_out, uint8_t* mask_out,
+                      uint8_t* cand_img, uint8_t* cand_img_n, uint8_t* cand_mask,
+                      uint8_t* cand_mask_n);
 
 /* Synthetic-input generator recipe is NOT here (synth/ owns it). */
 

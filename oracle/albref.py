@@ -32,6 +32,8 @@ KINDS = {
 INTERP = {"nearest": 0, "bilinear": 1}
 BORDER = {"constant": 0, "reflect_101": 1}
 MAX_PARAMS = 8
+MAX_CAND = 8       # ALBREF_MAX_CAND
+TIE_BAND = 1e-4    # ALBREF_TIE_BAND
 
 
 class AlbrefOp(ctypes.Structure):
@@ -101,6 +103,10 @@ def lib():
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_float,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.albref_apply_cand.argtypes = [P(AlbrefOp), ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
+                                        ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -289,6 +295,52 @@ def apply(specs, seed, image_index, img, mask=None, boxes=None, labels=None,
         res["boxes"] = bo[:k].copy()
         res["labels"] = lo[:k].copy()
     return res
+
+
+def apply_cand(specs, seed, image_index, img, mask=None, _ops=None):
+    """albref_apply_cand: as apply() (no boxes) plus the nearest-tie candidate
+    sets of every output pixel: image_cand (oh, ow, MAX_CAND, c) with
+    image_cand_n (oh, ow) members (0 = any), likewise mask_cand / mask_cand_n."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    if img.ndim == 2:
+        img = img[:, :, None]
+    h, w, c = img.shape
+    ops, n = _ops if _ops is not None else make_ops(specs)
+    oh, ow = output_shape(specs, h, w)
+    ends_norm = n > 0 and ops[n - 1].kind == KINDS["Normalize"]
+    out = None if ends_norm else np.zeros((oh, ow, c), np.uint8)
+    nchw = np.zeros((3, oh, ow), np.float32) if ends_norm else None
+    ci = np.zeros((oh, ow, MAX_CAND, c), np.uint8)
+    cin = np.zeros((oh, ow), np.uint8)
+    mk = cm = cmn = None
+    if mask is not None:
+        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+        assert mask.shape == (h, w)
+        mk = np.zeros((oh, ow), np.uint8)
+        cm = np.zeros((oh, ow, MAX_CAND), np.uint8)
+        cmn = np.zeros((oh, ow), np.uint8)
+
+    def ptr(a):
+        return None if a is None else a.ctypes.data
+
+    _check(lib().albref_apply_cand(ops, n, seed, image_index, img.ctypes.data, h, w, c, ptr(mask),
+                                   ptr(out), ptr(nchw), ptr(mk), ci.ctypes.data, cin.ctypes.data,
+                                   ptr(cm), ptr(cmn)))
+    return {"image": None if out is None else (out if c > 1 else out[:, :, 0]), "nchw": nchw,
+            "mask": mk, "image_cand": ci, "image_cand_n": cin, "mask_cand": cm, "mask_cand_n": cmn}
+
+
+def apply_batch_cand(specs, seed, first_image_index, images, masks=None, threads=1):
+    ops = make_ops(specs)
+
+    def one(i):
+        return apply_cand(specs, seed, first_image_index + i, images[i],
+                          None if masks is None else masks[i], _ops=ops)
+
+    if threads <= 1:
+        return [one(i) for i in range(len(images))]
+    with ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(one, range(len(images))))
 
 
 def apply_batch(specs, seed, first_image_index, images, masks=None, boxes=None, labels=None,

@@ -27,7 +27,8 @@ OBJ = os.path.join(OBJ_ROOT, hashlib.sha1(" ".join(ARCH + FLAGS).encode()).hexdi
 
 
 def _deps():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "alb_b200.h")])
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) +
+                  [os.path.join(ROOT, "include", "alb_b200.h")])
 
 
 def _compile(src, force):

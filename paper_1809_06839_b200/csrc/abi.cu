@@ -487,7 +487,14 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
         e.img0 = i0;
         e.slot = st.eq_slot;
         e.tab = tab;
-        CUDA_TRY(cudaMemsetAsync(e.hist + (size_t)i0 * 768, 0, (size_t)(i1 - i0) * 768 * sizeof(uint32_t), stream));
+        // a failed memset must still join the box work forked above before
+        // returning (else the caller's stream is not ordered after it)
+        const cudaError_t me = cudaMemsetAsync(e.hist + (size_t)i0 * 768, 0,
+                                               (size_t)(i1 - i0) * 768 * sizeof(uint32_t), stream);
+        if (me != cudaSuccess) {
+          if (P->max_boxes > 0) side_join(stream);
+          return fail(ALB_E_CUDA, std::string("memset failed: ") + cudaGetErrorString(me));
+        }
         launch_eq_hist(e, stream);
         launch_eq_lut(e, stream);
         break;
@@ -983,6 +990,11 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
     CUDA_TRY(cudaMalloc(&P->d_gauss, sizeof(double) * P->gauss.size()));
     CUDA_TRY(cudaMemcpy(P->d_gauss, P->gauss.data(), sizeof(double) * P->gauss.size(), cudaMemcpyHostToDevice));
   }
+  // label / box work forks onto this thread's side stream: create it now, so
+  // alb_apply from this thread creates nothing (checked; on failure the work
+  // runs in order on the caller's stream)
+  if ((mask_in || max_boxes > 0) && !side_init())
+    return fail(ALB_E_CUDA, "could not create the side stream for label / box work");
   // ------------------------------------------------------------ workspace
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };

@@ -1,4 +1,4 @@
-// elastic.cu -- K12 ElasticTransform (SPEC.md:333-338, PAPER.md:85; reading
+// elastic.cu -- K12 ElasticTransform (SPEC.md:338-346, PAPER.md:102, 106; reading
 // R32): the displacement field is rebuilt on chip from the counter-based raw
 // planes (nothing per-image in HBM), blurred in fp64 and used to remap the
 // image (and mask) from global memory.

@@ -188,6 +188,9 @@ int persistent_grid(const void* fn, int threads, size_t smem, int n_units);
 // returns a stream ordered after everything enqueued on s so far; side_join(s)
 // orders s after everything enqueued on the side stream.  Work that touches
 // disjoint buffers (labels vs pixels, boxes) overlaps through it.
+// side_init() creates the side stream of the calling thread ahead of time
+// (false if that failed: fork then returns s itself, join is a no-op).
+bool side_init();
 cudaStream_t side_fork(cudaStream_t s);
 void side_join(cudaStream_t s);
 

@@ -8,34 +8,36 @@
 #include <map>
 #include <mutex>
 #include <set>
+#include <tuple>
 #include <utility>
 
 namespace alb {
 
 namespace {
 std::mutex g_mu;
-std::map<std::pair<const void*, size_t>, int> g_occ;
-std::set<const void*> g_fn_set;
-int g_sms = 0;
+// keyed by device: the dynamic shared-memory attribute and the occupancy are
+// per (device context, function), the SM count per device
+std::map<std::tuple<int, const void*, size_t>, int> g_occ;
+std::set<std::pair<int, const void*>> g_fn_set;
+std::map<int, int> g_sms;
 }  // namespace
 
 int persistent_grid(const void* fn, int threads, size_t smem, int n_units) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (g_sms == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      g_sms = 148;
-  }
-  const auto key = std::make_pair(fn, smem);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  int& sms = g_sms[dev];
+  if (sms == 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms = 148;
+  const auto key = std::make_tuple(dev, fn, smem);
   auto it = g_occ.find(key);
   int occ;
   if (it == g_occ.end()) {
-    // the attribute is per function: raise it to the opt-in maximum once, so
-    // launches of the same kernel with different smem sizes all stay legal
-    if (g_fn_set.insert(fn).second) {
-      int dev = 0, mx = 0;
-      cudaGetDevice(&dev);
+    // the attribute is per function and device: raise it to the opt-in
+    // maximum once, so launches of the same kernel with different smem sizes
+    // all stay legal
+    if (g_fn_set.insert(std::make_pair(dev, fn)).second) {
+      int mx = 0;
       cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
       cudaFuncAttributes fa{};
       cudaFuncGetAttributes(&fa, fn);
@@ -50,7 +52,7 @@ int persistent_grid(const void* fn, int threads, size_t smem, int n_units) {
   } else {
     occ = it->second;
   }
-  return std::min(n_units, g_sms * occ);
+  return std::min(n_units, sms * occ);
 }
 
 namespace {
@@ -63,30 +65,46 @@ struct SideStream {
     if (s) cudaStreamDestroy(s);
   }
 };
-// created on first use per (host thread, device), destroyed at thread exit
+// one per (host thread, device), destroyed at thread exit.  Created by
+// side_init() -- alb_plan_create calls it for plans with label / box work, so
+// alb_apply on the plan's thread creates nothing -- or on first use from
+// another thread.  If creation fails the side stream is the caller's stream
+// itself: label / box work then runs in order on it (correct, not overlapped).
 SideStream& side_stream() {
   thread_local SideStream t[64];
   int dev = 0;
-  cudaGetDevice(&dev);
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   SideStream& r = t[dev & 63];
   if (!r.s) {
-    cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+    cudaStream_t s = nullptr;
+    cudaEvent_t f = nullptr, j = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaEventCreateWithFlags(&f, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventCreateWithFlags(&j, cudaEventDisableTiming) == cudaSuccess) {
+      r.s = s; r.fork = f; r.join = j;
+    } else {
+      if (f) cudaEventDestroy(f);
+      if (s) cudaStreamDestroy(s);
+      cudaGetLastError();  // reported as "no side stream" below, not as a launch error
+    }
   }
   return r;
 }
 }  // namespace
 
+bool side_init() { return side_stream().s != nullptr; }
+
 cudaStream_t side_fork(cudaStream_t s) {
   SideStream& r = side_stream();
-  cudaEventRecord(r.fork, s);
+  if (!r.s) return s;
+  cudaEventRecord(r.fork, s);  // failures surface through cudaGetLastError at the end of the apply
   cudaStreamWaitEvent(r.s, r.fork, 0);
   return r.s;
 }
 
 void side_join(cudaStream_t s) {
   SideStream& r = side_stream();
+  if (!r.s || r.s == s) return;
   cudaEventRecord(r.join, r.s);
   cudaStreamWaitEvent(s, r.join, 0);
 }

@@ -88,7 +88,7 @@ __device__ void sample_image(const PrepArgs& a, int i, double (*sp)[kMaxParams],
       case ALB_PAD_TO_SIZE: case ALB_RESIZE:
         nh = o.out_h; nw = o.out_w;
         break;
-      case ALB_GRID_DISTORTION: {  // x factors: draws 1..n+1, y factors: n+2..2n+2 (SPEC.md:330)
+      case ALB_GRID_DISTORTION: {  // x factors: draws 1..n+1, y factors: n+2..2n+2 (SPEC.md:332)
         if (!a.grid) break;  // alb_sample_params: gates and params only
         double* e = a.grid + ((size_t)i * a.n_grid + g_ord++) * kGridStride;
         grid_knots(o, a.seed, gi, k, 1, w, e);

@@ -106,3 +106,53 @@ def cmp_exact(gpu, ref):
             bad = np.argwhere(g != r)
             raise AssertionError("image %d differs at %d positions, first %s: gpu %s ref %s" % (
                 i, len(bad), bad[0].tolist(), g[tuple(bad[0])], r[tuple(bad[0])]))
+
+
+def run_oracle_cand(specs, images, seed=0, first=0, masks=None, threads=8):
+    """Oracle outputs plus nearest-tie candidate sets (albref_apply_cand)."""
+    from oracle import albref as A
+    return A.apply_batch_cand(specs, seed, first, images, masks, threads)
+
+
+def cmp_cand(gpu, ref, which="mask", min_exact=0.999):
+    """Nearest-sample tolerance (SURVEY.md §8(c) "Mask nearest", R20): every
+    pixel equals the oracle's, except where the oracle flagged a source
+    coordinate within 1e-4 px of a .5 tie -- there the GPU value must be one
+    of the oracle's candidate values (either neighbour) -- and >= min_exact
+    of the pixels are exact.  `which` is "mask" or "image"."""
+    tot = eq = 0
+    for i, (g, o) in enumerate(zip(gpu, ref)):
+        r, cv, cn = o[which], o[which + "_cand"], o[which + "_cand_n"]
+        assert g.shape == r.shape, (i, g.shape, r.shape)
+        g3 = g.reshape(g.shape[0], g.shape[1], -1)
+        r3 = r.reshape(g3.shape)
+        cv = cv.reshape(g3.shape[0], g3.shape[1], cv.shape[2], -1)
+        diff = (g3 != r3).any(-1)
+        tot += diff.size
+        eq += int((~diff).sum())
+        for y, x in np.argwhere(diff):
+            n = int(cn[y, x])
+            ok = n == 0 or any(np.array_equal(cv[y, x, k], g3[y, x]) for k in range(n))
+            assert ok, ("image %d (%d,%d): gpu %s, oracle %s, outside the tie band (candidates %s)"
+                        % (i, y, x, g3[y, x].tolist(), r3[y, x].tolist(),
+                           cv[y, x, :n].tolist()))
+    frac = eq / max(1, tot)
+    assert frac >= min_exact, "exact fraction %.6f < %.4f" % (frac, min_exact)
+    return frac
+
+
+def random_masks(sizes, seed=0, device="cuda", levels=256):
+    """Label planes of independent random labels per pixel: every neighbour
+    differs, so any wrong nearest decision shows up as a wrong label."""
+    rng = np.random.default_rng(seed)
+    ims = [rng.integers(0, levels, size=(h, w), dtype=np.uint8) for h, w in sizes]
+    return to_device_batch([m[:, :, None] for m in ims], channels=1, device=device), ims
+
+
+def cmp_boxes(res, ref, tol=1e-5):
+    """Box co-transform: same keep set and labels, coordinates within tol."""
+    for i in range(len(ref)):
+        k = int(res["count"][i])
+        assert k == len(ref[i]["labels"]), (i, k, len(ref[i]["labels"]))
+        assert np.array_equal(res["labels"][i, :k], ref[i]["labels"]), i
+        assert np.abs(res["boxes"][i, :k] - ref[i]["boxes"]).max(initial=0) <= tol, i

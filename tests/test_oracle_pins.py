@@ -776,7 +776,7 @@ def test_grid_axis_hand_example():
 
 
 def test_grid_axis_monotone_span_and_knots():
-    """SPEC.md:330-332: over 1000 random draws the axis map is strictly
+    """SPEC.md:332, 337: over 1000 random draws the axis map is strictly
     monotone, keeps the span (src[0] = 0, src[L-1] = L-1 exactly), passes
     through the rescaled knots s_i = (L-1) c_i / S (exact rational arithmetic)
     and is linear inside each cell with slope n f_i / S."""
@@ -806,7 +806,7 @@ def test_grid_axis_monotone_span_and_knots():
 
 
 def test_grid_identity_at_zero_limit():
-    """SPEC.md:331: distort_limit = 0 is the identity, bit-exact, for both
+    """SPEC.md:335: distort_limit = 0 is the identity, bit-exact, for both
     interpolations, image and mask, any n (also n > L - 1) and degenerate sizes."""
     rng = np.random.default_rng(7)
     for (h, w) in [(1, 1), (1, 17), (23, 1), (19, 31), (64, 48)]:
@@ -819,7 +819,7 @@ def test_grid_identity_at_zero_limit():
 
 
 def _grid_maps(lo, hi, n, h, w, seed, idx, slot=0):
-    """factor draws as SPEC.md:330 orders them: x steps j = 1..n+1, then y steps"""
+    """factor draws as SPEC.md:332 orders them: x steps j = 1..n+1, then y steps"""
     fx = [1.0 + lo + (hi - lo) * A.draw(seed, idx, slot, 1 + i) for i in range(n + 1)]
     fy = [1.0 + lo + (hi - lo) * A.draw(seed, idx, slot, n + 2 + i) for i in range(n + 1)]
     return A.grid_axis(w, n, fx), A.grid_axis(h, n, fy)
@@ -872,7 +872,7 @@ def _elastic(alpha, sigma, interp="bilinear", border="reflect_101", p=1.0):
 
 
 def test_elastic_gauss_kernel():
-    """SPEC.md:337 / invariant SPEC.md:341: symmetric, nonnegative, sums to 1
+    """SPEC.md:341 / invariant SPEC.md:350: symmetric, nonnegative, sums to 1
     (1e-12), radius ceil(3 sigma), weights proportional to math.exp(-k^2/2s^2)."""
     import math
     for sigma in (0.1, 0.5, 1.0, 1.7, 3.0, 4.0, 7.3, 16.0):
@@ -900,7 +900,7 @@ def _reflect_idx(i, n):
 def test_elastic_field_direct_2d_convolution():
     """separable blur == direct 2-D convolution (1e-9) on small
     fields, incl. kernels wider than the image (repeated reflection); the raw
-    planes come from the draws in SPEC.md:337's order (u plane, then v plane,
+    planes come from the draws in SPEC.md:341's order (u plane, then v plane,
     row-major) -- a transposed or swapped plane fails."""
     import math
     for (h, w, sigma, alpha) in [(9, 9, 1.0, 3.0), (9, 9, 2.5, 1.0), (5, 12, 1.3, 7.0), (1, 6, 0.7, 2.0),
@@ -922,7 +922,7 @@ def test_elastic_field_direct_2d_convolution():
 
 
 def test_elastic_bound_and_identity():
-    """SPEC.md:338: |displacement| <= alpha (convexity); SPEC.md:336: alpha = 0
+    """SPEC.md:345: |displacement| <= alpha (convexity); SPEC.md:344: alpha = 0
     is the identity bit-exact (nearest and bilinear, image and mask)."""
     rng = np.random.default_rng(32)
     for _ in range(40):
@@ -976,3 +976,81 @@ def test_elastic_validation_and_boxes_rejected():
     with pytest.raises(A.OracleError) as e:
         run(_elastic(5.0, 2.0), img, boxes=np.array([[0.1, 0.1, 0.5, 0.5]], np.float32))
     assert e.value.code == -5
+
+
+# ------------------------------------------ nearest-tie candidate sets (R20)
+
+def test_cand_outputs_equal_apply_and_contain_result():
+    """albref_apply_cand returns albref_apply's outputs unchanged, and every
+    pixel's own value is a member of its candidate set."""
+    rng = np.random.default_rng(77)
+    cases = [([{"kind": "Rotate", "lo": [-90.0], "hi": [90.0], "interp": "nearest",
+                "border": "reflect_101"}], (41, 57)),
+             ([{"kind": "ShiftScaleRotate", "lo": [-.06, -.06, .9, -45.0], "hi": [.06, .06, 1.1, 45.0],
+                "interp": "bilinear", "border": "constant", "fill": (3, 4, 5), "mask_fill": 9},
+               {"kind": "RandomCrop", "size": (30, 20)}, {"kind": "HorizontalFlip", "p": 0.5}], (50, 60)),
+             ([{"kind": "Resize", "size": (37, 23), "interp": "nearest"}, {"kind": "ShiftHSV",
+               "lo": [-20, -.1, -.1], "hi": [20, .1, .1]}, {"kind": "Equalize"}], (61, 44)),
+             ([{"kind": "ElasticTransform", "lo": [30.0, 3.0], "hi": [30.0, 3.0], "interp": "nearest"},
+               {"kind": "Rotate90", "lo": [1], "hi": [1]}, {"kind": "PadToSize", "size": (70, 50)},
+               {"kind": "Grayscale"}], (40, 33))]
+    for specs, (h, w) in cases:
+        img = rand_img(h, w, rng=rng)
+        mask = rng.integers(0, 256, size=(h, w), dtype=np.uint8)
+        for seed in range(4):
+            a = A.apply(specs, seed, 3, img, mask)
+            b = A.apply_cand(specs, seed, 3, img, mask)
+            assert np.array_equal(a["image"], b["image"]) and np.array_equal(a["mask"], b["mask"])
+            for which, val in (("image", b["image"]), ("mask", b["mask"])):
+                cv, cn = b[which + "_cand"], b[which + "_cand_n"]
+                v3 = val.reshape(val.shape[0], val.shape[1], -1)
+                cv = cv.reshape(cv.shape[0], cv.shape[1], cv.shape[2], -1)
+                for y in range(v3.shape[0]):
+                    for x in range(v3.shape[1]):
+                        n = cn[y, x]
+                        assert n == 0 or any(np.array_equal(cv[y, x, k], v3[y, x]) for k in range(n))
+
+
+def test_cand_exact_ties_brute_force():
+    """Resize 4 -> 2 (nearest) samples x_s = (x + 0.5) 2 - 0.5 = 2x + 0.5:
+    every output is an exact .5 tie.  round_half_up picks
+    column 2x + 1; the candidate set is exactly {in[2x], in[2x+1]}, and an
+    HFlip afterwards moves the sets with the pixels (O2)."""
+    img = np.array([[[10, 11, 12], [20, 21, 22], [30, 31, 32], [40, 41, 42]]], np.uint8)
+    mask = np.array([[1, 2, 3, 4]], np.uint8)
+    rz = {"kind": "Resize", "size": (2, 1), "interp": "nearest"}
+    for specs, order in (([rz], [0, 1]), ([rz, {"kind": "HorizontalFlip"}], [1, 0])):
+        o = A.apply_cand(specs, 0, 0, img, mask)
+        for x, src in enumerate(order):
+            assert o["image"][0, x].tolist() == img[0, 2 * src + 1].tolist()
+            assert o["mask"][0, x] == mask[0, 2 * src + 1]
+            assert o["image_cand_n"][0, x] == 2 and o["mask_cand_n"][0, x] == 2
+            assert sorted(o["mask_cand"][0, x, :2].tolist()) == [mask[0, 2 * src], mask[0, 2 * src + 1]]
+            got = sorted(map(tuple, o["image_cand"][0, x, :2].tolist()))
+            assert got == sorted([tuple(img[0, 2 * src]), tuple(img[0, 2 * src + 1])])
+
+
+def test_cand_no_ties_on_integer_coordinates():
+    """Rotate 90 on a square image maps pixel centres onto pixel centres
+    (SPEC.md:196, 218): no source coordinate is near a tie, every set is the
+    singleton of the result."""
+    img = rand_img(31, 31)
+    mask = RNG.integers(0, 256, size=(31, 31), dtype=np.uint8)
+    o = A.apply_cand([{"kind": "Rotate", "lo": [90.0], "hi": [90.0], "interp": "nearest"}], 0, 0,
+                     img, mask)
+    assert (o["image_cand_n"] == 1).all() and (o["mask_cand_n"] == 1).all()
+    assert np.array_equal(o["mask"], np.rot90(mask, 1))
+
+
+def test_cand_band_rate_matches_survey():
+    """SSR on 512^2 (cfg3): the 1e-4 px band holds about 0.04% of the mask
+    pixels (SURVEY.md §8(c) tolerance table: 2 axes x 2e-4 of each unit)."""
+    img = rand_img(512, 512)
+    mask = RNG.integers(0, 256, size=(512, 512), dtype=np.uint8)
+    specs = [{"kind": "ShiftScaleRotate", "lo": [-.0625, -.0625, .9, -45.0],
+              "hi": [.0625, .0625, 1.1, 45.0], "interp": "bilinear", "border": "reflect_101"}]
+    rates = []
+    for seed in range(3):
+        o = A.apply_cand(specs, seed, 0, img, mask)
+        rates.append(float((o["mask_cand_n"] != 1).mean()))
+    assert 1e-4 < np.mean(rates) < 1e-3, rates
