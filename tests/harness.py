@@ -156,3 +156,45 @@ def cmp_boxes(res, ref, tol=1e-5):
         assert k == len(ref[i]["labels"]), (i, k, len(ref[i]["labels"]))
         assert np.array_equal(res["labels"][i, :k], ref[i]["labels"]), i
         assert np.abs(res["boxes"][i, :k] - ref[i]["boxes"]).max(initial=0) <= tol, i
+
+
+def resize_exact_ties(img, nh, nw):
+    """Per output element of a bilinear Resize of `img` (h, w, c) to nh x nw
+    (R9), True where the exact rational blend value is k + 1/2:
+    x_s = ((2d+1) W - nw) / (2 nw), so the value is N / (4 nw nh) with integer
+    N (integer arithmetic, no floating point).  At these ties round-half-up
+    is decided by each implementation's rounding of its inexact weights
+    (reading R33), so either neighbour is a correct result."""
+    img = img.astype(np.int64)
+    H, W = img.shape[:2]
+
+    def icoord(n_src, n_dst):
+        d = np.arange(n_dst)
+        num = (2 * d + 1) * n_src - n_dst
+        x0 = np.where(num <= 0, 0, num // (2 * n_dst))
+        wgt = np.where(num <= 0, 0, num % (2 * n_dst))
+        cl = x0 >= n_src - 1
+        return np.where(cl, n_src - 1, x0), np.where(cl, 0, wgt)
+
+    y0, wy = icoord(H, nh)
+    x0, wx = icoord(W, nw)
+    y1, x1 = np.minimum(y0 + 1, H - 1), np.minimum(x0 + 1, W - 1)
+    D = 4 * nw * nh
+    h0 = (2 * nw - wx)[None, :, None] * img[y0][:, x0] + wx[None, :, None] * img[y0][:, x1]
+    h1 = (2 * nw - wx)[None, :, None] * img[y1][:, x0] + wx[None, :, None] * img[y1][:, x1]
+    N = (2 * nh - wy)[:, None, None] * h0 + wy[:, None, None] * h1
+    return (2 * N) % (2 * D) == D
+
+
+def cmp_resize(gpu, ref, inputs, min_exact=0.999):
+    """Resize tolerance: max |d| <= 1 and >= min_exact exact, OR (structured
+    ratios, R33) every difference sits on an exact .5 tie of the blend."""
+    try:
+        return cmp_interp(gpu, ref, min_exact)
+    except AssertionError:
+        for g, r, im in zip(gpu, ref, inputs):
+            d = g.astype(np.int32) - r.astype(np.int32)
+            assert np.abs(d).max(initial=0) <= 1
+            tie = resize_exact_ties(im, g.shape[0], g.shape[1])
+            assert not ((d != 0) & ~tie).any(), int(((d != 0) & ~tie).sum())
+        return None

@@ -17,8 +17,8 @@ import torch
 
 from synth import configs as C
 from synth import gen
-from tests.harness import (cmp_boxes, cmp_cand, cmp_exact, cmp_interp, random_masks, run_gpu,
-                           run_oracle, run_oracle_cand)
+from tests.harness import (cmp_boxes, cmp_cand, cmp_exact, cmp_interp, cmp_resize, random_masks,
+                           run_gpu, run_oracle, run_oracle_cand)
 
 pytestmark = pytest.mark.gpu
 
@@ -49,7 +49,10 @@ def _run_all(specs, sizes, first, seed, min_vis, image_cmp):
     ref = run_oracle(specs, imgs, seed=seed, first=first, masks=mk, boxes=bx, labels=lb,
                      count=cnt, min_visibility=min_vis)
     cand = run_oracle_cand(specs, imgs, seed=seed, first=first, masks=mk)
-    image_cmp(res["images"], [o["image"] for o in ref])
+    if image_cmp == "resize":  # one Resize op: exact .5 ties of structured ratios (R33)
+        cmp_resize(res["images"], [o["image"] for o in ref], imgs)
+    else:
+        image_cmp(res["images"], [o["image"] for o in ref])
     cmp_cand(res["masks"], cand, "mask")
     cmp_boxes(res, ref)
     return res, ref
@@ -151,7 +154,8 @@ def test_boxes_image_mask_through_op(name, min_vis):
     sizes = gen.cfg2_sizes(20, first_image_index=700)
     exact = all(s["kind"] in ("HorizontalFlip", "VerticalFlip", "PadToSize", "RandomCrop", "Crop")
                 for s in specs)
-    _run_all(specs, sizes, 700, 31, min_vis, cmp_exact if exact else cmp_interp)
+    resize = len(specs) == 1 and specs[0]["kind"] == "Resize"
+    _run_all(specs, sizes, 700, 31, min_vis, "resize" if resize else cmp_exact if exact else cmp_interp)
 
 
 # ---------------------------------------------------------------- Normalize

@@ -15,7 +15,8 @@ import torch
 from synth import configs as C
 from synth import gen
 from tests.harness import (cmp_boxes, cmp_cand, cmp_exact, cmp_interp, out_batch, random_masks,
-                           run_gpu, run_oracle, run_oracle_cand, to_device_batch)
+                           resize_exact_ties, run_gpu, run_oracle, run_oracle_cand,
+                           to_device_batch)
 
 pytestmark = pytest.mark.gpu
 
@@ -611,25 +612,8 @@ def test_resize_structured_downscale_differs_only_at_exact_ties():
     b = gen.gen_images([(H, W)], seed=12, first_image_index=77, device="cuda")
     specs = [{"kind": "Resize", "size": (nw, nh)}]
     g = run_gpu(specs, b, seed=5, first=77)["images"][0].astype(np.int64)
-    img = b.image(0).astype(np.int64)
     r = run_oracle(specs, [b.image(0)], seed=5, first=77, threads=1)[0]["image"].astype(np.int64)
-
-    def icoord(n_src, n_dst):  # x0 = floor(s), weight = remainder, s = ((2d+1) n_src - n_dst) / (2 n_dst)
-        d = np.arange(n_dst)
-        num = (2 * d + 1) * n_src - n_dst
-        x0 = np.where(num <= 0, 0, num // (2 * n_dst))
-        w = np.where(num <= 0, 0, num % (2 * n_dst))
-        cl = x0 >= n_src - 1
-        return np.where(cl, n_src - 1, x0), np.where(cl, 0, w)
-
-    y0, wy = icoord(H, nh)
-    x0, wx = icoord(W, nw)
-    y1, x1 = np.minimum(y0 + 1, H - 1), np.minimum(x0 + 1, W - 1)
-    D = 4 * nw * nh
-    h0 = (2 * nw - wx)[None, :, None] * img[y0][:, x0] + wx[None, :, None] * img[y0][:, x1]
-    h1 = (2 * nw - wx)[None, :, None] * img[y1][:, x0] + wx[None, :, None] * img[y1][:, x1]
-    N = (2 * nh - wy)[:, None, None] * h0 + wy[:, None, None] * h1
-    tie = (2 * N) % (2 * D) == D  # exact value v = N / D is k + 1/2
+    tie = resize_exact_ties(b.image(0), nh, nw)  # exact value N / (4 nw nh) is k + 1/2
     diff = g != r
     assert np.abs(g - r).max() <= 1
     assert not (diff & ~tie).any(), int((diff & ~tie).sum())

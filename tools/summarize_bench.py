@@ -1,6 +1,17 @@
-"""Print the per-transform lines of bench.py JSON outputs."""
+"""Print the per-transform lines of bench.py JSON outputs (and the composed configs)."""
 import json
 import sys
+
+
+def show(tag, d):
+    r = d["roofline"]
+    print("%s value=%.0f %s ms/step=%.3f roof=%s %.3f e2e=%s" % (
+        tag, d["value"], d["unit"][:40], d["ms_per_step"], r.get("kernel"), r["frac"],
+        (d.get("e2e") or {}).get("value")))
+    for k, v in (d.get("per_transform") or {}).items():
+        print("   %-24s %12.0f img/s %7.3f ms frac %.3f" % (k, v["images_per_s"], v["ms_per_apply"],
+                                                           v["frac_of_peak"]))
+
 
 for f in sys.argv[1:]:
     try:
@@ -8,7 +19,8 @@ for f in sys.argv[1:]:
     except Exception as e:  # noqa: BLE001
         print(f, "unreadable", e)
         continue
-    print("%s value=%.0f %s ms/step=%.3f roof=%s %.3f" % (f, d["value"], d["unit"][:40], d["ms_per_step"],
-          d["roofline"].get("kernel"), d["roofline"]["frac"]))
-    for k, v in (d.get("per_transform") or {}).items():
-        print("   %-24s %12.0f img/s %7.3f ms frac %.3f" % (k, v["images_per_s"], v["ms_per_apply"], v["frac_of_peak"]))
+    show(f, d)
+    for k, v in (d.get("composed") or {}).items():
+        show("  " + k, v)
+    if d.get("clocks"):
+        print("   clocks", d["clocks"])
