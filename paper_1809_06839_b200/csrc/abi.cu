@@ -90,6 +90,7 @@ struct PlanStep {
   int eq_slot = -1;
   float min_scale = 1.0f;
   int rs_ring = 0, rs_sw = 0, rs_hw = 0;  // separable resample parameters (0 = old kernel)
+  int rs_q = 0;                           // quad-column resample: staged rows per unit (0 = off)
   int g_r = 0, g_off = 0;                  // ElasticTransform radius, weights offset in d_gauss
   double alpha = 0.0;
 };
@@ -414,6 +415,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.rs_ring = st.rs_ring;
     a.rs_sw = st.rs_sw;
     a.rs_hw = st.rs_hw;
+    a.rs_q = st.rs_q;
     a.seed = seed;
     a.first_image = (uint32_t)first_image_index;
     a.gauss = P->d_gauss ? P->d_gauss + st.g_off : nullptr;
@@ -912,6 +914,34 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
           }
           if (o.kind == ALB_GRID_DISTORTION) ratio = cratio = grid_stretch(o);
           else cratio = (double)max_ww / o.out_w;
+          if (st.stages.empty() && !st.normalize) {
+            // quad-column kernel: units = (image, 128-column strip, group of
+            // bands of R rows); the window of R rows is staged once per band
+            const int sw = std::min(max_ww, (int)std::ceil(128.0 * cratio) + 3);
+            for (int R : {64, 32, 16, 8, 4}) {
+              const int rows = (int)std::ceil(R * ratio) + 3;  // window rows of R output rows
+              if (resample_q4_smem(0, rows, sw, R, false) > (size_t)40 * 1024) continue;
+              st.rs_q = rows;
+              st.rs_sw = sw;
+              st.unit_rows = R;
+              break;
+            }
+            if (st.rs_q > 0) {
+              const int R = st.unit_rows;
+              int max_h = 0;
+              for (int i = 0; i < P->n; ++i) max_h = std::max(max_h, dims[i][st.slot1].first);
+              st.rs_hw = std::max(1, std::min(4, (max_h + R - 1) / R));  // bands per unit
+              for (int i = 0; i < P->n; ++i) {
+                const int H = dims[i][st.slot1].first, W = dims[i][st.slot1].second;
+                const int nb = (H + R - 1) / R;
+                if ((W + 127) / 128 > 256) { st.rs_q = 0; st.units.clear(); break; }
+                for (int bg = 0; bg * st.rs_hw < nb; ++bg)
+                  for (int x = 0, c = 0; x < W; x += 128, ++c) st.units.push_back(make_int2(i, (bg << 8) | c));
+              }
+              if (st.rs_q > 0) break;
+              st.rs_hw = 0;
+            }
+          }
           const int sw = (std::min(max_ww, (int)std::ceil(256.0 * cratio) + 3)) | 1;
           int nl = 0;
           for (auto& sg : st.stages) nl += (sg.type == ST_LUT || sg.type == ST_EQ);

@@ -64,6 +64,8 @@ struct StepArgs {
   int32_t img0, n_img;  // image range [img0, n_img) of this launch (per-image kernels)
   int32_t rs_ring, rs_sw, rs_hw;  // separable resample: ring rows (0 = old kernel), staged row
                                    // stride (words), output rows per group
+  int32_t rs_q;                    // quad-column resample: staged window rows per unit (0 = off);
+                                   // rs_sw = window columns per 128-column strip, unit_rows = R
   uint64_t seed;                   // Philox key of this apply (ElasticTransform raw planes)
   uint32_t first_image;            // global index of image 0
   const double* gauss;             // ElasticTransform: normalised weights w[0..2 g_r] (R32)
@@ -80,6 +82,9 @@ constexpr int kElBand = 256;  // output rows per ElasticTransform unit
 
 // shared memory of the separable resample kernel (resample.cu)
 size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize);
+// shared memory of the quad-column resample kernel: `rows` staged window rows of
+// `sw` columns, R output rows per unit (resample.cu)
+size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normalize);
 
 constexpr int kGeoBytes = 128;
 

@@ -586,6 +586,271 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
   }
 }
 
+// ====================================================== quad-column path
+// Bilinear, no mask, no fused stages (rs_q > 0).  The same separable
+// arithmetic as k_resample_sep (every output byte is bit-identical to it),
+// organised so that the per-pixel work is only the vertical lerp, the
+// rounding and the store:
+//   * work unit = (image, strip of 128 output columns, group of rs_hw bands of
+//     R output rows); CTA of 4 warps.  The strip's column table (fp64,
+//     definition order) is built once per unit; per band the window rows are
+//     staged, then warp w walks the band's rows [wR/4, (w+1)R/4) in increasing
+//     window-row order, independently of the other warps;
+//   * lane l owns the 4 adjacent output columns 4l..4l+3 of the strip: its 12
+//     output bytes pack into 3 words (byte permutes) and go out as 32-bit
+//     stores (a warp row = 384 contiguous bytes);
+//   * the band's source window is staged as RGBx words straight from global
+//     (16-byte aligned 16-pixel runs, stored unconditionally into row
+//     margins), with one pad word every 32 words so the lanes' taps (4 columns
+//     apart) fall in distinct banks;
+//   * per lane the current horizontal lerps H0, H1 and D = H1 - H0 of its 4
+//     columns live in registers (blue channels of column pairs on the paired
+//     fp32 pipe); a new window row costs 2 taps + 3 byte permutes + 3 paired FP
+//     ops per column.
+#ifndef ALB_Q4_MINB
+#define ALB_Q4_MINB 5  // CTAs per SM the register budget is sized for (measured)
+#endif
+constexpr int kQThreads = 128;
+constexpr int kQWarps = kQThreads / 32;
+constexpr int kQCols = 128;  // strip width: 32 lanes x 4 columns
+constexpr int kQMargin = 17; // stage words left of window column 0 (runs start >= 15 columns early)
+
+struct QRow {
+  float fy;
+  int s0, s1;  // window rows of the two taps (window frame)
+  int yo;      // output row
+};
+
+// staged words per window row of `sw` columns: left margin, padded columns
+// (one pad word per 32), right margin of a run
+// (odd, so consecutive staged rows start in different banks)
+__host__ __device__ inline int q_row_words(int sw) { return (kQMargin + (sw + 16) + (sw + 16) / 32 + 1) | 1; }
+
+__device__ __forceinline__ float2 f2neg(float2 v) { return make_float2(-v.x, -v.y); }
+
+template <int kOne, bool kNorm>
+__global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs a) {
+  extern __shared__ uint32_t sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const int R = a.unit_rows, SWP = q_row_words(a.rs_sw);
+  QRow* rowt = reinterpret_cast<QRow*>(sm);                 // [R]
+  int* win = reinterpret_cast<int*>(rowt + R);              // sxa, sxb
+  float4* colt = reinterpret_cast<float4*>(win + 4);        // [128] (x0, x1, fx) per column
+  uint32_t* stage = reinterpret_cast<uint32_t*>(colt + kQCols);  // [rows][SWP]
+
+  const int2 unit = a.units[blockIdx.x];
+  const int img = unit.x, bgrp = unit.y >> 8, strip = unit.y & 255;
+  const RsGeom g = rs_geom(a, img);
+  const int Wo = a.ddesc[img].width, Ho = a.ddesc[img].height;
+  const Map1 m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, Wo, Ho);
+  const int xs0 = strip * kQCols, cw = min(kQCols, Wo - xs0);
+  // column table: one strip column per thread (fp64, definition order O5)
+  double csx = 0.0, cf = 0.0;
+  if (tid < cw) {
+    csx = g_cx(g, m.ax * (xs0 + tid) + m.bx);
+    cf = floor(csx);
+  }
+  if (tid == 0 || tid == cw - 1) {  // the column map is monotone: the ends bound the window
+    const int lo = (int)cf, hi = min((int)cf + 1, g.ww - 1) + 1;
+    if (m.ax > 0) { if (tid == 0) win[0] = lo; if (tid == cw - 1) win[1] = hi; }
+    else { if (tid == 0) win[1] = hi; if (tid == cw - 1) win[0] = lo; }
+  }
+  __syncthreads();
+  const int sxa = win[0], sxb = win[1];
+  if (tid < cw) {  // (x0, x1) relative to the window origin, as padded word indices
+    const int x0 = (int)cf - sxa, x1 = min((int)cf + 1, g.ww - 1) - sxa;
+    colt[tid] = make_float4(__int_as_float(x0 + (x0 >> 5)), __int_as_float(x1 + (x1 >> 5)),
+                            (float)__dsub_rn(csx, cf), 0.f);
+  }
+  __syncthreads();
+  // this lane's 4 columns: tap byte offsets (row 0) and weights
+  uint32_t ta0[4], ta1[4];
+  float fx[4];
+  {
+    const uint32_t sbase = smem_u32(stage) + 4u * kQMargin;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 e = colt[min(4 * lane + k, cw - 1)];
+      ta0[k] = sbase + 4u * (uint32_t)__float_as_int(e.x);
+      ta1[k] = sbase + 4u * (uint32_t)__float_as_int(e.y);
+      fx[k] = e.z;
+    }
+  }
+  const alb_image_desc sd = a.sdesc[img];
+  const int X0 = g.wx0 + sxa, X1 = g.wx0 + sxb;  // absolute source columns of the window
+  const int nrun = (X1 - X0 + 30) >> 4;
+  uint8_t* gbase;
+  int dpitch;
+  {
+    const alb_image_desc dd = a.ddesc[img];
+    gbase = a.dst + dd.offset + (size_t)(xs0 + 4 * lane) * 3;
+    dpitch = dd.pitch;
+  }
+  const bool full = 4 * lane + 3 < cw;  // all 4 columns inside the strip
+  const bool aligned = ((uintptr_t)gbase & 3) == 0 && (dpitch & 3) == 0;
+  const int RW = (R + kQWarps - 1) / kQWarps;
+
+  // horizontal lerps of staged row `sr` for the 4 columns:
+  //   H = fma(fx, P1 - P0, P0 + 0.5)  (R, G paired per column; B paired per column pair)
+  auto hrow = [&](int sr, float2 (&hrg)[4], float2 (&hb)[2]) {
+    const uint32_t roff = 4u * (uint32_t)(sr * SWP);
+    constexpr uint32_t kM = 0x4B000000u;
+    auto cv = [](uint32_t t, uint32_t ch) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | ch)); };
+    const float2 nMh = make_float2(-8388607.5f, -8388607.5f);
+    uint32_t t0[4], t1[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t0[k]) : "r"(ta0[k] + roff));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t1[k]) : "r"(ta1[k] + roff));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 P0 = make_float2(cv(t0[k], 0), cv(t0[k], 1)), P1 = make_float2(cv(t1[k], 0), cv(t1[k], 1));
+      hrg[k] = __ffma2_rn(make_float2(fx[k], fx[k]), __fadd2_rn(P1, f2neg(P0)), __fadd2_rn(P0, nMh));
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float2 B0 = make_float2(cv(t0[2 * q], 2), cv(t0[2 * q + 1], 2));
+      const float2 B1 = make_float2(cv(t1[2 * q], 2), cv(t1[2 * q + 1], 2));
+      hb[q] = __ffma2_rn(make_float2(fx[2 * q], fx[2 * q + 1]), __fadd2_rn(B1, f2neg(B0)), __fadd2_rn(B0, nMh));
+    }
+  };
+
+  const int nb_img = (Ho + R - 1) / R;
+  const int b0 = bgrp * a.rs_hw, b1 = min(b0 + a.rs_hw, nb_img);
+  for (int band = b0; band < b1; ++band) {
+    const int y0 = band * R, nr = min(R, Ho - y0);
+    if (band > b0) __syncthreads();  // previous band's rows and stage fully consumed
+    for (int i = tid; i < nr; i += kQThreads) {  // row table in increasing window-row order
+      const int yo = m.ay > 0 ? y0 + i : y0 + nr - 1 - i;
+      const double sy = g_cy(g, m.ay * yo + m.by);
+      const double f = floor(sy);
+      QRow e;
+      e.fy = (float)__dsub_rn(sy, f);
+      e.s0 = (int)f;
+      e.s1 = min((int)f + 1, g.wh - 1);
+      e.yo = yo;
+      rowt[i] = e;
+    }
+    __syncthreads();
+    const int sya = rowt[0].s0, nrows = rowt[nr - 1].s1 - sya + 1;
+    {  // stage window rows [sya, sya + nrows) x columns [X0, X1) as padded RGBx words
+      // (row-relative 32-bit byte offsets; each item = one 16-pixel run whose
+      // first byte is 16-byte aligned, only blocks meeting [bx0, bx1) loaded)
+      const uint32_t mr = magic_of((uint32_t)nrows);
+      const int bx0 = 3 * X0, bx1 = 3 * X1;
+      const uint8_t* ibase = a.src + sd.offset + (size_t)(g.wy0 + sya) * sd.pitch;
+      for (int it = tid; it < nrows * nrun; it += kQThreads) {
+        const int k = fdiv(it, mr), r = it - k * nrows;
+        const uint8_t* srow = ibase + (size_t)r * sd.pitch;
+        const int ph = (int)((uintptr_t)srow & 15);
+        const int xa = (11 * (16 - ph)) & 15;
+        const int xs = X0 - ((X0 - xa) & 15) + 16 * k;
+        if (xs >= X1) continue;
+        const int b = 3 * xs;  // 16-byte aligned in memory
+        uint32_t w[12];
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          uint4 z = make_uint4(0, 0, 0, 0);
+          if (b + 16 * v < bx1 && b + 16 * v + 16 > bx0) z = __ldg(reinterpret_cast<const uint4*>(srow + b + 16 * v));
+          w[4 * v] = z.x; w[4 * v + 1] = z.y; w[4 * v + 2] = z.z; w[4 * v + 3] = z.w;
+        }
+        // all 16 pixels (those outside the window land in the row's margins)
+        uint32_t* drow = stage + r * SWP + kQMargin;
+        const int base = xs - X0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = base + i;
+          drow[c + (c >> 5)] = rgbx_raw(w, i);
+        }
+      }
+    }
+    __syncthreads();
+    const int i0 = warp * RW, i1 = min(i0 + RW, nr);
+    // two register sets of horizontal lerps; p = 0: H0 = A, H1 = B; p = 1: H0 = B,
+    // H1 = A.  Advancing by one window row refills the old H0 set (no moves).
+    float2 A[4], B[4], d[4], Ab[2], Bb[2], db[2];
+    int p = 0, c0 = -1, c1 = -1;  // window rows of H0 / H1
+    auto emit = [&](const QRow& rw, const float2 (&h0)[4], const float2 (&hb0)[2]) {
+      // V = fma(fy, D, H0); out = floor(V) (round half up: H carries the +0.5)
+      const float2 fy2 = make_float2(rw.fy, rw.fy);
+      const float2 mg = make_float2(8388608.f, 8388608.f);
+      uint32_t rq[4], gq[4], bq[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 R2 = fadd2_rm(__ffma2_rn(fy2, d[k], h0[k]), mg);
+        rq[k] = __float_as_uint(R2.x);
+        gq[k] = __float_as_uint(R2.y);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float2 B2 = fadd2_rm(__ffma2_rn(fy2, db[q], hb0[q]), mg);
+        bq[2 * q] = __float_as_uint(B2.x);
+        bq[2 * q + 1] = __float_as_uint(B2.y);
+      }
+      if (4 * lane >= cw) return;
+      uint8_t* orow = gbase + (size_t)rw.yo * dpitch;
+      // R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3
+      const uint32_t w0 = __byte_perm(__byte_perm(rq[0], gq[0], 0x0040u), __byte_perm(bq[0], rq[1], 0x0040u), 0x5410u);
+      const uint32_t w1 = __byte_perm(__byte_perm(gq[1], bq[1], 0x0040u), __byte_perm(rq[2], gq[2], 0x0040u), 0x5410u);
+      const uint32_t w2 = __byte_perm(__byte_perm(bq[2], rq[3], 0x0040u), __byte_perm(gq[3], bq[3], 0x0040u), 0x5410u);
+      if (full && aligned) {
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(orow);
+        __stcs(o32, w0);
+        __stcs(o32 + 1, w1);
+        __stcs(o32 + 2, w2);
+      } else {
+        const uint32_t ws[3] = {w0, w1, w2};
+        const int nbytes = 3 * min(4, cw - 4 * lane);
+#pragma unroll
+        for (int j = 0; j < 12; ++j)
+          if (j < nbytes) orow[j] = (uint8_t)(ws[j >> 2] >> (8 * (j & 3)));
+      }
+    };
+    auto diff = [&](const float2 (&h1)[4], const float2 (&hb1)[2], const float2 (&h0)[4], const float2 (&hb0)[2]) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[k] = __fadd2_rn(h1[k], f2neg(h0[k]));  // D = H1 - H0
+      db[0] = __fadd2_rn(hb1[0], f2neg(hb0[0]));
+      db[1] = __fadd2_rn(hb1[1], f2neg(hb0[1]));
+    };
+    for (int i = i0; i < i1; ++i) {
+      const QRow rw = rowt[i];
+      if (rw.s0 != c0 || rw.s1 != c1) {  // warp-uniform
+        if (rw.s0 == c1 && rw.s1 != rw.s0) {  // advance by one window row
+          p ^= 1;
+          if (p) { hrow(rw.s1 - sya, A, Ab); diff(A, Ab, B, Bb); }
+          else { hrow(rw.s1 - sya, B, Bb); diff(B, Bb, A, Ab); }
+        } else {
+          p = 0;
+          hrow(rw.s0 - sya, A, Ab);
+          if (rw.s1 != rw.s0) hrow(rw.s1 - sya, B, Bb);
+          else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) B[k] = A[k];
+            Bb[0] = Ab[0]; Bb[1] = Ab[1];
+          }
+          diff(B, Bb, A, Ab);
+        }
+        c0 = rw.s0;
+        c1 = rw.s1;
+      }
+      if (p) emit(rw, B, Bb);
+      else emit(rw, A, Ab);
+    }
+  }
+}
+
+size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normalize) {
+  (void)n_lut_stages;
+  (void)normalize;
+  return (size_t)R * sizeof(QRow) + 16 + kQCols * 16 + (size_t)rows * q_row_words(sw) * 4;
+}
+
+static void launch_q4(const StepArgs& a, size_t smem, cudaStream_t s) {
+  persistent_grid((const void*)k_resample_q4<kStagesNone, false>, kQThreads, smem, a.n_units);  // smem attribute
+  k_resample_q4<kStagesNone, false><<<a.n_units, kQThreads, smem, s>>>(a);
+}
+
 size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize) {
   return (size_t)n_lut_stages * kLutWords * 4 + 128 + kSepMaxBand * sizeof(SepRow) + 256 + 16 +
          (size_t)((ring * sw + 3) & ~3) * 4 + 64 + (size_t)ring * sep_raw_pitch(sw) + 64 +
@@ -627,6 +892,10 @@ static void launch_resample_t(const StepArgs& a, size_t smem, cudaStream_t s) {
 void launch_resample(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
   const int mode = stage_mode(a);
+  if (a.rs_q > 0) {  // quad-column path: rs_q staged window rows, rs_sw window columns per unit
+    launch_q4(a, resample_q4_smem(0, a.rs_q, a.rs_sw, a.unit_rows, false), s);
+    return;
+  }
   if (a.rs_ring > 0) {  // separable path (planner checked capacity)
     const size_t smem = resample_sep_smem(count_lut_stages(a), a.rs_ring, a.rs_sw, a.rs_hw, a.normalize != 0);
     ALB_DISPATCH_STAGES(mode, launch_sep_t, a, smem, s)
