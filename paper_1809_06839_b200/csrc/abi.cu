@@ -379,7 +379,8 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     }
   };
 
-  for (const PlanStep& st : P->steps) {
+  for (size_t si = 0; si < P->steps.size(); ++si) {
+    const PlanStep& st = P->steps[si];
     StepArgs a{};
     a.src = img_buf(st.src);
     a.sdesc = st.src_l ? st.src_l->d : nullptr;
@@ -477,6 +478,32 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
         }
         break;
       case SK_EQ: {
+        // single-pass Equalize when its LUT pass is a plain packed, co-aligned
+        // pointwise step holding only the Equalize stage (K8, one kernel)
+        if (si + 1 < P->steps.size()) {
+          const PlanStep& ap = P->steps[si + 1];
+          bool fuse = ap.kind == SK_POINT && ap.stages.size() == 1 && ap.stages[0].type == ST_EQ &&
+                      !ap.normalize && ap.flat && ap.src == st.src;
+          uint8_t* dst = img_buf(ap.dst);
+          for (int i = i0; i < i1 && fuse; ++i) {
+            const uintptr_t sp = (uintptr_t)a.src + st.src_l->h[i].offset;
+            const uintptr_t dp = (uintptr_t)dst + ap.dst_l->h[i].offset;
+            fuse = ((sp ^ dp) & 15) == 0;
+          }
+          if (fuse) {
+            StepArgs f = a;
+            f.dst = dst;
+            f.ddesc = ap.dst_l->d;
+            f.n_stages = 1;
+            f.stages[0] = ap.stages[0];
+            f.flat = 1;
+            f.vec_ok = 1;
+            f.normalize = 0;
+            launch_eq_fused(f, stream);
+            ++si;  // the LUT pass ran inside
+            break;
+          }
+        }
         EqArgs e{};
         e.src = a.src;
         e.sdesc = a.sdesc;

@@ -202,6 +202,9 @@ void side_join(cudaStream_t s);
 // kernel entry points (launch helpers live next to each kernel)
 void launch_prep(const PrepArgs& a, cudaStream_t s);
 void launch_point(const StepArgs& a, cudaStream_t s);
+// Equalize + its LUT pass in one kernel (one CTA per image; flat, co-aligned,
+// the pointwise step holding only the Equalize stage)
+void launch_eq_fused(const StepArgs& a, cudaStream_t s);
 void launch_rowgather(const StepArgs& a, cudaStream_t s);
 void launch_resample(const StepArgs& a, cudaStream_t s);
 void launch_affine(const StepArgs& a, cudaStream_t s);

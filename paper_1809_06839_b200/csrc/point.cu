@@ -322,6 +322,191 @@ static void launch_px(const StepArgs& a, size_t smem, cudaStream_t s) {
   else launch_px_n<kOne, false>(a, smem, s);
 }
 
+// ============================================== single-pass Equalize (K8)
+// Equalize then nothing else in the pointwise step, packed image rows, 16-byte
+// co-aligned buffers: ONE kernel, one CTA of 1024 threads per image.
+//   1. histogram: lane-private shared histograms hl[bin][lane] (conflict-free
+//      atomics, as k_eq_hist_lane), 16-byte loads that keep their lines in
+//      L2 (evict_last): the image is read from HBM once;
+//   2. per channel: the 256 counts are scanned (warp shuffles), c_min is the
+//      count of the first non-empty bin and LUT[v] = floor((2*255*max(cdf -
+//      c_min, 0) + D) / (2 D)), D = N - c_min, in 64-bit integers (identity
+//      when D == 0) -- the arithmetic of k_eq_lut / reading R15;
+//   3. the LUT is replicated per lane over the histogram's shared memory and
+//      the image is re-read (from L2, evict_first: last use) and written
+//      through the single-LUT byte path of k_point_lut.
+#ifndef ALB_EQF_THREADS
+#define ALB_EQF_THREADS 1024  // one CTA per SM (measured: 1024 x 1 beats 512 x 2, 0.49 vs 0.56 ms)
+#endif
+constexpr int kEqF = ALB_EQF_THREADS;
+constexpr size_t kEqFSmem = 8192 + 768 * 32 * 4 + 2 * 768 * 4 + 768;  // 8 KB alignment slack + hist + counts + prefixes + LUT
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_evict_last(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+
+__global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
+  extern __shared__ uint32_t sm_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t raw_addr = (uint32_t)__cvta_generic_to_shared(sm_raw);
+  uint32_t* hl = sm_raw + (((8192u - (raw_addr & 8191u)) & 8191u) >> 2);  // 8 KB aligned, [768][32]
+  uint32_t* cnt = hl + 768 * 32;                                          // [768]
+  uint32_t* pre = cnt + 768;                                              // [768]
+  uint8_t* lut8 = reinterpret_cast<uint8_t*>(pre + 768);                  // [768]
+  __shared__ uint32_t wsum[24];
+  __shared__ int first[3];
+  const int img = a.img0 + blockIdx.x;  // one CTA per image of the launch range
+  const alb_image_desc sd = a.sdesc[img];
+  const uint8_t* src = a.src + sd.offset;
+  const int n = sd.height * sd.width * 3;
+  for (int i = tid; i < 768 * 32; i += kEqF) hl[i] = 0;
+  if (tid < 3) first[tid] = 256;
+  __syncthreads();
+  // ---- 1. histogram
+  {
+    uint32_t* hw = hl + lane;
+    const uint32_t hl_base = (uint32_t)__cvta_generic_to_shared(hl) + 4u * (uint32_t)lane;
+    int bA = (int)((16 - ((uintptr_t)src & 15)) & 15);
+    if (bA > n) bA = n;
+    const int bE = bA + ((n - bA) / 16) * 16;
+    for (int b = tid; b < bA; b += kEqF) atomicAdd(&hw[((b % 3) * 256 + src[b]) * 32], 1u);
+    for (int b = bE + tid; b < n; b += kEqF) atomicAdd(&hw[((b % 3) * 256 + src[b]) * 32], 1u);
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + bA);
+    const int nv = (bE - bA) / 16;
+    constexpr int kV = 4;  // vectors in flight per thread (64 KB per SM)
+    const uint64_t pol = policy_evict_last();
+    for (int v0 = tid; v0 < nv; v0 += kV * kEqF) {
+      uint4 t[kV];
+#pragma unroll
+      for (int k = 0; k < kV; ++k)
+        if (v0 + k * kEqF < nv) t[k] = ld_evict_last(s4 + v0 + k * kEqF, pol);
+#pragma unroll
+      for (int k = 0; k < kV; ++k) {
+        const int v = v0 + k * kEqF;
+        if (v >= nv) break;
+        const uint32_t w[4] = {t[k].x, t[k].y, t[k].z, t[k].w};
+        const int ph = (bA + 16 * v) % 3;
+        const uint32_t b0 = hl_base + (uint32_t)ph * 32768u;
+        const uint32_t b1 = hl_base + (uint32_t)(ph == 2 ? 0 : ph + 1) * 32768u;
+        const uint32_t b2 = hl_base + (uint32_t)(ph == 0 ? 2 : ph - 1) * 32768u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t cb = (j % 3 == 0) ? b0 : ((j % 3 == 1) ? b1 : b2);
+          const uint32_t xb = __byte_perm(w[j >> 2], 0u, 0x4440u + (uint32_t)(j & 3));
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(xb * 128u + cb) : "memory");
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- 2. counts, per-channel inclusive scan, c_min, LUT (bin t = 0..767:
+  //         channel c = t >> 8, value t & 255; the CTA's warps cover the bins in rounds)
+  for (int t = tid; t < 768; t += kEqF) {
+    uint32_t h = 0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) h += hl[t * 32 + ((l + t) & 31)];
+    uint32_t inc = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[t >> 5] = inc;
+    if (h > 0) atomicMin(&first[t >> 8], t & 255);
+    cnt[t] = h;
+    pre[t] = inc;  // inclusive prefix within the bin's warp-sized group
+  }
+  __syncthreads();
+  for (int t = tid; t < 768; t += kEqF) {
+    const int c = t >> 8, v = t & 255;
+    uint32_t inc = pre[t];
+    for (int w = c * 8; w < (t >> 5); ++w) inc += wsum[w];  // earlier groups of the channel
+    const int64_t N = (int64_t)sd.width * sd.height;
+    const int64_t cmin = first[c] < 256 ? (int64_t)cnt[c * 256 + first[c]] : 0;
+    const int64_t D = N - cmin;
+    int out;
+    if (D == 0) {
+      out = v;
+    } else {
+      int64_t num = (int64_t)inc - cmin;
+      if (num < 0) num = 0;
+      out = (int)((2 * 255 * num + D) / (2 * D));
+    }
+    lut8[t] = (uint8_t)out;
+  }
+  __syncthreads();
+  // ---- 3. lane-replicated LUT over the histogram, then the LUT pass
+  {
+    const uint32_t* t32 = reinterpret_cast<const uint32_t*>(lut8);
+    for (int idx = tid; idx < kLutWords; idx += kEqF) hl[idx] = t32[idx >> 5];
+  }
+  __syncthreads();
+  uint32_t* sm = hl;
+  StageCtx x;
+  init_stages(a, x);  // one ST_EQ stage at shared word 0
+  StepArgs ai = a;
+  ai.unit_size = n;  // the whole image is one segment
+  const Seg sg = make_seg(ai, make_int2(img, 0));
+  if (tid < kThreads) scalar_edges<kStagesGeneric>(ai, sg, x, sm, lane);
+  if (sg.bE <= sg.bA) return;
+  const uint32_t lb = (uint32_t)__cvta_generic_to_shared(sm) | (4u * lane);
+  const int nv = (sg.bE - sg.bA) / 16;
+  const uint4* s4 = reinterpret_cast<const uint4*>(sg.src + sg.bA);
+  uint4* d4 = reinterpret_cast<uint4*>(sg.dst + sg.bA);
+  for (int v0 = tid; v0 < nv; v0 += kEqF * kU) {
+    uint4 in[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int v = v0 + k * kEqF;
+      if (v < nv) in[k] = __ldcs(s4 + v);
+    }
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int v = v0 + k * kEqF;
+      if (v < nv) {
+        const int ph = v % 3;
+        uint32_t w[4] = {in[k].x, in[k].y, in[k].z, in[k].w};
+        const uint32_t c0 = lb + (uint32_t)ph * 8192u;
+        const uint32_t c1 = lb + (uint32_t)(ph == 2 ? 0 : ph + 1) * 8192u;
+        const uint32_t c2 = lb + (uint32_t)(ph == 0 ? 2 : ph - 1) * 8192u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t r[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int jj = q * 4 + j;
+            const uint32_t cb = (jj % 3 == 0) ? c0 : ((jj % 3 == 1) ? c1 : c2);
+            const uint32_t t = j == 0 ? (w[q] << 5) : mulhi_pow2(w[q], 37 - 8 * j);
+            const uint32_t addr = (t & 0x1F80u) | cb;
+            asm("ld.shared.u32 %0, [%1];" : "=r"(r[j]) : "r"(addr));
+          }
+          const uint32_t xs = w[q] & 0x03030303u;
+          const uint32_t y = xs | (xs >> 4) | 0x00400040u;
+          const uint32_t lo = __byte_perm(r[0], r[1], y);
+          const uint32_t hi = __byte_perm(r[2], r[3], y >> 16);
+          w[q] = __byte_perm(lo, hi, 0x5410u);
+        }
+        __stcs(d4 + v, make_uint4(w[0], w[1], w[2], w[3]));
+      }
+    }
+  }
+}
+
+void launch_eq_fused(const StepArgs& a, cudaStream_t s) {
+  const int n = a.n_img - a.img0;
+  if (n <= 0) return;
+  persistent_grid((const void*)k_eq_fused, kEqF, kEqFSmem, n);  // smem attribute
+  k_eq_fused<<<n, kEqF, kEqFSmem, s>>>(a);
+}
+
 void launch_point(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
   const int nl = count_lut_stages(a);

@@ -93,4 +93,6 @@ EXTRA_OPS = {"Rot90k1": [{"kind": "Rotate90", "lo": [1], "hi": [1]}],
              "D4e2": [{"kind": "D4", "lo": [2], "hi": [2]}],
              "Grid5": [{"kind": "GridDistortion", "lo": [-0.3], "hi": [0.3], "num_steps": 5}],
              "Elastic": [{"kind": "ElasticTransform", "lo": [34.0, 4.0], "hi": [34.0, 4.0], "border": "reflect_101"}],
-             "Grid5n": [{"kind": "GridDistortion", "lo": [-0.3], "hi": [0.3], "num_steps": 5, "interp": "nearest"}]}
+             "Grid5n": [{"kind": "GridDistortion", "lo": [-0.3], "hi": [0.3], "num_steps": 5, "interp": "nearest"}],
+             # SSR whose scale range reaches below 0.9: runs the one-CTA-per-tile affine kernel
+             "SSRgen": [op("ShiftScaleRotate", lo=[-0.0625, -0.0625, 0.89, -45.0], hi=SSR_HI, **WARP)]}
