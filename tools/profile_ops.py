@@ -1,5 +1,12 @@
-"""Run selected cfg2-menu transforms (or cfg3/4/5 pipelines) a few times on the
-full cfg2 corpus -- a small command for ncu captures (tools only)."""
+"""Run selected cfg2-menu transforms, or the composed configs, a few times --
+a small command for ncu captures (tools only).
+
+    python tools/profile_ops.py --ops Rotate,Resize512,cfg3:Rotate,cfg4,cfg5 [--reps R] [--n N]
+
+cfg2 names run on the first N images of the cfg2 corpus; "cfg3:<op>" runs the
+cfg3 op on 256 512x512 images with masks, "cfg4" the fused Compose on 1024
+500x375 images, "cfg5" the co-transform on 512 1024x1024 images with masks and
+boxes (the bench workloads)."""
 import argparse
 import os
 import sys
@@ -16,17 +23,44 @@ ap.add_argument("--ops", default="Rotate,Resize512,ShiftHSV,Grayscale")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--n", type=int, default=2000)
 a = ap.parse_args()
-sizes = gen.cfg2_sizes(a.n)
-b = gen.gen_images(sizes, seed=0, device="cuda")
-inl = Layout(b.desc, 3)
-for name in a.ops.split(","):
-    specs = C.EXTRA_OPS.get(name) or C.CFG2_MENU[name]
+
+
+def run(specs, sizes, masks=False, boxes=False):
+    n = len(sizes)
+    b = gen.gen_images(sizes, seed=0, device="cuda")
     p = Pipeline(specs)
     osz = [p.output_shape(h, w) for h, w in sizes]
-    ob = gen.empty_batch(osz, 3, "cuda")
-    plan = Plan(p, inl, Layout(ob.desc, 3))
+    norm = specs[-1]["kind"] == "Normalize"
+    ob = None if norm else gen.empty_batch(osz, 3, "cuda")
+    nchw = torch.empty((n, 3) + tuple(osz[0]), device="cuda") if norm else None
+    mi = mo = None
+    bx = None
+    if masks:
+        bxs, lb, cnt, mi = gen.gen_boxes(sizes, seed=0)
+        mi = mi.to("cuda")
+        mo = gen.empty_batch(osz, 1, "cuda")
+        if boxes:
+            bx = [torch.from_numpy(t).cuda() for t in (bxs, lb, cnt)]
+    plan = Plan(p, Layout(b.desc, 3), None if norm else Layout(ob.desc, 3),
+                None if mi is None else Layout(mi.desc, 1), None if mo is None else Layout(mo.desc, 1),
+                C.CFG5_MAX_BOXES if bx else 0, C.CFG5_MIN_VISIBILITY if bx else 0.0)
     ws = plan.workspace()
+    bo = [torch.empty_like(t) for t in bx] if bx else [None] * 3
+    bi = bx or [None] * 3
     for r in range(a.reps):
-        plan.apply(r, 0, b.buf, ob.buf, workspace=ws)
-torch.cuda.synchronize()
+        plan.apply(r, 0, b.buf, None if ob is None else ob.buf, nchw, None if mi is None else mi.buf,
+                   None if mo is None else mo.buf, bi[0], bi[1], bi[2], bo[0], bo[1], bo[2], workspace=ws)
+    torch.cuda.synchronize()
+
+
+for name in a.ops.split(","):
+    if name.startswith("cfg3:"):
+        run(C.CFG3_OPS[name[5:]], [(512, 512)] * C.CONFIGS[3]["n"], masks=True)
+    elif name == "cfg4":
+        run(C.CFG4_OPS, [(375, 500)] * C.CONFIGS[4]["n"])
+    elif name == "cfg5":
+        run(C.CFG5_OPS, [(1024, 1024)] * C.CONFIGS[5]["n"], masks=True, boxes=True)
+    else:
+        specs = C.EXTRA_OPS.get(name) or C.CFG2_MENU[name]
+        run(specs, gen.cfg2_sizes(a.n))
 print("ok")
