@@ -941,13 +941,24 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
           }
           if (o.kind == ALB_GRID_DISTORTION) ratio = cratio = grid_stretch(o);
           else cratio = (double)max_ww / o.out_w;
-          if (st.stages.empty() && !st.normalize) {
+          // stage program of the step (stage_mode of stages.cuh)
+          int qmode = kStagesNone;
+          if (st.stages.size() == 1) {
+            qmode = st.stages[0].type;
+          } else if (st.stages.size() == 2) {
+            const int t0 = st.stages[0].type, t1 = st.stages[1].type;
+            qmode = (t0 == ST_HSV && t1 == ST_LUT) ? kStagesHsvLut : (t0 == ST_LUT && t1 == ST_HSV) ? kStagesLutHsv : -1;
+          } else if (st.stages.size() > 2) {
+            qmode = -1;
+          }
+          if (resample_q4_program_ok(qmode)) {
             // quad-column kernel: units = (image, 128-column strip, group of
             // bands of R rows); the window of R rows is staged once per band
             const int sw = std::min(max_ww, (int)std::ceil(128.0 * cratio) + 3);
             for (int R : {64, 32, 16, 8, 4}) {
               const int rows = (int)std::ceil(R * ratio) + 3;  // window rows of R output rows
-              if (resample_q4_smem(0, rows, sw, R, false) > (size_t)40 * 1024) continue;
+              const int nl = (qmode == ST_LUT || qmode == kStagesHsvLut || qmode == kStagesLutHsv) ? 1 : 0;
+              if (resample_q4_smem(nl, rows, sw, R, st.normalize) > (size_t)40 * 1024) continue;
               st.rs_q = rows;
               st.rs_sw = sw;
               st.unit_rows = R;
@@ -959,7 +970,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
               for (int i = 0; i < P->n; ++i) max_h = std::max(max_h, dims[i][st.slot1].first);
               st.rs_hw = std::max(1, std::min(4, (max_h + R - 1) / R));  // bands per unit
               for (int i = 0; i < P->n; ++i) {
-                const int H = dims[i][st.slot1].first, W = dims[i][st.slot1].second;
+                const int H = dims[i][st.slot1].first, W = st.normalize ? P->out_w : dims[i][st.slot1].second;
                 const int nb = (H + R - 1) / R;
                 if ((W + 127) / 128 > 256) { st.rs_q = 0; st.units.clear(); break; }
                 for (int bg = 0; bg * st.rs_hw < nb; ++bg)

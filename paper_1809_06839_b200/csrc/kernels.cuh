@@ -85,6 +85,8 @@ size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normali
 // shared memory of the quad-column resample kernel: `rows` staged window rows of
 // `sw` columns, R output rows per unit (resample.cu)
 size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normalize);
+// stage programs the quad-column kernel runs (stage_mode values)
+bool resample_q4_program_ok(int mode);
 
 constexpr int kGeoBytes = 128;
 

@@ -628,11 +628,70 @@ __host__ __device__ inline int q_row_words(int sw) { return (kQMargin + (sw + 16
 
 __device__ __forceinline__ float2 f2neg(float2 v) { return make_float2(-v.x, -v.y); }
 
+// Stage programs of the quad kernel (kOne as apply_stages_t: none, one LUT,
+// HSV, gray, HSV -> LUT, LUT -> HSV) on 4 pixels, with the LUT as a compact
+// 3 x 256-byte table (the CTA handles one image): same values, no lane
+// replication (so the stage costs 768 bytes of shared memory, not 24 KB).
+struct QStages {
+  float dh, ds, dv;  // HSV stage
+  int on;            // HSV / gray gate
+  int hsv_first;     // HSV -> LUT (1) or LUT -> HSV (0)
+};
+
+template <int kOne>
+__device__ __forceinline__ void q_stages(const QStages& q, const uint8_t* lut8, uint32_t (&r)[4], uint32_t (&g)[4],
+                                         uint32_t (&b)[4]) {
+  auto lut = [&]() {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      r[k] = lut8[r[k]];
+      g[k] = lut8[256 + g[k]];
+      b[k] = lut8[512 + b[k]];
+    }
+  };
+  auto hsv = [&]() {
+    if (!q.on) return;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t r2[2] = {r[2 * h], r[2 * h + 1]}, g2[2] = {g[2 * h], g[2 * h + 1]}, b2[2] = {b[2 * h], b[2 * h + 1]};
+      hsv_shift_px2(q.dh, q.ds, q.dv, r2, g2, b2);
+      r[2 * h] = r2[0]; r[2 * h + 1] = r2[1];
+      g[2 * h] = g2[0]; g[2 * h + 1] = g2[1];
+      b[2 * h] = b2[0]; b[2 * h + 1] = b2[1];
+    }
+  };
+  if constexpr (kOne == ST_LUT) {
+    lut();
+  } else if constexpr (kOne == ST_HSV) {
+    hsv();
+  } else if constexpr (kOne == ST_GRAY) {
+    if (q.on) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = g[k] = b[k] = gray_px(r[k], g[k], b[k]);
+    }
+  } else if constexpr (kOne == kStagesHsvLut) {
+    hsv();
+    lut();
+  } else if constexpr (kOne == kStagesLutHsv) {
+    lut();
+    hsv();
+  }
+}
+
+__host__ __device__ inline bool q_stage_program_ok(int mode) {
+  return mode == kStagesNone || mode == ST_LUT || mode == ST_HSV || mode == ST_GRAY || mode == kStagesHsvLut ||
+         mode == kStagesLutHsv;
+}
+
+bool resample_q4_program_ok(int mode) { return q_stage_program_ok(mode); }
+
 template <int kOne, bool kNorm>
 __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int R = a.unit_rows, SWP = q_row_words(a.rs_sw);
+  float* nls = reinterpret_cast<float*>(sm + (a.rs_q * SWP + 3) / 4 * 4 + R * 4 + 4 + 4 * kQCols);  // [768] (kNorm)
+  uint8_t* lut8 = reinterpret_cast<uint8_t*>(nls + (kNorm ? 768 : 0));                                 // [768] (LUT stage)
   QRow* rowt = reinterpret_cast<QRow*>(sm);                 // [R]
   int* win = reinterpret_cast<int*>(rowt + R);              // sxa, sxb
   float4* colt = reinterpret_cast<float4*>(win + 4);        // [128] (x0, x1, fx) per column
@@ -641,7 +700,34 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
   const int2 unit = a.units[blockIdx.x];
   const int img = unit.x, bgrp = unit.y >> 8, strip = unit.y & 255;
   const RsGeom g = rs_geom(a, img);
-  const int Wo = a.ddesc[img].width, Ho = a.ddesc[img].height;
+  const int Wo = kNorm ? a.out_w : a.ddesc[img].width, Ho = kNorm ? a.out_h : a.ddesc[img].height;
+  QStages qs{0.f, 0.f, 0.f, 0, 0};
+  if constexpr (kOne != kStagesNone) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (s >= a.n_stages) break;
+      const Stage st = a.stages[s];
+      if (st.type == ST_LUT) {
+        const uint8_t* t = a.tab.luts + ((size_t)img * a.tab.n_luts + st.lut) * 768;
+        for (int i = tid; i < 192; i += kQThreads)
+          reinterpret_cast<uint32_t*>(lut8)[i] = __ldg(reinterpret_cast<const uint32_t*>(t) + i);
+      } else {  // HSV / gray: gate (+ params), as load_stages
+        qs.on = fired_of(a.tab, img, st.slot) ? 1 : 0;
+        if (st.type == ST_HSV) {
+          const double* q = prm_of(a.tab, img, st.slot);
+          double w = q[0] / 60.0;
+          w -= 6.0 * floor(w / 6.0);
+          qs.dh = (float)w;
+          qs.ds = (float)q[1];
+          qs.dv = (float)q[2];
+          qs.hsv_first = s == 0;
+        }
+      }
+    }
+  }
+  if constexpr (kNorm) {
+    for (int i = tid; i < 768; i += kQThreads) nls[i] = __ldg(a.tab.norm_lut + i);
+  }
   const Map1 m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, Wo, Ho);
   const int xs0 = strip * kQCols, cw = min(kQCols, Wo - xs0);
   // column table: one strip column per thread (fp64, definition order O5)
@@ -679,9 +765,9 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
   const alb_image_desc sd = a.sdesc[img];
   const int X0 = g.wx0 + sxa, X1 = g.wx0 + sxb;  // absolute source columns of the window
   const int nrun = (X1 - X0 + 30) >> 4;
-  uint8_t* gbase;
-  int dpitch;
-  {
+  uint8_t* gbase = nullptr;
+  int dpitch = 0;
+  if constexpr (!kNorm) {
     const alb_image_desc dd = a.ddesc[img];
     gbase = a.dst + dd.offset + (size_t)(xs0 + 4 * lane) * 3;
     dpitch = dd.pitch;
@@ -788,7 +874,32 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
         bq[2 * q] = __float_as_uint(B2.x);
         bq[2 * q + 1] = __float_as_uint(B2.y);
       }
+      if constexpr (kOne != kStagesNone || kNorm) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { rq[k] &= 0xffu; gq[k] &= 0xffu; bq[k] &= 0xffu; }
+      }
+      if constexpr (kOne != kStagesNone) q_stages<kOne>(qs, lut8, rq, gq, bq);
       if (4 * lane >= cw) return;
+      if constexpr (kNorm) {  // fp32 NCHW planes: one float4 per plane when 4 columns fit
+        const size_t plane = (size_t)Ho * Wo;
+        float* o = a.nchw + (size_t)img * 3 * plane + (size_t)rw.yo * Wo + xs0 + 4 * lane;
+        if (full && ((Wo & 3) == 0)) {
+          __stcs(reinterpret_cast<float4*>(o), make_float4(nls[rq[0]], nls[rq[1]], nls[rq[2]], nls[rq[3]]));
+          __stcs(reinterpret_cast<float4*>(o + plane),
+                 make_float4(nls[256 + gq[0]], nls[256 + gq[1]], nls[256 + gq[2]], nls[256 + gq[3]]));
+          __stcs(reinterpret_cast<float4*>(o + 2 * plane),
+                 make_float4(nls[512 + bq[0]], nls[512 + bq[1]], nls[512 + bq[2]], nls[512 + bq[3]]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (4 * lane + k < cw) {
+              __stcs(o + k, nls[rq[k]]);
+              __stcs(o + plane + k, nls[256 + gq[k]]);
+              __stcs(o + 2 * plane + k, nls[512 + bq[k]]);
+            }
+        }
+        return;
+      }
       uint8_t* orow = gbase + (size_t)rw.yo * dpitch;
       // R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3
       const uint32_t w0 = __byte_perm(__byte_perm(rq[0], gq[0], 0x0040u), __byte_perm(bq[0], rq[1], 0x0040u), 0x5410u);
@@ -841,14 +952,20 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
 }
 
 size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normalize) {
-  (void)n_lut_stages;
-  (void)normalize;
-  return (size_t)R * sizeof(QRow) + 16 + kQCols * 16 + (size_t)rows * q_row_words(sw) * 4;
+  // row table, window origin, column table, staged rows, [Normalize table], [compact LUT]
+  return (size_t)R * sizeof(QRow) + 16 + kQCols * 16 + (size_t)(rows * q_row_words(sw) + 3) / 4 * 16 +
+         (normalize ? 768 * 4 : 0) + (n_lut_stages ? 768 : 0);
 }
 
-static void launch_q4(const StepArgs& a, size_t smem, cudaStream_t s) {
-  persistent_grid((const void*)k_resample_q4<kStagesNone, false>, kQThreads, smem, a.n_units);  // smem attribute
-  k_resample_q4<kStagesNone, false><<<a.n_units, kQThreads, smem, s>>>(a);
+template <int kOne>
+static void launch_q4_t(const StepArgs& a, size_t smem, cudaStream_t s) {
+  if (a.normalize) {
+    persistent_grid((const void*)k_resample_q4<kOne, true>, kQThreads, smem, a.n_units);  // smem attribute
+    k_resample_q4<kOne, true><<<a.n_units, kQThreads, smem, s>>>(a);
+  } else {
+    persistent_grid((const void*)k_resample_q4<kOne, false>, kQThreads, smem, a.n_units);
+    k_resample_q4<kOne, false><<<a.n_units, kQThreads, smem, s>>>(a);
+  }
 }
 
 size_t resample_sep_smem(int n_lut_stages, int ring, int sw, int g, bool normalize) {
@@ -893,7 +1010,15 @@ void launch_resample(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
   const int mode = stage_mode(a);
   if (a.rs_q > 0) {  // quad-column path: rs_q staged window rows, rs_sw window columns per unit
-    launch_q4(a, resample_q4_smem(0, a.rs_q, a.rs_sw, a.unit_rows, false), s);
+    const size_t smem = resample_q4_smem(count_lut_stages(a), a.rs_q, a.rs_sw, a.unit_rows, a.normalize != 0);
+    switch (mode) {  // the planner admits only these programs (q_stage_program_ok)
+      case ST_LUT: launch_q4_t<ST_LUT>(a, smem, s); break;
+      case ST_HSV: launch_q4_t<ST_HSV>(a, smem, s); break;
+      case ST_GRAY: launch_q4_t<ST_GRAY>(a, smem, s); break;
+      case kStagesHsvLut: launch_q4_t<kStagesHsvLut>(a, smem, s); break;
+      case kStagesLutHsv: launch_q4_t<kStagesLutHsv>(a, smem, s); break;
+      default: launch_q4_t<kStagesNone>(a, smem, s); break;
+    }
     return;
   }
   if (a.rs_ring > 0) {  // separable path (planner checked capacity)

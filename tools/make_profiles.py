@@ -28,7 +28,9 @@ M = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
      'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum', 'launch__grid_size', 'launch__block_size']
 SCALE = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'nsecond': 1e-6, 'usecond': 1e-3, 'msecond': 1.0,
          'ns': 1e-6, 'us': 1e-3, 'ms': 1.0}
-KERNELS_PER_OP = {'Equalize': 2}  # k_eq_hist + the LUT apply
+KERNELS_PER_OP = {}  # kernels per transform in the capture order (Equalize is one fused kernel since r2)
+PEAK = json.load(open(os.path.join(ROOT, 'MEASURED_PEAKS.json')))['hbm_gbs'] if os.path.exists(
+    os.path.join(ROOT, 'MEASURED_PEAKS.json')) else 6650.0
 
 
 def num(v, unit):
@@ -36,7 +38,11 @@ def num(v, unit):
 
 
 def read_rep(rep):
-    out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    """kernels of an ncu report (.ncu-rep) or of its raw-page CSV (made on the box)"""
+    if rep.endswith('.csv'):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     res = []
@@ -57,12 +63,15 @@ def read_rep(rep):
 def main():
     args = sys.argv[1:]
     tag = args[0]
-    fulls, launches, benches = [], None, []
+    fulls, launches, benches, comps = [], None, [], []
     i = 1
     while i < len(args):
         if args[i] == '--full':
             rep, _, ops = args[i + 1].partition(':')
             fulls.append((rep, ops.split(',')))
+            i += 2
+        elif args[i] == '--comp':  # a report of other kernels: one table row per kernel
+            comps.append(args[i + 1])
             i += 2
         elif args[i] == '--launches':
             launches = args[i + 1]
@@ -119,6 +128,26 @@ def main():
                        '(ncu --set full, %s)' % tag)
         with open(tj, 'w') as f:
             json.dump(old, f, indent=1)
+    if comps:
+        cl = ['# ncu summary (%s): kernels of the composed configs and the next-row transforms' % tag, '',
+              '`ncu --set full --clock-control none`, one launch per kernel, cold L2 (see tools/gpu_r2_ncu.sh '
+              'for the commands: cfg3 Rotate with masks, cfg4 fused Compose, cfg5 co-transform with masks and '
+              'boxes; Rot90, GridDistortion, ElasticTransform on 500 cfg2 images).', '',
+              '| report | kernel | time ms | DRAM read MB | DRAM write MB | DRAM GB/s | frac of %.0f GB/s | '
+              'issue active %% | warps active %% | regs | warp-inst | FMA pipe %% | ALU pipe %% |' % PEAK,
+              '|---|---|---|---|---|---|---|---|---|---|---|---|---|']
+        for rep in comps:
+            for d in read_rep(rep):
+                t = d.get(M[0], 0.0)
+                rd = d.get(M[1], 0.0) / 1e6
+                wr = d.get(M[2], 0.0) / 1e6
+                gbs = (rd + wr) / t if t else 0.0
+                cl.append('| %s | %s | %.4f | %.1f | %.1f | %.0f | %.3f | %.1f | %.1f | %d | %.3g | %.1f | %.1f |' % (
+                    os.path.basename(rep).replace('_raw.csv', ''), d['name'].split('(')[0][:48], t, rd, wr, gbs,
+                    gbs / PEAK, d.get(M[4], 0.0), d.get(M[5], 0.0), int(d.get(M[6], 0)), d.get(M[7], 0.0),
+                    d.get(M[8], 0.0), d.get(M[9], 0.0)))
+        with open(os.path.join(out_dir, '%s_ncu_comp.md' % tag), 'w') as f:
+            f.write('\n'.join(cl) + '\n')
     if launches:
         t = defaultdict(float)
         c = defaultdict(int)
