@@ -129,7 +129,8 @@ __device__ __forceinline__ bool fired_of(const Tables& t, int img, int slot) {
 //      c = v - v s sat(2 - min(|k-2|, |k-8|, |k-14|)),
 //    the periodic form of SPEC.md:419's sector table sat(min(k', 4-k')),
 //    k' = k mod 6; h6 is moved down one period when >= 5 (exactly), which
-//    leaves k < 10 so the |k-14| term is never the minimum and is dropped;
+//    leaves h6 in [-1, 5), k < 10, so the |k-14| term is never the minimum;
+//    for R |k-2| >= 2 and for B |k-8| > 2, so only G needs two terms;
 //  * out = floor(255 c + 0.5) from the mantissa of a round-down add.
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -157,15 +158,18 @@ __device__ __forceinline__ void hsv_shift_px(float dh6w, float ds, float dv, uin
   const float s = __saturatef(fmaf(d, fminf(rcp_approx(mx), 2.f), ds));
   const float v = __saturatef(fmaf(mx, 1.f / 255.f, dv));
   const float vs = v * s;
-  auto chan = [&](float n) {  // k = h6 + n; offsets folded: k - 2, k - 8
-    const float m = fminf(fabsf(h6 + (n - 2.f)), fabsf(h6 + (n - 8.f)));
-    const float t = __saturatef(2.f - m);
+  // channel n: k = h6 + n, t = sat(2 - min(|k - 2|, |k - 8|)).  With h6 in
+  // [-1, 5): for R (n = 5) |k - 2| = h6 + 3 >= 2, for B (n = 1) |k - 8| =
+  // 7 - h6 > 2, so those terms can only give t = 0 -- the same value the
+  // other term gives there (exact; verified on every byte triple by the GPU
+  // parity tests) -- and R, B need one term each; G needs both.
+  auto out = [&](float t) {
     const float y = fmaf(255.f, fmaf(-vs, t, v), 0.5f);
     return __float_as_uint(__fadd_rd(y, M)) & 0xffu;
   };
-  r = chan(5.f);
-  g = chan(3.f);
-  b = chan(1.f);
+  r = out(__saturatef(2.f - fabsf(h6 + (5.f - 8.f))));
+  g = out(__saturatef(2.f - fminf(fabsf(h6 + (3.f - 2.f)), fabsf(h6 + (3.f - 8.f)))));
+  b = out(__saturatef(2.f - fabsf(h6 + (1.f - 2.f))));
 }
 
 // Two pixels at once on the paired fp32 pipe (FADD2 / FFMA2 / FMUL2 where
@@ -205,18 +209,20 @@ __device__ __forceinline__ void hsv_shift_px2b(float dh6w, float ds, float dv, f
   vv = make_float2(__saturatef(vv.x), __saturatef(vv.y));
   const float2 vs = __fmul2_rn(vv, sv);
   const float2 nvs = make_float2(-vs.x, -vs.y);
-  auto chan = [&](float n, uint32_t (&out)[2]) {
-    const float2 k2 = f2add(h6, make_float2(n - 2.f, n - 2.f));
-    const float2 k8 = f2add(h6, make_float2(n - 8.f, n - 8.f));
-    const float2 t = make_float2(__saturatef(2.f - fminf(fabsf(k2.x), fabsf(k8.x))),
-                                 __saturatef(2.f - fminf(fabsf(k2.y), fabsf(k8.y))));
+  // t per channel as hsv_shift_px (R and B need one term each, G both)
+  auto emit = [&](float2 t, uint32_t (&out)[2]) {
     const float2 y = f2fma(make_float2(255.f, 255.f), f2fma(nvs, t, vv), make_float2(0.5f, 0.5f));
     out[0] = __float_as_uint(__fadd_rd(y.x, M));
     out[1] = __float_as_uint(__fadd_rd(y.y, M));
   };
-  chan(5.f, ro);
-  chan(3.f, go);
-  chan(1.f, bo);
+  const float2 kr = f2add(h6, make_float2(5.f - 8.f, 5.f - 8.f));
+  emit(make_float2(__saturatef(2.f - fabsf(kr.x)), __saturatef(2.f - fabsf(kr.y))), ro);
+  const float2 kg2 = f2add(h6, make_float2(3.f - 2.f, 3.f - 2.f));
+  const float2 kg8 = f2add(h6, make_float2(3.f - 8.f, 3.f - 8.f));
+  emit(make_float2(__saturatef(2.f - fminf(fabsf(kg2.x), fabsf(kg8.x))),
+                   __saturatef(2.f - fminf(fabsf(kg2.y), fabsf(kg8.y)))), go);
+  const float2 kb = f2add(h6, make_float2(1.f - 2.f, 1.f - 2.f));
+  emit(make_float2(__saturatef(2.f - fabsf(kb.x)), __saturatef(2.f - fabsf(kb.y))), bo);
 }
 __device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, uint32_t (&r)[2], uint32_t (&g)[2],
                                               uint32_t (&b)[2]) {
