@@ -18,6 +18,10 @@
 
 using namespace alb;
 
+#ifndef ALB_Q4_BUDGET_KB
+#define ALB_Q4_BUDGET_KB 40  // shared-memory budget of one quad-resample CTA (sets the band height)
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -958,7 +962,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
             for (int R : {64, 32, 16, 8, 4}) {
               const int rows = (int)std::ceil(R * ratio) + 3;  // window rows of R output rows
               const int nl = (qmode == ST_LUT || qmode == kStagesHsvLut || qmode == kStagesLutHsv) ? 1 : 0;
-              if (resample_q4_smem(nl, rows, sw, R, st.normalize) > (size_t)40 * 1024) continue;
+              if (resample_q4_smem(nl, rows, sw, R, st.normalize) > (size_t)ALB_Q4_BUDGET_KB * 1024) continue;
               st.rs_q = rows;
               st.rs_sw = sw;
               st.unit_rows = R;
