@@ -898,28 +898,19 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
 // -- exactly the decision the fused masked kernel makes.  One
 // CTA per 64 x 64 output tile; labels are read straight from global (1 byte
 // per pixel, L1/L2 resident neighbourhood).
-__global__ void __launch_bounds__(kAfThreads) k_affine_mask(StepArgs a) {
-  const int2 unit = a.units[blockIdx.x];
-  const int img = unit.x;
-  __shared__ ImgState sis;  // per-image state, one word per thread
-  {
-    constexpr int kW = (int)sizeof(ImgState) / 4;
-    if (threadIdx.x < kW)
-      reinterpret_cast<uint32_t*>(&sis)[threadIdx.x] = __ldcg(
-          reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.geo) + (size_t)img * kGeoBytes) +
-          threadIdx.x);
-    __syncthreads();
-  }
-  const ImgState& is = sis;
+// kFast: a full 64 x 64 tile whose nearest taps all lie inside the source
+// mask (decided per tile from its fp64 corner coordinates, with a 1-pixel
+// margin): no border resolution, no row / column predicates.
+template <bool kFast>
+__device__ __forceinline__ void affine_mask_tile(const StepArgs& a, const ImgState& is, int img, int tx0, int ty0,
+                                                 int tw, int th) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
-  const int tw = min(kTileW, is.Wo - tx0), th = min(kTileH, is.Ho - ty0);
   const alb_image_desc msd = a.msdesc[img], mdd = a.mddesc[img];
   const uint8_t* msrc = a.msrc + msd.offset;
   uint8_t* mdst = a.mdst + mdd.offset + (size_t)ty0 * mdd.pitch + tx0;
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
   const float2 A14 = make_float2(is.Af[1], is.Af[3]);
-  const int ncol = tw > 32 ? 2 : 1;
+  const int ncol = kFast ? 2 : (tw > 32 ? 2 : 1);
   int xw[2];
 #pragma unroll
   for (int j = 0; j < 2; ++j) xw[j] = is.m.ax * min(tx0 + lane + 32 * j, is.Wo - 1) + is.m.bx;
@@ -934,7 +925,7 @@ __global__ void __launch_bounds__(kAfThreads) k_affine_mask(StepArgs a) {
   for (int i = 0; i < kR; ++i) {
     const int row = warp * kR + i;
     src_off[i][0] = src_off[i][1] = -1;
-    if (row >= th) continue;
+    if (!kFast && row >= th) continue;
     const int yw = is.m.ay * (ty0 + row) + is.m.by;
     if ((yw >> 4) != cur_cy) {
       cur_cy = yw >> 4;
@@ -957,10 +948,14 @@ __global__ void __launch_bounds__(kAfThreads) k_affine_mask(StepArgs a) {
       const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
       const int nx = aix[j] + (int)(__float_as_uint(tq.x) - kMagic15Bits) + (fr.x >= 0.5f ? 1 : 0);
       const int ny = aiy[j] + (int)(__float_as_uint(tq.y) - kMagic15Bits) + (fr.y >= 0.5f ? 1 : 0);
-      bool ri, ci;
-      const int yy = border_idx(ny, msd.height, reflect, ri);
-      const int xx = border_idx(nx, msd.width, reflect, ci);
-      src_off[i][j] = (ri && ci) ? yy * msd.pitch + xx : -1;
+      if constexpr (kFast) {
+        src_off[i][j] = ny * msd.pitch + nx;
+      } else {
+        bool ri, ci;
+        const int yy = border_idx(ny, msd.height, reflect, ri);
+        const int xx = border_idx(nx, msd.width, reflect, ci);
+        src_off[i][j] = (ri && ci) ? yy * msd.pitch + xx : -1;
+      }
     }
   }
   uint8_t v[kR][2];
@@ -968,16 +963,58 @@ __global__ void __launch_bounds__(kAfThreads) k_affine_mask(StepArgs a) {
   for (int i = 0; i < kR; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
-      v[i][j] = src_off[i][j] >= 0 ? __ldg(msrc + src_off[i][j]) : (uint8_t)a.mask_fill;
+      v[i][j] = (kFast || src_off[i][j] >= 0) ? __ldg(msrc + src_off[i][j]) : (uint8_t)a.mask_fill;
 #pragma unroll
   for (int i = 0; i < kR; ++i) {
     const int row = warp * kR + i;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int c = lane + 32 * j;
-      if (row < th && j < ncol && c < tw) mdst[(size_t)row * mdd.pitch + c] = v[i][j];
+      if (kFast || (row < th && j < ncol && c < tw)) mdst[(size_t)row * mdd.pitch + c] = v[i][j];
     }
   }
+}
+
+__global__ void __launch_bounds__(kAfThreads, 4) k_affine_mask(StepArgs a) {
+  const int2 unit = a.units[blockIdx.x];
+  const int img = unit.x;
+  __shared__ ImgState sis;  // per-image state, one word per thread
+  __shared__ int s_fast;
+  const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
+  {
+    constexpr int kW = (int)sizeof(ImgState) / 4;
+    const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.geo) +
+                                                             (size_t)img * kGeoBytes);
+    if (threadIdx.x < kW) reinterpret_cast<uint32_t*>(&sis)[threadIdx.x] = __ldcg(gsrc + threadIdx.x);
+    if (threadIdx.x == 32) {  // interior test from the tile's fp64 corners (1 px margin)
+      const ImgState& g = *reinterpret_cast<const ImgState*>(gsrc);
+      const int Wo = __ldcg(&g.Wo), Ho = __ldcg(&g.Ho);
+      const int tw = min(kTileW, Wo - tx0), th = min(kTileH, Ho - ty0);
+      int fast = tw == kTileW && th == kTileH;
+      if (fast) {
+        const int ax = __ldcg(&g.m.ax), bx = __ldcg(&g.m.bx), ay = __ldcg(&g.m.ay), by = __ldcg(&g.m.by);
+        double A[6];
+        for (int q = 0; q < 6; ++q) A[q] = __ldcg(&g.A[q]);
+        const double xa = ax * tx0 + bx, xb = ax * (tx0 + tw - 1) + bx;
+        const double ya = ay * ty0 + by, yb = ay * (ty0 + th - 1) + by;
+        double lx = 1e300, hx = -1e300, ly = 1e300, hy = -1e300;
+        for (int c = 0; c < 4; ++c) {
+          const double xw = (c & 1) ? xb : xa, yw = (c & 2) ? yb : ya;
+          const double sx = fma(A[0], xw, fma(A[1], yw, A[2])), sy = fma(A[3], xw, fma(A[4], yw, A[5]));
+          lx = fmin(lx, sx); hx = fmax(hx, sx); ly = fmin(ly, sy); hy = fmax(hy, sy);
+        }
+        const alb_image_desc msd = a.msdesc[img];
+        fast = floor(lx) - 1.0 >= 0.0 && floor(hx) + 2.0 <= (double)(msd.width - 1) && floor(ly) - 1.0 >= 0.0 &&
+               floor(hy) + 2.0 <= (double)(msd.height - 1);
+      }
+      s_fast = fast;
+    }
+    __syncthreads();
+  }
+  const ImgState& is = sis;
+  const int tw = min(kTileW, is.Wo - tx0), th = min(kTileH, is.Ho - ty0);
+  if (s_fast) affine_mask_tile<true>(a, is, img, tx0, ty0, tw, th);
+  else affine_mask_tile<false>(a, is, img, tx0, ty0, tw, th);
 }
 
 static size_t affine_smem(const StepArgs& a) {
