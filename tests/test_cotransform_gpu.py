@@ -190,3 +190,55 @@ def test_normalize_table_every_value_closed_form():
         m, s = Fraction(MEAN[c]), Fraction(STD[c])
         want = np.array([float((Fraction(v, 255) - m) / s) for v in range(256)], np.float32)
         assert np.array_equal(g[c, 0], want), c
+
+
+# ---------------------------- fused resample stage programs (quad-column kernel)
+
+STAGE_PROGRAMS = {
+    "lut": [C.op("Brightness", lo=[0.8], hi=[1.2])],
+    "hsv": [C.op("ShiftHSV", lo=[-20.0, -0.1, -0.1], hi=[20.0, 0.1, 0.1])],
+    "gray": [C.op("Grayscale", p=0.5)],
+    "hsv_lut": [C.op("ShiftHSV", lo=[-20.0, -0.1, -0.1], hi=[20.0, 0.1, 0.1]),
+                C.op("BrightnessContrast", lo=[0.8, 0.8], hi=[1.2, 1.2])],
+    "lut_hsv": [C.op("Gamma", lo=[0.8], hi=[1.2]),
+                C.op("ShiftHSV", lo=[-20.0, -0.1, -0.1], hi=[20.0, 0.1, 0.1], p=0.7)],
+}
+
+
+@pytest.mark.parametrize("norm", [False, True])
+@pytest.mark.parametrize("prog", list(STAGE_PROGRAMS))
+def test_resample_stage_programs_fused_equals_unfused(prog, norm):
+    """A resize followed by a pointwise program (and Normalize) runs as ONE
+    kernel; it must equal the chain of single-op GPU applies with the drawn
+    parameters fixed, bit for bit (reading R21 (i)), and the oracle at >= 99.9%
+    exact (R21 (iii))."""
+    from paper_1809_06839_b200 import Pipeline
+    rs = C.op("Resize", size=(256, 192), interp="bilinear")
+    tail = [C.op("Normalize", mean=MEAN, std=STD)] if norm else []
+    specs = [rs] + STAGE_PROGRAMS[prog] + tail
+    sizes = gen.cfg2_sizes(6, first_image_index=900)
+    b = gen.gen_images(sizes, seed=0, first_image_index=900, device="cuda")
+    fused = run_gpu(specs, b, seed=41, first=900)
+    prm, fired = Pipeline(specs).sample_params(41, 900, sizes)
+    imgs = [b.image(i) for i in range(len(sizes))]
+    from tests.harness import to_device_batch
+    for i in range(len(sizes)):
+        x = run_gpu([rs], to_device_batch([imgs[i]]))["out_batch"]
+        for k, o in enumerate(STAGE_PROGRAMS[prog], start=1):
+            if not fired[i, k]:
+                continue
+            q = [float(v) for v in prm[i, k, :3]]
+            fixed = dict(o, p=1.0, lo=q[:len(o.get("lo", []))], hi=q[:len(o.get("lo", []))])
+            x = run_gpu([fixed], x)["out_batch"]
+        if norm:
+            got = run_gpu(tail, x)["nchw"][0]
+            assert np.array_equal(got, fused["nchw"][i]), i
+        else:
+            assert np.array_equal(x.image(0), fused["images"][i]), i
+    ref = run_oracle(specs, imgs, seed=41, first=900)
+    if norm:
+        g = fused["nchw"]
+        r = np.stack([o["nchw"] for o in ref])
+        assert (g == r).mean() >= 0.999
+    else:
+        cmp_interp(fused["images"], [o["image"] for o in ref], max_abs=8 if "hsv" in prog else 1)
