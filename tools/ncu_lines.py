@@ -33,3 +33,6 @@ tots = sum(x[1] for x in res)
 print('total warp-inst %d, stall samples %d' % (tot, tots))
 for x in sorted(res, reverse=True)[:top]:
     print('%5.1f%% %5.1f%%  %s:%s  %s' % (100.0 * x[0] / tot, 100.0 * x[1] / max(tots, 1), x[2], x[3], x[4]))
+print('--- by stall samples')
+for x in sorted(res, key=lambda r: -r[1])[:top]:
+    print('%5.1f%% %5.1f%%  %s:%s  %s' % (100.0 * x[0] / tot, 100.0 * x[1] / max(tots, 1), x[2], x[3], x[4]))
