@@ -242,3 +242,69 @@ def test_resample_stage_programs_fused_equals_unfused(prog, norm):
         assert (g == r).mean() >= 0.999
     else:
         cmp_interp(fused["images"], [o["image"] for o in ref], max_abs=8 if "hsv" in prog else 1)
+
+
+# ----------------------------------------- CUDA-graph capture with side streams
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg5"])
+def test_masked_boxed_apply_captures_into_cuda_graph(cfg):
+    """alb_apply forks label / box work onto the plan's side stream and joins
+    it back; captured into a CUDA graph (fork / join become graph edges) and
+    replayed, images, masks and boxes equal the eager results."""
+    from paper_1809_06839_b200 import Layout, Pipeline, Plan
+    from tests.harness import out_batch
+    specs = C.CFG3_OPS["ShiftScaleRotate"] if cfg == "cfg3" else C.CFG5_OPS
+    sizes = [(512, 512)] * 4 if cfg == "cfg3" else [(1024, 1024)] * 3
+    b, bx, lb, cnt, masks = _targets(sizes, 60)
+    pipe = Pipeline(specs)
+    osz = [pipe.output_shape(h, w) for h, w in sizes]
+    ob, mo = out_batch(osz, 3), out_batch(osz, 1)
+    nb = bx.shape[1] if cfg == "cfg5" else 0
+    plan = Plan(pipe, Layout(b.desc, 3), Layout(ob.desc, 3), Layout(masks.desc, 1), Layout(mo.desc, 1), nb,
+                C.CFG5_MIN_VISIBILITY)
+    ws = plan.workspace()
+    bi = [torch.from_numpy(t).cuda() for t in (bx, lb, cnt)] if nb else [None] * 3
+    bo = [torch.full_like(t, -1) for t in bi] if nb else [None] * 3
+
+    def go(stream=None):
+        plan.apply(9, 60, b.buf, ob.buf, None, masks.buf, mo.buf, bi[0], bi[1], bi[2], bo[0], bo[1], bo[2],
+                   workspace=ws, stream=stream)
+
+    go()
+    torch.cuda.synchronize()
+    want = [ob.buf.clone(), mo.buf.clone()] + ([t.clone() for t in bo] if nb else [])
+    ob.buf.fill_(0xAB)
+    mo.buf.fill_(0xAB)
+    for t in (bo if nb else []):
+        t.fill_(-1)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        go(stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    got = [ob.buf, mo.buf] + (list(bo) if nb else [])
+    for x, y in zip(got, want):
+        assert torch.equal(x, y)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_plan_on_second_device_same_process():
+    """Launch caches (dynamic shared-memory attribute, occupancy, SM count) are
+    per device: a Rotate plan (large dynamic shared memory) on cuda:1 after one
+    on cuda:0 in the same process runs and matches cuda:0 bit for bit."""
+    from paper_1809_06839_b200 import Layout, Pipeline, Plan
+    specs = C.CFG2_MENU["Rotate"]
+    sizes = gen.cfg2_sizes(4)
+    outs = []
+    for dev in ("cuda:0", "cuda:1"):
+        with torch.cuda.device(dev):
+            b = gen.gen_images(sizes, seed=0, device=dev)
+            pipe = Pipeline(specs)
+            from tests.harness import out_batch
+            ob = out_batch([pipe.output_shape(h, w) for h, w in sizes], 3, device=dev)
+            plan = Plan(pipe, Layout(b.desc, 3), Layout(ob.desc, 3))
+            plan.apply(3, 0, b.buf, ob.buf, workspace=plan.workspace(dev))
+            torch.cuda.synchronize(dev)
+            outs.append(ob.buf.cpu())
+    assert torch.equal(outs[0], outs[1])
