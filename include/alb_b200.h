@@ -181,7 +181,10 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
                            int32_t max_boxes, float min_visibility, alb_plan** plan);
 void alb_plan_destroy(alb_plan* plan);
 alb_status alb_plan_workspace_size(const alb_plan* plan, size_t* bytes);
-/* Number of kernel launches one alb_apply of this plan enqueues. */
+/* Number of kernel launches one alb_apply of this plan enqueues (the
+ * single-pass Equalize counted as one launch: it is taken when the buffers
+ * are 16-byte co-aligned, as device allocations are; otherwise Equalize runs
+ * as histogram + LUT + LUT-pass kernels, two more). */
 int32_t alb_plan_num_launches(const alb_plan* plan);
 
 /* Apply the plan to one batch (device pointers): SPEC.md:482-490 apply(p,

@@ -95,6 +95,7 @@ struct PlanStep {
   float min_scale = 1.0f;
   int rs_ring = 0, rs_sw = 0, rs_hw = 0;  // separable resample parameters (0 = old kernel)
   int rs_q = 0;                           // quad-column resample: staged rows per unit (0 = off)
+  int self_sample = 0;                    // the kernel draws its images' params itself (no K0)
   int g_r = 0, g_off = 0;                  // ElasticTransform radius, weights offset in d_gauss
   double alpha = 0.0;
 };
@@ -347,7 +348,9 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
   pa.norm_slot = P->norm_slot;
   pa.grid = (double*)(ws + P->off_grid);
   pa.n_grid = P->n_grid;
-  launch_prep(pa, stream);
+  // K0, unless the plan's only step is an integer geometric map whose kernel
+  // draws its images' params itself (flips / crops / pads: one launch)
+  if (!(P->steps.size() == 1 && P->steps[0].self_sample)) launch_prep(pa, stream);
   if (P->max_boxes > 0) {  // (boxes only on full-range launches; side stream, beside the pixel steps)
     BoxArgs b{};
     b.boxes_in = boxes_in;
@@ -421,6 +424,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.rs_sw = st.rs_sw;
     a.rs_hw = st.rs_hw;
     a.rs_q = st.rs_q;
+    a.self_sample = st.self_sample;
     a.seed = seed;
     a.first_image = (uint32_t)first_image_index;
     a.gauss = P->d_gauss ? P->d_gauss + st.g_off : nullptr;
@@ -784,6 +788,12 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
     }
     return fail(ALB_E_UNKNOWN_OP, "unhandled op kind");
   }
+  // a lone integer-map step (flips, crops, pads) samples its own params: no
+  // LUT, Normalize table, grid knots or box tables are needed from K0
+#ifndef ALB_NO_SELF_SAMPLE
+  if (steps.size() == 1 && steps[0].kind == SK_ROW && P->n_luts == 0 && P->norm_slot < 0 && max_boxes == 0)
+    steps[0].self_sample = 1;
+#endif
   // LUT count per step must fit shared memory (<= 4 stages of 24 KB)
   for (auto& st : steps) {
     int nl = 0;
@@ -1030,6 +1040,11 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
     }
     total_units += st.units.size() + st.munits.size();
   }
+  // self-sampling pays only for few CTAs per image (every CTA draws its image's
+  // params; measured: RandomCrop64 0.021 -> 0.017 ms, but the flips and the
+  // pad, ~6 CTAs per image, 1-2% slower than one K0 launch)
+  for (auto& st : steps)
+    if (st.self_sample && st.units.size() > 2 * (size_t)std::max(P->n, 1)) st.self_sample = 0;
   // units are generated image by image: image i owns [ustart[i], ustart[i+1])
   for (auto& st : steps) {
     for (int pass = 0; pass < 2; ++pass) {
@@ -1087,13 +1102,17 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   P->off_mbuf[0] = take(max_minter + 64);
   P->off_mbuf[1] = take(max_minter + 64);
   P->ws_bytes = off;
-  // launches per apply
-  int L = 1;  // prep
-  for (auto& st : steps) {
+  // launches per apply (Equalize counted as the single-pass kernel when its
+  // LUT pass is a packed step -- buffers 16-byte co-aligned, as torch gives)
+  int L = (steps.size() == 1 && steps[0].self_sample) ? 0 : 1;  // prep
+  for (size_t si = 0; si < steps.size(); ++si) {
+    const PlanStep& st = steps[si];
     if (st.kind == SK_ROW || st.kind == SK_D4) {
       L += (st.has_image ? 1 : 0) + (st.has_mask ? 1 : 0);
     } else if (st.kind == SK_EQ) {
-      L += 2;
+      const bool fused = si + 1 < steps.size() && steps[si + 1].kind == SK_POINT && steps[si + 1].stages.size() == 1 &&
+                         !steps[si + 1].normalize && steps[si + 1].flat;
+      L += fused ? 0 : 2;  // the LUT pass (the next step) is the single-pass kernel when fused
     } else if (st.kind == SK_AFFINE) {  // setup + image kernel (+ label kernel beside the pipelined one)
       const bool generic = st.interp == ALB_INTERP_NEAREST || st.normalize || st.min_scale < 0.9f ||
                            st.unit_size < 14040;

@@ -64,6 +64,7 @@ struct StepArgs {
   int32_t img0, n_img;  // image range [img0, n_img) of this launch (per-image kernels)
   int32_t rs_ring, rs_sw, rs_hw;  // separable resample: ring rows (0 = old kernel), staged row
                                    // stride (words), output rows per group
+  int32_t self_sample;             // 1: the kernel draws its images' params itself (no K0 launch)
   int32_t rs_q;                    // quad-column resample: staged window rows per unit (0 = off);
                                    // rs_sw = window columns per 128-column strip, unit_rows = R
   uint64_t seed;                   // Philox key of this apply (ElasticTransform raw planes)
@@ -119,6 +120,91 @@ struct BoxArgs {
   Tables tab;
   const alb_op* ops;
 };
+
+// Gate + parameters of every slot of one image and the dims each slot sees
+// (O1: the gate is draw 0 of its slot, always drawn;
+// the params follow in the op's documented order; shape-changing ops update
+// the dims only when fired).  prm [n_ops][kMaxParams], fired [n_ops], dims
+// [n_ops + 1][2] (h, w).  Used by K0 (prep.cu) and, for pipelines whose only
+// step is an integer geometric map, by that step's kernel itself (no K0).
+__device__ __forceinline__ void sample_core(const alb_op* ops, int n_ops, uint64_t seed, uint32_t gi, int h, int w,
+                                            double* prm, uint8_t* fired, int32_t* dims) {
+  for (int k = 0; k < n_ops; ++k) {
+    const alb_op& o = ops[k];
+    double q[kMaxParams];
+#pragma unroll
+    for (int j = 0; j < kMaxParams; ++j) q[j] = 0.0;
+    const bool f = draw_u(seed, gi, k, 0) < o.p;  // gate: draw 0, always drawn
+    dims[2 * k + 0] = h;
+    dims[2 * k + 1] = w;
+    int nh = h, nw = w;
+    switch (o.kind) {
+      case ALB_ROTATE: case ALB_BRIGHTNESS: case ALB_CONTRAST: case ALB_GAMMA:
+        q[0] = urange(o.lo[0], o.hi[0], draw_u(seed, gi, k, 1));
+        break;
+      case ALB_BRIGHTNESS_CONTRAST:
+        for (int j = 0; j < 2; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(seed, gi, k, 1 + j));
+        break;
+      case ALB_SHIFT_RGB: case ALB_SHIFT_HSV:
+        for (int j = 0; j < 3; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(seed, gi, k, 1 + j));
+        break;
+      case ALB_SHIFT_SCALE_ROTATE:
+        for (int j = 0; j < 4; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(seed, gi, k, 1 + j));
+        break;
+      case ALB_RANDOM_CROP:
+        q[0] = (double)uint_draw(draw_u(seed, gi, k, 1), w - o.out_w + 1);
+        q[1] = (double)uint_draw(draw_u(seed, gi, k, 2), h - o.out_h + 1);
+        nh = o.out_h; nw = o.out_w;
+        break;
+      case ALB_CROP:
+        q[0] = (double)o.crop_x; q[1] = (double)o.crop_y;
+        nh = o.out_h; nw = o.out_w;
+        break;
+      case ALB_RANDOM_SIZED_CROP: {
+        const int ms = h < w ? h : w;
+        const int hi = o.max_side < ms ? o.max_side : ms;
+        const int side = o.min_side + uint_draw(draw_u(seed, gi, k, 1), hi - o.min_side + 1);
+        q[0] = (double)side;
+        q[1] = (double)uint_draw(draw_u(seed, gi, k, 2), w - side + 1);
+        q[2] = (double)uint_draw(draw_u(seed, gi, k, 3), h - side + 1);
+        nh = o.out_h; nw = o.out_w;
+        break;
+      }
+      case ALB_PAD_TO_SIZE: case ALB_RESIZE:
+        nh = o.out_h; nw = o.out_w;
+        break;
+      case ALB_ROT90: case ALB_D4:  // element, uniform over the integer range
+        q[0] = o.lo[0] + (double)uint_draw(draw_u(seed, gi, k, 1), (int)(o.hi[0] - o.lo[0]) + 1);
+        if ((int)q[0] & 1) { nh = w; nw = h; }
+        break;
+      default: break;  // GridDistortion knots: K0 (prep.cu)
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxParams; ++j) prm[(size_t)k * kMaxParams + j] = q[j];
+    fired[k] = f ? 1 : 0;
+    if (f) { h = nh; w = nw; }
+  }
+  dims[2 * n_ops + 0] = h;
+  dims[2 * n_ops + 1] = w;
+}
+
+// Per-image tables of ONE image in shared memory, sampled by the kernel itself
+// (StepArgs::self_sample): a Tables view whose image 0 is that image.
+struct SelfTables {
+  double prm[kMaxOps * kMaxParams];
+  uint8_t fired[kMaxOps];
+  int32_t dims[2 * (kMaxOps + 1)];
+};
+__device__ __forceinline__ Tables self_sample_tables(const StepArgs& a, int img, SelfTables& st) {
+  const alb_image_desc sd = a.channels == 3 ? a.sdesc[img] : a.msdesc[img];
+  sample_core(a.ops, a.tab.n_ops, a.seed, a.first_image + (uint32_t)img, sd.height, sd.width, st.prm, st.fired,
+              st.dims);
+  Tables t = a.tab;
+  t.params = st.prm;
+  t.fired = st.fired;
+  t.dims = st.dims;
+  return t;
+}
 
 // ±1 affine integer map output -> input with a valid output rectangle.
 struct Map1 {

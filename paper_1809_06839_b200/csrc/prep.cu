@@ -39,80 +39,28 @@ __device__ void grid_knots(const alb_op& o, uint64_t seed, uint32_t gi, int k, i
 }
 
 // gate + params of every slot of image i and the dims each slot sees (the
-// walk of DESIGN.md O1); sp / sf (may be null) receive copies for the LUT build
+// walk of DESIGN.md O1, sample_core in kernels.cuh); sp / sf (may be null)
+// receive copies for the LUT build
 __device__ void sample_image(const PrepArgs& a, int i, double (*sp)[kMaxParams], uint8_t* sf) {
   const uint32_t gi = a.first_image + (uint32_t)i;
-  int h = a.in_desc[i].height, w = a.in_desc[i].width;
+  double* prm = a.params + (size_t)i * a.n_ops * kMaxParams;
+  uint8_t* fired = a.fired + (size_t)i * a.n_ops;
+  int32_t* dims = a.dims + (size_t)i * (a.n_ops + 1) * 2;
+  sample_core(a.ops, a.n_ops, a.seed, gi, a.in_desc[i].height, a.in_desc[i].width, prm, fired, dims);
   int g_ord = 0;
   for (int k = 0; k < a.n_ops; ++k) {
     const alb_op& o = a.ops[k];
-    double q[kMaxParams];
-#pragma unroll
-    for (int j = 0; j < kMaxParams; ++j) q[j] = 0.0;
-    const bool fired = draw_u(a.seed, gi, k, 0) < o.p;  // gate: draw 0, always drawn
-    a.dims[((size_t)i * (a.n_ops + 1) + k) * 2 + 0] = h;
-    a.dims[((size_t)i * (a.n_ops + 1) + k) * 2 + 1] = w;
-    int nh = h, nw = w;
-    switch (o.kind) {
-      case ALB_ROTATE: case ALB_BRIGHTNESS: case ALB_CONTRAST: case ALB_GAMMA:
-        q[0] = urange(o.lo[0], o.hi[0], draw_u(a.seed, gi, k, 1));
-        break;
-      case ALB_BRIGHTNESS_CONTRAST:
-        for (int j = 0; j < 2; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(a.seed, gi, k, 1 + j));
-        break;
-      case ALB_SHIFT_RGB: case ALB_SHIFT_HSV:
-        for (int j = 0; j < 3; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(a.seed, gi, k, 1 + j));
-        break;
-      case ALB_SHIFT_SCALE_ROTATE:
-        for (int j = 0; j < 4; ++j) q[j] = urange(o.lo[j], o.hi[j], draw_u(a.seed, gi, k, 1 + j));
-        break;
-      case ALB_RANDOM_CROP:
-        q[0] = (double)uint_draw(draw_u(a.seed, gi, k, 1), w - o.out_w + 1);
-        q[1] = (double)uint_draw(draw_u(a.seed, gi, k, 2), h - o.out_h + 1);
-        nh = o.out_h; nw = o.out_w;
-        break;
-      case ALB_CROP:
-        q[0] = (double)o.crop_x; q[1] = (double)o.crop_y;
-        nh = o.out_h; nw = o.out_w;
-        break;
-      case ALB_RANDOM_SIZED_CROP: {
-        const int ms = h < w ? h : w;
-        const int hi = o.max_side < ms ? o.max_side : ms;
-        const int side = o.min_side + uint_draw(draw_u(a.seed, gi, k, 1), hi - o.min_side + 1);
-        q[0] = (double)side;
-        q[1] = (double)uint_draw(draw_u(a.seed, gi, k, 2), w - side + 1);
-        q[2] = (double)uint_draw(draw_u(a.seed, gi, k, 3), h - side + 1);
-        nh = o.out_h; nw = o.out_w;
-        break;
-      }
-      case ALB_PAD_TO_SIZE: case ALB_RESIZE:
-        nh = o.out_h; nw = o.out_w;
-        break;
-      case ALB_GRID_DISTORTION: {  // x factors: draws 1..n+1, y factors: n+2..2n+2
-        if (!a.grid) break;  // alb_sample_params: gates and params only
-        double* e = a.grid + ((size_t)i * a.n_grid + g_ord++) * kGridStride;
-        grid_knots(o, a.seed, gi, k, 1, w, e);
-        grid_knots(o, a.seed, gi, k, o.num_steps + 2, h, e + kGridAxis);
-        break;
-      }
-      case ALB_ROT90: case ALB_D4:  // element, uniform over the integer range
-        q[0] = o.lo[0] + (double)uint_draw(draw_u(a.seed, gi, k, 1), (int)(o.hi[0] - o.lo[0]) + 1);
-        if ((int)q[0] & 1) { nh = w; nw = h; }
-        break;
-      default: break;
+    if (o.kind == ALB_GRID_DISTORTION && a.grid) {  // x factors: draws 1..n+1, y factors: n+2..2n+2
+      double* e = a.grid + ((size_t)i * a.n_grid + g_ord++) * kGridStride;
+      grid_knots(o, a.seed, gi, k, 1, dims[2 * k + 1], e);
+      grid_knots(o, a.seed, gi, k, o.num_steps + 2, dims[2 * k], e + kGridAxis);
     }
-    double* dst = a.params + ((size_t)i * a.n_ops + k) * kMaxParams;
+    if (sp) {
 #pragma unroll
-    for (int j = 0; j < kMaxParams; ++j) {
-      dst[j] = q[j];
-      if (sp) sp[k][j] = q[j];
+      for (int j = 0; j < kMaxParams; ++j) sp[k][j] = prm[(size_t)k * kMaxParams + j];
     }
-    if (sf) sf[k] = fired ? 1 : 0;
-    a.fired[(size_t)i * a.n_ops + k] = fired ? 1 : 0;
-    if (fired) { h = nh; w = nw; }
+    if (sf) sf[k] = fired[k];
   }
-  a.dims[((size_t)i * (a.n_ops + 1) + a.n_ops) * 2 + 0] = h;
-  a.dims[((size_t)i * (a.n_ops + 1) + a.n_ops) * 2 + 1] = w;
 }
 
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {

@@ -112,7 +112,15 @@ __global__ void __launch_bounds__(kRgThreads, 6) k_rowgather(StepArgs a, uint32_
       sd = C == 3 ? a.sdesc[img] : a.msdesc[img];
       dd = C == 3 ? a.ddesc[img] : a.mddesc[img];
       Wo = dd.width; Ho = dd.height; Ws = sd.width;
-      if (threadIdx.x == 0) smap = compose_exact(a.ops, a.tab, img, a.slot0, a.slot1, Wo, Ho);
+      if (threadIdx.x == 0) {
+        if (a.self_sample) {  // the only step: draw this image's params here (no K0)
+          SelfTables st;
+          const Tables t = self_sample_tables(a, img, st);
+          smap = compose_exact(a.ops, t, 0, a.slot0, a.slot1, Wo, Ho);
+        } else {
+          smap = compose_exact(a.ops, a.tab, img, a.slot0, a.slot1, Wo, Ho);
+        }
+      }
       nbmax = 2 + Wo / NPX;
       mnb = magic_of((uint32_t)nbmax);
       __syncthreads();
@@ -208,7 +216,15 @@ __global__ void __launch_bounds__(kRgThreads) k_rowflip(StepArgs a) {
   const alb_image_desc sd = C == 3 ? a.sdesc[img] : a.msdesc[img];
   const alb_image_desc dd = C == 3 ? a.ddesc[img] : a.mddesc[img];
   const int Wo = dd.width, Ho = dd.height;
-  if (threadIdx.x == 0) smap = compose_exact(a.ops, a.tab, img, a.slot0, a.slot1, Wo, Ho);
+  if (threadIdx.x == 0) {
+    if (a.self_sample) {  // the only step: draw this image's params here (no K0)
+      SelfTables st;
+      const Tables t = self_sample_tables(a, img, st);
+      smap = compose_exact(a.ops, t, 0, a.slot0, a.slot1, Wo, Ho);
+    } else {
+      smap = compose_exact(a.ops, a.tab, img, a.slot0, a.slot1, Wo, Ho);
+    }
+  }
   __syncthreads();
   const Map1 m = smap;
   const uint8_t* sbase = (C == 3 ? a.src : a.msrc) + sd.offset;
