@@ -288,6 +288,36 @@ def timed_steps(W, seeds, stream, dist, dev):
     return float(t.item()), {l: [a.elapsed_time(b) / 1e3 for a, b in ev[l]] for l in labels}
 
 
+def graph_times(W, seeds, dev):
+    """Per transform: the step's applies (one per seed) captured into CUDA
+    graphs before timing, then replayed back to back between two events on a
+    side stream: the kernels without per-launch host overhead or gaps.
+    Returns {label: seconds per apply}."""
+    s = torch.cuda.Stream(dev)
+    out = {}
+    for label in W.menu:
+        graphs = []
+        for seed in seeds:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                W.apply(label, seed, s)
+            graphs.append(g)
+        for g in graphs:  # warm
+            g.replay()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            for g in graphs:
+                g.replay()
+            e1.record(s)
+        torch.cuda.synchronize()
+        out[label] = e0.elapsed_time(e1) / 1e3 / len(graphs)
+        del graphs
+    return out
+
+
 def e2e_run(W, args, stream, dist, dev, world):
     """The same metric end to end through the public API with HOST buffers:
     every step copies its inputs from pinned host memory and its results back,
@@ -400,6 +430,12 @@ def measure(cfg, args, dev, rank, world, dist, peak, peak_src, local):
                       "ms_per_apply": round(tot / len(ts) * 1e3, 4),
                       "ms_median": round(statistics.median(ts) * 1e3, 4),
                       "alg_GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
+    if args.graph:  # each apply replayed from a CUDA graph (launch-bound ops)
+        g_times = graph_times(W, seeds, dev)
+        for label in labels:
+            tg = g_times[label]
+            per[label]["ms_per_apply_graph"] = round(tg * 1e3, 4)
+            per[label]["frac_of_peak_graph"] = round(bytes_per[label] / len(seeds) / tg / 1e9 / peak, 4)
     dom = max(labels, key=lambda l: sum(op_times[l]))
     dom_gbs = bytes_per[dom] / sum(op_times[dom]) / 1e9
     traffic = None
@@ -462,6 +498,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="skip the per-transform CUDA-graph replay timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -9,8 +9,10 @@ def show(tag, d):
         tag, d["value"], d["unit"][:40], d["ms_per_step"], r.get("kernel"), r["frac"],
         (d.get("e2e") or {}).get("value")))
     for k, v in (d.get("per_transform") or {}).items():
-        print("   %-24s %12.0f img/s %7.3f ms frac %.3f" % (k, v["images_per_s"], v["ms_per_apply"],
-                                                           v["frac_of_peak"]))
+        print("   %-24s %12.0f img/s %7.3f ms frac %.3f%s" % (
+            k, v["images_per_s"], v["ms_per_apply"], v["frac_of_peak"],
+            "  graph %.3f ms frac %.3f" % (v["ms_per_apply_graph"], v["frac_of_peak_graph"])
+            if "ms_per_apply_graph" in v else ""))
 
 
 for f in sys.argv[1:]:
