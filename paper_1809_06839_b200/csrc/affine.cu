@@ -609,6 +609,10 @@ __device__ __forceinline__ void pipe_geom(const StepArgs& a, const GeomPre& pre,
       const float dy = (float)(vy[ord[e + 1]] - vy[ord[e]]);
       eiy[e] = dy != 0.f ? 1.f / dy : 0.f;
     }
+#ifdef ALB_AB_NOSPANS
+    for (int r = lane; r < fh; r += 32) { c->sx0[r] = 0; c->sx1[r] = (int16_t)fw; }
+    if (fh < 0)
+#endif
     for (int r = lane; r < fh; r += 32) {
       const float ya = (float)r - 1.01f, yb = (float)r + 1.01f;
       float xmn = 1e30f, xmx = -1e30f;
@@ -665,9 +669,11 @@ __device__ __forceinline__ void pipe_issue(const StepArgs& a, const TileCtx* c, 
       const uintptr_t g1 = (uintptr_t)(simg + (size_t)ry * sd.pitch + 3 * X1);
       const uintptr_t ga = g0 & ~(uintptr_t)15, gb = (g1 + 15) & ~(uintptr_t)15;
       const uint32_t d0 = smem_u32(raw + r * kRawPitch);
+#ifndef ALB_AB_NOFILL
       for (uintptr_t g = ga; g < gb; g += 16)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + (uint32_t)(g - ga)), "l"(g)
                      : "memory");
+#endif
     }
   }
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
@@ -721,10 +727,12 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
       if (u + 1 < u1) pipe_geom(a, pipe_prefetch(a, u + 1, lane), &ctx[(it_t + 1) % 3], &c, lane);
     } else {
       const int tid = threadIdx.x;
+#ifndef ALB_AB_NOCOPYOUT
       if (it_t > 0) {  // copy-out of the previous tile
         const TileCtx& p = ctx[(it_t + 2) % 3];
         copy_rows_out<kObFull, kCThreads>(p.drow0, p.dpitch, obuf, kObPitch, p.th, 3 * p.tw);
       }
+#endif
 #ifdef ALB_PROF
       { const long long t1 = clock64(); pr[6] += t1 - tq; tq = t1; }
 #endif
@@ -732,7 +740,11 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
         const double* A = c.is.A;
         const float A0f = c.is.Af[0], A3f = c.is.Af[2];
         const Map1 m = c.is.m;
+#ifdef ALB_AB_NOANCHOR
+        for (int e = tid; e < 0; e += kCThreads) {
+#else
         for (int e = tid; e < 64 * c.ncy; e += kCThreads) {
+#endif
           const int col = e & 63, q = e >> 6;
           const int xw = m.ax * min(c.tx0 + col, c.is.Wo - 1) + m.bx;
           const Anchor ae = cell_anchor(A, A0f, A3f, xw, c.cy0 + q);
@@ -752,7 +764,11 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
       const int Ws = sd.width, Hs = sd.height;
       const uint8_t* simg = a.src + sd.offset;
       // border columns from global (tiles at the image's left / right edge)
+#ifdef ALB_AB_NOBORDER
+      for (int it = tid; it < 0; it += kCThreads) {
+#else
       for (int it = tid; it < t.fh * t.P; it += kCThreads) {
+#endif
         const int j = fdiv(it, t.m_fh), r = it - j * t.fh;
         const int cc = j < t.ci0 ? j : t.ci1 + (j - t.ci0);
         if (cc < c.sx0[r] || cc >= c.sx1[r]) continue;
@@ -769,7 +785,11 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
       { const long long t1 = clock64(); pr[1] += t1 - tq; tq = t1; }
 #endif
       // raw RGB rows -> RGBx stage; thread -> (row = it % fh, run = it / fh)
+#ifdef ALB_AB_NORESTAGE
+      const int na = 0;
+#else
       const int na = t.fh * t.nrun;
+#endif
       for (int it = tid; it < na; it += kCThreads) {
         const int k = fdiv(it, t.m_fh), r = it - k * t.fh;
         const int X0 = t.fx0 + max((int)c.sx0[r], t.ci0), X1 = t.fx0 + min((int)c.sx1[r], t.ci1);
@@ -826,7 +846,11 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
       const uint8_t* drow0 = c.drow0;
       const int dpitch = c.dpitch;
       // two rows (row, row + kCW) per iteration: 4 independent pixels per lane
+#ifdef ALB_AB_NOCOMPUTE
+      for (int r0 = warp; r0 < 0; r0 += 2 * kCW) {
+#else
       for (int r0 = warp; r0 < th; r0 += 2 * kCW) {
+#endif
         const bool two = r0 + kCW < th;
         float dyl[2];
         int q[2];
