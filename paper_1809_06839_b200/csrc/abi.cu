@@ -19,7 +19,10 @@
 using namespace alb;
 
 #ifndef ALB_Q4_BUDGET_KB
-#define ALB_Q4_BUDGET_KB 40  // shared-memory budget of one quad-resample CTA (sets the band height)
+#define ALB_Q4_BUDGET_KB 72  // shared-memory budget of one quad-resample CTA (sets the band height)
+#endif
+#ifndef ALB_Q4_BANDS
+#define ALB_Q4_BANDS 8  // bands of one quad-resample unit (a CTA prefetches band b + 1 while computing b)
 #endif
 
 namespace {
@@ -982,7 +985,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
               const int R = st.unit_rows;
               int max_h = 0;
               for (int i = 0; i < P->n; ++i) max_h = std::max(max_h, dims[i][st.slot1].first);
-              st.rs_hw = std::max(1, std::min(4, (max_h + R - 1) / R));  // bands per unit
+              st.rs_hw = std::max(1, std::min(ALB_Q4_BANDS, (max_h + R - 1) / R));  // bands per unit
               for (int i = 0; i < P->n; ++i) {
                 const int H = dims[i][st.slot1].first, W = st.normalize ? P->out_w : dims[i][st.slot1].second;
                 const int nb = (H + R - 1) / R;

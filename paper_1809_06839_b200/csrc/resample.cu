@@ -599,21 +599,23 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
 //   * lane l owns the 4 adjacent output columns 4l..4l+3 of the strip: its 12
 //     output bytes pack into 3 words (byte permutes) and go out as 32-bit
 //     stores (a warp row = 384 contiguous bytes);
-//   * the band's source window is staged as RGBx words straight from global
-//     (16-byte aligned 16-pixel runs, stored unconditionally into row
-//     margins), with one pad word every 32 words so the lanes' taps (4 columns
-//     apart) fall in distinct banks;
+//   * the band's source window rows are copied raw (RGB bytes, the 16-byte
+//     aligned hull of each row) by cp.async into one of two buffers: band b + 1
+//     is in flight while band b computes (one CTA walks up to ALB_Q4_BANDS
+//     bands), so the global latency hides behind the arithmetic;
+//   * a column's two taps are the 6 bytes at 3 x0 in a staged row: three
+//     aligned 32-bit loads funnel-shifted by the row's byte phase (lane taps 12
+//     bytes = 3 words apart: distinct banks);
 //   * per lane the current horizontal lerps H0, H1 and D = H1 - H0 of its 4
 //     columns live in registers (blue channels of column pairs on the paired
-//     fp32 pipe); a new window row costs 2 taps + 3 byte permutes + 3 paired FP
-//     ops per column.
+//     fp32 pipe); a new window row costs 3 loads + 2 funnel shifts + 6 byte
+//     permutes + 3 paired FP ops per column.
 #ifndef ALB_Q4_MINB
-#define ALB_Q4_MINB 5  // CTAs per SM the register budget is sized for (measured)
+#define ALB_Q4_MINB 3  // CTAs per SM the register budget is sized for (measured: 3 x 72 KB)
 #endif
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kQCols = 128;  // strip width: 32 lanes x 4 columns
-constexpr int kQMargin = 17; // stage words left of window column 0 (runs start >= 15 columns early)
 
 struct QRow {
   float fy;
@@ -621,10 +623,9 @@ struct QRow {
   int yo;      // output row
 };
 
-// staged words per window row of `sw` columns: left margin, padded columns
-// (one pad word per 32), right margin of a run
-// (odd, so consecutive staged rows start in different banks)
-__host__ __device__ inline int q_row_words(int sw) { return (kQMargin + (sw + 16) + (sw + 16) / 32 + 1) | 1; }
+// raw staged row pitch (bytes): the 16-byte aligned hull of a window row of
+// `sw` columns (3 sw + 30 bytes) + the 3-word tap over-read, 16-byte multiple
+__host__ __device__ inline int q_raw_pitch(int sw) { return ((3 * sw + 30 + 12) + 15) & ~15; }
 
 __device__ __forceinline__ float2 f2neg(float2 v) { return make_float2(-v.x, -v.y); }
 
@@ -689,13 +690,14 @@ template <int kOne, bool kNorm>
 __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-  const int R = a.unit_rows, SWP = q_row_words(a.rs_sw);
-  float* nls = reinterpret_cast<float*>(sm + (a.rs_q * SWP + 3) / 4 * 4 + R * 4 + 4 + 4 * kQCols);  // [768] (kNorm)
-  uint8_t* lut8 = reinterpret_cast<uint8_t*>(nls + (kNorm ? 768 : 0));                                 // [768] (LUT stage)
-  QRow* rowt = reinterpret_cast<QRow*>(sm);                 // [R]
-  int* win = reinterpret_cast<int*>(rowt + R);              // sxa, sxb
-  float4* colt = reinterpret_cast<float4*>(win + 4);        // [128] (x0, x1, fx) per column
-  uint32_t* stage = reinterpret_cast<uint32_t*>(colt + kQCols);  // [rows][SWP]
+  const int R = a.unit_rows, RQ = a.rs_q, RP = q_raw_pitch(a.rs_sw);
+  QRow* rowt = reinterpret_cast<QRow*>(sm);                 // [2][R] (per band, double-buffered)
+  int* win = reinterpret_cast<int*>(rowt + 2 * R);          // sxa, sxb
+  float4* colt = reinterpret_cast<float4*>(win + 4);        // [128] (3 x0, fx) per column
+  int* rowph = reinterpret_cast<int*>(colt + kQCols);       // [2][RQ] byte phase of each staged row
+  uint8_t* raw = reinterpret_cast<uint8_t*>(rowph + ((2 * RQ + 3) & ~3));  // [2][RQ][RP] raw RGB rows (16-byte aligned)
+  float* nls = reinterpret_cast<float*>(raw + 2 * (size_t)RQ * RP + 16);  // [768] (kNorm)
+  uint8_t* lut8 = reinterpret_cast<uint8_t*>(nls + (kNorm ? 768 : 0));     // [768] (LUT stage)
 
   const int2 unit = a.units[blockIdx.x];
   const int img = unit.x, bgrp = unit.y >> 8, strip = unit.y & 255;
@@ -743,28 +745,29 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
   }
   __syncthreads();
   const int sxa = win[0], sxb = win[1];
-  if (tid < cw) {  // (x0, x1) relative to the window origin, as padded word indices
-    const int x0 = (int)cf - sxa, x1 = min((int)cf + 1, g.ww - 1) - sxa;
-    colt[tid] = make_float4(__int_as_float(x0 + (x0 >> 5)), __int_as_float(x1 + (x1 >> 5)),
-                            (float)__dsub_rn(csx, cf), 0.f);
+  if (tid < cw) {  // tap-0 byte offset in a staged row (the right tap is the next 3
+    // bytes; where it is clamped to the window's last column, x1 == x0 and the
+    // blend is P0 exactly, so the weight is set to 0 and the bytes read past
+    // the row's data do not matter)
+    const int x0 = (int)cf - sxa;
+    const bool clamped = (int)cf + 1 > g.ww - 1;
+    colt[tid] = make_float4(__int_as_float(3 * x0), clamped ? 0.f : (float)__dsub_rn(csx, cf), 0.f, 0.f);
   }
   __syncthreads();
-  // this lane's 4 columns: tap byte offsets (row 0) and weights
-  uint32_t ta0[4], ta1[4];
+  // this lane's 4 columns: tap byte offsets in a staged row and weights
+  uint32_t tb[4];
   float fx[4];
-  {
-    const uint32_t sbase = smem_u32(stage) + 4u * kQMargin;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 e = colt[min(4 * lane + k, cw - 1)];
-      ta0[k] = sbase + 4u * (uint32_t)__float_as_int(e.x);
-      ta1[k] = sbase + 4u * (uint32_t)__float_as_int(e.y);
-      fx[k] = e.z;
-    }
+  for (int k = 0; k < 4; ++k) {
+    const float4 e = colt[min(4 * lane + k, cw - 1)];
+    tb[k] = (uint32_t)__float_as_int(e.x);
+    fx[k] = e.y;
   }
   const alb_image_desc sd = a.sdesc[img];
   const int X0 = g.wx0 + sxa, X1 = g.wx0 + sxb;  // absolute source columns of the window
-  const int nrun = (X1 - X0 + 30) >> 4;
+  const int nch = (3 * (X1 - X0) + 30) >> 4;      // 16-byte chunks a staged row can span
+  const uint32_t mch = magic_of((uint32_t)nch);
+  const uint32_t raw_a = smem_u32(raw);
   uint8_t* gbase = nullptr;
   int dpitch = 0;
   if constexpr (!kNorm) {
@@ -778,35 +781,73 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
 
   // horizontal lerps of staged row `sr` for the 4 columns:
   //   H = fma(fx, P1 - P0, P0 + 0.5)  (R, G paired per column; B paired per column pair)
-  auto hrow = [&](int sr, float2 (&hrg)[4], float2 (&hb)[2]) {
-    const uint32_t roff = 4u * (uint32_t)(sr * SWP);
+  // the two taps of a column are the 6 bytes at (row data + 3 x0): three
+  // aligned words, funnel-shifted by the byte phase, give u0 = R0 G0 B0 R1 and
+  // u1 = G1 B1 . .
+  auto hrow = [&](uint32_t rbase, float2 (&hrg)[4], float2 (&hb)[2]) {
     constexpr uint32_t kM = 0x4B000000u;
     auto cv = [](uint32_t t, uint32_t ch) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | ch)); };
     const float2 nMh = make_float2(-8388607.5f, -8388607.5f);
-    uint32_t t0[4], t1[4];
+    uint32_t u0[4], u1[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t0[k]) : "r"(ta0[k] + roff));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t1[k]) : "r"(ta1[k] + roff));
+      const uint32_t o = rbase + tb[k], wa = o & ~3u;
+      uint32_t w0, w1, w2;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(wa));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w1) : "r"(wa + 4));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w2) : "r"(wa + 8));
+      u0[k] = __funnelshift_r(w0, w1, o << 3);
+      u1[k] = __funnelshift_r(w1, w2, o << 3);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float2 P0 = make_float2(cv(t0[k], 0), cv(t0[k], 1)), P1 = make_float2(cv(t1[k], 0), cv(t1[k], 1));
+      const float2 P0 = make_float2(cv(u0[k], 0), cv(u0[k], 1)), P1 = make_float2(cv(u0[k], 3), cv(u1[k], 0));
       hrg[k] = __ffma2_rn(make_float2(fx[k], fx[k]), __fadd2_rn(P1, f2neg(P0)), __fadd2_rn(P0, nMh));
     }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const float2 B0 = make_float2(cv(t0[2 * q], 2), cv(t0[2 * q + 1], 2));
-      const float2 B1 = make_float2(cv(t1[2 * q], 2), cv(t1[2 * q + 1], 2));
+      const float2 B0 = make_float2(cv(u0[2 * q], 2), cv(u0[2 * q + 1], 2));
+      const float2 B1 = make_float2(cv(u1[2 * q], 1), cv(u1[2 * q + 1], 1));
       hb[q] = __ffma2_rn(make_float2(fx[2 * q], fx[2 * q + 1]), __fadd2_rn(B1, f2neg(B0)), __fadd2_rn(B0, nMh));
     }
+  };
+  // window rows [sy0, sy0 + nrows) of band `band` (first / last output row in
+  // increasing window-row order, the same fp64 row coordinates as the table)
+  auto band_rows = [&](int band, int& sy0, int& nrows) {
+    const int y0 = band * R, nr = min(R, Ho - y0);
+    const int yf = m.ay > 0 ? y0 : y0 + nr - 1, yl = m.ay > 0 ? y0 + nr - 1 : y0;
+    sy0 = (int)floor(g_cy(g, m.ay * yf + m.by));
+    nrows = min((int)floor(g_cy(g, m.ay * yl + m.by)) + 1, g.wh - 1) - sy0 + 1;
+  };
+  // asynchronous copy of a band's window rows into raw buffer `bi`: row r's
+  // 16-byte aligned hull of [X0, X1) lands at raw[bi][r] + 16 k; its data
+  // starts at byte phase rowph[bi][r]
+  auto issue = [&](int band, int bi) {
+    int sy0, nrows;
+    band_rows(band, sy0, nrows);
+    const uint8_t* ibase = a.src + sd.offset + (size_t)(g.wy0 + sy0) * sd.pitch + 3 * X0;
+    const uint32_t rb = raw_a + (uint32_t)(bi * RQ * RP);
+    for (int it = tid; it < nrows * nch; it += kQThreads) {
+      const int r = fdiv(it, mch), kk = it - r * nch;
+      const uintptr_t g0 = (uintptr_t)(ibase + (size_t)r * sd.pitch);
+      const uintptr_t ga = g0 & ~(uintptr_t)15, gb = (g0 + 3 * (X1 - X0) + 15) & ~(uintptr_t)15;
+      if (kk == 0) rowph[bi * RQ + r] = (int)(g0 - ga);
+      if (ga + 16 * kk < gb)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(rb + (uint32_t)(r * RP + 16 * kk)),
+                     "l"(ga + 16 * kk)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
   const int nb_img = (Ho + R - 1) / R;
   const int b0 = bgrp * a.rs_hw, b1 = min(b0 + a.rs_hw, nb_img);
+  issue(b0, 0);
   for (int band = b0; band < b1; ++band) {
-    const int y0 = band * R, nr = min(R, Ho - y0);
-    if (band > b0) __syncthreads();  // previous band's rows and stage fully consumed
+    const int y0 = band * R, nr = min(R, Ho - y0), bi = (band - b0) & 1;
+    if (band > b0) __syncthreads();  // previous band's rows and raw buffer fully consumed
+    if (band + 1 < b1) issue(band + 1, bi ^ 1);  // lands while this band computes
+    QRow* rt = rowt + bi * R;
     for (int i = tid; i < nr; i += kQThreads) {  // row table in increasing window-row order
       const int yo = m.ay > 0 ? y0 + i : y0 + nr - 1 - i;
       const double sy = g_cy(g, m.ay * yo + m.by);
@@ -816,42 +857,15 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
       e.s0 = (int)f;
       e.s1 = min((int)f + 1, g.wh - 1);
       e.yo = yo;
-      rowt[i] = e;
+      rt[i] = e;
     }
+    if (band + 1 < b1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
-    const int sya = rowt[0].s0, nrows = rowt[nr - 1].s1 - sya + 1;
-    {  // stage window rows [sya, sya + nrows) x columns [X0, X1) as padded RGBx words
-      // (row-relative 32-bit byte offsets; each item = one 16-pixel run whose
-      // first byte is 16-byte aligned, only blocks meeting [bx0, bx1) loaded)
-      const uint32_t mr = magic_of((uint32_t)nrows);
-      const int bx0 = 3 * X0, bx1 = 3 * X1;
-      const uint8_t* ibase = a.src + sd.offset + (size_t)(g.wy0 + sya) * sd.pitch;
-      for (int it = tid; it < nrows * nrun; it += kQThreads) {
-        const int k = fdiv(it, mr), r = it - k * nrows;
-        const uint8_t* srow = ibase + (size_t)r * sd.pitch;
-        const int ph = (int)((uintptr_t)srow & 15);
-        const int xa = (11 * (16 - ph)) & 15;
-        const int xs = X0 - ((X0 - xa) & 15) + 16 * k;
-        if (xs >= X1) continue;
-        const int b = 3 * xs;  // 16-byte aligned in memory
-        uint32_t w[12];
-#pragma unroll
-        for (int v = 0; v < 3; ++v) {
-          uint4 z = make_uint4(0, 0, 0, 0);
-          if (b + 16 * v < bx1 && b + 16 * v + 16 > bx0) z = __ldg(reinterpret_cast<const uint4*>(srow + b + 16 * v));
-          w[4 * v] = z.x; w[4 * v + 1] = z.y; w[4 * v + 2] = z.z; w[4 * v + 3] = z.w;
-        }
-        // all 16 pixels (those outside the window land in the row's margins)
-        uint32_t* drow = stage + r * SWP + kQMargin;
-        const int base = xs - X0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int c = base + i;
-          drow[c + (c >> 5)] = rgbx_raw(w, i);
-        }
-      }
-    }
-    __syncthreads();
+    const int sya = rt[0].s0;
+    const uint32_t rb = raw_a + (uint32_t)(bi * RQ * RP);
+    const int* ph = rowph + bi * RQ;
+    auto rbase = [&](int s) { return rb + (uint32_t)((s - sya) * RP + ph[s - sya]); };
     const int i0 = warp * RW, i1 = min(i0 + RW, nr);
     // two register sets of horizontal lerps; p = 0: H0 = A, H1 = B; p = 1: H0 = B,
     // H1 = A.  Advancing by one window row refills the old H0 set (no moves).
@@ -905,6 +919,10 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
       const uint32_t w0 = __byte_perm(__byte_perm(rq[0], gq[0], 0x0040u), __byte_perm(bq[0], rq[1], 0x0040u), 0x5410u);
       const uint32_t w1 = __byte_perm(__byte_perm(gq[1], bq[1], 0x0040u), __byte_perm(rq[2], gq[2], 0x0040u), 0x5410u);
       const uint32_t w2 = __byte_perm(__byte_perm(bq[2], rq[3], 0x0040u), __byte_perm(gq[3], bq[3], 0x0040u), 0x5410u);
+#ifdef ALB_AB_Q4_NOSTORE
+      if (w0 == 0x12345678u && w1 == 0x9abcdef0u && w2 == 0x0fedcba9u) *orow = 1;
+      return;
+#endif
       if (full && aligned) {
         uint32_t* o32 = reinterpret_cast<uint32_t*>(orow);
         __stcs(o32, w0);
@@ -924,17 +942,21 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
       db[0] = __fadd2_rn(hb1[0], f2neg(hb0[0]));
       db[1] = __fadd2_rn(hb1[1], f2neg(hb0[1]));
     };
+#ifdef ALB_AB_Q4_NOCOMPUTE
+    for (int i = i0; i < i0; ++i) {
+#else
     for (int i = i0; i < i1; ++i) {
-      const QRow rw = rowt[i];
+#endif
+      const QRow rw = rt[i];
       if (rw.s0 != c0 || rw.s1 != c1) {  // warp-uniform
         if (rw.s0 == c1 && rw.s1 != rw.s0) {  // advance by one window row
           p ^= 1;
-          if (p) { hrow(rw.s1 - sya, A, Ab); diff(A, Ab, B, Bb); }
-          else { hrow(rw.s1 - sya, B, Bb); diff(B, Bb, A, Ab); }
+          if (p) { hrow(rbase(rw.s1), A, Ab); diff(A, Ab, B, Bb); }
+          else { hrow(rbase(rw.s1), B, Bb); diff(B, Bb, A, Ab); }
         } else {
           p = 0;
-          hrow(rw.s0 - sya, A, Ab);
-          if (rw.s1 != rw.s0) hrow(rw.s1 - sya, B, Bb);
+          hrow(rbase(rw.s0), A, Ab);
+          if (rw.s1 != rw.s0) hrow(rbase(rw.s1), B, Bb);
           else {
 #pragma unroll
             for (int k = 0; k < 4; ++k) B[k] = A[k];
@@ -952,9 +974,10 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
 }
 
 size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normalize) {
-  // row table, window origin, column table, staged rows, [Normalize table], [compact LUT]
-  return (size_t)R * sizeof(QRow) + 16 + kQCols * 16 + (size_t)(rows * q_row_words(sw) + 3) / 4 * 16 +
-         (normalize ? 768 * 4 : 0) + (n_lut_stages ? 768 : 0);
+  // 2 row tables, window origin, column table, 2 x row phases, 2 raw row
+  // buffers (+16 B over-read slack), [Normalize table], [compact LUT]
+  return (size_t)2 * R * sizeof(QRow) + 16 + kQCols * 16 + (size_t)((2 * rows + 3) & ~3) * 4 +
+         (size_t)2 * rows * q_raw_pitch(sw) + 16 + (normalize ? 768 * 4 : 0) + (n_lut_stages ? 768 : 0);
 }
 
 template <int kOne>
