@@ -21,6 +21,9 @@ using namespace alb;
 #ifndef ALB_Q4_BUDGET_KB
 #define ALB_Q4_BUDGET_KB 72  // shared-memory budget of one quad-resample CTA (sets the band height)
 #endif
+#ifndef ALB_Q4_MAXRC
+#define ALB_Q4_MAXRC 4  // largest quad-resample band height 4 << rc
+#endif
 #ifndef ALB_Q4_BANDS
 #define ALB_Q4_BANDS 8  // bands of one quad-resample unit (a CTA prefetches band b + 1 while computing b)
 #endif
@@ -970,30 +973,39 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
           }
           if (resample_q4_program_ok(qmode)) {
             // quad-column kernel: units = (image, 128-column strip, group of
-            // bands of R rows); the window of R rows is staged once per band
+            // bands of R_i rows); the window rows of a band are staged once.
+            // Staged-row capacity from the budget (row tables sized for 64
+            // rows); each image takes the largest band height R_i whose
+            // window rows (ceil(R_i * its ratio) + 3) fit the capacity.
             const int sw = std::min(max_ww, (int)std::ceil(128.0 * cratio) + 3);
-            for (int R : {64, 32, 16, 8, 4}) {
-              const int rows = (int)std::ceil(R * ratio) + 3;  // window rows of R output rows
-              const int nl = (qmode == ST_LUT || qmode == kStagesHsvLut || qmode == kStagesLutHsv) ? 1 : 0;
-              if (resample_q4_smem(nl, rows, sw, R, st.normalize) > (size_t)ALB_Q4_BUDGET_KB * 1024) continue;
-              st.rs_q = rows;
+            const int nl = (qmode == ST_LUT || qmode == kStagesHsvLut || qmode == kStagesLutHsv) ? 1 : 0;
+            int cap = 0;
+            while (resample_q4_smem(nl, cap + 1, sw, 64, st.normalize) <= (size_t)ALB_Q4_BUDGET_KB * 1024) ++cap;
+            if (cap >= 8) {
+              st.rs_q = cap;
+              int need = 0;  // staged rows the chosen band heights actually need
               st.rs_sw = sw;
-              st.unit_rows = R;
-              break;
-            }
-            if (st.rs_q > 0) {
-              const int R = st.unit_rows;
-              int max_h = 0;
-              for (int i = 0; i < P->n; ++i) max_h = std::max(max_h, dims[i][st.slot1].first);
-              st.rs_hw = std::max(1, std::min(ALB_Q4_BANDS, (max_h + R - 1) / R));  // bands per unit
-              for (int i = 0; i < P->n; ++i) {
+              st.unit_rows = 64;  // row-table capacity; the band height is per unit
+              st.rs_hw = ALB_Q4_BANDS;  // bands per unit
+              for (int i = 0; i < P->n && st.rs_q > 0; ++i) {
+                int wh = dims[i][st.slot0].first, ww = dims[i][st.slot0].second;
+                if (o.kind == ALB_RANDOM_SIZED_CROP) wh = ww = std::min(o.max_side, std::min(wh, ww));
+                const double ri = o.kind == ALB_GRID_DISTORTION ? ratio : (double)wh / o.out_h;
+                int rc = -1;  // R_i = 4 << rc
+                for (int c = ALB_Q4_MAXRC; c >= 0; --c)
+                  if ((int)std::ceil((4 << c) * ri) + 3 <= cap) { rc = c; break; }
                 const int H = dims[i][st.slot1].first, W = st.normalize ? P->out_w : dims[i][st.slot1].second;
-                const int nb = (H + R - 1) / R;
-                if ((W + 127) / 128 > 256) { st.rs_q = 0; st.units.clear(); break; }
+                if (rc < 0 || (W + 127) / 128 > 256) { st.rs_q = 0; st.units.clear(); break; }
+                need = std::max(need, (int)std::ceil((4 << rc) * ri) + 3);
+                const int nb = (H + (4 << rc) - 1) / (4 << rc);
                 for (int bg = 0; bg * st.rs_hw < nb; ++bg)
-                  for (int x = 0, c = 0; x < W; x += 128, ++c) st.units.push_back(make_int2(i, (bg << 8) | c));
+                  for (int x = 0, c = 0; x < W; x += 128, ++c)
+                    st.units.push_back(make_int2(i, (rc << 28) | (bg << 8) | c));
               }
-              if (st.rs_q > 0) break;
+              if (st.rs_q > 0) {
+                st.rs_q = need;  // shared memory for the rows used, not the whole budget
+                break;
+              }
               st.rs_hw = 0;
             }
           }

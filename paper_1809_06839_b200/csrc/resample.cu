@@ -690,9 +690,9 @@ template <int kOne, bool kNorm>
 __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-  const int R = a.unit_rows, RQ = a.rs_q, RP = q_raw_pitch(a.rs_sw);
-  QRow* rowt = reinterpret_cast<QRow*>(sm);                 // [2][R] (per band, double-buffered)
-  int* win = reinterpret_cast<int*>(rowt + 2 * R);          // sxa, sxb
+  const int RT = a.unit_rows, RQ = a.rs_q, RP = q_raw_pitch(a.rs_sw);
+  QRow* rowt = reinterpret_cast<QRow*>(sm);                 // [2][RT] (per band, double-buffered)
+  int* win = reinterpret_cast<int*>(rowt + 2 * RT);         // sxa, sxb
   float4* colt = reinterpret_cast<float4*>(win + 4);        // [128] (3 x0, fx) per column
   int* rowph = reinterpret_cast<int*>(colt + kQCols);       // [2][RQ] byte phase of each staged row
   uint8_t* raw = reinterpret_cast<uint8_t*>(rowph + ((2 * RQ + 3) & ~3));  // [2][RQ][RP] raw RGB rows (16-byte aligned)
@@ -700,7 +700,8 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
   uint8_t* lut8 = reinterpret_cast<uint8_t*>(nls + (kNorm ? 768 : 0));     // [768] (LUT stage)
 
   const int2 unit = a.units[blockIdx.x];
-  const int img = unit.x, bgrp = unit.y >> 8, strip = unit.y & 255;
+  // unit.y = (rc << 28) | (band group << 8) | strip; band height R = 4 << rc (planner, per image)
+  const int img = unit.x, bgrp = (unit.y >> 8) & 0xfffff, strip = unit.y & 255, R = 4 << (unit.y >> 28);
   const RsGeom g = rs_geom(a, img);
   const int Wo = kNorm ? a.out_w : a.ddesc[img].width, Ho = kNorm ? a.out_h : a.ddesc[img].height;
   QStages qs{0.f, 0.f, 0.f, 0, 0};
@@ -832,7 +833,11 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
       const uintptr_t g0 = (uintptr_t)(ibase + (size_t)r * sd.pitch);
       const uintptr_t ga = g0 & ~(uintptr_t)15, gb = (g0 + 3 * (X1 - X0) + 15) & ~(uintptr_t)15;
       if (kk == 0) rowph[bi * RQ + r] = (int)(g0 - ga);
+#ifdef ALB_AB_Q4_NOSTAGE
+      if (kk < 0)
+#else
       if (ga + 16 * kk < gb)
+#endif
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(rb + (uint32_t)(r * RP + 16 * kk)),
                      "l"(ga + 16 * kk)
                      : "memory");
@@ -847,7 +852,7 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
     const int y0 = band * R, nr = min(R, Ho - y0), bi = (band - b0) & 1;
     if (band > b0) __syncthreads();  // previous band's rows and raw buffer fully consumed
     if (band + 1 < b1) issue(band + 1, bi ^ 1);  // lands while this band computes
-    QRow* rt = rowt + bi * R;
+    QRow* rt = rowt + bi * RT;
     for (int i = tid; i < nr; i += kQThreads) {  // row table in increasing window-row order
       const int yo = m.ay > 0 ? y0 + i : y0 + nr - 1 - i;
       const double sy = g_cy(g, m.ay * yo + m.by);
