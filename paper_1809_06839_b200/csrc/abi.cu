@@ -27,6 +27,7 @@ using namespace alb;
 #ifndef ALB_Q4_BANDS
 #define ALB_Q4_BANDS 8  // bands of one quad-resample unit (a CTA prefetches band b + 1 while computing b)
 #endif
+static_assert(ALB_Q4_BANDS >= 1 && ALB_Q4_BANDS <= 16, "the quad-resample kernel keeps <= 16 bands' window rows");
 
 namespace {
 

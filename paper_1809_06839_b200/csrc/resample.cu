@@ -692,8 +692,8 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int RT = a.unit_rows, RQ = a.rs_q, RP = q_raw_pitch(a.rs_sw);
   QRow* rowt = reinterpret_cast<QRow*>(sm);                 // [2][RT] (per band, double-buffered)
-  int* win = reinterpret_cast<int*>(rowt + 2 * RT);         // sxa, sxb
-  float4* colt = reinterpret_cast<float4*>(win + 4);        // [128] (3 x0, fx) per column
+  int* win = reinterpret_cast<int*>(rowt + 2 * RT);         // sxa, sxb, -, -, then [16] (sy0, nrows) per band
+  float4* colt = reinterpret_cast<float4*>(win + 36);       // [128] (3 x0, fx) per column
   int* rowph = reinterpret_cast<int*>(colt + kQCols);       // [2][RQ] byte phase of each staged row
   uint8_t* raw = reinterpret_cast<uint8_t*>(rowph + ((2 * RQ + 3) & ~3));  // [2][RQ][RP] raw RGB rows (16-byte aligned)
   float* nls = reinterpret_cast<float*>(raw + 2 * (size_t)RQ * RP + 16);  // [768] (kNorm)
@@ -754,6 +754,18 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
     const bool clamped = (int)cf + 1 > g.ww - 1;
     colt[tid] = make_float4(__int_as_float(3 * x0), clamped ? 0.f : (float)__dsub_rn(csx, cf), 0.f, 0.f);
   }
+  const int nb_img = (Ho + R - 1) / R;
+  const int b0 = bgrp * a.rs_hw, b1 = min(b0 + a.rs_hw, nb_img);
+  // window rows [sy0, sy0 + nrows) of each band of the unit (first / last
+  // output row in increasing window-row order, the same fp64 row coordinates
+  // as the row table), once per unit
+  if (tid < b1 - b0) {
+    const int y0 = (b0 + tid) * R, nr = min(R, Ho - y0);
+    const int yf = m.ay > 0 ? y0 : y0 + nr - 1, yl = m.ay > 0 ? y0 + nr - 1 : y0;
+    const int sy0 = (int)floor(g_cy(g, m.ay * yf + m.by));
+    win[4 + 2 * tid] = sy0;
+    win[5 + 2 * tid] = min((int)floor(g_cy(g, m.ay * yl + m.by)) + 1, g.wh - 1) - sy0 + 1;
+  }
   __syncthreads();
   // this lane's 4 columns: tap byte offsets in a staged row and weights
   uint32_t tb[4];
@@ -766,8 +778,8 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
   }
   const alb_image_desc sd = a.sdesc[img];
   const int X0 = g.wx0 + sxa, X1 = g.wx0 + sxb;  // absolute source columns of the window
-  const int nch = (3 * (X1 - X0) + 30) >> 4;      // 16-byte chunks a staged row can span
-  const uint32_t mch = magic_of((uint32_t)nch);
+  const int nq = ((3 * (X1 - X0) + 30) >> 4) / 4 + 1;  // groups of 4 16-byte chunks a staged row can span
+  const uint32_t mq = magic_of((uint32_t)nq);
   const uint32_t raw_a = smem_u32(raw);
   uint8_t* gbase = nullptr;
   int dpitch = 0;
@@ -812,41 +824,35 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
       hb[q] = __ffma2_rn(make_float2(fx[2 * q], fx[2 * q + 1]), __fadd2_rn(B1, f2neg(B0)), __fadd2_rn(B0, nMh));
     }
   };
-  // window rows [sy0, sy0 + nrows) of band `band` (first / last output row in
-  // increasing window-row order, the same fp64 row coordinates as the table)
-  auto band_rows = [&](int band, int& sy0, int& nrows) {
-    const int y0 = band * R, nr = min(R, Ho - y0);
-    const int yf = m.ay > 0 ? y0 : y0 + nr - 1, yl = m.ay > 0 ? y0 + nr - 1 : y0;
-    sy0 = (int)floor(g_cy(g, m.ay * yf + m.by));
-    nrows = min((int)floor(g_cy(g, m.ay * yl + m.by)) + 1, g.wh - 1) - sy0 + 1;
-  };
   // asynchronous copy of a band's window rows into raw buffer `bi`: row r's
   // 16-byte aligned hull of [X0, X1) lands at raw[bi][r] + 16 k; its data
   // starts at byte phase rowph[bi][r]
   auto issue = [&](int band, int bi) {
-    int sy0, nrows;
-    band_rows(band, sy0, nrows);
+    const int sy0 = win[4 + 2 * (band - b0)], nrows = win[5 + 2 * (band - b0)];
     const uint8_t* ibase = a.src + sd.offset + (size_t)(g.wy0 + sy0) * sd.pitch + 3 * X0;
     const uint32_t rb = raw_a + (uint32_t)(bi * RQ * RP);
-    for (int it = tid; it < nrows * nch; it += kQThreads) {
-      const int r = fdiv(it, mch), kk = it - r * nch;
+    // item = (row, group of 4 consecutive chunks): one address computation per 64 bytes
+    for (int it = tid; it < nrows * nq; it += kQThreads) {
+      const int r = fdiv(it, mq), j = it - r * nq;
       const uintptr_t g0 = (uintptr_t)(ibase + (size_t)r * sd.pitch);
       const uintptr_t ga = g0 & ~(uintptr_t)15, gb = (g0 + 3 * (X1 - X0) + 15) & ~(uintptr_t)15;
-      if (kk == 0) rowph[bi * RQ + r] = (int)(g0 - ga);
+      if (j == 0) rowph[bi * RQ + r] = (int)(g0 - ga);
+      const uintptr_t gs = ga + 64 * j;
+      const uint32_t ds = rb + (uint32_t)(r * RP + 64 * j);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
 #ifdef ALB_AB_Q4_NOSTAGE
-      if (kk < 0)
+        if (q < 0)
 #else
-      if (ga + 16 * kk < gb)
+        if (gs + 16 * q < gb)
 #endif
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(rb + (uint32_t)(r * RP + 16 * kk)),
-                     "l"(ga + 16 * kk)
-                     : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(ds + 16u * q), "l"(gs + 16 * q)
+                       : "memory");
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  const int nb_img = (Ho + R - 1) / R;
-  const int b0 = bgrp * a.rs_hw, b1 = min(b0 + a.rs_hw, nb_img);
   issue(b0, 0);
   for (int band = b0; band < b1; ++band) {
     const int y0 = band * R, nr = min(R, Ho - y0), bi = (band - b0) & 1;
@@ -981,7 +987,7 @@ __global__ void __launch_bounds__(kQThreads, ALB_Q4_MINB) k_resample_q4(StepArgs
 size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normalize) {
   // 2 row tables, window origin, column table, 2 x row phases, 2 raw row
   // buffers (+16 B over-read slack), [Normalize table], [compact LUT]
-  return (size_t)2 * R * sizeof(QRow) + 16 + kQCols * 16 + (size_t)((2 * rows + 3) & ~3) * 4 +
+  return (size_t)2 * R * sizeof(QRow) + 144 + kQCols * 16 + (size_t)((2 * rows + 3) & ~3) * 4 +
          (size_t)2 * rows * q_raw_pitch(sw) + 16 + (normalize ? 768 * 4 : 0) + (n_lut_stages ? 768 : 0);
 }
 
