@@ -712,3 +712,20 @@ def test_apply_captures_into_cuda_graph(name):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("kind", ["Resize", "RandomSizedCrop"])
+def test_quad_resample_mixed_ratio_batch(kind):
+    """One batch whose images need very different window-row counts per output
+    row (tiny, huge, very wide, very tall, square): the quad resampler's planner
+    gives each image its own band height (K5), and every image must
+    still match the oracle (<= 1 LSB, >= 99.9% exact)."""
+    sizes = [(37, 53), (1023, 771), (260, 1900), (512, 512), (1500, 97), (3, 5), (700, 700)]
+    if kind == "Resize":
+        specs = [{"kind": "Resize", "size": (300, 200)}]
+    else:
+        specs = [{"kind": "RandomSizedCrop", "side": (2, 1500), "size": (300, 200), "interp": "bilinear"}]
+    b = gen.gen_images(sizes, seed=21, first_image_index=0, device="cuda")
+    g = run_gpu(specs, b, seed=9)["images"]
+    r = run_oracle(specs, [b.image(i) for i in range(len(sizes))], seed=9)
+    cmp_interp(g, [x["image"] for x in r])
