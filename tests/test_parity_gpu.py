@@ -719,13 +719,26 @@ def test_quad_resample_mixed_ratio_batch(kind):
     """One batch whose images need very different window-row counts per output
     row (tiny, huge, very wide, very tall, square): the quad resampler's planner
     gives each image its own band height (K5), and every image must
-    still match the oracle (<= 1 LSB, >= 99.9% exact)."""
+    still match the oracle: <= 1 LSB and >= 99.9% exact, or every difference
+    an exact .5 tie of the rational blend of the image's (crop) window
+    (upsampling tiny windows makes such ties common, R33)."""
+    from oracle import albref as A
     sizes = [(37, 53), (1023, 771), (260, 1900), (512, 512), (1500, 97), (3, 5), (700, 700)]
     if kind == "Resize":
         specs = [{"kind": "Resize", "size": (300, 200)}]
     else:
         specs = [{"kind": "RandomSizedCrop", "side": (2, 1500), "size": (300, 200), "interp": "bilinear"}]
     b = gen.gen_images(sizes, seed=21, first_image_index=0, device="cuda")
+    imgs = [b.image(i) for i in range(len(sizes))]
     g = run_gpu(specs, b, seed=9)["images"]
-    r = run_oracle(specs, [b.image(i) for i in range(len(sizes))], seed=9)
-    cmp_interp(g, [x["image"] for x in r])
+    r = run_oracle(specs, imgs, seed=9)
+    for i, (gi, ri) in enumerate(zip(g, [x["image"] for x in r])):
+        win = imgs[i]
+        if kind == "RandomSizedCrop":
+            side, x0, y0 = (int(v) for v in A.sample_params(specs, 9, i, *sizes[i])[0][0][:3])
+            win = win[y0:y0 + side, x0:x0 + side]
+        d = gi.astype(np.int32) - ri.astype(np.int32)
+        assert np.abs(d).max(initial=0) <= 1, i
+        if (d == 0).mean() < 0.999:  # below the interpolation bar only through exact ties
+            tie = resize_exact_ties(win, 200, 300)
+            assert not ((d != 0) & ~tie).any(), (i, int(((d != 0) & ~tie).sum()))
