@@ -261,9 +261,10 @@ class Workload:
 def timed_steps(W, seeds, stream, dist, dev):
     """Time len(seeds) steps (every transform of the menu once per step) between
     a barrier + synchronize on both sides; per-apply CUDA events on the launch
-    stream.  Returns (max-over-ranks elapsed s, {label: [s per apply]})."""
+    stream.  Returns (max-over-ranks elapsed s, {label: [s per apply]}, [s per step])."""
     labels = list(W.menu)
     ev = {label: [] for label in labels}
+    bounds = []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -271,6 +272,9 @@ def timed_steps(W, seeds, stream, dist, dev):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for s in seeds:
+        eb = torch.cuda.Event(enable_timing=True)
+        eb.record(stream)
+        bounds.append(eb)
         for label in labels:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -285,7 +289,9 @@ def timed_steps(W, seeds, stream, dist, dev):
     t = torch.tensor([t0.elapsed_time(t1) / 1e3], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item()), {l: [a.elapsed_time(b) / 1e3 for a, b in ev[l]] for l in labels}
+    bounds.append(t1)
+    steps = [a.elapsed_time(b) / 1e3 for a, b in zip(bounds[:-1], bounds[1:])]
+    return float(t.item()), {l: [a.elapsed_time(b) / 1e3 for a, b in ev[l]] for l in labels}, steps
 
 
 def graph_times(W, seeds, dev):
@@ -419,7 +425,7 @@ def measure(cfg, args, dev, rank, world, dist, peak, peak_src, local):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.5)
-    elapsed, op_times = timed_steps(W, seeds, stream, dist, dev)
+    elapsed, op_times, step_times = timed_steps(W, seeds, stream, dist, dev)
     clocks.stop()
     per = {}
     for label in labels:
@@ -455,11 +461,25 @@ def measure(cfg, args, dev, rank, world, dist, peak, peak_src, local):
                              "apply duration (CUDA events on the launch stream around the "
                              "whole alb_apply, K0 parameter launch included)"},
         "per_transform": per,
+        "trials": trials_of(step_times, world * W.n),
         "e2e": e2e,
         "gpu_launches": args.steps * W.launches(),
         "clocks": clocks.summary(),
     }
     return W, res
+
+
+def trials_of(step_times, images_per_step, n=5):
+    """the K timed steps as n consecutive trials (this rank's
+    CUDA events between step boundaries); images/s of each and the median."""
+    if len(step_times) < n:
+        n = len(step_times)
+    if n == 0:
+        return None
+    k = len(step_times) // n
+    ips = [images_per_step * k / sum(step_times[i * k:(i + 1) * k]) for i in range(n)]
+    return {"n": n, "steps_each": k, "images_per_s": [round(v, 1) for v in ips],
+            "median": round(statistics.median(ips), 1)}
 
 
 def cpu_baseline(W, args):
