@@ -565,7 +565,8 @@ def main():
                "vs_baseline": None, "dtype": "u8",
                "data": "synthetic (seeded gradient+noise, synth/gen.py)",
                "config": head["config"], "roofline": head["roofline"],
-               "per_transform": head["per_transform"], "cpu_baseline": cpu, "e2e": head["e2e"],
+               "per_transform": head["per_transform"], "trials": head["trials"], "cpu_baseline": cpu,
+               "e2e": head["e2e"],
                "gpu_launches": head["gpu_launches"] + sum(c["gpu_launches"] for c in composed.values()),
                "clocks": head["clocks"]}
         if composed:
