@@ -752,10 +752,20 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       continue;
     }
     if (is_lut_kind(kind) || kind == ALB_SHIFT_HSV || kind == ALB_GRAYSCALE) {
-      if (!(geo_open || point_open)) {
+      // a step whose kernel already carries kMaxStages stages (or 4 LUT-type
+      // stages: the shared-memory LUT budget) is closed; a new pointwise step
+      // takes the rest of the chain
+      bool full = false;
+      if (geo_open || point_open) {
+        int nl = 0;
+        for (auto& sg : steps.back().stages) nl += (sg.type == ST_LUT || sg.type == ST_EQ);
+        full = steps.back().stages.size() >= (size_t)kMaxStages || (is_lut_kind(kind) && nl >= 4);
+      }
+      if (!(geo_open || point_open) || full) {
         PlanStep st; st.kind = SK_POINT; st.slot0 = k; st.slot1 = k;
         steps.push_back(st);
         point_open = true;
+        geo_open = false;
       }
       PlanStep& b = steps.back();
       if (b.stages.size() >= (size_t)kMaxStages) return fail(ALB_E_UNSUPPORTED, "too many pointwise stages");
@@ -780,7 +790,8 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       continue;
     }
     if (kind == ALB_EQUALIZE) {
-      if (P->has_eq) return fail(ALB_E_UNSUPPORTED, "at most one Equalize per pipeline");
+      // several Equalize ops run in stream order and reuse one histogram / LUT
+      // workspace region (each SK_EQ step rebuilds it from its own input)
       PlanStep st; st.kind = SK_EQ; st.slot0 = k; st.slot1 = k + 1; st.eq_slot = k;
       steps.push_back(st);
       PlanStep ap; ap.kind = SK_POINT; ap.slot0 = k; ap.slot1 = k + 1;

@@ -76,6 +76,10 @@ __global__ void __launch_bounds__(256) k_eq_lut(EqArgs a) {
   __shared__ uint32_t s_first;
   const alb_image_desc sd = a.sdesc[img];
   const int64_t N = (int64_t)sd.width * sd.height;
+  if (!fired_of(a.tab, img, a.slot)) {  // gate not fired: the op is the identity
+    for (int c = 0; c < 3; ++c) a.lut[(size_t)img * 768 + c * 256 + v] = (uint8_t)v;
+    return;
+  }
   for (int c = 0; c < 3; ++c) {
     const uint32_t hv = a.hist[(size_t)img * 768 + c * 256 + v];
     if (v == 0) s_first = 256;

@@ -370,11 +370,13 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
   const alb_image_desc sd = a.sdesc[img];
   const uint8_t* src = a.src + sd.offset;
   const int n = sd.height * sd.width * 3;
+  // gate not fired (a.stages[0] is this step's ST_EQ stage): identity LUT, no histogram
+  const bool on = fired_of(a.tab, img, a.stages[0].slot);
   for (int i = tid; i < 768 * 32; i += kEqF) hl[i] = 0;
   if (tid < 3) first[tid] = 256;
   __syncthreads();
   // ---- 1. histogram
-  {
+  if (on) {
     uint32_t* hw = hl + lane;
     const uint32_t hl_base = (uint32_t)__cvta_generic_to_shared(hl) + 4u * (uint32_t)lane;
     int bA = (int)((16 - ((uintptr_t)src & 15)) & 15);
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
       if (num < 0) num = 0;
       out = (int)((2 * 255 * num + D) / (2 * D));
     }
-    lut8[t] = (uint8_t)out;
+    lut8[t] = on ? (uint8_t)out : (uint8_t)v;
   }
   __syncthreads();
   // ---- 3. lane-replicated LUT over the histogram, then the LUT pass

@@ -742,3 +742,46 @@ def test_quad_resample_mixed_ratio_batch(kind):
         if (d == 0).mean() < 0.999:  # below the interpolation bar only through exact ties
             tie = resize_exact_ties(win, 200, 300)
             assert not ((d != 0) & ~tie).any(), (i, int(((d != 0) & ~tie).sum()))
+
+
+def _ops(*names_p):
+    from synth.configs import op
+    table = {"B": ("Brightness", dict(lo=[0.8], hi=[1.2])), "C": ("Contrast", dict(lo=[0.8], hi=[1.2])),
+             "G": ("Gamma", dict(lo=[0.8], hi=[1.2])), "R": ("ShiftRGB", dict(lo=[-20.0] * 3, hi=[20.0] * 3)),
+             "Y": ("Grayscale", {}), "E": ("Equalize", {}), "H": ("HorizontalFlip", {}),
+             "V": ("VerticalFlip", {})}
+    out = []
+    for n in names_p:
+        kind, kw = table[n[0]]
+        out.append(op(kind, p=0.5 if n.endswith("?") else 1.0, **kw))
+    return out
+
+
+@pytest.mark.parametrize("chain", ["E?", "E?B", "EBE", "HEGYEV", "E?B?E?C?E"])
+def test_several_equalize_ops_bit_exact(chain):
+    """Several Equalize ops in one pipeline (each SK_EQ step rebuilds the
+    histogram / LUT workspace from its own input, in stream order), and gated
+    Equalize (p = 0.5: an image whose gate does not fire is left unchanged,
+    through the single-pass kernel "E?" and the histogram + LUT path "E?B"):
+    bit-exact."""
+    import re
+    specs = _ops(*re.findall(r"[A-Z]\??", chain))
+    sizes = gen.cfg2_sizes(24, first_image_index=3)
+    b = gen.gen_images(sizes, seed=4, first_image_index=3, device="cuda")
+    g = run_gpu(specs, b, seed=11, first=3)["images"]
+    r = run_oracle(specs, [b.image(i) for i in range(len(sizes))], seed=11, first=3)
+    cmp_exact(g, [x["image"] for x in r])
+
+
+@pytest.mark.parametrize("lead", ["", "H", "V?"])
+def test_long_pointwise_chain_splits_into_steps(lead):
+    """Nine alternating LUT / Grayscale stages (more than one kernel's four):
+    the planner closes full steps and continues in new pointwise steps, behind
+    a fused flip or alone; integer arithmetic throughout, so bit-exact."""
+    chain = ["B", "Y", "G", "Y", "C", "Y", "R", "Y", "B?"]
+    specs = _ops(*([lead] if lead else []), *chain)
+    sizes = gen.cfg2_sizes(16, first_image_index=40)
+    b = gen.gen_images(sizes, seed=6, first_image_index=40, device="cuda")
+    g = run_gpu(specs, b, seed=2, first=40)["images"]
+    r = run_oracle(specs, [b.image(i) for i in range(len(sizes))], seed=2, first=40)
+    cmp_exact(g, [x["image"] for x in r])
