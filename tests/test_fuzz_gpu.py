@@ -1,0 +1,188 @@
+"""Seeded random pipelines through the planner, GPU vs oracle.
+
+Exact pipelines: random chains of the integer-exact ops (flips, RandomCrop,
+Crop, PadToSize, Rot90, D4, the LUT colour ops, Grayscale, Equalize, each with
+a random gate probability) on small ragged batches with label masks, ending in
+Normalize when the shapes are uniform.  Every output byte (and mask label) is
+a pure function of the inputs and the drawn parameters, so the GPU must match
+the oracle bit for bit (fp32 Normalize: bit-equal, R21) whatever
+fusion / step split / self-sampling the planner picks.
+
+Interpolating pipelines: random exact geometric ops, then one resampling op
+(Resize, RandomSizedCrop: <= 1 LSB, and per image >= 99.9% exact or every
+difference an exact rational .5 tie of its window's blend, R33 -- upsampled
+tiny windows hit many) or one warp (Rotate, ShiftScaleRotate) followed by more
+exact geometric ops (which only permute or pad pixels, so they do not amplify
+a 1-LSB blend difference: <= 1 LSB and >= 99.9% exact)."""
+import numpy as np
+import pytest
+import torch
+
+from synth import gen
+from tests.harness import cmp_exact, cmp_interp, random_masks, resize_exact_ties, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    from paper_1809_06839_b200 import build
+    build.build()
+    assert torch.cuda.is_available()
+
+
+def _p(rng):
+    return float(rng.choice([1.0, 1.0, 0.5, 0.25]))
+
+
+def _geo_exact(rng, shapes):
+    """One exact geometric op valid for every image shape; returns (spec, new shapes)."""
+    hs = [h for h, _ in shapes]
+    ws = [w for _, w in shapes]
+    square = all(h == w for h, w in shapes)
+    k = rng.integers(0, 7)
+    if k == 0:
+        return {"kind": "HorizontalFlip", "p": _p(rng)}, shapes
+    if k == 1:
+        return {"kind": "VerticalFlip", "p": _p(rng)}, shapes
+    if k == 2:
+        ch, cw = int(rng.integers(1, min(hs) + 1)), int(rng.integers(1, min(ws) + 1))
+        return {"kind": "RandomCrop", "size": (cw, ch)}, [(ch, cw)] * len(shapes)
+    if k == 3:
+        ch, cw = int(rng.integers(1, min(hs) + 1)), int(rng.integers(1, min(ws) + 1))
+        oy, ox = int(rng.integers(0, min(hs) - ch + 1)), int(rng.integers(0, min(ws) - cw + 1))
+        return {"kind": "Crop", "size": (cw, ch), "origin": (ox, oy)}, [(ch, cw)] * len(shapes)
+    if k == 4:
+        ph, pw = max(hs) + int(rng.integers(0, 9)), max(ws) + int(rng.integers(0, 9))
+        fill = [int(v) for v in rng.integers(0, 256, 3)]
+        return ({"kind": "PadToSize", "size": (pw, ph), "fill": fill, "mask_fill": int(rng.integers(0, 256))},
+                [(ph, pw)] * len(shapes))
+    # Rot90 (elements 0..3) / D4 (0..7): an odd element transposes the shape,
+    # so a ragged / non-square batch takes one fixed element (p = 1 when odd)
+    kind, top = ("Rotate90", 3) if k == 5 else ("D4", 7)
+    if square:
+        lo = int(rng.integers(0, top + 1))
+        hi = int(rng.integers(lo, top + 1))
+        return {"kind": kind, "lo": [lo], "hi": [hi], "p": _p(rng)}, shapes
+    e = int(rng.integers(0, top + 1))
+    if e % 2:
+        return {"kind": kind, "lo": [e], "hi": [e], "p": 1.0}, [(w, h) for h, w in shapes]
+    return {"kind": kind, "lo": [e], "hi": [e], "p": _p(rng)}, shapes
+
+
+def _point(rng):
+    k = rng.integers(0, 7)
+    if k == 0:
+        return {"kind": "Brightness", "lo": [0.7], "hi": [1.3], "p": _p(rng)}
+    if k == 1:
+        return {"kind": "Contrast", "lo": [0.7], "hi": [1.3], "p": _p(rng)}
+    if k == 2:
+        return {"kind": "BrightnessContrast", "lo": [0.8, 0.8], "hi": [1.2, 1.2], "p": _p(rng)}
+    if k == 3:
+        return {"kind": "Gamma", "lo": [0.7], "hi": [1.4], "p": _p(rng)}
+    if k == 4:
+        return {"kind": "ShiftRGB", "lo": [-30.0] * 3, "hi": [30.0] * 3, "p": _p(rng)}
+    if k == 5:
+        return {"kind": "Grayscale", "p": _p(rng)}
+    return {"kind": "Equalize", "p": _p(rng)}
+
+
+def _batch(rng, n):
+    sizes = [(int(rng.integers(4, 70)), int(rng.integers(4, 70))) for _ in range(n)]
+    if rng.random() < 0.3:  # square batches reach the odd Rot90 / D4 elements
+        s = int(rng.integers(4, 60))
+        sizes = [(s, s)] * n
+    return sizes
+
+
+def _exact_pipeline(rng, sizes):
+    shapes = list(sizes)
+    specs = []
+    for _ in range(int(rng.integers(1, 9))):
+        if rng.random() < 0.45:
+            s, shapes = _geo_exact(rng, shapes)
+        else:
+            s = _point(rng)
+        specs.append(s)
+    if len(set(shapes)) == 1 and rng.random() < 0.3:
+        specs.append({"kind": "Normalize", "mean": [0.485, 0.456, 0.406], "std": [0.229, 0.224, 0.225]})
+    return specs
+
+
+@pytest.mark.parametrize("case", range(150))
+def test_fuzz_exact_pipelines(case):
+    rng = np.random.default_rng(1000 + case)
+    n = int(rng.integers(1, 7))
+    sizes = _batch(rng, n)
+    specs = _exact_pipeline(rng, sizes)
+    b = gen.gen_images(sizes, seed=case, first_image_index=case, device="cuda")
+    has_norm = specs[-1]["kind"] == "Normalize"
+    mb, mk = random_masks(sizes, seed=case) if not has_norm else (None, None)
+    seed, first = int(rng.integers(0, 2**31)), int(rng.integers(0, 10**6))
+    g = run_gpu(specs, b, seed=seed, first=first, masks=mb)
+    imgs = [b.image(i) for i in range(n)]
+    r = run_oracle(specs, imgs, seed=seed, first=first, masks=mk)
+    if has_norm:
+        ref = np.stack([x["nchw"] for x in r]).astype(np.float32)
+        assert np.array_equal(g["nchw"].view(np.uint32), ref.view(np.uint32)), specs
+    else:
+        cmp_exact(g["images"], [x["image"] for x in r])
+        cmp_exact(g["masks"], [x["mask"] for x in r])
+
+
+@pytest.mark.parametrize("case", range(48))
+def test_fuzz_one_interpolating_op(case):
+    rng = np.random.default_rng(5000 + case)
+    n = int(rng.integers(1, 6))
+    sizes = [(int(rng.integers(24, 120)), int(rng.integers(24, 120))) for _ in range(n)]
+    shapes = list(sizes)
+    specs = []
+    for _ in range(int(rng.integers(0, 3))):
+        s, shapes = _geo_exact(rng, shapes)
+        specs.append(s)
+    k = case % 4
+    if k == 0:
+        oh, ow = int(rng.integers(8, 150)), int(rng.integers(8, 150))
+        specs.append({"kind": "Resize", "size": (ow, oh), "interp": "bilinear"})
+    elif k == 1:
+        lo = max(1, min(min(h, w) for h, w in shapes) // 3)
+        specs.append({"kind": "RandomSizedCrop", "side": (lo, 10**4), "size": (64, 48), "interp": "bilinear"})
+    elif k == 2:
+        specs.append({"kind": "Rotate", "lo": [-90.0], "hi": [90.0], "p": _p(rng), "interp": "bilinear",
+                      "border": str(rng.choice(["constant", "reflect_101"]))})
+    else:
+        specs.append({"kind": "ShiftScaleRotate", "lo": [-0.0625, -0.0625, 0.9, -45.0],
+                      "hi": [0.0625, 0.0625, 1.1, 45.0], "interp": "bilinear",
+                      "border": str(rng.choice(["constant", "reflect_101"]))})
+    idx = len(specs) - 1  # slot of the interpolating op
+    if k == 0:
+        shapes = [(oh, ow)] * n
+    elif k == 1:
+        shapes = [(48, 64)] * n
+    for _ in range(int(rng.integers(0, 3)) if k in (2, 3) else 0):  # exact geometric ops after a warp
+        sp, shapes = _geo_exact(rng, shapes)
+        specs.append(sp)
+    b = gen.gen_images(sizes, seed=case, first_image_index=case, device="cuda")
+    imgs = [b.image(i) for i in range(n)]
+    seed = int(rng.integers(0, 2**31))
+    g = run_gpu(specs, b, seed=seed, first=case)
+    r = run_oracle(specs, imgs, seed=seed, first=case)
+    if k in (0, 1):
+        # resample last: every difference must be <= 1 and, unless the image
+        # is >= 99.9% exact, an exact rational .5 tie of the blend of its
+        # window (upsampled tiny windows hit many, R33)
+        from oracle import albref as A
+        pre = run_oracle(specs[:idx], imgs, seed=seed, first=case) if idx else [{"image": im} for im in imgs]
+        for i in range(n):
+            d = g["images"][i].astype(np.int32) - r[i]["image"].astype(np.int32)
+            assert np.abs(d).max(initial=0) <= 1, (i, specs)
+            if (d == 0).mean() >= 0.999:
+                continue
+            win = pre[i]["image"]
+            if k == 1:
+                side, x0, y0 = (int(v) for v in A.sample_params(specs, seed, case + i, *sizes[i])[0][idx][:3])
+                win = win[y0:y0 + side, x0:x0 + side]
+            tie = resize_exact_ties(win, *g["images"][i].shape[:2])
+            assert not ((d != 0) & ~tie).any(), (i, int(((d != 0) & ~tie).sum()), specs)
+    else:  # warps (then exact geometric ops): the 99.9% bar
+        cmp_interp(g["images"], [x["image"] for x in r])
