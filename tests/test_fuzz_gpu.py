@@ -223,3 +223,51 @@ def test_fuzz_boxes_through_exact_chains(case):
     cmp_exact(g["images"], [x["image"] for x in r])
     cmp_exact(g["masks"], [x["mask"] for x in r])
     cmp_boxes(g, r)
+
+
+@pytest.mark.parametrize("case", range(32))
+def test_fuzz_hsv_and_free_form_warps(case):
+    """Exact chains, then one ShiftHSV, GridDistortion or ElasticTransform
+    (random parameters, gate, border, interpolation), then exact geometric ops
+    (pure permutations / pads): images at the interpolation bar (nearest ones
+    through the tie-band candidates), masks through the candidates (R20)."""
+    rng = np.random.default_rng(13000 + case)
+    n = int(rng.integers(1, 5))
+    sizes = [(int(rng.integers(16, 90)), int(rng.integers(16, 90))) for _ in range(n)]
+    shapes = list(sizes)
+    specs = []
+    for _ in range(int(rng.integers(0, 3))):
+        if rng.random() < 0.5:
+            s, shapes = _geo_exact(rng, shapes)
+        else:
+            s = _point(rng)
+        specs.append(s)
+    k = case % 3
+    interp = str(rng.choice(["bilinear", "bilinear", "nearest"]))
+    border = str(rng.choice(["constant", "reflect_101"]))
+    if k == 0:
+        specs.append({"kind": "ShiftHSV", "lo": [-30.0, -0.2, -0.2], "hi": [30.0, 0.2, 0.2], "p": _p(rng)})
+        interp = "bilinear"
+    elif k == 1:
+        a = float(rng.uniform(0.05, 0.45))
+        specs.append({"kind": "GridDistortion", "lo": [-a], "hi": [a], "num_steps": int(rng.integers(1, 9)),
+                      "p": _p(rng), "interp": interp, "border": border})
+    else:
+        al, sg = float(rng.uniform(5, 60)), float(rng.uniform(2, 8))
+        specs.append({"kind": "ElasticTransform", "lo": [al, sg], "hi": [al, sg], "p": _p(rng),
+                      "interp": interp, "border": border})
+    for _ in range(int(rng.integers(0, 3))):
+        s, shapes = _geo_exact(rng, shapes)
+        specs.append(s)
+    b = gen.gen_images(sizes, seed=case, first_image_index=case, device="cuda")
+    imgs = [b.image(i) for i in range(n)]
+    mb, mk = random_masks(sizes, seed=case)
+    seed = int(rng.integers(0, 2**31))
+    g = run_gpu(specs, b, seed=seed, first=case, masks=None if k == 0 else mb)
+    r = run_oracle_cand(specs, imgs, seed=seed, first=case, masks=None if k == 0 else mk)
+    if interp == "nearest":
+        cmp_cand(g["images"], r, "image")
+    else:
+        cmp_interp(g["images"], [x["image"] for x in r])
+    if k != 0:
+        cmp_cand(g["masks"], r, "mask")
