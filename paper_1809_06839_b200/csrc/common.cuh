@@ -116,6 +116,20 @@ __device__ __forceinline__ bool fired_of(const Tables& t, int img, int slot) {
   return t.fired[(size_t)img * t.n_ops + slot] != 0;
 }
 
+// ---- paired fp32 helpers (sm_100 f32x2 pipe)
+__device__ __forceinline__ unsigned long long f2u(float2 v) {
+  return ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x);
+}
+__device__ __forceinline__ float2 u2f(unsigned long long u) {
+  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
+}
+// round-toward-minus-infinity paired add: floor(v) + 1.5*2^23 for |v| < 2^22
+__device__ __forceinline__ float2 fadd2_rm(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+
 // ---------------------------------------------------------------- HSV (fp32)
 // hexcone RGB->HSV, shift (h mod 360, s/v clamped), HSV->RGB, round half up
 // (O9, reading R29).  Branch-free (no lane divergence):
@@ -212,8 +226,9 @@ __device__ __forceinline__ void hsv_shift_px2b(float dh6w, float ds, float dv, f
   // t per channel as hsv_shift_px (R and B need one term each, G both)
   auto emit = [&](float2 t, uint32_t (&out)[2]) {
     const float2 y = f2fma(make_float2(255.f, 255.f), f2fma(nvs, t, vv), make_float2(0.5f, 0.5f));
-    out[0] = __float_as_uint(__fadd_rd(y.x, M));
-    out[1] = __float_as_uint(__fadd_rd(y.y, M));
+    const float2 q = fadd2_rm(y, make_float2(M, M));  // both pixels' round-down adds in one op
+    out[0] = __float_as_uint(q.x);
+    out[1] = __float_as_uint(q.y);
   };
   const float2 kr = f2add(h6, make_float2(5.f - 8.f, 5.f - 8.f));
   emit(make_float2(__saturatef(2.f - fabsf(kr.x)), __saturatef(2.f - fabsf(kr.y))), ro);

@@ -383,20 +383,6 @@ __device__ __forceinline__ uint32_t rgbx_raw(const uint32_t (&w)[12], int i) {
   return __byte_perm(w[q], hi, (uint32_t)k * 0x111u + 0x210u);
 }
 
-// ---- paired fp32 helpers (sm_100 f32x2 pipe)
-__device__ __forceinline__ unsigned long long f2u(float2 v) {
-  return ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x);
-}
-__device__ __forceinline__ float2 u2f(unsigned long long u) {
-  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
-}
-// round-toward-minus-infinity paired add: floor(v) + 1.5*2^23 for |v| < 2^22
-__device__ __forceinline__ float2 fadd2_rm(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
-  return u2f(r);
-}
-
 // Bilinear blend of 4 RGBx taps (O5/O7 weights), fp32, per channel
 //   h0 = fma(fx, p10 - p00, p00 + .5); h1 = fma(fx, p11 - p01, p01 + .5);
 //   v  = fma(fy, h1 - h0, h0);   out = floor(v)        (= round_half_up)
