@@ -231,15 +231,17 @@ class Workload:
                                      mol=mol, ws=plan.workspace(dev), specs=specs)
         self.layouts = (in_l, m_l)
 
-    def apply(self, label, seed, stream, img_in=None, mask_in=None, boxes_in=None):
+    def apply(self, label, seed, stream, img_in=None, mask_in=None, boxes_in=None, res=None):
+        """res: optional (out buffer, nchw, mask out buffer, box outs, workspace)
+        replacing the plan's own (a second in-flight copy, bench e2e)."""
         P = self.plans[label]
+        out, nchw, mo, bo, ws = res or (None if P["out"] is None else P["out"].buf, P["nchw"],
+                                        None if P["mo"] is None else P["mo"].buf, P["bo"], P["ws"])
         bi = boxes_in or self.boxes or [None] * 3
-        bo = P["bo"] or [None] * 3
+        bo = bo or [None] * 3
         masks_in = mask_in if mask_in is not None else (None if self.masks is None else self.masks.buf)
-        P["plan"].apply(seed, self.first, self.batch.buf if img_in is None else img_in,
-                        None if P["out"] is None else P["out"].buf, P["nchw"], masks_in,
-                        None if P["mo"] is None else P["mo"].buf, bi[0], bi[1], bi[2],
-                        bo[0], bo[1], bo[2], workspace=P["ws"], stream=stream)
+        P["plan"].apply(seed, self.first, self.batch.buf if img_in is None else img_in, out, nchw, masks_in,
+                        mo, bi[0], bi[1], bi[2], bo[0], bo[1], bo[2], workspace=ws, stream=stream)
 
     def alg_bytes(self, seeds):
         hw = np.array(self.sizes, np.int32)
@@ -329,68 +331,93 @@ def e2e_run(W, args, stream, dist, dev, world):
     every step copies its inputs from pinned host memory and its results back,
     inside the timed region.  Unmasked plans use alb_apply_host (chunked,
     copies overlapping the kernels); masked / boxed plans copy images, masks and
-    boxes in with torch and call alb_apply."""
+    boxes in with torch and call alb_apply.  Two applies are in flight on two
+    streams (transform i of the menu on stream i % 2; a one-transform menu
+    alternates steps, with a second set of device buffers and workspace), so
+    one apply's result copy overlaps the next one's input copy: the host link
+    carries both directions at once."""
     labels = list(W.menu)
+    streams = [stream, torch.cuda.Stream(dev)]
+    by_step = len(labels) == 1
     host_in = W.batch.buf.cpu().pin_memory()
-    dev_in = torch.empty_like(W.batch.buf)
+    dev_in = [torch.empty_like(W.batch.buf) for _ in streams]
     hm = dm = hb = db = None
     if W.masks is not None:
         hm = W.masks.buf.cpu().pin_memory()
-        dm = torch.empty_like(W.masks.buf)
+        dm = [torch.empty_like(W.masks.buf) for _ in streams]
     if W.boxes is not None:
         hb = [t.cpu().pin_memory() for t in W.boxes]
-        db = [torch.empty_like(t) for t in W.boxes]
-    # one pinned host arena for every transform's results (each D2H lands at
-    # the arena's start; the bytes read back per step are still every result):
-    # keeps pinned memory at ~2 corpora per rank, so 8 ranks fit the host
-    hosts = {}
-    outs_of = {}
-    arena_bytes = 0
+        db = [[torch.empty_like(t) for t in W.boxes] for _ in streams]
+    # device results per (transform, stream): the plan's own on its first
+    # stream, a twin set (and workspace) on the second when steps alternate
+    res = {}
+    home = {label: 0 if by_step else li % 2 for li, label in enumerate(labels)}
     for label in labels:
         P = W.plans[label]
-        outs = [P["out"].buf if P["out"] is not None else P["nchw"]]
-        if P["mo"] is not None:
-            outs.append(P["mo"].buf)
-        if P["bo"] is not None:
-            outs += P["bo"]
-        outs_of[label] = outs
-        arena_bytes = max(arena_bytes, sum(o.numel() * o.element_size() for o in outs))
-    arena = torch.empty(arena_bytes + 256 * 8, dtype=torch.uint8).pin_memory()
+        res[(label, home[label])] = (None if P["out"] is None else P["out"].buf, P["nchw"],
+                                     None if P["mo"] is None else P["mo"].buf, P["bo"], P["ws"])
+        if by_step:
+            o, n, m, b, w = res[(label, 0)]
+            res[(label, 1)] = tuple(None if t is None else ([torch.empty_like(x) for x in t] if isinstance(t, list)
+                                                            else torch.empty_like(t)) for t in (o, n, m, b, w))
+    # one pinned host arena per stream for every transform's results (each
+    # D2H lands at its arena's start; the bytes read back per step are still
+    # every result): ~3 corpora of pinned memory per rank
+    arena_bytes = 0
     for label in labels:
-        views, pos = [], 0
-        for o in outs_of[label]:
-            nb = o.numel() * o.element_size()
-            views.append((arena[pos:pos + nb].view(o.dtype).view(o.shape), o))
-            pos = (pos + nb + 255) // 256 * 256
-        hosts[label] = views
+        o, n, m, b, _ = res[(label, home[label])]
+        arena_bytes = max(arena_bytes, sum(t.numel() * t.element_size() for t in [o if o is not None else n] +
+                                           ([m] if m is not None else []) + (b or [])))
+    arenas = [torch.empty(arena_bytes + 256 * 8, dtype=torch.uint8).pin_memory() for _ in streams]
 
-    def step(seed):
-        for label in labels:
+    def host_views(j, outs):
+        views, pos = [], 0
+        for o in outs:
+            nb = o.numel() * o.element_size()
+            views.append((arenas[j][pos:pos + nb].view(o.dtype).view(o.shape), o))
+            pos = (pos + nb + 255) // 256 * 256
+        return views
+
+    hosts = {}
+    for (label, j), (o, n, m, b, w) in res.items():
+        hosts[(label, j)] = host_views(j, [o if o is not None else n] + ([m] if m is not None else []) + (b or []))
+
+    def step(seed, si):
+        for li, label in enumerate(labels):
+            j = si % 2 if by_step else home[label]
+            st = streams[j]
             P = W.plans[label]
+            r = res[(label, j)]
             if hm is None and hb is None:
-                (ho, do), = hosts[label]
-                P["plan"].apply_host(seed, W.first, host_in, dev_in, ho, do, P["ws"], stream)
+                (ho, do), = hosts[(label, j)]
+                P["plan"].apply_host(seed, W.first, host_in, dev_in[j], ho, do, r[4], st)
                 continue
-            with torch.cuda.stream(stream):
-                dev_in.copy_(host_in, non_blocking=True)
+            with torch.cuda.stream(st):
+                dev_in[j].copy_(host_in, non_blocking=True)
                 if hm is not None:
-                    dm.copy_(hm, non_blocking=True)
+                    dm[j].copy_(hm, non_blocking=True)
                 if hb is not None:
-                    for d, h in zip(db, hb):
+                    for d, h in zip(db[j], hb):
                         d.copy_(h, non_blocking=True)
-                W.apply(label, seed, stream, img_in=dev_in, mask_in=dm, boxes_in=db)
-                for ho, do in hosts[label]:
+                W.apply(label, seed, st, img_in=dev_in[j], mask_in=None if dm is None else dm[j],
+                        boxes_in=None if db is None else db[j], res=r)
+                for ho, do in hosts[(label, j)]:
                     ho.copy_(do, non_blocking=True)
 
-    step(args.seed)  # warm
+    step(args.seed, 0)  # warm
+    step(args.seed, 1)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    streams[1].wait_event(e0)
     for s in range(args.e2e_steps):
-        step(args.seed + s)
+        step(args.seed + s, s)
+    j1 = torch.cuda.Event()
+    j1.record(streams[1])
+    stream.wait_event(j1)
     e1.record(stream)
     torch.cuda.synchronize()
     te = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=dev)
@@ -400,14 +427,14 @@ def e2e_run(W, args, stream, dist, dev, world):
     in_bytes = host_in.numel() + (hm.numel() if hm is not None else 0) + \
         (sum(t.numel() * t.element_size() for t in hb) if hb is not None else 0)
     h2d = len(labels) * in_bytes
-    d2h = sum(h.numel() * h.element_size() for v in hosts.values() for h, _ in v)
+    d2h = sum(h.numel() * h.element_size() for (label, j), v in hosts.items() if j == home[label] for h, _ in v)
     return {"value": round(world * W.n * args.e2e_steps / float(te.item()), 2),
             "unit": unit_of(W.cfg, W.menu),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "path": "alb_apply_host (pinned host in -> HBM -> kernels -> pinned host out, 16 "
-                    "image chunks, copies overlap kernels)" if hm is None and hb is None else
-                    "pinned host images/masks/boxes -> HBM (torch copies), alb_apply, "
-                    "results -> pinned host, on one stream"}
+            "path": ("alb_apply_host (pinned host in -> HBM -> kernels -> pinned host out, 16 image chunks, "
+                     "copies overlap kernels)" if hm is None and hb is None else
+                     "pinned host images/masks/boxes -> HBM (torch copies), alb_apply, results -> pinned host")
+                    + "; two applies in flight on two streams"}
 
 
 def measure(cfg, args, dev, rank, world, dist, peak, peak_src, local):
