@@ -16,10 +16,10 @@
  *  - Pixel / mask / box buffers passed to alb_apply are DEVICE pointers owned
  *    by the caller.  The library owns only its opaque handles (pipeline,
  *    layout, plan), the small device tables a plan uploads at creation and a
- *    side stream per (device, host thread) for label / box work, which
- *    alb_plan_create creates for its thread.  alb_apply allocates no memory;
- *    it creates the side stream only when called with a masked / boxed plan
- *    from a thread other than the one that created the plan.
+ *    small pool of side streams per (device, host thread) for label / box
+ *    work, which alb_plan_create creates for its thread.  alb_apply allocates
+ *    no memory; it creates the pool only when called with a masked / boxed
+ *    plan from a thread other than the one that created the plan.
  *  - Images are HWC uint8, RGB, row-major, x = column, y = row, origin top
  *    left.  A batch is ragged: image i lives at
  *    base + desc[i].offset with desc[i].pitch >= width*channels bytes per row.
@@ -203,8 +203,10 @@ int32_t alb_plan_num_launches(const alb_plan* plan);
  * memset of its histogram workspace) and nothing else -- no host
  * synchronisation, allocation or copy -- so it can be captured into a CUDA
  * graph and replayed (seed and pointers are baked into the graph).  Label
- * (mask) and box work may run on a library-owned side stream (one per
- * device and host thread), forked from `stream` by an event after the
+ * (mask) and box work may run on a library-owned side stream (one of a
+ * pool of 4 per device and host thread, always the same one for a given
+ * `stream`, so applies on different caller streams overlap their label
+ * work too), forked from `stream` by an event after the
  * work already enqueued there and joined back into `stream` before the call
  * returns, so `stream` ordering holds as if everything ran on it; if that
  * stream could not be created, the label / box work runs on `stream`.

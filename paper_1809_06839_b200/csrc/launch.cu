@@ -65,16 +65,22 @@ struct SideStream {
     if (s) cudaStreamDestroy(s);
   }
 };
-// one per (host thread, device), destroyed at thread exit.  Created by
-// side_init() -- alb_plan_create calls it for plans with label / box work, so
-// alb_apply on the plan's thread creates nothing -- or on first use from
-// another thread.  If creation fails the side stream is the caller's stream
-// itself: label / box work then runs in order on it (correct, not overlapped).
-SideStream& side_stream() {
-  thread_local SideStream t[64];
+// kSidePool per (host thread, device), destroyed at thread exit; a caller
+// stream always forks to the same pool entry (hash of the stream handle), so
+// applies on one stream keep their order while applies on different caller
+// streams (two batches in flight) mostly get independent side streams.
+// Created by side_init() -- alb_plan_create calls it for plans with label /
+// box work, so alb_apply on the plan's thread creates nothing -- or on first
+// use from another thread.  If creation fails the side stream is the caller's
+// stream itself: label / box work then runs in order on it (correct, not
+// overlapped).
+constexpr int kSidePool = 4;
+
+SideStream& side_entry(int idx) {
+  thread_local SideStream t[64][kSidePool];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
-  SideStream& r = t[dev & 63];
+  SideStream& r = t[dev & 63][idx];
   if (!r.s) {
     cudaStream_t s = nullptr;
     cudaEvent_t f = nullptr, j = nullptr;
@@ -90,12 +96,21 @@ SideStream& side_stream() {
   }
   return r;
 }
+
+SideStream& side_stream(cudaStream_t caller) {
+  const uintptr_t h = (uintptr_t)caller;
+  return side_entry((int)(((h >> 4) ^ (h >> 12)) % kSidePool));
+}
 }  // namespace
 
-bool side_init() { return side_stream().s != nullptr; }
+bool side_init() {
+  bool ok = true;
+  for (int i = 0; i < kSidePool; ++i) ok = side_entry(i).s != nullptr && ok;
+  return ok;
+}
 
 cudaStream_t side_fork(cudaStream_t s) {
-  SideStream& r = side_stream();
+  SideStream& r = side_stream(s);
   if (!r.s) return s;
   cudaEventRecord(r.fork, s);  // failures surface through cudaGetLastError at the end of the apply
   cudaStreamWaitEvent(r.s, r.fork, 0);
@@ -103,7 +118,7 @@ cudaStream_t side_fork(cudaStream_t s) {
 }
 
 void side_join(cudaStream_t s) {
-  SideStream& r = side_stream();
+  SideStream& r = side_stream(s);
   if (!r.s || r.s == s) return;
   cudaEventRecord(r.join, r.s);
   cudaStreamWaitEvent(s, r.join, 0);
