@@ -590,6 +590,8 @@ def main():
             composed["cfg%d" % cfg] = res
         del W
         torch.cuda.empty_cache()
+        if hasattr(torch._C, "_host_emptyCache"):  # return this config's pinned host buffers
+            torch._C._host_emptyCache()
 
     if rank == 0:
         out = {"metric": METRIC, "value": head["value"], "unit": head["unit"],
