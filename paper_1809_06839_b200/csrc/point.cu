@@ -132,6 +132,14 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
     const int nv = (s.bE - s.bA) / 16;
     const uint4* s4 = reinterpret_cast<const uint4*>(s.src + s.bA);
     uint4* d4 = reinterpret_cast<uint4*>(s.dst + s.bA);
+    // vector v starts on channel v % 3 (16 = 1 mod 3); with kThreads = 1 and
+    // kThreads * kU = 0 (mod 3), thread t's k-th vector of every pass starts
+    // on channel (t + k) % 3: the three channel table bases are rotated at
+    // compile time instead of recomputed per vector
+    static_assert(kThreads % 3 == 1 && (kThreads * kU) % 3 == 0, "vector phases must repeat per pass");
+    const int pt = threadIdx.x % 3;
+    const uint32_t cbt[3] = {lb + (uint32_t)pt * 8192u, lb + (uint32_t)(pt == 2 ? 0 : pt + 1) * 8192u,
+                             lb + (uint32_t)(pt == 0 ? 2 : pt - 1) * 8192u};
     for (int v0 = threadIdx.x; v0 < nv; v0 += kThreads * kU) {
       uint4 in[kU];
 #pragma unroll
@@ -146,9 +154,7 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
           const int ph = v % 3;  // channel of byte j is (ph + j) % 3 (segment starts on a pixel)
           uint32_t w[4] = {in[k].x, in[k].y, in[k].z, in[k].w};
           if constexpr (kNL1) {
-            const uint32_t c0 = lb + (uint32_t)ph * 8192u;
-            const uint32_t c1 = lb + (uint32_t)(ph == 2 ? 0 : ph + 1) * 8192u;
-            const uint32_t c2 = lb + (uint32_t)(ph == 0 ? 2 : ph - 1) * 8192u;
+            const uint32_t c0 = cbt[k % 3], c1 = cbt[(k + 1) % 3], c2 = cbt[(k + 2) % 3];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               uint32_t r[4];
@@ -358,7 +364,7 @@ __device__ __forceinline__ uint4 ld_evict_last(const uint4* p, uint64_t pol) {
 
 __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
   extern __shared__ uint32_t sm_raw[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t raw_addr = (uint32_t)__cvta_generic_to_shared(sm_raw);
   uint32_t* hl = sm_raw + (((8192u - (raw_addr & 8191u)) & 8191u) >> 2);  // 8 KB aligned, [768][32]
   uint32_t* cnt = hl + 768 * 32;                                          // [768]
@@ -388,6 +394,13 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
     const int nv = (bE - bA) / 16;
     constexpr int kV = 4;  // vectors in flight per thread (64 KB per SM)
     const uint64_t pol = policy_evict_last();
+    // vector v starts on channel (bA + v) % 3; thread tid's k-th vector of
+    // pass j on (bA + tid + k + j) % 3 (kEqF = 1 and kV * kEqF = 1 mod 3):
+    // three bin-table bases, rotated by one per pass and renamed per k
+    static_assert(kEqF % 3 == 1 && (kV * kEqF) % 3 == 1, "histogram vector phases");
+    const int p0 = (bA + tid) % 3;
+    uint32_t hb[3] = {hl_base + (uint32_t)p0 * 32768u, hl_base + (uint32_t)(p0 == 2 ? 0 : p0 + 1) * 32768u,
+                      hl_base + (uint32_t)(p0 == 0 ? 2 : p0 - 1) * 32768u};
     for (int v0 = tid; v0 < nv; v0 += kV * kEqF) {
       uint4 t[kV];
 #pragma unroll
@@ -398,10 +411,7 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
         const int v = v0 + k * kEqF;
         if (v >= nv) break;
         const uint32_t w[4] = {t[k].x, t[k].y, t[k].z, t[k].w};
-        const int ph = (bA + 16 * v) % 3;
-        const uint32_t b0 = hl_base + (uint32_t)ph * 32768u;
-        const uint32_t b1 = hl_base + (uint32_t)(ph == 2 ? 0 : ph + 1) * 32768u;
-        const uint32_t b2 = hl_base + (uint32_t)(ph == 0 ? 2 : ph - 1) * 32768u;
+        const uint32_t b0 = hb[k % 3], b1 = hb[(k + 1) % 3], b2 = hb[(k + 2) % 3];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const uint32_t cb = (j % 3 == 0) ? b0 : ((j % 3 == 1) ? b1 : b2);
@@ -409,6 +419,10 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
           asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(xb * 128u + cb) : "memory");
         }
       }
+      const uint32_t r0 = hb[0];  // next pass starts one channel later
+      hb[0] = hb[1];
+      hb[1] = hb[2];
+      hb[2] = r0;
     }
   }
   __syncthreads();
@@ -466,6 +480,11 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
   const int nv = (sg.bE - sg.bA) / 16;
   const uint4* s4 = reinterpret_cast<const uint4*>(sg.src + sg.bA);
   uint4* d4 = reinterpret_cast<uint4*>(sg.dst + sg.bA);
+  // channel table bases rotated at compile time (as k_point_lut)
+  static_assert(kEqF % 3 == 1 && (kEqF * kU) % 3 == 0, "vector phases must repeat per pass");
+  const int pt = tid % 3;
+  const uint32_t cbt[3] = {lb + (uint32_t)pt * 8192u, lb + (uint32_t)(pt == 2 ? 0 : pt + 1) * 8192u,
+                           lb + (uint32_t)(pt == 0 ? 2 : pt - 1) * 8192u};
   for (int v0 = tid; v0 < nv; v0 += kEqF * kU) {
     uint4 in[kU];
 #pragma unroll
@@ -477,11 +496,8 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
     for (int k = 0; k < kU; ++k) {
       const int v = v0 + k * kEqF;
       if (v < nv) {
-        const int ph = v % 3;
         uint32_t w[4] = {in[k].x, in[k].y, in[k].z, in[k].w};
-        const uint32_t c0 = lb + (uint32_t)ph * 8192u;
-        const uint32_t c1 = lb + (uint32_t)(ph == 2 ? 0 : ph + 1) * 8192u;
-        const uint32_t c2 = lb + (uint32_t)(ph == 0 ? 2 : ph - 1) * 8192u;
+        const uint32_t c0 = cbt[k % 3], c1 = cbt[(k + 1) % 3], c2 = cbt[(k + 2) % 3];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint32_t r[4];
