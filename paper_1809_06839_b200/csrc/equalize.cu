@@ -137,6 +137,14 @@ __global__ void __launch_bounds__(kEqLThreads) k_eq_hist_lane(EqArgs a) {
   for (int b = bE + tid; b < n; b += kEqLThreads) atomicAdd(&hw[((b % 3) * 256 + src[b]) * 32], 1u);
   const uint4* s4 = reinterpret_cast<const uint4*>(src + bA);
   const int nv = (bE - bA) / 16;
+  // vector v starts on channel (bA + v) % 3 (16 = 1 mod 3): thread tid's k-th
+  // vector of pass j on (bA + tid + k + 2 j) % 3; the three bin-table bases
+  // (shared byte address of (channel c, value x, lane) = base_c + 128 x) are
+  // renamed per k and rotated by two per pass
+  static_assert(kEqLThreads % 3 == 1 && (2 * kEqLThreads) % 3 == 2, "histogram vector phases");
+  const int p0 = (bA + tid) % 3;
+  uint32_t hb[3] = {hl_base + (uint32_t)p0 * 32768u, hl_base + (uint32_t)(p0 == 2 ? 0 : p0 + 1) * 32768u,
+                    hl_base + (uint32_t)(p0 == 0 ? 2 : p0 - 1) * 32768u};
   for (int v0 = tid; v0 < nv; v0 += 2 * kEqLThreads) {
     uint4 t[2];
 #pragma unroll
@@ -147,12 +155,8 @@ __global__ void __launch_bounds__(kEqLThreads) k_eq_hist_lane(EqArgs a) {
       const int v = v0 + k * kEqLThreads;
       if (v >= nv) break;
       const uint32_t w[4] = {t[k].x, t[k].y, t[k].z, t[k].w};
-      const int ph = (bA + 16 * v) % 3;
-      // shared byte address of (channel c, value x, lane) = base_c + 128 x:
       // one byte extract (PRMT), one IMAD, one RED per byte
-      const uint32_t b0 = hl_base + (uint32_t)ph * 32768u;
-      const uint32_t b1 = hl_base + (uint32_t)(ph == 2 ? 0 : ph + 1) * 32768u;
-      const uint32_t b2 = hl_base + (uint32_t)(ph == 0 ? 2 : ph - 1) * 32768u;
+      const uint32_t b0 = hb[k % 3], b1 = hb[(k + 1) % 3], b2 = hb[(k + 2) % 3];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const uint32_t cb = (j % 3 == 0) ? b0 : ((j % 3 == 1) ? b1 : b2);
@@ -160,6 +164,10 @@ __global__ void __launch_bounds__(kEqLThreads) k_eq_hist_lane(EqArgs a) {
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(x * 128u + cb) : "memory");
       }
     }
+    const uint32_t r0 = hb[0];  // next pass starts two channels later
+    hb[0] = hb[2];
+    hb[2] = hb[1];
+    hb[1] = r0;
   }
   __syncthreads();
   for (int i = tid; i < 768; i += kEqLThreads) {
