@@ -104,6 +104,14 @@ __device__ __forceinline__ uint32_t mulhi_pow2(uint32_t x, int k) {
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << k));
   return r;
 }
+// byte permute with a run-time selector whose nibbles are known to be
+// 0..7 (no sign-replicate bit): PTX prmt directly, so the compiler does not
+// mask the selector first as it must for __byte_perm
+__device__ __forceinline__ uint32_t prmt_raw(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
 
 template <bool kNL1>
 __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
@@ -172,8 +180,8 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
               // upper two bytes are dropped by the final permute)
               const uint32_t xs = w[q] & 0x03030303u;
               const uint32_t y = xs | (xs >> 4) | 0x00400040u;  // byte k: (v_k & 3) | (4 + (v_{k+1} & 3)) << 4
-              const uint32_t lo = __byte_perm(r[0], r[1], y);
-              const uint32_t hi = __byte_perm(r[2], r[3], y >> 16);
+              const uint32_t lo = prmt_raw(r[0], r[1], y);
+              const uint32_t hi = prmt_raw(r[2], r[3], y >> 16);
               w[q] = __byte_perm(lo, hi, 0x5410u);
             }
           } else {
@@ -511,8 +519,8 @@ __global__ void __launch_bounds__(kEqF, 1024 / kEqF) k_eq_fused(StepArgs a) {
           }
           const uint32_t xs = w[q] & 0x03030303u;
           const uint32_t y = xs | (xs >> 4) | 0x00400040u;
-          const uint32_t lo = __byte_perm(r[0], r[1], y);
-          const uint32_t hi = __byte_perm(r[2], r[3], y >> 16);
+          const uint32_t lo = prmt_raw(r[0], r[1], y);
+          const uint32_t hi = prmt_raw(r[2], r[3], y >> 16);
           w[q] = __byte_perm(lo, hi, 0x5410u);
         }
         __stcs(d4 + v, make_uint4(w[0], w[1], w[2], w[3]));
