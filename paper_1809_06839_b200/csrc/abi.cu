@@ -432,6 +432,11 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.rs_hw = st.rs_hw;
     a.rs_q = st.rs_q;
     a.self_sample = st.self_sample;
+    a.lut_k0 = a.lut_k1 = 0;
+    if (st.self_sample && st.kind == SK_POINT) {
+      a.lut_k0 = P->lut_k0[st.stages[0].lut];
+      a.lut_k1 = P->lut_k1[st.stages[0].lut];
+    }
     a.seed = seed;
     a.first_image = (uint32_t)first_image_index;
     a.gauss = P->d_gauss ? P->d_gauss + st.g_off : nullptr;
@@ -811,6 +816,10 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
 #ifndef ALB_NO_SELF_SAMPLE
   if (steps.size() == 1 && steps[0].kind == SK_ROW && P->n_luts == 0 && P->norm_slot < 0 && max_boxes == 0)
     steps[0].self_sample = 1;
+  // ... and so does a lone one-LUT pointwise step (its CTAs build the LUT)
+  if (steps.size() == 1 && steps[0].kind == SK_POINT && !steps[0].normalize && P->norm_slot < 0 &&
+      max_boxes == 0 && P->n_luts == 1 && steps[0].stages.size() == 1 && steps[0].stages[0].type == ST_LUT)
+    steps[0].self_sample = 1;
 #endif
   // LUT count per step must fit shared memory (<= 4 stages of 24 KB)
   for (auto& st : steps) {
@@ -1070,8 +1079,10 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   // self-sampling pays only for few CTAs per image (every CTA draws its image's
   // params; measured: RandomCrop64 0.021 -> 0.017 ms, but the flips and the
   // pad, ~6 CTAs per image, 1-2% slower than one K0 launch)
+  // (LUT steps: ~2 units of 240 KB per image; measured)
   for (auto& st : steps)
-    if (st.self_sample && st.units.size() > 2 * (size_t)std::max(P->n, 1)) st.self_sample = 0;
+    if (st.self_sample && st.units.size() > (st.kind == SK_POINT ? 4 : 2) * (size_t)std::max(P->n, 1))
+      st.self_sample = 0;
   // units are generated image by image: image i owns [ustart[i], ustart[i+1])
   for (auto& st : steps) {
     for (int pass = 0; pass < 2; ++pass) {

@@ -65,6 +65,7 @@ struct StepArgs {
   int32_t rs_ring, rs_sw, rs_hw;  // separable resample: ring rows (0 = old kernel), staged row
                                    // stride (words), output rows per group
   int32_t self_sample;             // 1: the kernel draws its images' params itself (no K0 launch)
+  int32_t lut_k0, lut_k1;          // self-sampling LUT step: op slots [lut_k0, lut_k1) of its one LUT
   int32_t rs_q;                    // quad-column resample: staged window rows per unit (0 = off);
                                    // rs_sw = window columns per 128-column strip, unit_rows = R
   uint64_t seed;                   // Philox key of this apply (ElasticTransform raw planes)
@@ -204,6 +205,23 @@ __device__ __forceinline__ Tables self_sample_tables(const StepArgs& a, int img,
   t.fired = st.fired;
   t.dims = st.dims;
   return t;
+}
+
+// one LUT op applied to channel c's value x (fp64, no contraction; K0 and the
+// self-sampling LUT kernel share it, so their tables are identical)
+__device__ __forceinline__ int lut_entry(int kind, const double* q, int c, int x) {
+  const double v = (double)x;
+  switch (kind) {
+    case ALB_BRIGHTNESS: return clip_round_d(__dmul_rn(v, q[0]));
+    case ALB_CONTRAST: return clip_round_d(__dadd_rn(127.5, __dmul_rn(__dsub_rn(v, 127.5), q[0])));
+    case ALB_BRIGHTNESS_CONTRAST: {
+      const double t = (double)clip_round_d(__dmul_rn(v, q[0]));
+      return clip_round_d(__dadd_rn(127.5, __dmul_rn(__dsub_rn(t, 127.5), q[1])));
+    }
+    case ALB_GAMMA: return clip_round_d(__dmul_rn(255.0, pow(__ddiv_rn(v, 255.0), q[0])));
+    case ALB_SHIFT_RGB: return clip_round_d(__dadd_rn(v, q[c]));
+    default: return x;
+  }
 }
 
 // ±1 affine integer map output -> input with a valid output rectangle.

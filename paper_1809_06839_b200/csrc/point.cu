@@ -113,6 +113,37 @@ __device__ __forceinline__ uint32_t prmt_raw(uint32_t a, uint32_t b, uint32_t se
   return r;
 }
 
+// Self-sampling LUT step (StepArgs::self_sample; one LUT stage, the plan's
+// only step): image img's gate + params drawn here by thread 0 (sample_core,
+// as K0), the composed 3 x 256 LUT built by the CTA in fp64 with the same
+// lut_entry as K0, then replicated per lane into the stage's shared table
+// exactly as load_stages does from K0's global table.
+struct SelfLut {
+  double prm[kMaxOps * kMaxParams];
+  int32_t dims[2 * (kMaxOps + 1)];
+  uint8_t fired[kMaxOps];
+  uint32_t lut[192];  // 768 bytes
+};
+__device__ __forceinline__ void self_lut(const StepArgs& a, int img, uint32_t* sm, const StageCtx& x, SelfLut& t) {
+  if (threadIdx.x == 0) {
+    const alb_image_desc sd = a.sdesc[img];
+    sample_core(a.ops, a.tab.n_ops, a.seed, a.first_image + (uint32_t)img, sd.height, sd.width, t.prm, t.fired,
+                t.dims);
+  }
+  __syncthreads();
+  uint8_t* l8 = reinterpret_cast<uint8_t*>(t.lut);
+  for (int e = threadIdx.x; e < 768; e += kThreads) {
+    const int c = e >> 8;
+    int v = e & 255;
+    for (int k = a.lut_k0; k < a.lut_k1; ++k)
+      if (t.fired[k]) v = lut_entry(a.ops[k].kind, t.prm + k * kMaxParams, c, v);
+    l8[e] = (uint8_t)v;
+  }
+  __syncthreads();
+  uint32_t* dst = sm + x.smb[0];
+  for (int idx = threadIdx.x; idx < kLutWords; idx += kThreads) dst[idx] = t.lut[idx >> 5];
+}
+
 template <bool kNL1>
 __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
   extern __shared__ uint32_t sm_raw[];
@@ -126,11 +157,13 @@ __global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
   int u0, u1;
   unit_range(a.n_units, u0, u1);
   int cur_img = -1;
+  __shared__ SelfLut self_t;
   for (int u = u0; u < u1; ++u) {
     const int2 unit = a.units[u];
     if (unit.x != cur_img) {
       __syncthreads();
-      load_stages(a, unit.x, sm, x, kThreads);
+      if (kNL1 && a.self_sample) self_lut(a, unit.x, sm, x, self_t);
+      else load_stages(a, unit.x, sm, x, kThreads);
       __syncthreads();
       cur_img = unit.x;
     }

@@ -6,21 +6,6 @@
 
 namespace alb {
 
-__device__ int lut_entry(int kind, const double* q, int c, int x) {
-  const double v = (double)x;
-  switch (kind) {
-    case ALB_BRIGHTNESS: return clip_round_d(__dmul_rn(v, q[0]));
-    case ALB_CONTRAST: return clip_round_d(__dadd_rn(127.5, __dmul_rn(__dsub_rn(v, 127.5), q[0])));
-    case ALB_BRIGHTNESS_CONTRAST: {
-      const double t = (double)clip_round_d(__dmul_rn(v, q[0]));
-      return clip_round_d(__dadd_rn(127.5, __dmul_rn(__dsub_rn(t, 127.5), q[1])));
-    }
-    case ALB_GAMMA: return clip_round_d(__dmul_rn(255.0, pow(__ddiv_rn(v, 255.0), q[0])));
-    case ALB_SHIFT_RGB: return clip_round_d(__dadd_rn(v, q[c]));
-    default: return x;
-  }
-}
-
 // GridDistortion knot displacements of one axis (reading R31, in the
 // order DESIGN.md states): factors f_i = 1 + U(lo, hi) from draws j0 + i,
 // c_{i+1} = c_i + f_i, e_i = (L-1) c_i / S - (L-1) i / n, e_0 = e_n = 0.
