@@ -433,7 +433,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.rs_q = st.rs_q;
     a.self_sample = st.self_sample;
     a.lut_k0 = a.lut_k1 = 0;
-    if (st.self_sample && st.kind == SK_POINT) {
+    if (st.self_sample && st.kind == SK_POINT && st.stages[0].type == ST_LUT) {
       a.lut_k0 = P->lut_k0[st.stages[0].lut];
       a.lut_k1 = P->lut_k1[st.stages[0].lut];
     }
@@ -819,6 +819,12 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   // ... and so does a lone one-LUT pointwise step (its CTAs build the LUT)
   if (steps.size() == 1 && steps[0].kind == SK_POINT && !steps[0].normalize && P->norm_slot < 0 &&
       max_boxes == 0 && P->n_luts == 1 && steps[0].stages.size() == 1 && steps[0].stages[0].type == ST_LUT)
+    steps[0].self_sample = 1;
+  // ... and a lone HSV / gray pointwise step (parameters only, no tables)
+  if (steps.size() == 1 && steps[0].kind == SK_POINT && !steps[0].normalize && P->norm_slot < 0 &&
+      max_boxes == 0 && P->n_luts == 0 && !steps[0].stages.empty() &&
+      std::all_of(steps[0].stages.begin(), steps[0].stages.end(),
+                  [](const Stage& g) { return g.type == ST_HSV || g.type == ST_GRAY; }))
     steps[0].self_sample = 1;
 #endif
   // LUT count per step must fit shared memory (<= 4 stages of 24 KB)

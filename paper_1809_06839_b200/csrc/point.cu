@@ -145,7 +145,7 @@ __device__ __forceinline__ void self_lut(const StepArgs& a, int img, uint32_t* s
 }
 
 template <bool kNL1>
-__global__ void __launch_bounds__(kThreads) k_point_lut(StepArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_point_lut(StepArgs a) {
   extern __shared__ uint32_t sm_raw[];
   const int lane = threadIdx.x & 31;
   // 8 KB-aligned LUT base (the launch reserves 8 KB of slack)
@@ -254,11 +254,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_point_px(StepArgs a) {
   unit_range(a.n_units, u0, u1);
   int cur_img = -1;
   const float* nl = a.tab.norm_lut;
+  __shared__ SelfLut self_t;  // self-sampling (HSV / gray only): thread 0's draws for the image
   for (int u = u0; u < u1; ++u) {
     const int2 unit = a.units[u];
     if (unit.x != cur_img) {
       __syncthreads();
-      load_stages(a, unit.x, sm, x, kThreads);
+      if (a.self_sample) {
+        if (threadIdx.x == 0) {
+          const alb_image_desc sd = a.sdesc[unit.x];
+          sample_core(a.ops, a.tab.n_ops, a.seed, a.first_image + (uint32_t)unit.x, sd.height, sd.width, self_t.prm,
+                      self_t.fired, self_t.dims);
+        }
+        __syncthreads();
+        Tables t = a.tab;
+        t.params = self_t.prm;
+        t.fired = self_t.fired;
+        load_px_params(a, t, 0, x);
+      } else {
+        load_stages(a, unit.x, sm, x, kThreads);
+      }
       __syncthreads();
       cur_img = unit.x;
     }

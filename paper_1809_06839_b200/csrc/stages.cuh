@@ -50,6 +50,28 @@ __device__ __forceinline__ void init_stages(const StepArgs& a, StageCtx& x) {
 // warp's 32 lookups hit 32 distinct banks) and fetch per-stage params.
 // Caller brackets with __syncthreads().
 __device__ __forceinline__ void load_stages(const StepArgs& a, int img, uint32_t* sm, StageCtx& x,
+                                            int nthreads);
+
+// Per-stage HSV / gray params of image `img` of table view `tab` (no LUT stages).
+__device__ __forceinline__ void load_px_params(const StepArgs& a, const Tables& tab, int img, StageCtx& x) {
+#pragma unroll
+  for (int s = 0; s < kMaxStages; ++s) {
+    const int t = x.type[s];
+    if (t == ST_HSV || t == ST_GRAY) {
+      x.on[s] = fired_of(tab, img, a.stages[s].slot) ? 1 : 0;
+      if (t == ST_HSV) {
+        const double* q = prm_of(tab, img, a.stages[s].slot);
+        double w = q[0] / 60.0;          // hue shift in sixths of a turn, wrapped to [0, 6)
+        w -= 6.0 * floor(w / 6.0);
+        x.dh[s] = (float)w;
+        x.ds[s] = (float)q[1];
+        x.dv[s] = (float)q[2];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void load_stages(const StepArgs& a, int img, uint32_t* sm, StageCtx& x,
                                             int nthreads) {
 #pragma unroll
   for (int s = 0; s < kMaxStages; ++s) {
