@@ -785,3 +785,27 @@ def test_long_pointwise_chain_splits_into_steps(lead):
     g = run_gpu(specs, b, seed=2, first=40)["images"]
     r = run_oracle(specs, [b.image(i) for i in range(len(sizes))], seed=2, first=40)
     cmp_exact(g, [x["image"] for x in r])
+
+
+@pytest.mark.parametrize("spec", [
+    {"kind": "ShiftHSV", "lo": [-30.0, -0.2, -0.2], "hi": [30.0, 0.2, 0.2], "p": 0.5},
+    {"kind": "Grayscale", "p": 0.5},
+    {"kind": "Brightness", "lo": [0.7], "hi": [1.3], "p": 0.5},
+    {"kind": "Gamma", "lo": [0.7], "hi": [1.4], "p": 0.5},
+    {"kind": "Equalize", "p": 0.5},
+])
+def test_lone_gated_pointwise_ops_self_sample(spec):
+    """A lone pointwise op (the planner lets its kernel draw the parameters and
+    build the LUT itself, no K0 launch) with a gate p = 0.5: images whose gate
+    does not fire are unchanged, the others match the oracle (LUT ops, gray,
+    Equalize exact; HSV at the interpolation bar)."""
+    sizes = gen.cfg2_sizes(40, first_image_index=11)
+    b = gen.gen_images(sizes, seed=8, first_image_index=11, device="cuda")
+    g = run_gpu([spec], b, seed=77, first=11)["images"]
+    r = [x["image"] for x in run_oracle([spec], [b.image(i) for i in range(len(sizes))], seed=77, first=11)]
+    if spec["kind"] == "ShiftHSV":
+        cmp_interp(g, r)
+    else:
+        cmp_exact(g, r)
+    same = sum(np.array_equal(gi, b.image(i)) for i, gi in enumerate(g))
+    assert 0 < same < len(sizes)  # both gate outcomes occur in the batch
