@@ -145,7 +145,10 @@ __device__ __forceinline__ void self_lut(const StepArgs& a, int img, uint32_t* s
 }
 
 template <bool kNL1>
-__global__ void __launch_bounds__(kThreads, 4) k_point_lut(StepArgs a) {
+#ifndef ALB_LUT_MINB
+#define ALB_LUT_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, ALB_LUT_MINB) k_point_lut(StepArgs a) {
   extern __shared__ uint32_t sm_raw[];
   const int lane = threadIdx.x & 31;
   // 8 KB-aligned LUT base (the launch reserves 8 KB of slack)
@@ -245,7 +248,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_point_lut(StepArgs a) {
 // pixel-wise chain (HSV / gray / mixed / Normalize output); kNorm is
 // compile-time so the unused output path is not issued per pixel
 template <int kOne, bool kNorm>
-__global__ void __launch_bounds__(kThreads, 4) k_point_px(StepArgs a) {
+#ifndef ALB_PX_MINB
+#define ALB_PX_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, ALB_PX_MINB) k_point_px(StepArgs a) {
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31;
   StageCtx x;
