@@ -140,7 +140,7 @@ struct alb_plan {
   bool has_eq = false;
   // workspace layout
   size_t off_params = 0, off_fired = 0, off_dims = 0, off_luts = 0, off_norm = 0,
-         off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, off_geo = 0, off_grid = 0,
+         off_eqh = 0, off_eql = 0, off_buf[2] = {0, 0}, off_mbuf[2] = {0, 0}, off_geo = 0, off_tiles = 0, off_grid = 0,
          ws_bytes = 0;
   int n_grid = 0;  // GridDistortion slots (per-image knot tables in the workspace)
   std::vector<double> gauss;  // ElasticTransform weights of every elastic step (host copy)
@@ -425,6 +425,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.tab = tab;
     a.ops = P->d_ops;
     a.geo = ws + P->off_geo;
+    a.tiles = st.kind == SK_AFFINE ? ws + P->off_tiles + (st.units_off + st.ustart[i0]) * kTileInfoBytes : nullptr;
     a.img0 = i0;
     a.n_img = i1;
     a.rs_ring = st.rs_ring;
@@ -1139,6 +1140,10 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   P->off_eqh = take(P->has_eq ? nn * 768 * sizeof(uint32_t) : 0);
   P->off_eql = take(P->has_eq ? nn * 768 : 0);
   P->off_geo = take(nn * kGeoBytes);  // per-image affine state (affine steps)
+  size_t aff_units_end = 0;  // per-unit tile state of affine steps, indexed like the unit table
+  for (const auto& st : steps)
+    if (st.kind == SK_AFFINE) aff_units_end = std::max(aff_units_end, st.units_off + st.units.size());
+  P->off_tiles = take(aff_units_end * kTileInfoBytes);
   for (const alb_op& o : P->ops) P->n_grid += o.kind == ALB_GRID_DISTORTION;
   P->off_grid = take(nn * P->n_grid * kGridStride * sizeof(double));  // knot displacements (R31)
   P->off_buf[0] = take(max_inter + 64);

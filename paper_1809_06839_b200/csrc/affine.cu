@@ -34,6 +34,8 @@
 // (generic variant).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 
 #include "stages.cuh"
 
@@ -916,6 +918,303 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_affine_rt -- raw-tap affine kernel (the bilinear u8 fast path).
+//
+// One 64 x 64 output tile at a time per CTA (persistent over a contiguous
+// unit range), four CTAs per SM so the phases of different CTAs overlap
+// instead of an in-CTA producer pipeline.  Per tile:
+//   0. (k_affine_setup_units, one thread per unit, before the kernel) the
+//      tile's source footprint from its fp64 corners -> TileInfo;
+//   1. footprint rows are copied RAW (RGB bytes) by 16-byte cp.async into
+//      rows of pitch kRPitch, two threads per row; row r starts at
+//      r * kRPitch + 16 + (its global 16-byte phase), so every copy is
+//      aligned on both sides; rows outside the image are the reflect-101
+//      source rows (border_idx), copied the same way; a table holds each
+//      row's base (rb[r], rb[r + 1]); meanwhile the previous tile's output is
+//      copied out;
+//   2. border columns (x < 0 or x >= W) are filled from the reflected column
+//      of the same staged row (or the fill value), one pixel per thread;
+//   3. compute: warp w owns output rows [8w, 8w + 8), lane = columns lane and
+//      lane + 32; the same fp64-cell-anchor / fp32-offset coordinates and the
+//      same paired-fp32 blend as k_affine / k_affine_pipe (bit-identical
+//      outputs), taps = 3 aligned 32-bit shared loads per tap row
+//      funnel-shifted by the tap address's byte phase (no RGB -> RGBx
+//      restage); bytes go to the pre-shifted output row buffer.
+constexpr int kRThreads = 256;
+constexpr int kRRows = 108;   // footprint rows (fh <= 104 for a 64-px tile at scale >= 0.9)
+constexpr int kRPitch = 368;  // raw row pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk) for fw <= 107
+constexpr int kRMaxW = (kRPitch - 46) / 3;
+constexpr int kROffTab = 0;                 // int2 [kRRows]: (rb[r], rb[r + 1])
+constexpr int kROffRaw = kRRows * 8 + 16;   // raw rows [kRRows][kRPitch]
+constexpr int kRSmem = kROffRaw + kRRows * kRPitch + 16;
+static_assert(kROffRaw % 16 == 0, "16-byte aligned raw rows");
+
+struct TileInfo {
+  int fx0, fy0, fw, fh;  // source footprint (bilinear halo + 1 px rounding margin)
+  int img, txy, twh;     // image; tile origin tx0 | ty0 << 16; extent tw | th << 16
+  uint32_t mb;           // magic of the border pass's per-row item count
+};
+static_assert(sizeof(TileInfo) == kTileInfoBytes, "TileInfo is the per-unit scratch record");
+
+// footprint of the output tile [tx0, tx0 + tw) x [ty0, ty0 + th) (warp-output
+// coordinates through the fused post map), the bound every affine kernel uses
+__device__ __forceinline__ void tile_footprint(const ImgState& s, int tx0, int ty0, int tw, int th, int& fx0,
+                                               int& fy0, int& fw, int& fh) {
+  const Map1& m = s.m;
+  const int xwa = m.ax * tx0 + m.bx, xwb = m.ax * (tx0 + tw - 1) + m.bx;
+  const int ywa = m.ay * ty0 + m.by, ywb = m.ay * (ty0 + th - 1) + m.by;
+  double lx = 1e300, hx = -1e300, ly = 1e300, hy = -1e300;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double xw = (c & 1) ? max(xwa, xwb) : min(xwa, xwb);
+    const double yw = (c & 2) ? max(ywa, ywb) : min(ywa, ywb);
+    const double sx = fma(s.A[0], xw, fma(s.A[1], yw, s.A[2]));
+    const double sy = fma(s.A[3], xw, fma(s.A[4], yw, s.A[5]));
+    lx = fmin(lx, sx); hx = fmax(hx, sx); ly = fmin(ly, sy); hy = fmax(hy, sy);
+  }
+  fx0 = (int)floor(lx) - 1;
+  fy0 = (int)floor(ly) - 1;
+  fw = (int)floor(hx) + 2 - fx0 + 1;
+  fh = (int)floor(hy) + 2 - fy0 + 1;
+}
+
+// Per-unit setup of the raw-tap kernel (one thread per unit): the image's
+// affine state (written by the image's first unit of this launch, read by
+// the label kernel too) and the tile's footprint record.
+__global__ void k_affine_setup_units(StepArgs a) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.n_units) return;
+  const int2 unit = a.units[u];
+  const int img = unit.x;
+  const AfCoef cf = af_coef(a, img);
+  ImgState s;
+  for (int k = 0; k < 6; ++k) s.A[k] = cf.A[k];
+  s.Af[0] = (float)cf.A[0]; s.Af[1] = (float)cf.A[1];
+  s.Af[2] = (float)cf.A[3]; s.Af[3] = (float)cf.A[4];
+  s.Wo = a.ddesc[img].width;
+  s.Ho = a.ddesc[img].height;
+  s.m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, s.Wo, s.Ho);
+  s.tiles_x = (s.Wo + kTileW - 1) / kTileW;
+  s.pad = 0;
+  if (u == 0 || a.units[u - 1].x != img)
+    *reinterpret_cast<ImgState*>(reinterpret_cast<uint8_t*>(a.geo) + (size_t)img * kGeoBytes) = s;
+  TileInfo t;
+  const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
+  const int tw = min(kTileW, s.Wo - tx0), th = min(kTileH, s.Ho - ty0);
+  tile_footprint(s, tx0, ty0, tw, th, t.fx0, t.fy0, t.fw, t.fh);
+  t.img = img;
+  t.txy = tx0 | (ty0 << 16);
+  t.twh = tw | (th << 16);
+  const alb_image_desc sd = a.sdesc[img];
+  const int xa = min(max(t.fx0, 0), sd.width), xb = max(min(t.fx0 + t.fw, sd.width), xa);
+  const bool fill_rows = a.border != ALB_BORDER_REFLECT_101 && (t.fy0 < 0 || t.fy0 + t.fh > sd.height);
+  const int ncols = fill_rows ? t.fw : (xa - t.fx0) + (t.fx0 + t.fw - xb);
+  t.mb = magic_of((uint32_t)max(ncols, 1));
+  reinterpret_cast<TileInfo*>(a.tiles)[u] = t;
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+template <int kOne>
+#ifndef ALB_RT_MINB
+#define ALB_RT_MINB 4  // CTAs per SM the raw-tap kernel is compiled for (register cap)
+#endif
+__global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a) {
+  extern __shared__ uint32_t sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  StageCtx x;
+  init_stages(a, x);
+  uint8_t* smb = reinterpret_cast<uint8_t*>(sm + x.n_lut * kLutWords);
+  int* rtab = reinterpret_cast<int*>(smb + kROffTab);
+  uint8_t* raw = smb + kROffRaw;
+  const uint32_t tab_a = smem_u32(rtab);
+  const uint32_t raw_a = smem_u32(raw);
+  const bool reflect = a.border == ALB_BORDER_REFLECT_101;
+  const TileInfo* tinfo = reinterpret_cast<const TileInfo*>(a.tiles);
+
+  int u0, u1;
+  unit_range(a.n_units, u0, u1);
+  int lut_img = -1;
+  for (int u = u0; u < u1; ++u) {
+    const TileInfo t = tinfo[u];
+    const int img = t.img;
+    const int fx0 = t.fx0, fy0 = t.fy0, fw = t.fw, fh = t.fh;
+    const int tx0 = t.txy & 0xffff, ty0 = t.txy >> 16, tw = t.twh & 0xffff, th = t.twh >> 16;
+    const alb_image_desc sd = a.sdesc[img];
+    const int Ws = sd.width, Hs = sd.height;
+    const uint8_t* simg = a.src + sd.offset;
+    const bool fits = fw <= kRMaxW && fh <= kRRows;
+    if (kOne != kStagesNone && img != lut_img) {  // LUTs are read only in the compute phase
+      load_stages(a, img, sm, x, kRThreads);
+      lut_img = img;
+    }
+    // ---- 1. raw row copies: thread 2r + h copies chunks h, h + 2, ... of row r
+    const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);  // in-image columns [xa, xb)
+    if (fits && tid < 2 * fh) {
+      const int r = tid >> 1, h = tid & 1;
+      bool in;
+      const int ry = border_idx(fy0 + r, Hs, reflect, in);
+      const uintptr_t g = (uintptr_t)(simg + (size_t)(in ? ry : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+      if (in) {
+        const uintptr_t g0 = g + 3 * (xa - fx0), ge = g0 + 3 * (xb - xa);
+        // column fx0 (address g) sits at r * kRPitch + 16 + (g & 15)
+        const uint32_t d0 = raw_a + (uint32_t)(r * kRPitch + 16) - (uint32_t)(g & ~(uintptr_t)15);
+        for (uintptr_t gk = (g0 & ~(uintptr_t)15) + 16 * h; gk < ge; gk += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + (uint32_t)gk), "l"(gk) : "memory");
+      }
+      // rb[r] (h = 0) / rb[r + 1] (h = 1)
+      const int rr = min(r + h, fh - 1);
+      uintptr_t gr = g;
+      if (h) {
+        bool in1;
+        const int ry1 = border_idx(fy0 + rr, Hs, reflect, in1);
+        gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+      }
+      rtab[tid] = (int)raw_a + rr * kRPitch + 16 + (int)(gr & 15);  // shared address of column fx0
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    // ---- 2. border columns / constant-fill rows
+    if (fits) {
+      const int ncl = xa - fx0, nb = ncl + (fx0 + fw - xb);
+      const bool fill_rows = !reflect && (fy0 < 0 || fy0 + fh > Hs);
+      if (nb > 0 || fill_rows) {
+        const int ncols = fill_rows ? fw : nb;  // fill rows: every column
+        for (int it = tid; it < fh * ncols; it += kRThreads) {
+          const int r = fdiv(it, t.mb), j = it - r * ncols;
+          bool rin;
+          const int ry = border_idx(fy0 + r, Hs, reflect, rin);
+          int c;
+          if (fill_rows) {
+            c = j;
+            if (rin && c >= xa - fx0 && c < xb - fx0) continue;  // in-image pixel of a kept row
+          } else {
+            c = j < ncl ? j : (xb - fx0) + (j - ncl);
+          }
+          const int rb = rtab[2 * r] - (int)raw_a;
+          bool cin;
+          const int rx = border_idx(fx0 + c, Ws, reflect, cin);
+          uint32_t v;
+          if (!rin || !cin) {
+            v = a.fill;
+          } else if (rx >= xa && rx < xb) {
+            const uint8_t* s = raw + rb + 3 * (rx - fx0);
+            v = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16);
+          } else {
+            v = fetch_rgb(simg + (size_t)ry * sd.pitch, rx);
+          }
+          uint8_t* d = raw + rb + 3 * c;
+          d[0] = (uint8_t)v;
+          d[1] = (uint8_t)(v >> 8);
+          d[2] = (uint8_t)(v >> 16);
+        }
+        __syncthreads();
+      }
+    }
+    // ---- 3. compute
+    const alb_image_desc dd = a.ddesc[img];
+    uint8_t* drow0 = a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3;
+    {
+      const ImgState* gis =
+          reinterpret_cast<const ImgState*>(reinterpret_cast<const uint8_t*>(a.geo) + (size_t)img * kGeoBytes);
+      const int m_ax = gis->m.ax, m_bx = gis->m.bx, m_ay = gis->m.ay, m_by = gis->m.by;
+      const int Wo = gis->Wo;
+      const float A0f = gis->Af[0], A3f = gis->Af[2];
+      const float2 A14 = make_float2(gis->Af[1], gis->Af[3]);
+      int xw[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) xw[j] = m_ax * min(tx0 + lane + 32 * j, Wo - 1) + m_bx;
+      const int row0 = warp * kRowsPerWarp;
+      uint8_t* dlane = drow0 + 3 * lane;
+      const int nrows = min(kRowsPerWarp, th - row0);
+      // the body for one kind of tile (staged taps or global taps)
+      auto rows = [&](auto staged) {
+        constexpr bool kStaged = decltype(staged)::value;
+        int cur_cy = -0x7fffffff;
+        float2 bxy[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        uint32_t cxo[2] = {0u, 0u}, cyo[2] = {0u, 0u};
+        int aix[2] = {0, 0}, aiy[2] = {0, 0};
+        for (int i = 0; i < nrows; ++i) {
+          const int row = row0 + i;
+          const int yw = m_ay * (ty0 + row) + m_by;
+          if ((yw >> 4) != cur_cy) {  // warp-uniform: fp64 anchors of this cell row
+            cur_cy = yw >> 4;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              {
+                const Anchor an = cell_anchor(gis->A, A0f, A3f, xw[j], cur_cy);
+                bxy[j] = make_float2(an.bx, an.by);
+                aix[j] = an.ix;
+                aiy[j] = an.iy;
+                // tap byte address = rb[row] + 3 * qxb + cxo; row entry = 8 * qyb + cyo
+                cxo[j] = 3u * (uint32_t)(an.ix - fx0) - 3u * kMagic15Bits;
+                cyo[j] = tab_a + 8u * ((uint32_t)(an.iy - fy0) - kMagic15Bits);
+              }
+            }
+          }
+          const float dyl = (float)(yw & 15);
+          uint8_t* orow = dlane + (size_t)row * dd.pitch;  // column lane; lane + 32 is 96 bytes on
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {  // both columns always (clamped): the two pixels interleave
+            const int c = lane + 32 * j;
+            const float2 l = __ffma2_rn(A14, make_float2(dyl, dyl), bxy[j]);
+            const float2 tq = fadd2_rm(l, make_float2(kMagic15, kMagic15));  // floor + 1.5*2^23
+            const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
+            const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
+            const uint32_t qxb = __float_as_uint(tq.x), qyb = __float_as_uint(tq.y);
+            uint32_t r, g, b;
+            if constexpr (kStaged) {
+              const uint32_t cb = qxb * 3u + cxo[j];
+              uint32_t ta;
+              asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(ta) : "r"(qyb), "r"(cyo[j]));
+              const uint2 rbp = lds64(ta);
+              const uint32_t a0 = rbp.x + cb, a1 = rbp.y + cb;  // shared byte addresses of the taps
+              const uint32_t b0 = a0 & ~3u, b1 = a1 & ~3u;
+              const uint32_t w00 = lds32(b0), w01 = lds32(b0 + 4), w02 = lds32(b0 + 8);
+              const uint32_t w10 = lds32(b1), w11 = lds32(b1 + 4), w12 = lds32(b1 + 8);
+              const uint32_t s0 = a0 << 3, s1 = a1 << 3;
+              bilerp3_raw(__funnelshift_r(w00, w01, s0), __funnelshift_r(w01, w02, s0),
+                          __funnelshift_r(w10, w11, s1), __funnelshift_r(w11, w12, s1), fr, r, g, b);
+            } else {  // footprint beyond the staging capacity: taps from global
+              auto tap = [&](int px_, int py_) -> uint32_t {
+                bool ri, ci;
+                const int yy = border_idx(py_, Hs, reflect, ri), xx = border_idx(px_, Ws, reflect, ci);
+                return (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
+              };
+              const int X = aix[j] + (int)(qxb - kMagic15Bits), Y = aiy[j] + (int)(qyb - kMagic15Bits);
+              bilerp3(tap(X, Y), tap(X + 1, Y), tap(X, Y + 1), tap(X + 1, Y + 1), fr, r, g, b);
+            }
+            if constexpr (kOne != kStagesNone) {
+              r &= 0xffu; g &= 0xffu; b &= 0xffu;
+              apply_stages_t<kOne>(x, sm, lane, r, g, b);
+            }
+            if (c < tw) {  // straight to global: a warp's byte stores cover 96 contiguous bytes
+              orow[96 * j] = (uint8_t)r;
+              orow[96 * j + 1] = (uint8_t)g;
+              orow[96 * j + 2] = (uint8_t)b;
+            }
+          }
+        }
+      };
+      if (fits) rows(std::true_type{});
+      else rows(std::false_type{});
+    }
+    __syncthreads();  // tile consumed: raw rows free
+  }
+}
+
 // Nearest-label mask warp beside the pipelined image kernel (cfg3 / cfg5):
 // the same fp64 cell anchors and fp32 local offsets as the image kernels, so
 // a mask pixel takes the label at its image source coordinate rounded half up
@@ -1052,12 +1351,19 @@ static void launch_affine_v(const StepArgs& a, size_t smem, cudaStream_t s) {
   k_affine<kOne, kMask, kMode><<<a.n_units, kAfThreads, smem, s>>>(a);  // one CTA per tile
 }
 
+// the raw-tap kernel serves the bilinear u8 path (ALB_AFFINE_PIPE=1 selects
+// the pipelined kernel instead, an A/B switch kept for measurements)
+static bool affine_fast(const StepArgs& a) {
+  return !(a.interp == ALB_INTERP_NEAREST || a.normalize || a.min_scale < 0.9f || a.unit_size < 14040);
+}
+
+static bool affine_rt(const StepArgs& a) { return affine_fast(a) && std::getenv("ALB_AFFINE_PIPE") == nullptr; }
+
 template <int kOne>
 static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
   // fast variant always stages: a 64x64 tile's footprint (+halo) at scale
   // >= 0.9 is at most fw, fh <= 104 and S <= fw + 31, i.e. <= 14040 words
-  const bool generic = a.interp == ALB_INTERP_NEAREST || a.normalize || a.min_scale < 0.9f ||
-                       a.unit_size < 14040;
+  const bool generic = !affine_fast(a);
   const bool mask = a.mdst != nullptr;
   if (generic) {
     if (mask) launch_affine_v<kOne, true, 1>(a, smem, s);
@@ -1074,14 +1380,24 @@ static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
     if (mask) {  // label kernel on a side stream, overlapping the image kernel (fork / join by events)
       k_affine_mask<<<a.n_units, kAfThreads, 0, side_fork(s)>>>(a);
     }
-    k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(ai);
+    if (!affine_rt(a)) {  // A/B switch: the round-2 pipelined kernel
+      k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(ai);
+    } else {
+      const size_t rsmem = (size_t)count_lut_stages(a) * kLutWords * 4 + kRSmem;
+      const int rgrid = std::max(persistent_grid((const void*)k_affine_rt<kOne>, kRThreads, rsmem, a.n_units),
+                                 (a.n_units + 15) / 16);
+      k_affine_rt<kOne><<<rgrid, kRThreads, rsmem, s>>>(ai);
+    }
     if (mask) side_join(s);
   }
 }
 
 void launch_affine(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
-  k_affine_setup<<<(a.n_img - a.img0 + 127) / 128, 128, 0, s>>>(a);  // per-image state for both kernels
+  if (affine_rt(a))  // per-image state + per-tile footprints
+    k_affine_setup_units<<<(a.n_units + 127) / 128, 128, 0, s>>>(a);
+  else  // per-image state for both kernels
+    k_affine_setup<<<(a.n_img - a.img0 + 127) / 128, 128, 0, s>>>(a);
   const size_t smem = affine_smem(a);
   const int mode = stage_mode(a);
   ALB_DISPATCH_STAGES(mode, launch_affine_t, a, smem, s)

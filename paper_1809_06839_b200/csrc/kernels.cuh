@@ -61,6 +61,7 @@ struct StepArgs {
   Tables tab;
   const alb_op* ops;
   void* geo;  // workspace scratch: per-image affine state, kGeoBytes each
+  void* tiles;  // workspace scratch: per-unit affine tile state (kTileInfoBytes each), indexed like units
   int32_t img0, n_img;  // image range [img0, n_img) of this launch (per-image kernels)
   int32_t rs_ring, rs_sw, rs_hw;  // separable resample: ring rows (0 = old kernel), staged row
                                    // stride (words), output rows per group
@@ -91,6 +92,7 @@ size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normaliz
 bool resample_q4_program_ok(int mode);
 
 constexpr int kGeoBytes = 128;
+constexpr int kTileInfoBytes = 32;
 
 // Equalize (R15): histogram + LUT.
 struct EqArgs {

@@ -431,6 +431,29 @@ __device__ __forceinline__ void bilerp3(uint32_t t00, uint32_t t10, uint32_t t01
   b = __float_as_uint(__fadd_rd(vb, 8388608.f));
 }
 
+// bilerp3 on raw tap rows: u = bytes R0 G0 B0 R1 | G1 B1 . . of the upper
+// tap row (the two pixels x0, x0 + 1), v likewise for the lower row.  The
+// same arithmetic as bilerp3, bit for bit; only the byte selections differ.
+__device__ __forceinline__ void bilerp3_raw(uint32_t u0, uint32_t u1, uint32_t v0, uint32_t v1, float2 f,
+                                            uint32_t& r, uint32_t& g, uint32_t& b) {
+  constexpr uint32_t kM = 0x4B000000u;  // 2^23
+  auto cv = [](uint32_t t, uint32_t c) { return __uint_as_float(__byte_perm(t, kM, 0x7540u | c)); };
+  const float2 P00 = make_float2(cv(u0, 0), cv(u0, 1)), P10 = make_float2(cv(u0, 3), cv(u1, 0));
+  const float2 P01 = make_float2(cv(v0, 0), cv(v0, 1)), P11 = make_float2(cv(v0, 3), cv(v1, 0));
+  const float2 B0 = make_float2(cv(u0, 2), cv(v0, 2)), B1 = make_float2(cv(u1, 1), cv(v1, 1));
+  const float2 nMh = make_float2(-8388607.5f, -8388607.5f);
+  const float2 fx2 = make_float2(f.x, f.x);
+  const float2 H0 = __ffma2_rn(fx2, __fadd2_rn(P10, make_float2(-P00.x, -P00.y)), __fadd2_rn(P00, nMh));
+  const float2 H1 = __ffma2_rn(fx2, __fadd2_rn(P11, make_float2(-P01.x, -P01.y)), __fadd2_rn(P01, nMh));
+  const float2 HB = __ffma2_rn(fx2, __fadd2_rn(B1, make_float2(-B0.x, -B0.y)), __fadd2_rn(B0, nMh));
+  const float2 V = __ffma2_rn(make_float2(f.y, f.y), __fadd2_rn(H1, make_float2(-H0.x, -H0.y)), H0);
+  const float vb = fmaf(f.y, HB.y - HB.x, HB.x);
+  const float2 R2 = fadd2_rm(V, make_float2(8388608.f, 8388608.f));
+  r = __float_as_uint(R2.x);
+  g = __float_as_uint(R2.y);
+  b = __float_as_uint(__fadd_rd(vb, 8388608.f));
+}
+
 // Copy bytes [lo, hi) of one 16-byte chunk, smem -> global, both 16-aligned:
 // naturally aligned pieces when the range touches an end of the chunk.
 __device__ __forceinline__ void copy_partial(uint8_t* d, const uint8_t* s, int lo, int hi) {
