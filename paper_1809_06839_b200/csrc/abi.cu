@@ -425,7 +425,7 @@ static alb_status launch_range(const alb_plan* P, uint64_t seed, uint64_t first_
     a.tab = tab;
     a.ops = P->d_ops;
     a.geo = ws + P->off_geo;
-    a.tiles = st.kind == SK_AFFINE ? ws + P->off_tiles + (st.units_off + st.ustart[i0]) * kTileInfoBytes : nullptr;
+    a.tiles = st.kind == SK_AFFINE ? ws + P->off_tiles + (st.units_off + st.ustart[i0]) * kAffSub * kTileInfoBytes : nullptr;
     a.img0 = i0;
     a.n_img = i1;
     a.rs_ring = st.rs_ring;
@@ -1143,7 +1143,7 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
   size_t aff_units_end = 0;  // per-unit tile state of affine steps, indexed like the unit table
   for (const auto& st : steps)
     if (st.kind == SK_AFFINE) aff_units_end = std::max(aff_units_end, st.units_off + st.units.size());
-  P->off_tiles = take(aff_units_end * kTileInfoBytes);
+  P->off_tiles = take(aff_units_end * kAffSub * kTileInfoBytes);
   for (const alb_op& o : P->ops) P->n_grid += o.kind == ALB_GRID_DISTORTION;
   P->off_grid = take(nn * P->n_grid * kGridStride * sizeof(double));  // knot displacements (R31)
   P->off_buf[0] = take(max_inter + 64);

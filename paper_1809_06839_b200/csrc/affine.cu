@@ -941,13 +941,27 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
 //      outputs), taps = 3 aligned 32-bit shared loads per tap row
 //      funnel-shifted by the tap address's byte phase (no RGB -> RGBx
 //      restage); bytes go to the pre-shifted output row buffer.
-constexpr int kRThreads = 256;
-constexpr int kRRows = 108;   // footprint rows (fh <= 104 for a 64-px tile at scale >= 0.9)
-constexpr int kRPitch = 368;  // raw row pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk) for fw <= 107
+constexpr int kRTH = ALB_RT_TH;          // output rows per CTA tile
+// measured (Rotate, cfg2 corpus): 256 threads x 1 buffer x 4 CTAs / SM 1.31 ms;
+// 512 x 2 buffers x 2 CTAs 1.47 ms; 256 x 2 buffers 1.48 ms; 64 x 32 half
+// tiles (8 CTAs / SM) 1.32 ms
+#ifndef ALB_RT_NT
+#define ALB_RT_NT 256
+#endif
+#ifndef ALB_RT_NB
+#define ALB_RT_NB 1
+#endif
+constexpr int kRThreads = ALB_RT_NT;     // threads per CTA
+constexpr int kRNB = ALB_RT_NB;          // raw-row buffers: 2 = the next tile's copies overlap the compute
+constexpr int kRWarpRows = kRTH / (kRThreads / 32);  // output rows per warp
+constexpr int kRRows = kRTH == 64 ? 108 : 88;  // footprint rows (fh <= 104 / 84 at scale >= 0.9)
+constexpr int kRPitch = kRTH == 64 ? 368 : 304;  // raw row pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk), fw <= 107 / 86
 constexpr int kRMaxW = (kRPitch - 46) / 3;
 constexpr int kROffTab = 0;                 // int2 [kRRows]: (rb[r], rb[r + 1])
 constexpr int kROffRaw = kRRows * 8 + 16;   // raw rows [kRRows][kRPitch]
-constexpr int kRSmem = kROffRaw + kRRows * kRPitch + 16;
+constexpr int kRBuf = kROffRaw + kRRows * kRPitch + 16;  // one buffer: row table + raw rows
+constexpr int kRSmem = kRNB * kRBuf;
+static_assert(kRBuf % 16 == 0, "16-byte aligned buffers");
 static_assert(kROffRaw % 16 == 0, "16-byte aligned raw rows");
 
 struct TileInfo {
@@ -983,8 +997,9 @@ __device__ __forceinline__ void tile_footprint(const ImgState& s, int tx0, int t
 // affine state (written by the image's first unit of this launch, read by
 // the label kernel too) and the tile's footprint record.
 __global__ void k_affine_setup_units(StepArgs a) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= a.n_units) return;
+  const int st = blockIdx.x * blockDim.x + threadIdx.x;
+  if (st >= a.n_units * kAffSub) return;
+  const int u = st / kAffSub, sub = st - u * kAffSub;
   const int2 unit = a.units[u];
   const int img = unit.x;
   const AfCoef cf = af_coef(a, img);
@@ -997,12 +1012,16 @@ __global__ void k_affine_setup_units(StepArgs a) {
   s.m = compose_exact(a.ops, a.tab, img, a.slot0 + 1, a.slot1, s.Wo, s.Ho);
   s.tiles_x = (s.Wo + kTileW - 1) / kTileW;
   s.pad = 0;
-  if (u == 0 || a.units[u - 1].x != img)
+  if (sub == 0 && (u == 0 || a.units[u - 1].x != img))
     *reinterpret_cast<ImgState*>(reinterpret_cast<uint8_t*>(a.geo) + (size_t)img * kGeoBytes) = s;
   TileInfo t;
-  const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH;
-  const int tw = min(kTileW, s.Wo - tx0), th = min(kTileH, s.Ho - ty0);
-  tile_footprint(s, tx0, ty0, tw, th, t.fx0, t.fy0, t.fw, t.fh);
+  const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH + sub * kRTH;
+  const int tw = min(kTileW, s.Wo - tx0), th = max(min(kRTH, s.Ho - ty0), 0);
+  if (th > 0) {
+    tile_footprint(s, tx0, ty0, tw, th, t.fx0, t.fy0, t.fw, t.fh);
+  } else {  // empty half of a short unit
+    t.fx0 = t.fy0 = t.fw = t.fh = 0;
+  }
   t.img = img;
   t.txy = tx0 | (ty0 << 16);
   t.twh = tw | (th << 16);
@@ -1011,7 +1030,7 @@ __global__ void k_affine_setup_units(StepArgs a) {
   const bool fill_rows = a.border != ALB_BORDER_REFLECT_101 && (t.fy0 < 0 || t.fy0 + t.fh > sd.height);
   const int ncols = fill_rows ? t.fw : (xa - t.fx0) + (t.fx0 + t.fw - xb);
   t.mb = magic_of((uint32_t)max(ncols, 1));
-  reinterpret_cast<TileInfo*>(a.tiles)[u] = t;
+  reinterpret_cast<TileInfo*>(a.tiles)[st] = t;
 }
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
@@ -1026,9 +1045,88 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   return v;
 }
 
+// issue the raw row copies of tile t: thread 2r + h copies chunks h, h + 2, ...
+// of footprint row r into the rows at raw_a and writes rtab[2r + h] =
+// rb[r + h] (shared address of the row's column fx0)
+__device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, int* rtab, uint32_t raw_a,
+                                         bool reflect, int tid) {
+  const int fx0 = t.fx0, fy0 = t.fy0, fw = t.fw, fh = t.fh;
+  if (!(fw <= kRMaxW && fh <= kRRows)) return;
+  const alb_image_desc sd = a.sdesc[t.img];
+  const int Ws = sd.width, Hs = sd.height;
+  const uint8_t* simg = a.src + sd.offset;
+  const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);  // in-image columns [xa, xb)
+  for (int e = tid; e < 2 * fh; e += kRThreads) {
+    const int r = e >> 1, h = e & 1;
+    bool in;
+    const int ry = border_idx(fy0 + r, Hs, reflect, in);
+    const uintptr_t g = (uintptr_t)(simg + (size_t)(in ? ry : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+    if (in && xb > xa) {  // (no in-image column: the border pass fills the whole row)
+      const uintptr_t g0 = g + 3 * (xa - fx0), ge = g0 + 3 * (xb - xa);
+      // column fx0 (address g) sits at r * kRPitch + 16 + (g & 15)
+      const uint32_t d0 = raw_a + (uint32_t)(r * kRPitch + 16) - (uint32_t)(g & ~(uintptr_t)15);
+      for (uintptr_t gk = (g0 & ~(uintptr_t)15) + 16 * h; gk < ge; gk += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + (uint32_t)gk), "l"(gk) : "memory");
+    }
+    const int rr = min(r + h, fh - 1);
+    uintptr_t gr = g;
+    if (h) {
+      bool in1;
+      const int ry1 = border_idx(fy0 + rr, Hs, reflect, in1);
+      gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+    }
+    rtab[e] = (int)raw_a + rr * kRPitch + 16 + (int)(gr & 15);
+  }
+}
+
+// border columns (x < 0 or x >= W) and constant-fill rows of a staged tile;
+// returns whether it wrote anything (block-uniform)
+__device__ __forceinline__ bool rt_border(const StepArgs& a, const TileInfo& t, const int* rtab, uint8_t* raw,
+                                          uint32_t raw_a, bool reflect, int tid) {
+  const int fx0 = t.fx0, fy0 = t.fy0, fw = t.fw, fh = t.fh;
+  if (!(fw <= kRMaxW && fh <= kRRows)) return false;
+  const alb_image_desc sd = a.sdesc[t.img];
+  const int Ws = sd.width, Hs = sd.height;
+  const uint8_t* simg = a.src + sd.offset;
+  const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);
+  const int ncl = xa - fx0, nb = ncl + (fx0 + fw - xb);
+  const bool fill_rows = !reflect && (fy0 < 0 || fy0 + fh > Hs);
+  if (nb == 0 && !fill_rows) return false;
+  const int ncols = fill_rows ? fw : nb;  // fill rows: every column
+  for (int it = tid; it < fh * ncols; it += kRThreads) {
+    const int r = fdiv(it, t.mb), j = it - r * ncols;
+    bool rin;
+    const int ry = border_idx(fy0 + r, Hs, reflect, rin);
+    int c;
+    if (fill_rows) {
+      c = j;
+      if (rin && c >= xa - fx0 && c < xb - fx0) continue;  // in-image pixel of a kept row
+    } else {
+      c = j < ncl ? j : (xb - fx0) + (j - ncl);
+    }
+    const int rb = rtab[2 * r] - (int)raw_a;
+    bool cin;
+    const int rx = border_idx(fx0 + c, Ws, reflect, cin);
+    uint32_t v;
+    if (!rin || !cin) {
+      v = a.fill;
+    } else if (rx >= xa && rx < xb) {
+      const uint8_t* s = raw + rb + 3 * (rx - fx0);
+      v = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16);
+    } else {
+      v = fetch_rgb(simg + (size_t)ry * sd.pitch, rx);
+    }
+    uint8_t* d = raw + rb + 3 * c;
+    d[0] = (uint8_t)v;
+    d[1] = (uint8_t)(v >> 8);
+    d[2] = (uint8_t)(v >> 16);
+  }
+  return true;
+}
+
 template <int kOne>
 #ifndef ALB_RT_MINB
-#define ALB_RT_MINB 4  // CTAs per SM the raw-tap kernel is compiled for (register cap)
+#define ALB_RT_MINB (1024 / kRThreads)  // CTAs per SM (64-register cap)
 #endif
 __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a) {
   extern __shared__ uint32_t sm[];
@@ -1036,182 +1134,137 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
   StageCtx x;
   init_stages(a, x);
   uint8_t* smb = reinterpret_cast<uint8_t*>(sm + x.n_lut * kLutWords);
-  int* rtab = reinterpret_cast<int*>(smb + kROffTab);
-  uint8_t* raw = smb + kROffRaw;
-  const uint32_t tab_a = smem_u32(rtab);
-  const uint32_t raw_a = smem_u32(raw);
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
   const TileInfo* tinfo = reinterpret_cast<const TileInfo*>(a.tiles);
+  auto rtab_of = [&](int buf) { return reinterpret_cast<int*>(smb + buf * kRBuf + kROffTab); };
+  auto raw_of = [&](int buf) { return smb + buf * kRBuf + kROffRaw; };
 
   int u0, u1;
   unit_range(a.n_units, u0, u1);
+  const int ubeg = u0 * kAffSub, uend = u1 * kAffSub;
   int lut_img = -1;
-  for (int u = u0; u < u1; ++u) {
+  if (kRNB == 2 && ubeg < uend) {
+    rt_stage(a, tinfo[ubeg], rtab_of(0), smem_u32(raw_of(0)), reflect, tid);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int u = ubeg; u < uend; ++u) {
+    const int cur = kRNB == 2 ? (u - ubeg) & 1 : 0;
+    int* rtab = rtab_of(cur);
+    uint8_t* raw = raw_of(cur);
+    const uint32_t tab_a = smem_u32(rtab), raw_a = smem_u32(raw);
     const TileInfo t = tinfo[u];
+    if (kRNB == 1) {
+      rt_stage(a, t, rtab, raw_a, reflect, tid);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     const int img = t.img;
     const int fx0 = t.fx0, fy0 = t.fy0, fw = t.fw, fh = t.fh;
     const int tx0 = t.txy & 0xffff, ty0 = t.txy >> 16, tw = t.twh & 0xffff, th = t.twh >> 16;
-    const alb_image_desc sd = a.sdesc[img];
-    const int Ws = sd.width, Hs = sd.height;
-    const uint8_t* simg = a.src + sd.offset;
     const bool fits = fw <= kRMaxW && fh <= kRRows;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();  // tile u's rows landed; (two buffers) every warp is done with tile u - 1
+    bool bar = rt_border(a, t, rtab, raw, raw_a, reflect, tid);
     if (kOne != kStagesNone && img != lut_img) {  // LUTs are read only in the compute phase
       load_stages(a, img, sm, x, kRThreads);
       lut_img = img;
+      bar = true;
     }
-    // ---- 1. raw row copies: thread 2r + h copies chunks h, h + 2, ... of row r
-    const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);  // in-image columns [xa, xb)
-    if (fits && tid < 2 * fh) {
-      const int r = tid >> 1, h = tid & 1;
-      bool in;
-      const int ry = border_idx(fy0 + r, Hs, reflect, in);
-      const uintptr_t g = (uintptr_t)(simg + (size_t)(in ? ry : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
-      if (in) {
-        const uintptr_t g0 = g + 3 * (xa - fx0), ge = g0 + 3 * (xb - xa);
-        // column fx0 (address g) sits at r * kRPitch + 16 + (g & 15)
-        const uint32_t d0 = raw_a + (uint32_t)(r * kRPitch + 16) - (uint32_t)(g & ~(uintptr_t)15);
-        for (uintptr_t gk = (g0 & ~(uintptr_t)15) + 16 * h; gk < ge; gk += 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + (uint32_t)gk), "l"(gk) : "memory");
-      }
-      // rb[r] (h = 0) / rb[r + 1] (h = 1)
-      const int rr = min(r + h, fh - 1);
-      uintptr_t gr = g;
-      if (h) {
-        bool in1;
-        const int ry1 = border_idx(fy0 + rr, Hs, reflect, in1);
-        gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
-      }
-      rtab[tid] = (int)raw_a + rr * kRPitch + 16 + (int)(gr & 15);  // shared address of column fx0
+    if (bar) __syncthreads();
+    if (kRNB == 2 && u + 1 < uend) {  // the next tile's copies overlap this tile's compute
+      rt_stage(a, tinfo[u + 1], rtab_of(cur ^ 1), smem_u32(raw_of(cur ^ 1)), reflect, tid);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
-    // ---- 2. border columns / constant-fill rows
-    if (fits) {
-      const int ncl = xa - fx0, nb = ncl + (fx0 + fw - xb);
-      const bool fill_rows = !reflect && (fy0 < 0 || fy0 + fh > Hs);
-      if (nb > 0 || fill_rows) {
-        const int ncols = fill_rows ? fw : nb;  // fill rows: every column
-        for (int it = tid; it < fh * ncols; it += kRThreads) {
-          const int r = fdiv(it, t.mb), j = it - r * ncols;
-          bool rin;
-          const int ry = border_idx(fy0 + r, Hs, reflect, rin);
-          int c;
-          if (fill_rows) {
-            c = j;
-            if (rin && c >= xa - fx0 && c < xb - fx0) continue;  // in-image pixel of a kept row
-          } else {
-            c = j < ncl ? j : (xb - fx0) + (j - ncl);
-          }
-          const int rb = rtab[2 * r] - (int)raw_a;
-          bool cin;
-          const int rx = border_idx(fx0 + c, Ws, reflect, cin);
-          uint32_t v;
-          if (!rin || !cin) {
-            v = a.fill;
-          } else if (rx >= xa && rx < xb) {
-            const uint8_t* s = raw + rb + 3 * (rx - fx0);
-            v = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16);
-          } else {
-            v = fetch_rgb(simg + (size_t)ry * sd.pitch, rx);
-          }
-          uint8_t* d = raw + rb + 3 * c;
-          d[0] = (uint8_t)v;
-          d[1] = (uint8_t)(v >> 8);
-          d[2] = (uint8_t)(v >> 16);
-        }
-        __syncthreads();
-      }
-    }
-    // ---- 3. compute
+    const alb_image_desc sd = a.sdesc[img];
+    const int Ws = sd.width, Hs = sd.height;
+    const uint8_t* simg = a.src + sd.offset;
+    const ImgState* gis =
+        reinterpret_cast<const ImgState*>(reinterpret_cast<const uint8_t*>(a.geo) + (size_t)img * kGeoBytes);
+    const int m_ax = gis->m.ax, m_bx = gis->m.bx, m_ay = gis->m.ay, m_by = gis->m.by;
+    const int Wo = gis->Wo;
+    const float A0f = gis->Af[0], A3f = gis->Af[2];
     const alb_image_desc dd = a.ddesc[img];
     uint8_t* drow0 = a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3;
     {
-      const ImgState* gis =
-          reinterpret_cast<const ImgState*>(reinterpret_cast<const uint8_t*>(a.geo) + (size_t)img * kGeoBytes);
-      const int m_ax = gis->m.ax, m_bx = gis->m.bx, m_ay = gis->m.ay, m_by = gis->m.by;
-      const int Wo = gis->Wo;
-      const float A0f = gis->Af[0], A3f = gis->Af[2];
       const float2 A14 = make_float2(gis->Af[1], gis->Af[3]);
       int xw[2];
 #pragma unroll
       for (int j = 0; j < 2; ++j) xw[j] = m_ax * min(tx0 + lane + 32 * j, Wo - 1) + m_bx;
-      const int row0 = warp * kRowsPerWarp;
+      const int row0 = warp * kRWarpRows;
       uint8_t* dlane = drow0 + 3 * lane;
-      const int nrows = min(kRowsPerWarp, th - row0);
+      const int nrows = min(kRWarpRows, th - row0);
       // the body for one kind of tile (staged taps or global taps)
       auto rows = [&](auto staged) {
         constexpr bool kStaged = decltype(staged)::value;
-        int cur_cy = -0x7fffffff;
-        float2 bxy[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        uint32_t cxo[2] = {0u, 0u}, cyo[2] = {0u, 0u};
-        int aix[2] = {0, 0}, aiy[2] = {0, 0};
-        for (int i = 0; i < nrows; ++i) {
-          const int row = row0 + i;
-          const int yw = m_ay * (ty0 + row) + m_by;
-          if ((yw >> 4) != cur_cy) {  // warp-uniform: fp64 anchors of this cell row
-            cur_cy = yw >> 4;
+        const bool st0 = lane < tw, st1 = lane + 32 < tw;
+        const size_t pitch = dd.pitch;
+        uint8_t* orow = dlane + (size_t)row0 * pitch;  // column lane; lane + 32 is 96 bytes on
+        int i = 0;
+        while (i < nrows) {  // segments of rows in one 16-row cell row (yw moves by m_ay = +-1)
+          const int yw0 = m_ay * (ty0 + row0 + i) + m_by;
+          const int cy = yw0 >> 4;
+          const int iend = min(nrows, i + (m_ay > 0 ? 16 - (yw0 & 15) : (yw0 & 15) + 1));
+          float2 bxy[2];
+          uint32_t cxo[2], cyo[2];
+          int aix[2], aiy[2];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              {
-                const Anchor an = cell_anchor(gis->A, A0f, A3f, xw[j], cur_cy);
-                bxy[j] = make_float2(an.bx, an.by);
-                aix[j] = an.ix;
-                aiy[j] = an.iy;
-                // tap byte address = rb[row] + 3 * qxb + cxo; row entry = 8 * qyb + cyo
-                cxo[j] = 3u * (uint32_t)(an.ix - fx0) - 3u * kMagic15Bits;
-                cyo[j] = tab_a + 8u * ((uint32_t)(an.iy - fy0) - kMagic15Bits);
-              }
-            }
+          for (int j = 0; j < 2; ++j) {  // fp64 anchors of this cell row
+            const Anchor an = cell_anchor(gis->A, A0f, A3f, xw[j], cy);
+            bxy[j] = make_float2(an.bx, an.by);
+            aix[j] = an.ix;
+            aiy[j] = an.iy;
+            // tap byte address = rb[row] + 3 * qxb + cxo; row entry = 8 * qyb + cyo
+            cxo[j] = 3u * (uint32_t)(an.ix - fx0) - 3u * kMagic15Bits;
+            cyo[j] = tab_a + 8u * ((uint32_t)(an.iy - fy0) - kMagic15Bits);
           }
-          const float dyl = (float)(yw & 15);
-          uint8_t* orow = dlane + (size_t)row * dd.pitch;  // column lane; lane + 32 is 96 bytes on
+          float dyl = (float)(yw0 & 15);
+          const float ddy = (float)m_ay;
+          for (; i < iend; ++i, dyl += ddy, orow += pitch) {
+            uint32_t rr[2], gg[2], bb[2];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {  // both columns always (clamped): the two pixels interleave
-            const int c = lane + 32 * j;
-            const float2 l = __ffma2_rn(A14, make_float2(dyl, dyl), bxy[j]);
-            const float2 tq = fadd2_rm(l, make_float2(kMagic15, kMagic15));  // floor + 1.5*2^23
-            const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
-            const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
-            const uint32_t qxb = __float_as_uint(tq.x), qyb = __float_as_uint(tq.y);
-            uint32_t r, g, b;
-            if constexpr (kStaged) {
-              const uint32_t cb = qxb * 3u + cxo[j];
-              uint32_t ta;
-              asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(ta) : "r"(qyb), "r"(cyo[j]));
-              const uint2 rbp = lds64(ta);
-              const uint32_t a0 = rbp.x + cb, a1 = rbp.y + cb;  // shared byte addresses of the taps
-              const uint32_t b0 = a0 & ~3u, b1 = a1 & ~3u;
-              const uint32_t w00 = lds32(b0), w01 = lds32(b0 + 4), w02 = lds32(b0 + 8);
-              const uint32_t w10 = lds32(b1), w11 = lds32(b1 + 4), w12 = lds32(b1 + 8);
-              const uint32_t s0 = a0 << 3, s1 = a1 << 3;
-              bilerp3_raw(__funnelshift_r(w00, w01, s0), __funnelshift_r(w01, w02, s0),
-                          __funnelshift_r(w10, w11, s1), __funnelshift_r(w11, w12, s1), fr, r, g, b);
-            } else {  // footprint beyond the staging capacity: taps from global
-              auto tap = [&](int px_, int py_) -> uint32_t {
-                bool ri, ci;
-                const int yy = border_idx(py_, Hs, reflect, ri), xx = border_idx(px_, Ws, reflect, ci);
-                return (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
-              };
-              const int X = aix[j] + (int)(qxb - kMagic15Bits), Y = aiy[j] + (int)(qyb - kMagic15Bits);
-              bilerp3(tap(X, Y), tap(X + 1, Y), tap(X, Y + 1), tap(X + 1, Y + 1), fr, r, g, b);
+            for (int j = 0; j < 2; ++j) {  // both columns always (clamped): the two pixels interleave
+              const float2 l = __ffma2_rn(A14, make_float2(dyl, dyl), bxy[j]);
+              const float2 tq = fadd2_rm(l, make_float2(kMagic15, kMagic15));  // floor + 1.5*2^23
+              const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
+              const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
+              const uint32_t qxb = __float_as_uint(tq.x), qyb = __float_as_uint(tq.y);
+              uint32_t r, g, b;
+              if constexpr (kStaged) {
+                const uint32_t cb = qxb * 3u + cxo[j];
+                uint32_t ta;
+                asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(ta) : "r"(qyb), "r"(cyo[j]));
+                const uint2 rbp = lds64(ta);
+                const uint32_t a0 = rbp.x + cb, a1 = rbp.y + cb;  // shared byte addresses of the taps
+                const uint32_t b0 = a0 & ~3u, b1 = a1 & ~3u;
+                const uint32_t w00 = lds32(b0), w01 = lds32(b0 + 4), w02 = lds32(b0 + 8);
+                const uint32_t w10 = lds32(b1), w11 = lds32(b1 + 4), w12 = lds32(b1 + 8);
+                const uint32_t s0 = a0 << 3, s1 = a1 << 3;
+                bilerp3_raw(__funnelshift_r(w00, w01, s0), __funnelshift_r(w01, w02, s0),
+                            __funnelshift_r(w10, w11, s1), __funnelshift_r(w11, w12, s1), fr, r, g, b);
+              } else {  // footprint beyond the staging capacity: taps from global
+                auto tap = [&](int px_, int py_) -> uint32_t {
+                  bool ri, ci;
+                  const int yy = border_idx(py_, Hs, reflect, ri), xx = border_idx(px_, Ws, reflect, ci);
+                  return (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
+                };
+                const int X = aix[j] + (int)(qxb - kMagic15Bits), Y = aiy[j] + (int)(qyb - kMagic15Bits);
+                bilerp3(tap(X, Y), tap(X + 1, Y), tap(X, Y + 1), tap(X + 1, Y + 1), fr, r, g, b);
+              }
+              if constexpr (kOne != kStagesNone) {
+                r &= 0xffu; g &= 0xffu; b &= 0xffu;
+                apply_stages_t<kOne>(x, sm, lane, r, g, b);
+              }
+              rr[j] = r; gg[j] = g; bb[j] = b;
             }
-            if constexpr (kOne != kStagesNone) {
-              r &= 0xffu; g &= 0xffu; b &= 0xffu;
-              apply_stages_t<kOne>(x, sm, lane, r, g, b);
-            }
-            if (c < tw) {  // straight to global: a warp's byte stores cover 96 contiguous bytes
-              orow[96 * j] = (uint8_t)r;
-              orow[96 * j + 1] = (uint8_t)g;
-              orow[96 * j + 2] = (uint8_t)b;
-            }
+            // straight to global: a warp's byte stores cover 96 contiguous bytes
+            if (st0) { orow[0] = (uint8_t)rr[0]; orow[1] = (uint8_t)gg[0]; orow[2] = (uint8_t)bb[0]; }
+            if (st1) { orow[96] = (uint8_t)rr[1]; orow[97] = (uint8_t)gg[1]; orow[98] = (uint8_t)bb[1]; }
           }
         }
       };
       if (fits) rows(std::true_type{});
       else rows(std::false_type{});
     }
-    __syncthreads();  // tile consumed: raw rows free
+    if (kRNB == 1) __syncthreads();  // tile consumed: raw rows free
   }
 }
 
@@ -1395,7 +1448,7 @@ static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
 void launch_affine(const StepArgs& a, cudaStream_t s) {
   if (a.n_units <= 0) return;
   if (affine_rt(a))  // per-image state + per-tile footprints
-    k_affine_setup_units<<<(a.n_units + 127) / 128, 128, 0, s>>>(a);
+    k_affine_setup_units<<<(a.n_units * kAffSub + 127) / 128, 128, 0, s>>>(a);
   else  // per-image state for both kernels
     k_affine_setup<<<(a.n_img - a.img0 + 127) / 128, 128, 0, s>>>(a);
   const size_t smem = affine_smem(a);

@@ -93,6 +93,12 @@ bool resample_q4_program_ok(int mode);
 
 constexpr int kGeoBytes = 128;
 constexpr int kTileInfoBytes = 32;
+// raw-tap affine kernel: output rows per CTA tile (64 = the whole 64x64 unit,
+// 32 = the unit as two 64x32 halves, each its own TileInfo record)
+#ifndef ALB_RT_TH
+#define ALB_RT_TH 64
+#endif
+constexpr int kAffSub = 64 / ALB_RT_TH;  // TileInfo records per affine unit
 
 // Equalize (R15): histogram + LUT.
 struct EqArgs {

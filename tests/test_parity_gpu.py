@@ -809,3 +809,49 @@ def test_lone_gated_pointwise_ops_self_sample(spec):
         cmp_exact(g, r)
     same = sum(np.array_equal(gi, b.image(i)) for i, gi in enumerate(g))
     assert 0 < same < len(sizes)  # both gate outcomes occur in the batch
+
+
+# ------------------------------------------- raw-tap affine kernel (k_affine_rt)
+
+AFFINE_FAR = [((1200, 180), 45.0, "reflect_101"), ((180, 1200), 80.0, "reflect_101"),
+              ((1500, 140), 33.0, "constant"), ((97, 1301), -61.0, "constant")]
+
+
+@pytest.mark.parametrize("case", range(len(AFFINE_FAR)))
+def test_affine_far_outside_footprints(case):
+    """Long thin images rotated so that many tiles' source footprints lie
+    wholly left / right of / above / below the image (no in-image column or
+    row to copy: every staged pixel comes from the border pass), vs the oracle."""
+    (h, w), ang, border = AFFINE_FAR[case]
+    specs = [{"kind": "Rotate", "lo": [ang], "hi": [ang], "interp": "bilinear", "border": border}]
+    b = gen.gen_images([(h, w), (w, h)], seed=31 + case, device="cuda")
+    g = run_gpu(specs, b, seed=2, first=0)["images"]
+    r = [o["image"] for o in run_oracle(specs, [b.image(i) for i in range(2)], seed=2, first=0)]
+    cmp_interp(g, r)
+
+
+@pytest.mark.parametrize("name", ["Rotate", "ShiftScaleRotate", "SSR+flips+BC", "SSR+crop", "SSR+HSV",
+                                  "Rotate-constant"])
+def test_affine_rt_equals_pipelined_kernel(name, monkeypatch):
+    """The raw-tap kernel and the round-2 pipelined kernel (ALB_AFFINE_PIPE=1)
+    share the coordinate and blend arithmetic: their outputs are equal byte
+    for byte on a cfg2-like ragged batch, fused post ops and stages included."""
+    ssr = C.CFG2_MENU["ShiftScaleRotate"]
+    specs = {"Rotate": C.CFG2_MENU["Rotate"], "ShiftScaleRotate": ssr,
+             "SSR+flips+BC": ssr + [C.op("VerticalFlip"), C.op("HorizontalFlip", p=0.5),
+                                    C.op("BrightnessContrast", lo=[0.8, 0.8], hi=[1.2, 1.2])],
+             "SSR+crop": ssr + [C.op("RandomCrop", size=(200, 200))],
+             "SSR+HSV": ssr + [C.op("ShiftHSV", lo=[-20.0, -0.1, -0.1], hi=[20.0, 0.1, 0.1])],
+             "Rotate-constant": [C.op("Rotate", lo=[-90.0], hi=[90.0], interp="bilinear",
+                                      border="constant")]}[name]
+    b = gen.gen_images(gen.cfg2_sizes(120), seed=8, device="cuda")
+    outs = []
+    for pipe in (False, True):
+        if pipe:
+            monkeypatch.setenv("ALB_AFFINE_PIPE", "1")
+        else:
+            monkeypatch.delenv("ALB_AFFINE_PIPE", raising=False)
+        outs.append(run_gpu(specs, b, seed=4, first=0)["images"])
+    monkeypatch.delenv("ALB_AFFINE_PIPE", raising=False)
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
