@@ -1162,10 +1162,11 @@ alb_status alb_plan_create(const alb_pipeline* p, const alb_layout* in, const al
       const bool fused = si + 1 < steps.size() && steps[si + 1].kind == SK_POINT && steps[si + 1].stages.size() == 1 &&
                          !steps[si + 1].normalize && steps[si + 1].flat;
       L += fused ? 0 : 2;  // the LUT pass (the next step) is the single-pass kernel when fused
-    } else if (st.kind == SK_AFFINE) {  // setup + image kernel (+ label kernel beside the pipelined one)
+    } else if (st.kind == SK_AFFINE) {  // setup + image kernel (the raw-tap kernel gathers the labels too;
+                                         // the pipelined one, ALB_AFFINE_PIPE=1, has a label kernel beside it)
       const bool generic = st.interp == ALB_INTERP_NEAREST || st.normalize || st.min_scale < 0.9f ||
                            st.unit_size < 14040;
-      L += 2 + (st.has_mask && !generic ? 1 : 0);
+      L += 2 + (st.has_mask && !generic && std::getenv("ALB_AFFINE_PIPE") != nullptr ? 1 : 0);
     } else {
       L += 1;
     }

@@ -1124,11 +1124,14 @@ __device__ __forceinline__ bool rt_border(const StepArgs& a, const TileInfo& t, 
   return true;
 }
 
-template <int kOne>
+template <int kOne, bool kMask>
 #ifndef ALB_RT_MINB
 #define ALB_RT_MINB (1024 / kRThreads)  // CTAs per SM (64-register cap)
 #endif
 __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a) {
+  // kMask: the nearest label of every output pixel too (cfg3 / cfg5), from the
+  // pixel's own coordinates -- the decision k_affine_mask makes -- gathered
+  // straight from the source mask (L1-resident neighbourhood)
   extern __shared__ uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   StageCtx x;
@@ -1193,6 +1196,23 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
       uint8_t* dlane = drow0 + 3 * lane;
       const int nrows = min(kRWarpRows, th - row0);
       // the body for one kind of tile (staged taps or global taps)
+      // label gathers: the tile's nearest taps all inside the mask (footprint
+      // test) -> no border resolution
+      const uint8_t* msrc = nullptr;
+      uint8_t* morow = nullptr;
+      int mpitch = 0, Wm = 0, Hm = 0;
+      size_t mdpitch = 0;
+      bool minner = false;
+      if constexpr (kMask) {
+        const alb_image_desc msd = a.msdesc[img], mdd = a.mddesc[img];
+        msrc = a.msrc + msd.offset;
+        mpitch = msd.pitch;
+        Wm = msd.width;
+        Hm = msd.height;
+        mdpitch = mdd.pitch;
+        morow = a.mdst + mdd.offset + (size_t)(ty0 + row0) * mdpitch + tx0 + lane;
+        minner = fx0 >= 0 && fy0 >= 0 && fx0 + fw <= Wm && fy0 + fh <= Hm;
+      }
       auto rows = [&](auto staged) {
         constexpr bool kStaged = decltype(staged)::value;
         const bool st0 = lane < tw, st1 = lane + 32 < tw;
@@ -1220,6 +1240,7 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
           const float ddy = (float)m_ay;
           for (; i < iend; ++i, dyl += ddy, orow += pitch) {
             uint32_t rr[2], gg[2], bb[2];
+            uint8_t mv[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {  // both columns always (clamped): the two pixels interleave
               const float2 l = __ffma2_rn(A14, make_float2(dyl, dyl), bxy[j]);
@@ -1227,6 +1248,17 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
               const float2 fl = __fadd2_rn(tq, make_float2(-kMagic15, -kMagic15));
               const float2 fr = __fadd2_rn(l, make_float2(-fl.x, -fl.y));
               const uint32_t qxb = __float_as_uint(tq.x), qyb = __float_as_uint(tq.y);
+              if constexpr (kMask) {  // nearest: round half up
+                const int nx = aix[j] + (int)(qxb - kMagic15Bits) + (fr.x >= 0.5f ? 1 : 0);
+                const int ny = aiy[j] + (int)(qyb - kMagic15Bits) + (fr.y >= 0.5f ? 1 : 0);
+                if (minner) {
+                  mv[j] = __ldg(msrc + ny * mpitch + nx);
+                } else {
+                  bool ri, ci;
+                  const int yy = border_idx(ny, Hm, reflect, ri), xx = border_idx(nx, Wm, reflect, ci);
+                  mv[j] = (ri && ci) ? __ldg(msrc + yy * mpitch + xx) : (uint8_t)a.mask_fill;
+                }
+              }
               uint32_t r, g, b;
               if constexpr (kStaged) {
                 const uint32_t cb = qxb * 3u + cxo[j];
@@ -1258,6 +1290,11 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
             // straight to global: a warp's byte stores cover 96 contiguous bytes
             if (st0) { orow[0] = (uint8_t)rr[0]; orow[1] = (uint8_t)gg[0]; orow[2] = (uint8_t)bb[0]; }
             if (st1) { orow[96] = (uint8_t)rr[1]; orow[97] = (uint8_t)gg[1]; orow[98] = (uint8_t)bb[1]; }
+            if constexpr (kMask) {
+              if (st0) morow[0] = mv[0];
+              if (st1) morow[32] = mv[1];
+              morow += mdpitch;
+            }
           }
         }
       };
@@ -1430,18 +1467,21 @@ static void launch_affine_t(const StepArgs& a, size_t smem, cudaStream_t s) {
     // hardware re-balances CTAs across SMs (measured: 16 > 8, 32 > persistent)
     const int grid = std::max(persistent_grid((const void*)k_affine_pipe<kOne>, kPThreads, psmem, a.n_units),
                               (a.n_units + 15) / 16);
-    if (mask) {  // label kernel on a side stream, overlapping the image kernel (fork / join by events)
-      k_affine_mask<<<a.n_units, kAfThreads, 0, side_fork(s)>>>(a);
-    }
-    if (!affine_rt(a)) {  // A/B switch: the round-2 pipelined kernel
+    if (!affine_rt(a)) {  // A/B switch: the round-2 pipelined kernel; labels beside it
+      if (mask) k_affine_mask<<<a.n_units, kAfThreads, 0, side_fork(s)>>>(a);  // side stream (fork / join)
       k_affine_pipe<kOne><<<grid, kPThreads, psmem, s>>>(ai);
+      if (mask) side_join(s);
     } else {
       const size_t rsmem = (size_t)count_lut_stages(a) * kLutWords * 4 + kRSmem;
-      const int rgrid = std::max(persistent_grid((const void*)k_affine_rt<kOne>, kRThreads, rsmem, a.n_units),
-                                 (a.n_units + 15) / 16);
-      k_affine_rt<kOne><<<rgrid, kRThreads, rsmem, s>>>(ai);
+#ifndef ALB_RT_TPC
+#define ALB_RT_TPC 8  // units per CTA (0: one persistent wave, units split evenly; measured 8 < 16 < 32 < 0)
+#endif
+      const void* fn = mask ? (const void*)k_affine_rt<kOne, true> : (const void*)k_affine_rt<kOne, false>;
+      const int pg = persistent_grid(fn, kRThreads, rsmem, a.n_units);
+      const int rgrid = ALB_RT_TPC > 0 ? std::max(pg, (a.n_units + ALB_RT_TPC - 1) / ALB_RT_TPC) : pg;
+      if (mask) k_affine_rt<kOne, true><<<rgrid, kRThreads, rsmem, s>>>(a);  // image + labels in one kernel
+      else k_affine_rt<kOne, false><<<rgrid, kRThreads, rsmem, s>>>(ai);
     }
-    if (mask) side_join(s);
   }
 }
 

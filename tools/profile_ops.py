@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--ops", default="Rotate,Resize512,ShiftHSV,Grayscale")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--n", type=int, default=2000)
+ap.add_argument("--time", type=int, default=0, help="also time this many applies (CUDA events) after the reps")
 a = ap.parse_args()
 
 
@@ -47,10 +48,21 @@ def run(specs, sizes, masks=False, boxes=False):
     ws = plan.workspace()
     bo = [torch.empty_like(t) for t in bx] if bx else [None] * 3
     bi = bx or [None] * 3
-    for r in range(a.reps):
+    def apply(r):
         plan.apply(r, 0, b.buf, None if ob is None else ob.buf, nchw, None if mi is None else mi.buf,
                    None if mo is None else mo.buf, bi[0], bi[1], bi[2], bo[0], bo[1], bo[2], workspace=ws)
+    for r in range(a.reps):
+        apply(r)
     torch.cuda.synchronize()
+    if a.time:
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        for r in range(a.time):
+            apply(r)
+        e1.record()
+        torch.cuda.synchronize()
+        print("time %s %d images: %.3f ms per apply" % (specs[0]["kind"] if len(specs) == 1 else "compose", n,
+                                                         e0.elapsed_time(e1) / a.time))
 
 
 for name in a.ops.split(","):
