@@ -1124,6 +1124,11 @@ __device__ __forceinline__ bool rt_border(const StepArgs& a, const TileInfo& t, 
   return true;
 }
 
+#ifndef ALB_RT_ROWUNROLL
+#define ALB_RT_ROWUNROLL 1
+#endif
+constexpr int kRowUnroll = ALB_RT_ROWUNROLL;  // rows per unrolled step of the raw-tap kernel's row loop
+
 template <int kOne, bool kMask>
 #ifndef ALB_RT_MINB
 #define ALB_RT_MINB (1024 / kRThreads)  // CTAs per SM (64-register cap)
@@ -1238,6 +1243,7 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
           }
           float dyl = (float)(yw0 & 15);
           const float ddy = (float)m_ay;
+#pragma unroll kRowUnroll
           for (; i < iend; ++i, dyl += ddy, orow += pitch) {
             uint32_t rr[2], gg[2], bb[2];
             uint8_t mv[2];
