@@ -957,8 +957,9 @@ constexpr int kRWarpRows = kRTH / (kRThreads / 32);  // output rows per warp
 constexpr int kRRows = kRTH == 64 ? 108 : 88;  // footprint rows (fh <= 104 / 84 at scale >= 0.9)
 constexpr int kRPitch = kRTH == 64 ? 368 : 304;  // raw row pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk), fw <= 107 / 86
 constexpr int kRMaxW = (kRPitch - 46) / 3;
-constexpr int kROffTab = 0;                 // int2 [kRRows]: (rb[r], rb[r + 1])
-constexpr int kROffRaw = kRRows * 8 + 16;   // raw rows [kRRows][kRPitch]
+constexpr int kROffTab = 0;                  // int2 [kRRows]: (rb[r], rb[r + 1])
+constexpr int kROffSpan = kRRows * 8;        // int [kRRows]: staged columns s0 | s1 << 16 of row r
+constexpr int kROffRaw = (kRRows * 12 + 31) / 16 * 16;  // raw rows [kRRows][kRPitch]
 constexpr int kRBuf = kROffRaw + kRRows * kRPitch + 16;  // one buffer: row table + raw rows
 constexpr int kRSmem = kRNB * kRBuf;
 static_assert(kRBuf % 16 == 0, "16-byte aligned buffers");
@@ -968,17 +969,19 @@ struct TileInfo {
   int fx0, fy0, fw, fh;  // source footprint (bilinear halo + 1 px rounding margin)
   int img, txy, twh;     // image; tile origin tx0 | ty0 << 16; extent tw | th << 16
   uint32_t mb;           // magic of the border pass's per-row item count
+  float vx[4], vy[4];    // the tile's corners in source space, relative to (fx0, fy0), parallelogram order
 };
 static_assert(sizeof(TileInfo) == kTileInfoBytes, "TileInfo is the per-unit scratch record");
 
 // footprint of the output tile [tx0, tx0 + tw) x [ty0, ty0 + th) (warp-output
 // coordinates through the fused post map), the bound every affine kernel uses
 __device__ __forceinline__ void tile_footprint(const ImgState& s, int tx0, int ty0, int tw, int th, int& fx0,
-                                               int& fy0, int& fw, int& fh) {
+                                               int& fy0, int& fw, int& fh, float* vx = nullptr,
+                                               float* vy = nullptr) {
   const Map1& m = s.m;
   const int xwa = m.ax * tx0 + m.bx, xwb = m.ax * (tx0 + tw - 1) + m.bx;
   const int ywa = m.ay * ty0 + m.by, ywb = m.ay * (ty0 + th - 1) + m.by;
-  double lx = 1e300, hx = -1e300, ly = 1e300, hy = -1e300;
+  double lx = 1e300, hx = -1e300, ly = 1e300, hy = -1e300, cx[4], cy[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const double xw = (c & 1) ? max(xwa, xwb) : min(xwa, xwb);
@@ -986,11 +989,57 @@ __device__ __forceinline__ void tile_footprint(const ImgState& s, int tx0, int t
     const double sx = fma(s.A[0], xw, fma(s.A[1], yw, s.A[2]));
     const double sy = fma(s.A[3], xw, fma(s.A[4], yw, s.A[5]));
     lx = fmin(lx, sx); hx = fmax(hx, sx); ly = fmin(ly, sy); hy = fmax(hy, sy);
+    cx[c] = sx;
+    cy[c] = sy;
   }
   fx0 = (int)floor(lx) - 1;
   fy0 = (int)floor(ly) - 1;
   fw = (int)floor(hx) + 2 - fx0 + 1;
   fh = (int)floor(hy) + 2 - fy0 + 1;
+  if (vx != nullptr) {  // corners in parallelogram order (0, 1, 3, 2), relative to the footprint origin
+    const int ord[4] = {0, 1, 3, 2};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      vx[e] = (float)(cx[ord[e]] - fx0);
+      vy[e] = (float)(cy[ord[e]] - fy0);
+    }
+  }
+}
+
+// Columns [s0, s1) (relative to fx0) of footprint row r that the tile's
+// bilinear taps can touch: the parallelogram of the tile's source points cut
+// by the strip y in [r - 1, r + 1] (a source row is tapped by points within
+// one row of it), widened by the right tap and a rounding margin -- the same
+// fp32 construction as the pipelined kernel's per-row spans.
+__device__ __forceinline__ void row_span(const TileInfo& t, int r, int& s0, int& s1) {
+  const float ya = (float)r - 1.01f, yb = (float)r + 1.01f;
+  float xmn = 1e30f, xmx = -1e30f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int e1 = (e + 1) & 3;
+    const float ex = t.vx[e], ey = t.vy[e];
+    const float edx = t.vx[e1] - ex, dy = t.vy[e1] - ey;
+    if (ey >= ya && ey <= yb) { xmn = fminf(xmn, ex); xmx = fmaxf(xmx, ex); }
+    if (dy != 0.f) {
+      const float eiy = 1.f / dy;
+#pragma unroll
+      for (int bnd = 0; bnd < 2; ++bnd) {
+        const float tt = ((bnd ? yb : ya) - ey) * eiy;
+        if (tt >= -1e-4f && tt <= 1.0001f) {
+          const float xx = fmaf(tt, edx, ex);
+          xmn = fminf(xmn, xx);
+          xmx = fmaxf(xmx, xx);
+        }
+      }
+    }
+  }
+  s0 = 0;
+  s1 = 0;
+  if (xmx >= xmn) {
+    s0 = max((int)floorf(xmn) - 1, 0);
+    s1 = min((int)floorf(xmx) + 3, t.fw);
+    if (s1 < s0) s1 = s0;
+  }
 }
 
 // Per-unit setup of the raw-tap kernel (one thread per unit): the image's
@@ -1018,9 +1067,10 @@ __global__ void k_affine_setup_units(StepArgs a) {
   const int tx0 = (unit.y & 0xffff) * kTileW, ty0 = (unit.y >> 16) * kTileH + sub * kRTH;
   const int tw = min(kTileW, s.Wo - tx0), th = max(min(kRTH, s.Ho - ty0), 0);
   if (th > 0) {
-    tile_footprint(s, tx0, ty0, tw, th, t.fx0, t.fy0, t.fw, t.fh);
+    tile_footprint(s, tx0, ty0, tw, th, t.fx0, t.fy0, t.fw, t.fh, t.vx, t.vy);
   } else {  // empty half of a short unit
     t.fx0 = t.fy0 = t.fw = t.fh = 0;
+    for (int e = 0; e < 4; ++e) t.vx[e] = t.vy[e] = 0.f;
   }
   t.img = img;
   t.txy = tx0 | (ty0 << 16);
@@ -1056,13 +1106,18 @@ __device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, i
   const int Ws = sd.width, Hs = sd.height;
   const uint8_t* simg = a.src + sd.offset;
   const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);  // in-image columns [xa, xb)
+  int* spans = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(rtab) + kROffSpan);
   for (int e = tid; e < 2 * fh; e += kRThreads) {
     const int r = e >> 1, h = e & 1;
+    int s0, s1;
+    row_span(t, r, s0, s1);  // only the columns the rotated tile's taps reach
+    if (h == 0) spans[r] = s0 | (s1 << 16);
+    const int ca = max(xa, fx0 + s0), cb = min(xb, fx0 + s1);
     bool in;
     const int ry = border_idx(fy0 + r, Hs, reflect, in);
     const uintptr_t g = (uintptr_t)(simg + (size_t)(in ? ry : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
-    if (in && xb > xa) {  // (no in-image column: the border pass fills the whole row)
-      const uintptr_t g0 = g + 3 * (xa - fx0), ge = g0 + 3 * (xb - xa);
+    if (in && cb > ca) {  // (no in-image column: the border pass fills the row)
+      const uintptr_t g0 = g + 3 * (ca - fx0), ge = g0 + 3 * (cb - ca);
       // column fx0 (address g) sits at r * kRPitch + 16 + (g & 15)
       const uint32_t d0 = raw_a + (uint32_t)(r * kRPitch + 16) - (uint32_t)(g & ~(uintptr_t)15);
       for (uintptr_t gk = (g0 & ~(uintptr_t)15) + 16 * h; gk < ge; gk += 32)
@@ -1093,8 +1148,10 @@ __device__ __forceinline__ bool rt_border(const StepArgs& a, const TileInfo& t, 
   const bool fill_rows = !reflect && (fy0 < 0 || fy0 + fh > Hs);
   if (nb == 0 && !fill_rows) return false;
   const int ncols = fill_rows ? fw : nb;  // fill rows: every column
+  const int* spans = reinterpret_cast<const int*>(reinterpret_cast<const uint8_t*>(rtab) + kROffSpan);
   for (int it = tid; it < fh * ncols; it += kRThreads) {
     const int r = fdiv(it, t.mb), j = it - r * ncols;
+    const int sp = spans[r], s0 = sp & 0xffff, s1 = sp >> 16;
     bool rin;
     const int ry = border_idx(fy0 + r, Hs, reflect, rin);
     int c;
@@ -1104,13 +1161,14 @@ __device__ __forceinline__ bool rt_border(const StepArgs& a, const TileInfo& t, 
     } else {
       c = j < ncl ? j : (xb - fx0) + (j - ncl);
     }
+    if (c < s0 || c >= s1) continue;  // no tap of the tile reads it
     const int rb = rtab[2 * r] - (int)raw_a;
     bool cin;
     const int rx = border_idx(fx0 + c, Ws, reflect, cin);
     uint32_t v;
     if (!rin || !cin) {
       v = a.fill;
-    } else if (rx >= xa && rx < xb) {
+    } else if (rx >= max(xa, fx0 + s0) && rx < min(xb, fx0 + s1)) {  // staged in this row
       const uint8_t* s = raw + rb + 3 * (rx - fx0);
       v = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16);
     } else {
