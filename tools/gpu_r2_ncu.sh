@@ -17,6 +17,10 @@ for r in full_cfg2 full_comp full_next; do
 done
 python tools/ncu_lines.py /tmp/full_cfg2.ncu-rep k_affine_rt 40 > gpurun_out/${TAG}_lines_affine.txt 2>&1
 python tools/ncu_lines.py /tmp/full_cfg2.ncu-rep k_resample_q4 40 > gpurun_out/${TAG}_lines_q4.txt 2>&1
-python tools/ncu_lines.py /tmp/full_comp.ncu-rep k_resample_sep 40 > gpurun_out/${TAG}_lines_cfg4.txt 2>&1
+python tools/ncu_lines.py /tmp/full_comp.ncu-rep k_resample 40 > gpurun_out/${TAG}_lines_cfg4.txt 2>&1
+python tools/ncu_lines.py /tmp/full_cfg2.ncu-rep k_eq_fused 40 > gpurun_out/${TAG}_lines_eq.txt 2>&1
+python tools/ncu_kstats.py /tmp/full_cfg2.ncu-rep k_affine_rt 288e6 > gpurun_out/${TAG}_kstats_affine.txt 2>&1
+python tools/ncu_kstats.py /tmp/full_cfg2.ncu-rep k_resample_q4 > gpurun_out/${TAG}_kstats_q4.txt 2>&1
+python tools/ncu_kstats.py /tmp/full_comp.ncu-rep k_affine_rt > gpurun_out/${TAG}_kstats_affine_cfg3.txt 2>&1
 ls -la gpurun_out/
 du -sh gpurun_out/
