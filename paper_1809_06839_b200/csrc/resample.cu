@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(256 / kCols, 3 * kCols) k_resample_sep(StepArg
 //     fp32 pipe); a new window row costs 3 loads + 2 funnel shifts + 6 byte
 //     permutes + 3 paired FP ops per column.
 #ifndef ALB_Q4_MINB
-#define ALB_Q4_MINB 3  // CTAs per SM the register budget is sized for (measured: 3 x 72 KB)
+#define ALB_Q4_MINB 4  // CTAs per SM the register budget is sized for (128 registers, no spills; cfg4 0.325 -> 0.295 ms vs 3)
 #endif
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
