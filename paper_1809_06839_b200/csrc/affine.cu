@@ -942,17 +942,14 @@ __global__ void __launch_bounds__(kPThreads, 2) k_affine_pipe(StepArgs a) {
 //      funnel-shifted by the tap address's byte phase (no RGB -> RGBx
 //      restage); bytes go to the pre-shifted output row buffer.
 constexpr int kRTH = ALB_RT_TH;          // output rows per CTA tile
-// measured (Rotate, cfg2 corpus): 256 threads x 1 buffer x 4 CTAs / SM 1.31 ms;
-// 512 x 2 buffers x 2 CTAs 1.47 ms; 256 x 2 buffers 1.48 ms; 64 x 32 half
-// tiles (8 CTAs / SM) 1.32 ms
+// measured (Rotate, cfg2 corpus): 256 threads x 1 raw buffer x 4 CTAs / SM
+// 1.31 ms; two raw buffers (the next tile's copies overlapping this tile's
+// compute) 512 x 2 CTAs 1.47 ms, 256 x 2 CTAs 1.48 ms; 64 x 32 half tiles
+// (8 CTAs / SM) 1.32 ms
 #ifndef ALB_RT_NT
 #define ALB_RT_NT 256
 #endif
-#ifndef ALB_RT_NB
-#define ALB_RT_NB 1
-#endif
 constexpr int kRThreads = ALB_RT_NT;     // threads per CTA
-constexpr int kRNB = ALB_RT_NB;          // raw-row buffers: 2 = the next tile's copies overlap the compute
 constexpr int kRWarpRows = kRTH / (kRThreads / 32);  // output rows per warp
 constexpr int kRRows = kRTH == 64 ? 108 : 88;  // footprint rows (fh <= 104 / 84 at scale >= 0.9)
 constexpr int kRPitch = kRTH == 64 ? 368 : 304;  // raw row pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk), fw <= 107 / 86
@@ -961,15 +958,27 @@ constexpr int kROffTab = 0;                  // int2 [kRRows]: (rb[r], rb[r + 1]
 constexpr int kROffSpan = kRRows * 8;        // int [kRRows]: staged columns s0 | s1 << 16 of row r
 constexpr int kROffRaw = (kRRows * 12 + 31) / 16 * 16;  // raw rows [kRRows][kRPitch]
 constexpr int kRBuf = kROffRaw + kRRows * kRPitch + 16;  // one buffer: row table + raw rows
-constexpr int kRSmem = kRNB * kRBuf;
+constexpr int kRSmem = kRBuf + 2 * kTileInfoBytes;  // raw rows + two tile records (current, next)
 static_assert(kRBuf % 16 == 0, "16-byte aligned buffers");
 static_assert(kROffRaw % 16 == 0, "16-byte aligned raw rows");
 
+// Everything the raw-tap kernel reads for one tile, in one record, so a CTA
+// prefetches the next tile's record into shared memory with cp.async while it
+// computes the current tile (no dependent global-load chain at a tile start).
 struct TileInfo {
   int fx0, fy0, fw, fh;  // source footprint (bilinear halo + 1 px rounding margin)
   int img, txy, twh;     // image; tile origin tx0 | ty0 << 16; extent tw | th << 16
   uint32_t mb;           // magic of the border pass's per-row item count
   float vx[4], vy[4];    // the tile's corners in source space, relative to (fx0, fy0), parallelogram order
+  double A[6];           // the image's inverse map (ImgState.A)
+  float Af[4];           // A0, A1, A3, A4 in fp32
+  int m_ax, m_bx, m_ay, m_by;  // fused post map (output -> warp-output coordinates)
+  int Wo, Ho, Ws, Hs;          // output / source dims
+  long long soff, doff;        // image offsets in the source / destination buffers
+  int spitch, dpitch, Wm, Hm;  // pitches; source mask dims
+  long long msoff, mdoff;      // mask offsets
+  int mspitch, mdpitch, pad0, pad1;
+  int pad[8];
 };
 static_assert(sizeof(TileInfo) == kTileInfoBytes, "TileInfo is the per-unit scratch record");
 
@@ -1075,7 +1084,22 @@ __global__ void k_affine_setup_units(StepArgs a) {
   t.img = img;
   t.txy = tx0 | (ty0 << 16);
   t.twh = tw | (th << 16);
-  const alb_image_desc sd = a.sdesc[img];
+  const alb_image_desc sd = a.sdesc[img], dd = a.ddesc[img];
+  for (int k = 0; k < 6; ++k) t.A[k] = s.A[k];
+  for (int k = 0; k < 4; ++k) t.Af[k] = s.Af[k];
+  t.m_ax = s.m.ax; t.m_bx = s.m.bx; t.m_ay = s.m.ay; t.m_by = s.m.by;
+  t.Wo = s.Wo; t.Ho = s.Ho; t.Ws = sd.width; t.Hs = sd.height;
+  t.soff = (long long)sd.offset; t.doff = (long long)dd.offset;
+  t.spitch = sd.pitch; t.dpitch = dd.pitch;
+  if (a.msdesc != nullptr && a.mddesc != nullptr) {
+    const alb_image_desc msd = a.msdesc[img], mdd = a.mddesc[img];
+    t.Wm = msd.width; t.Hm = msd.height; t.msoff = (long long)msd.offset; t.mdoff = (long long)mdd.offset;
+    t.mspitch = msd.pitch; t.mdpitch = mdd.pitch;
+  } else {
+    t.Wm = t.Hm = 0; t.msoff = t.mdoff = 0; t.mspitch = t.mdpitch = 0;
+  }
+  t.pad0 = t.pad1 = 0;
+  for (int k = 0; k < 8; ++k) t.pad[k] = 0;
   const int xa = min(max(t.fx0, 0), sd.width), xb = max(min(t.fx0 + t.fw, sd.width), xa);
   const bool fill_rows = a.border != ALB_BORDER_REFLECT_101 && (t.fy0 < 0 || t.fy0 + t.fh > sd.height);
   const int ncols = fill_rows ? t.fw : (xa - t.fx0) + (t.fx0 + t.fw - xb);
@@ -1102,9 +1126,9 @@ __device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, i
                                          bool reflect, int tid) {
   const int fx0 = t.fx0, fy0 = t.fy0, fw = t.fw, fh = t.fh;
   if (!(fw <= kRMaxW && fh <= kRRows)) return;
-  const alb_image_desc sd = a.sdesc[t.img];
-  const int Ws = sd.width, Hs = sd.height;
-  const uint8_t* simg = a.src + sd.offset;
+  const int Ws = t.Ws, Hs = t.Hs;
+  const uint8_t* simg = a.src + t.soff;
+  const size_t spitch = (size_t)t.spitch;
   const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);  // in-image columns [xa, xb)
   int* spans = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(rtab) + kROffSpan);
   for (int e = tid; e < 2 * fh; e += kRThreads) {
@@ -1115,7 +1139,7 @@ __device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, i
     const int ca = max(xa, fx0 + s0), cb = min(xb, fx0 + s1);
     bool in;
     const int ry = border_idx(fy0 + r, Hs, reflect, in);
-    const uintptr_t g = (uintptr_t)(simg + (size_t)(in ? ry : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+    const uintptr_t g = (uintptr_t)(simg + (size_t)(in ? ry : 0) * spitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
     if (in && cb > ca) {  // (no in-image column: the border pass fills the row)
       const uintptr_t g0 = g + 3 * (ca - fx0), ge = g0 + 3 * (cb - ca);
       // column fx0 (address g) sits at r * kRPitch + 16 + (g & 15)
@@ -1128,7 +1152,7 @@ __device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, i
     if (h) {
       bool in1;
       const int ry1 = border_idx(fy0 + rr, Hs, reflect, in1);
-      gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+      gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * spitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
     }
     rtab[e] = (int)raw_a + rr * kRPitch + 16 + (int)(gr & 15);
   }
@@ -1140,9 +1164,9 @@ __device__ __forceinline__ bool rt_border(const StepArgs& a, const TileInfo& t, 
                                           uint32_t raw_a, bool reflect, int tid) {
   const int fx0 = t.fx0, fy0 = t.fy0, fw = t.fw, fh = t.fh;
   if (!(fw <= kRMaxW && fh <= kRRows)) return false;
-  const alb_image_desc sd = a.sdesc[t.img];
-  const int Ws = sd.width, Hs = sd.height;
-  const uint8_t* simg = a.src + sd.offset;
+  const int Ws = t.Ws, Hs = t.Hs;
+  const uint8_t* simg = a.src + t.soff;
+  const size_t spitch = (size_t)t.spitch;
   const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);
   const int ncl = xa - fx0, nb = ncl + (fx0 + fw - xb);
   const bool fill_rows = !reflect && (fy0 < 0 || fy0 + fh > Hs);
@@ -1172,7 +1196,7 @@ __device__ __forceinline__ bool rt_border(const StepArgs& a, const TileInfo& t, 
       const uint8_t* s = raw + rb + 3 * (rx - fx0);
       v = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16);
     } else {
-      v = fetch_rgb(simg + (size_t)ry * sd.pitch, rx);
+      v = fetch_rgb(simg + (size_t)ry * spitch, rx);
     }
     uint8_t* d = raw + rb + 3 * c;
     d[0] = (uint8_t)v;
@@ -1202,33 +1226,37 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
   uint8_t* smb = reinterpret_cast<uint8_t*>(sm + x.n_lut * kLutWords);
   const bool reflect = a.border == ALB_BORDER_REFLECT_101;
   const TileInfo* tinfo = reinterpret_cast<const TileInfo*>(a.tiles);
-  auto rtab_of = [&](int buf) { return reinterpret_cast<int*>(smb + buf * kRBuf + kROffTab); };
-  auto raw_of = [&](int buf) { return smb + buf * kRBuf + kROffRaw; };
+  int* rtab = reinterpret_cast<int*>(smb + kROffTab);
+  uint8_t* raw = smb + kROffRaw;
+  const uint32_t tab_a = smem_u32(rtab), raw_a = smem_u32(raw);
+  TileInfo* ctx = reinterpret_cast<TileInfo*>(smb + kRBuf);  // [2]: this tile's and the next tile's record
+  // the record of tile v into ctx[k]: 16 threads x 16-byte cp.async
+  auto prefetch = [&](int v, int k) {
+    if (tid < kTileInfoBytes / 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(ctx + k) + 16u * tid),
+                   "l"(reinterpret_cast<const uint8_t*>(tinfo + v) + 16 * tid)
+                   : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
 
   int u0, u1;
   unit_range(a.n_units, u0, u1);
   const int ubeg = u0 * kAffSub, uend = u1 * kAffSub;
   int lut_img = -1;
-  if (kRNB == 2 && ubeg < uend) {
-    rt_stage(a, tinfo[ubeg], rtab_of(0), smem_u32(raw_of(0)), reflect, tid);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
+  if (ubeg < uend) prefetch(ubeg, 0);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
   for (int u = ubeg; u < uend; ++u) {
-    const int cur = kRNB == 2 ? (u - ubeg) & 1 : 0;
-    int* rtab = rtab_of(cur);
-    uint8_t* raw = raw_of(cur);
-    const uint32_t tab_a = smem_u32(rtab), raw_a = smem_u32(raw);
-    const TileInfo t = tinfo[u];
-    if (kRNB == 1) {
-      rt_stage(a, t, rtab, raw_a, reflect, tid);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-    }
+    const int cur = (u - ubeg) & 1;
+    const TileInfo& t = ctx[cur];
+    rt_stage(a, t, rtab, raw_a, reflect, tid);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     const int img = t.img;
     const int fx0 = t.fx0, fy0 = t.fy0, fw = t.fw, fh = t.fh;
     const int tx0 = t.txy & 0xffff, ty0 = t.txy >> 16, tw = t.twh & 0xffff, th = t.twh >> 16;
     const bool fits = fw <= kRMaxW && fh <= kRRows;
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();  // tile u's rows landed; (two buffers) every warp is done with tile u - 1
+    __syncthreads();  // tile u's rows landed
     bool bar = rt_border(a, t, rtab, raw, raw_a, reflect, tid);
     if (kOne != kStagesNone && img != lut_img) {  // LUTs are read only in the compute phase
       load_stages(a, img, sm, x, kRThreads);
@@ -1236,22 +1264,17 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
       bar = true;
     }
     if (bar) __syncthreads();
-    if (kRNB == 2 && u + 1 < uend) {  // the next tile's copies overlap this tile's compute
-      rt_stage(a, tinfo[u + 1], rtab_of(cur ^ 1), smem_u32(raw_of(cur ^ 1)), reflect, tid);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-    }
-    const alb_image_desc sd = a.sdesc[img];
-    const int Ws = sd.width, Hs = sd.height;
-    const uint8_t* simg = a.src + sd.offset;
-    const ImgState* gis =
-        reinterpret_cast<const ImgState*>(reinterpret_cast<const uint8_t*>(a.geo) + (size_t)img * kGeoBytes);
-    const int m_ax = gis->m.ax, m_bx = gis->m.bx, m_ay = gis->m.ay, m_by = gis->m.by;
-    const int Wo = gis->Wo;
-    const float A0f = gis->Af[0], A3f = gis->Af[2];
-    const alb_image_desc dd = a.ddesc[img];
-    uint8_t* drow0 = a.dst + dd.offset + (size_t)ty0 * dd.pitch + (size_t)tx0 * 3;
+    if (u + 1 < uend) prefetch(u + 1, cur ^ 1);  // lands while this tile computes
+    const int Ws = t.Ws, Hs = t.Hs;
+    const uint8_t* simg = a.src + t.soff;
+    const size_t spitch = (size_t)t.spitch;
+    const int m_ax = t.m_ax, m_bx = t.m_bx, m_ay = t.m_ay, m_by = t.m_by;
+    const int Wo = t.Wo;
+    const float A0f = t.Af[0], A3f = t.Af[2];
+    const size_t dpitch = (size_t)t.dpitch;
+    uint8_t* drow0 = a.dst + t.doff + (size_t)ty0 * dpitch + (size_t)tx0 * 3;
     {
-      const float2 A14 = make_float2(gis->Af[1], gis->Af[3]);
+      const float2 A14 = make_float2(t.Af[1], t.Af[3]);
       int xw[2];
 #pragma unroll
       for (int j = 0; j < 2; ++j) xw[j] = m_ax * min(tx0 + lane + 32 * j, Wo - 1) + m_bx;
@@ -1267,19 +1290,18 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
       size_t mdpitch = 0;
       bool minner = false;
       if constexpr (kMask) {
-        const alb_image_desc msd = a.msdesc[img], mdd = a.mddesc[img];
-        msrc = a.msrc + msd.offset;
-        mpitch = msd.pitch;
-        Wm = msd.width;
-        Hm = msd.height;
-        mdpitch = mdd.pitch;
-        morow = a.mdst + mdd.offset + (size_t)(ty0 + row0) * mdpitch + tx0 + lane;
+        msrc = a.msrc + t.msoff;
+        mpitch = t.mspitch;
+        Wm = t.Wm;
+        Hm = t.Hm;
+        mdpitch = (size_t)t.mdpitch;
+        morow = a.mdst + t.mdoff + (size_t)(ty0 + row0) * mdpitch + tx0 + lane;
         minner = fx0 >= 0 && fy0 >= 0 && fx0 + fw <= Wm && fy0 + fh <= Hm;
       }
       auto rows = [&](auto staged) {
         constexpr bool kStaged = decltype(staged)::value;
         const bool st0 = lane < tw, st1 = lane + 32 < tw;
-        const size_t pitch = dd.pitch;
+        const size_t pitch = dpitch;
         uint8_t* orow = dlane + (size_t)row0 * pitch;  // column lane; lane + 32 is 96 bytes on
         int i = 0;
         while (i < nrows) {  // segments of rows in one 16-row cell row (yw moves by m_ay = +-1)
@@ -1291,7 +1313,7 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
           int aix[2], aiy[2];
 #pragma unroll
           for (int j = 0; j < 2; ++j) {  // fp64 anchors of this cell row
-            const Anchor an = cell_anchor(gis->A, A0f, A3f, xw[j], cy);
+            const Anchor an = cell_anchor(t.A, A0f, A3f, xw[j], cy);
             bxy[j] = make_float2(an.bx, an.by);
             aix[j] = an.ix;
             aiy[j] = an.iy;
@@ -1340,7 +1362,7 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
                 auto tap = [&](int px_, int py_) -> uint32_t {
                   bool ri, ci;
                   const int yy = border_idx(py_, Hs, reflect, ri), xx = border_idx(px_, Ws, reflect, ci);
-                  return (ri && ci) ? fetch_rgb(simg + (size_t)yy * sd.pitch, xx) : a.fill;
+                  return (ri && ci) ? fetch_rgb(simg + (size_t)yy * spitch, xx) : a.fill;
                 };
                 const int X = aix[j] + (int)(qxb - kMagic15Bits), Y = aiy[j] + (int)(qyb - kMagic15Bits);
                 bilerp3(tap(X, Y), tap(X + 1, Y), tap(X, Y + 1), tap(X + 1, Y + 1), fr, r, g, b);
@@ -1365,7 +1387,8 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
       if (fits) rows(std::true_type{});
       else rows(std::false_type{});
     }
-    if (kRNB == 1) __syncthreads();  // tile consumed: raw rows free
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // the next tile's record landed
+    __syncthreads();  // tile consumed: raw rows free
   }
 }
 

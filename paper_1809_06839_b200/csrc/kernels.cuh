@@ -92,7 +92,7 @@ size_t resample_q4_smem(int n_lut_stages, int rows, int sw, int R, bool normaliz
 bool resample_q4_program_ok(int mode);
 
 constexpr int kGeoBytes = 128;
-constexpr int kTileInfoBytes = 64;
+constexpr int kTileInfoBytes = 256;
 // raw-tap affine kernel: output rows per CTA tile (64 = the whole 64x64 unit,
 // 32 = the unit as two 64x32 halves, each its own TileInfo record)
 #ifndef ALB_RT_TH
