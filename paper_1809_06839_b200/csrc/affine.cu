@@ -952,12 +952,20 @@ constexpr int kRTH = ALB_RT_TH;          // output rows per CTA tile
 constexpr int kRThreads = ALB_RT_NT;     // threads per CTA
 constexpr int kRWarpRows = kRTH / (kRThreads / 32);  // output rows per warp
 constexpr int kRRows = kRTH == 64 ? 108 : 88;  // footprint rows (fh <= 104 / 84 at scale >= 0.9)
-constexpr int kRPitch = kRTH == 64 ? 368 : 304;  // raw row pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk), fw <= 107 / 86
+constexpr int kRPitch = kRTH == 64 ? 368 : 304;  // row-table layout pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk), fw <= 107 / 86;
+                                                 // 92 words = -4 banks per row (a pitch of 384 = 0 banks: every row in one bank)
 constexpr int kRMaxW = (kRPitch - 46) / 3;
+#ifndef ALB_RT_LIN_TAN
+#define ALB_RT_LIN_TAN 1e30  // linear row layout when |tan(rotation)| <= this (0: never); measured cfg2 Rotate / SSR,
+                             // cfg3 Rotate: always 1.210 / 1.248 / 0.417 ms, 1.1: 1.210 / 1.248 / 0.424,
+                             // never: 1.223 / 1.264 / 0.433
+#endif
+constexpr double kRLinTan = ALB_RT_LIN_TAN;
 constexpr int kROffTab = 0;                  // int2 [kRRows]: (rb[r], rb[r + 1])
 constexpr int kROffSpan = kRRows * 8;        // int [kRRows]: staged columns s0 | s1 << 16 of row r
 constexpr int kROffRaw = (kRRows * 12 + 31) / 16 * 16;  // raw rows [kRRows][kRPitch]
-constexpr int kRBuf = kROffRaw + kRRows * kRPitch + 16;  // one buffer: row table + raw rows
+constexpr int kRRawBytes = kRRows * (kRPitch + 16);  // raw rows: the row-table layout or a linear one (P <= kRPitch + 16)
+constexpr int kRBuf = kROffRaw + kRRawBytes + 16;  // one buffer: row table + raw rows
 constexpr int kRSmem = kRBuf + 2 * kTileInfoBytes;  // raw rows + two tile records (current, next)
 static_assert(kRBuf % 16 == 0, "16-byte aligned buffers");
 static_assert(kROffRaw % 16 == 0, "16-byte aligned raw rows");
@@ -977,7 +985,8 @@ struct TileInfo {
   long long soff, doff;        // image offsets in the source / destination buffers
   int spitch, dpitch, Wm, Hm;  // pitches; source mask dims
   long long msoff, mdoff;      // mask offsets
-  int mspitch, mdpitch, pad0, pad1;
+  int mspitch, mdpitch;
+  int P, c0;  // linear row layout (every footprint row in the image): row r at c0 + r * P, P = spitch mod 16; P = 0: row table
   int pad[8];
 };
 static_assert(sizeof(TileInfo) == kTileInfoBytes, "TileInfo is the per-unit scratch record");
@@ -1098,7 +1107,23 @@ __global__ void k_affine_setup_units(StepArgs a) {
   } else {
     t.Wm = t.Hm = 0; t.msoff = t.mdoff = 0; t.mspitch = t.mdpitch = 0;
   }
-  t.pad0 = t.pad1 = 0;
+  // linear layout when no footprint row is reflected: row r of the footprint
+  // at c0 + r * P with P = spitch (mod 16), so every row's 16-byte copies stay
+  // aligned on both sides and a tap's shared address is affine in (x, y)
+  t.P = 0;
+  t.c0 = 0;
+  if (th > 0 && t.fy0 >= 0 && t.fy0 + t.fh <= sd.height) {
+    // P = spitch (mod 16), the smallest that holds a row; one more 16 bytes if
+    // P / 4 is within 2 of a multiple of 32 words (every row in one bank: a
+    // near-vertical walk of 32 lanes would hit one bank)
+    const int base = 3 * t.fw + 46;
+    int P = base + (((sd.pitch - base) % 16) + 16) % 16;
+    const int wq = (P / 4) & 31;
+    if (wq <= 2 || wq >= 30) P += 16;
+    t.P = ((long long)t.fh * P + 32 <= kRRawBytes && fabs(s.A[3]) <= kRLinTan * fabs(s.A[0])) ? P : 0;
+    const uintptr_t g0 = (uintptr_t)(a.src + sd.offset + (size_t)t.fy0 * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * t.fx0);
+    t.c0 = 16 + (int)(g0 & 15);
+  }
   for (int k = 0; k < 8; ++k) t.pad[k] = 0;
   const int xa = min(max(t.fx0, 0), sd.width), xb = max(min(t.fx0 + t.fw, sd.width), xa);
   const bool fill_rows = a.border != ALB_BORDER_REFLECT_101 && (t.fy0 < 0 || t.fy0 + t.fh > sd.height);
@@ -1140,21 +1165,24 @@ __device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, i
     bool in;
     const int ry = border_idx(fy0 + r, Hs, reflect, in);
     const uintptr_t g = (uintptr_t)(simg + (size_t)(in ? ry : 0) * spitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+    // column fx0 of row r (address g) sits at B_r: c0 + r * P (linear layout) or
+    // r * kRPitch + 16 + (g & 15) (row table); both keep B_r = g (mod 16)
+    const int Br = t.P ? t.c0 + r * t.P : r * kRPitch + 16 + (int)(g & 15);
     if (in && cb > ca) {  // (no in-image column: the border pass fills the row)
       const uintptr_t g0 = g + 3 * (ca - fx0), ge = g0 + 3 * (cb - ca);
-      // column fx0 (address g) sits at r * kRPitch + 16 + (g & 15)
-      const uint32_t d0 = raw_a + (uint32_t)(r * kRPitch + 16) - (uint32_t)(g & ~(uintptr_t)15);
+      const uint32_t d0 = raw_a + (uint32_t)Br - (uint32_t)g;
       for (uintptr_t gk = (g0 & ~(uintptr_t)15) + 16 * h; gk < ge; gk += 32)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + (uint32_t)gk), "l"(gk) : "memory");
     }
     const int rr = min(r + h, fh - 1);
-    uintptr_t gr = g;
+    int Brr = Br;
     if (h) {
       bool in1;
       const int ry1 = border_idx(fy0 + rr, Hs, reflect, in1);
-      gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * spitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+      const uintptr_t gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * spitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+      Brr = t.P ? t.c0 + rr * t.P : rr * kRPitch + 16 + (int)(gr & 15);
     }
-    rtab[e] = (int)raw_a + rr * kRPitch + 16 + (int)(gr & 15);
+    rtab[e] = (int)raw_a + Brr;
   }
 }
 
@@ -1298,8 +1326,10 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
         morow = a.mdst + t.mdoff + (size_t)(ty0 + row0) * mdpitch + tx0 + lane;
         minner = fx0 >= 0 && fy0 >= 0 && fx0 + fw <= Wm && fy0 + fh <= Hm;
       }
-      auto rows = [&](auto staged) {
+      const uint32_t lP = (uint32_t)t.P;
+      auto rows = [&](auto staged, auto linear) {
         constexpr bool kStaged = decltype(staged)::value;
+        constexpr bool kLinear = decltype(linear)::value;
         const bool st0 = lane < tw, st1 = lane + 32 < tw;
         const size_t pitch = dpitch;
         uint8_t* orow = dlane + (size_t)row0 * pitch;  // column lane; lane + 32 is 96 bytes on
@@ -1319,7 +1349,10 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
             aiy[j] = an.iy;
             // tap byte address = rb[row] + 3 * qxb + cxo; row entry = 8 * qyb + cyo
             cxo[j] = 3u * (uint32_t)(an.ix - fx0) - 3u * kMagic15Bits;
-            cyo[j] = tab_a + 8u * ((uint32_t)(an.iy - fy0) - kMagic15Bits);
+            if constexpr (kLinear)  // tap address = P * qyb + 3 * qxb + cyo
+              cyo[j] = raw_a + (uint32_t)t.c0 + lP * ((uint32_t)(an.iy - fy0) - kMagic15Bits) + cxo[j];
+            else
+              cyo[j] = tab_a + 8u * ((uint32_t)(an.iy - fy0) - kMagic15Bits);
           }
           float dyl = (float)(yw0 & 15);
           const float ddy = (float)m_ay;
@@ -1347,11 +1380,18 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
               }
               uint32_t r, g, b;
               if constexpr (kStaged) {
-                const uint32_t cb = qxb * 3u + cxo[j];
-                uint32_t ta;
-                asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(ta) : "r"(qyb), "r"(cyo[j]));
-                const uint2 rbp = lds64(ta);
-                const uint32_t a0 = rbp.x + cb, a1 = rbp.y + cb;  // shared byte addresses of the taps
+                uint32_t a0, a1;  // shared byte addresses of the two tap rows
+                if constexpr (kLinear) {
+                  a0 = qxb * 3u + (qyb * lP + cyo[j]);
+                  a1 = a0 + lP;
+                } else {
+                  const uint32_t cb = qxb * 3u + cxo[j];
+                  uint32_t ta;
+                  asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(ta) : "r"(qyb), "r"(cyo[j]));
+                  const uint2 rbp = lds64(ta);
+                  a0 = rbp.x + cb;
+                  a1 = rbp.y + cb;
+                }
                 const uint32_t b0 = a0 & ~3u, b1 = a1 & ~3u;
                 const uint32_t w00 = lds32(b0), w01 = lds32(b0 + 4), w02 = lds32(b0 + 8);
                 const uint32_t w10 = lds32(b1), w11 = lds32(b1 + 4), w12 = lds32(b1 + 8);
@@ -1384,8 +1424,9 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
           }
         }
       };
-      if (fits) rows(std::true_type{});
-      else rows(std::false_type{});
+      if (fits && lP != 0) rows(std::true_type{}, std::true_type{});
+      else if (fits) rows(std::true_type{}, std::false_type{});
+      else rows(std::false_type{}, std::false_type{});
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");  // the next tile's record landed
     __syncthreads();  // tile consumed: raw rows free
