@@ -6,12 +6,12 @@ set -x
 TAG=${TAG:-r2}
 OPS=${OPS:-HorizontalFlip,Rotate,ShiftScaleRotate,Brightness,ShiftHSV,Grayscale,PadToSize512,Resize512,RandomSizedCrop64-512,Equalize,RandomCrop64}
 python tools/profile_ops.py --ops $OPS --reps 1 > gpurun_out/plain_ops.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_(rowflip|rowgather|affine_rt|point|resample|eq_fused)" -c 14 -o /tmp/full_cfg2 python tools/profile_ops.py --ops $OPS --reps 1 > gpurun_out/ncu_full.log 2>&1; echo full=$?
+ncu -f --set full --clock-control none --import-source on -k regex:"k_(rowflip|rowgather|affine_rt|point|resample|eq_fused)" -c 14 -o /tmp/full_cfg2 python tools/profile_ops.py --ops $OPS --reps 1 > gpurun_out/ncu_full.log 2>&1; echo full=$?
 python tools/profile_ops.py --ops cfg3:Rotate,cfg4,cfg5 --reps 1 > gpurun_out/plain_comp.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_(affine|resample|boxes|prep)" -c 10 -o /tmp/full_comp python tools/profile_ops.py --ops cfg3:Rotate,cfg4,cfg5 --reps 1 > gpurun_out/ncu_comp.log 2>&1; echo comp=$?
+ncu -f --set full --clock-control none --import-source on -k regex:"k_(affine|resample|boxes|prep)" -c 10 -o /tmp/full_comp python tools/profile_ops.py --ops cfg3:Rotate,cfg4,cfg5 --reps 1 > gpurun_out/ncu_comp.log 2>&1; echo comp=$?
 NOPS=${NOPS:-Rot90k1,Grid5,Elastic}
 python tools/profile_ops.py --ops $NOPS --reps 1 > gpurun_out/plain_next.log 2>&1 && \
-ncu --set full --clock-control none -k regex:"k_(d4|resample|elastic)" -c 3 -o /tmp/full_next python tools/profile_ops.py --ops $NOPS --reps 1 --n 500 > gpurun_out/ncu_next.log 2>&1; echo next=$?
+ncu -f --set full --clock-control none -k regex:"k_(d4|resample|elastic)" -c 3 -o /tmp/full_next python tools/profile_ops.py --ops $NOPS --reps 1 --n 500 > gpurun_out/ncu_next.log 2>&1; echo next=$?
 for r in full_cfg2 full_comp full_next; do
   ncu -i /tmp/$r.ncu-rep --page raw --csv > gpurun_out/${TAG}_${r}_raw.csv 2>/dev/null
 done
