@@ -950,6 +950,10 @@ constexpr int kRTH = ALB_RT_TH;          // output rows per CTA tile
 #define ALB_RT_NT 256
 #endif
 constexpr int kRThreads = ALB_RT_NT;     // threads per CTA
+#ifndef ALB_RT_TPR
+#define ALB_RT_TPR 2  // threads per footprint row in the staging copies
+#endif
+constexpr int kRTpr = ALB_RT_TPR;
 constexpr int kRWarpRows = kRTH / (kRThreads / 32);  // output rows per warp
 constexpr int kRRows = kRTH == 64 ? 108 : 88;  // footprint rows (fh <= 104 / 84 at scale >= 0.9)
 constexpr int kRPitch = kRTH == 64 ? 368 : 304;  // row-table layout pitch: 16 + 15 (phase) + 3 * fw + 15 (last chunk), fw <= 107 / 86;
@@ -1156,8 +1160,8 @@ __device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, i
   const size_t spitch = (size_t)t.spitch;
   const int xa = min(max(fx0, 0), Ws), xb = max(min(fx0 + fw, Ws), xa);  // in-image columns [xa, xb)
   int* spans = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(rtab) + kROffSpan);
-  for (int e = tid; e < 2 * fh; e += kRThreads) {
-    const int r = e >> 1, h = e & 1;
+  for (int e = tid; e < kRTpr * fh; e += kRThreads) {
+    const int r = e / kRTpr, h = e % kRTpr;
     int s0, s1;
     row_span(t, r, s0, s1);  // only the columns the rotated tile's taps reach
     if (h == 0) spans[r] = s0 | (s1 << 16);
@@ -1171,18 +1175,21 @@ __device__ __forceinline__ void rt_stage(const StepArgs& a, const TileInfo& t, i
     if (in && cb > ca) {  // (no in-image column: the border pass fills the row)
       const uintptr_t g0 = g + 3 * (ca - fx0), ge = g0 + 3 * (cb - ca);
       const uint32_t d0 = raw_a + (uint32_t)Br - (uint32_t)g;
-      for (uintptr_t gk = (g0 & ~(uintptr_t)15) + 16 * h; gk < ge; gk += 32)
+      for (uintptr_t gk = (g0 & ~(uintptr_t)15) + 16 * h; gk < ge; gk += 16 * kRTpr)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + (uint32_t)gk), "l"(gk) : "memory");
     }
-    const int rr = min(r + h, fh - 1);
-    int Brr = Br;
-    if (h) {
-      bool in1;
-      const int ry1 = border_idx(fy0 + rr, Hs, reflect, in1);
-      const uintptr_t gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * spitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
-      Brr = t.P ? t.c0 + rr * t.P : rr * kRPitch + 16 + (int)(gr & 15);
+    // row-table entries rb[r] (h = 0) and rb[r + 1] (h = 1; the h = 0 thread too with one thread per row)
+    for (int hh = h; hh < (kRTpr == 1 ? 2 : min(h + 1, 2)); ++hh) {
+      const int rr = min(r + hh, fh - 1);
+      int Brr = Br;
+      if (hh) {
+        bool in1;
+        const int ry1 = border_idx(fy0 + rr, Hs, reflect, in1);
+        const uintptr_t gr = (uintptr_t)(simg + (size_t)(in1 ? ry1 : 0) * spitch) + (uintptr_t)(ptrdiff_t)(3 * fx0);
+        Brr = t.P ? t.c0 + rr * t.P : rr * kRPitch + 16 + (int)(gr & 15);
+      }
+      rtab[2 * r + hh] = (int)raw_a + Brr;
     }
-    rtab[e] = (int)raw_a + Brr;
   }
 }
 
