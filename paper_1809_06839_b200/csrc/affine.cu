@@ -991,7 +991,8 @@ struct TileInfo {
   long long msoff, mdoff;      // mask offsets
   int mspitch, mdpitch;
   int P, c0;  // linear row layout (every footprint row in the image): row r at c0 + r * P, P = spitch mod 16; P = 0: row table
-  int pad[8];
+  float eiy[4];  // 1 / (vy[e + 1] - vy[e]) per parallelogram edge (0 for a horizontal edge), for the row spans
+  int pad[4];
 };
 static_assert(sizeof(TileInfo) == kTileInfoBytes, "TileInfo is the per-unit scratch record");
 
@@ -1040,10 +1041,9 @@ __device__ __forceinline__ void row_span(const TileInfo& t, int r, int& s0, int&
   for (int e = 0; e < 4; ++e) {
     const int e1 = (e + 1) & 3;
     const float ex = t.vx[e], ey = t.vy[e];
-    const float edx = t.vx[e1] - ex, dy = t.vy[e1] - ey;
+    const float edx = t.vx[e1] - ex, eiy = t.eiy[e];
     if (ey >= ya && ey <= yb) { xmn = fminf(xmn, ex); xmx = fmaxf(xmx, ex); }
-    if (dy != 0.f) {
-      const float eiy = 1.f / dy;
+    if (eiy != 0.f) {
 #pragma unroll
       for (int bnd = 0; bnd < 2; ++bnd) {
         const float tt = ((bnd ? yb : ya) - ey) * eiy;
@@ -1128,7 +1128,11 @@ __global__ void k_affine_setup_units(StepArgs a) {
     const uintptr_t g0 = (uintptr_t)(a.src + sd.offset + (size_t)t.fy0 * sd.pitch) + (uintptr_t)(ptrdiff_t)(3 * t.fx0);
     t.c0 = 16 + (int)(g0 & 15);
   }
-  for (int k = 0; k < 8; ++k) t.pad[k] = 0;
+  for (int e = 0; e < 4; ++e) {
+    const float dy = t.vy[(e + 1) & 3] - t.vy[e];
+    t.eiy[e] = dy != 0.f ? 1.f / dy : 0.f;
+  }
+  for (int k = 0; k < 4; ++k) t.pad[k] = 0;
   const int xa = min(max(t.fx0, 0), sd.width), xb = max(min(t.fx0 + t.fw, sd.width), xa);
   const bool fill_rows = a.border != ALB_BORDER_REFLECT_101 && (t.fy0 < 0 || t.fy0 + t.fh > sd.height);
   const int ncols = fill_rows ? t.fw : (xa - t.fx0) + (t.fx0 + t.fw - xb);
