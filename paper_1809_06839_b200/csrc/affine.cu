@@ -1370,7 +1370,7 @@ __global__ void __launch_bounds__(kRThreads, ALB_RT_MINB) k_affine_rt(StepArgs a
 #pragma unroll kRowUnroll
           for (; i < iend; ++i, dyl += ddy, orow += pitch) {
             uint32_t rr[2], gg[2], bb[2];
-            uint8_t mv[2];
+            [[maybe_unused]] uint8_t mv[2];  // labels (kMask)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {  // both columns always (clamped): the two pixels interleave
               const float2 l = __ffma2_rn(A14, make_float2(dyl, dyl), bxy[j]);
