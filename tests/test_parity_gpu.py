@@ -855,3 +855,31 @@ def test_affine_rt_equals_pipelined_kernel(name, monkeypatch):
     monkeypatch.delenv("ALB_AFFINE_PIPE", raising=False)
     for x, y in zip(*outs):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("name", ["Rotate", "ShiftScaleRotate", "SSR+crop+flip", "Rotate-constant"])
+def test_affine_rt_labels_equal_label_kernel(name, monkeypatch):
+    """The raw-tap kernel gathers the nearest labels itself; the pipelined
+    path (ALB_AFFINE_PIPE=1) runs the separate label kernel k_affine_mask.
+    Both take the label at the same anchor coordinates, rounded half up:
+    images and masks equal byte for byte (random-label masks, so any other
+    decision would show)."""
+    ssr = C.CFG2_MENU["ShiftScaleRotate"]
+    specs = {"Rotate": C.CFG2_MENU["Rotate"], "ShiftScaleRotate": ssr,
+             "SSR+crop+flip": ssr + [C.op("RandomCrop", size=(64, 90)), C.op("HorizontalFlip", p=0.5)],
+             "Rotate-constant": [C.op("Rotate", lo=[-90.0], hi=[90.0], interp="bilinear",
+                                      border="constant")]}[name]
+    sizes = gen.cfg2_sizes(60) + [(97, 1301), (1200, 180)]
+    b = gen.gen_images(sizes, seed=5, device="cuda")
+    masks, _ = random_masks(sizes, seed=6)
+    outs = []
+    for pipe in (False, True):
+        if pipe:
+            monkeypatch.setenv("ALB_AFFINE_PIPE", "1")
+        else:
+            monkeypatch.delenv("ALB_AFFINE_PIPE", raising=False)
+        outs.append(run_gpu(specs, b, seed=3, first=0, masks=masks))
+    monkeypatch.delenv("ALB_AFFINE_PIPE", raising=False)
+    for key in ("images", "masks"):
+        for x, y in zip(outs[0][key], outs[1][key]):
+            assert np.array_equal(x, y), key
