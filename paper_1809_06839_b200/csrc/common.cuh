@@ -196,26 +196,10 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return _
 // Core on biased floats (2^23 + byte) in, biased bit patterns out (byte in
 // bits 0-7, 0x4B0000 above): callers that unpack / pack with byte permutes
 // skip the per-channel masks and ORs.
-__device__ __forceinline__ void hsv_shift_px2b(float dh6w, float ds, float dv, float2 Rb, float2 Gb, float2 Bb,
-                                               uint32_t (&ro)[2], uint32_t (&go)[2], uint32_t (&bo)[2]) {
+// the part after the hue (shared by both hsv_shift_px2b variants)
+__device__ __forceinline__ void hsv_tail2(float ds, float dv, float2 d, float2 mx, float2 rm, float2 h6r,
+                                          uint32_t (&ro)[2], uint32_t (&go)[2], uint32_t (&bo)[2]) {
   const float M = 8388608.f;
-  float2 mxb, mnb, pa, pb, off;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float R = i ? Rb.y : Rb.x, G = i ? Gb.y : Gb.x, B = i ? Bb.y : Bb.x;
-    const float hi = fmaxf(R, fmaxf(G, B)), lo = fminf(R, fminf(G, B));
-    const bool isr = hi == R;
-    const bool isg = !isr && hi == G;
-    const float A_ = isr ? G : (isg ? B : R), B_ = isr ? B : (isg ? R : G);
-    const float o = isr ? dh6w : (isg ? dh6w + 2.f : dh6w + 4.f);
-    if (i) { mxb.y = hi; mnb.y = lo; pa.y = A_; pb.y = B_; off.y = o; }
-    else { mxb.x = hi; mnb.x = lo; pa.x = A_; pb.x = B_; off.x = o; }
-  }
-  const float2 d = f2add(mxb, make_float2(-mnb.x, -mnb.y));
-  const float2 mx = f2add(mxb, make_float2(-M, -M));
-  const float2 rd = make_float2(fminf(rcp_approx(d.x), 2.f), fminf(rcp_approx(d.y), 2.f));
-  const float2 rm = make_float2(fminf(rcp_approx(mx.x), 2.f), fminf(rcp_approx(mx.y), 2.f));
-  const float2 h6r = f2fma(f2add(pa, make_float2(-pb.x, -pb.y)), rd, off);
   const float2 h6 = make_float2(h6r.x >= 5.f ? h6r.x - 6.f : h6r.x, h6r.y >= 5.f ? h6r.y - 6.f : h6r.y);
   float2 sv = f2fma(d, rm, make_float2(ds, ds));
   sv = make_float2(__saturatef(sv.x), __saturatef(sv.y));
@@ -239,6 +223,62 @@ __device__ __forceinline__ void hsv_shift_px2b(float dh6w, float ds, float dv, f
   const float2 kb = f2add(h6, make_float2(1.f - 2.f, 1.f - 2.f));
   emit(make_float2(__saturatef(2.f - fabsf(kb.x)), __saturatef(2.f - fabsf(kb.y))), bo);
 }
+// kCand3: the hue of both pixels from three candidates (dominant R, G, B)
+// computed on the paired pipe -- differences exact on biased integers, the
+// same fma a selected operand pair gives, so bit-identical -- then two
+// selects per pixel instead of six (ShiftHSV 0.475 -> 0.470 ms, A/B); the
+// fused resampler keeps the operand selects (-DALB_HSV_SEL_PAIRS: everywhere).
+template <bool kCand3 = true>
+__device__ __forceinline__ void hsv_shift_px2b(float dh6w, float ds, float dv, float2 Rb, float2 Gb, float2 Bb,
+                                               uint32_t (&ro)[2], uint32_t (&go)[2], uint32_t (&bo)[2]) {
+  const float M = 8388608.f;
+#ifdef ALB_HSV_SEL_PAIRS
+  constexpr bool kC3 = false;
+#else
+  constexpr bool kC3 = kCand3;
+#endif
+  if constexpr (kC3) {
+    float2 mxb, mnb;
+    bool isr[2], isg[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float R = i ? Rb.y : Rb.x, G = i ? Gb.y : Gb.x, B = i ? Bb.y : Bb.x;
+      const float hi = fmaxf(R, fmaxf(G, B)), lo = fminf(R, fminf(G, B));
+      isr[i] = hi == R;
+      isg[i] = !isr[i] && hi == G;
+      if (i) { mxb.y = hi; mnb.y = lo; }
+      else { mxb.x = hi; mnb.x = lo; }
+    }
+    const float2 d = f2add(mxb, make_float2(-mnb.x, -mnb.y));
+    const float2 mx = f2add(mxb, make_float2(-M, -M));
+    const float2 rd = make_float2(fminf(rcp_approx(d.x), 2.f), fminf(rcp_approx(d.y), 2.f));
+    const float2 rm = make_float2(fminf(rcp_approx(mx.x), 2.f), fminf(rcp_approx(mx.y), 2.f));
+    const float2 hr = f2fma(f2add(Gb, make_float2(-Bb.x, -Bb.y)), rd, make_float2(dh6w, dh6w));
+    const float2 hg = f2fma(f2add(Bb, make_float2(-Rb.x, -Rb.y)), rd, make_float2(dh6w + 2.f, dh6w + 2.f));
+    const float2 hb = f2fma(f2add(Rb, make_float2(-Gb.x, -Gb.y)), rd, make_float2(dh6w + 4.f, dh6w + 4.f));
+    const float2 h6r = make_float2(isr[0] ? hr.x : (isg[0] ? hg.x : hb.x), isr[1] ? hr.y : (isg[1] ? hg.y : hb.y));
+    hsv_tail2(ds, dv, d, mx, rm, h6r, ro, go, bo);
+  } else {
+    float2 mxb, mnb, pa, pb, off;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float R = i ? Rb.y : Rb.x, G = i ? Gb.y : Gb.x, B = i ? Bb.y : Bb.x;
+      const float hi = fmaxf(R, fmaxf(G, B)), lo = fminf(R, fminf(G, B));
+      const bool isr = hi == R;
+      const bool isg = !isr && hi == G;
+      const float A_ = isr ? G : (isg ? B : R), B_ = isr ? B : (isg ? R : G);
+      const float o = isr ? dh6w : (isg ? dh6w + 2.f : dh6w + 4.f);
+      if (i) { mxb.y = hi; mnb.y = lo; pa.y = A_; pb.y = B_; off.y = o; }
+      else { mxb.x = hi; mnb.x = lo; pa.x = A_; pb.x = B_; off.x = o; }
+    }
+    const float2 d = f2add(mxb, make_float2(-mnb.x, -mnb.y));
+    const float2 mx = f2add(mxb, make_float2(-M, -M));
+    const float2 rd = make_float2(fminf(rcp_approx(d.x), 2.f), fminf(rcp_approx(d.y), 2.f));
+    const float2 rm = make_float2(fminf(rcp_approx(mx.x), 2.f), fminf(rcp_approx(mx.y), 2.f));
+    const float2 h6r = f2fma(f2add(pa, make_float2(-pb.x, -pb.y)), rd, off);
+    hsv_tail2(ds, dv, d, mx, rm, h6r, ro, go, bo);
+  }
+}
 __device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, uint32_t (&r)[2], uint32_t (&g)[2],
                                               uint32_t (&b)[2]) {
   float2 Rb, Gb, Bb;
@@ -246,7 +286,7 @@ __device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, ui
   Gb.x = __uint_as_float(g[0] | 0x4B000000u); Gb.y = __uint_as_float(g[1] | 0x4B000000u);
   Bb.x = __uint_as_float(b[0] | 0x4B000000u); Bb.y = __uint_as_float(b[1] | 0x4B000000u);
   uint32_t ro[2], go[2], bo[2];
-  hsv_shift_px2b(dh6w, ds, dv, Rb, Gb, Bb, ro, go, bo);
+  hsv_shift_px2b<false>(dh6w, ds, dv, Rb, Gb, Bb, ro, go, bo);
   r[0] = ro[0] & 0xffu; r[1] = ro[1] & 0xffu; g[0] = go[0] & 0xffu; g[1] = go[1] & 0xffu;
   b[0] = bo[0] & 0xffu; b[1] = bo[1] & 0xffu;
 }
