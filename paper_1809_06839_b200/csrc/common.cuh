@@ -226,8 +226,8 @@ __device__ __forceinline__ void hsv_tail2(float ds, float dv, float2 d, float2 m
 // kCand3: the hue of both pixels from three candidates (dominant R, G, B)
 // computed on the paired pipe -- differences exact on biased integers, the
 // same fma a selected operand pair gives, so bit-identical -- then two
-// selects per pixel instead of six (ShiftHSV 0.475 -> 0.470 ms, A/B); the
-// fused resampler keeps the operand selects (-DALB_HSV_SEL_PAIRS: everywhere).
+// selects per pixel instead of six (ShiftHSV 0.475 -> 0.470 ms, cfg4 fused
+// resampler 0.308 -> 0.307 ms, A/B); -DALB_HSV_SEL_PAIRS: the operand selects.
 template <bool kCand3 = true>
 __device__ __forceinline__ void hsv_shift_px2b(float dh6w, float ds, float dv, float2 Rb, float2 Gb, float2 Bb,
                                                uint32_t (&ro)[2], uint32_t (&go)[2], uint32_t (&bo)[2]) {
@@ -286,7 +286,7 @@ __device__ __forceinline__ void hsv_shift_px2(float dh6w, float ds, float dv, ui
   Gb.x = __uint_as_float(g[0] | 0x4B000000u); Gb.y = __uint_as_float(g[1] | 0x4B000000u);
   Bb.x = __uint_as_float(b[0] | 0x4B000000u); Bb.y = __uint_as_float(b[1] | 0x4B000000u);
   uint32_t ro[2], go[2], bo[2];
-  hsv_shift_px2b<false>(dh6w, ds, dv, Rb, Gb, Bb, ro, go, bo);
+  hsv_shift_px2b(dh6w, ds, dv, Rb, Gb, Bb, ro, go, bo);
   r[0] = ro[0] & 0xffu; r[1] = ro[1] & 0xffu; g[0] = go[0] & 0xffu; g[1] = go[1] & 0xffu;
   b[0] = bo[0] & 0xffu; b[1] = bo[1] & 0xffu;
 }
